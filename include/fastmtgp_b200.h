@@ -1,0 +1,141 @@
+/* fastmtgp-b200 — C ABI of the B200 fast multitask-GP fit path (sm_100a, fp64).
+ *
+ * Drop-in boundary for the reference's structured-Gram seam
+ * (/root/reference/proj/include/fastmtgp/fast_gram.hpp:34-70) and for the model-level
+ * hot path it serves (gp_core.hpp:46-83).  Plain pointers and sizes only; host arrays
+ * are owned by the caller, device memory by the model handle.  Every entry point
+ * returns an fmtgp status code; fmtgp_last_error() holds the thread-local message.
+ *
+ * Conventions:
+ *   - task-indexed inputs/outputs are in INTERNAL order (descending n, stable), exactly
+ *     what fast_gram.hpp's functions take (R_internal, xi_internal; gp_core.cpp:19-32);
+ *   - observation / coefficient vectors are length N = sum n_l, task blocks in internal
+ *     order, points of a task in the design's natural (radical-inverse) order;
+ *   - pair (l, lp), l <= lp, enumerated row by row (fast_gram.cpp:35-40).
+ */
+#ifndef FASTMTGP_B200_H
+#define FASTMTGP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FMTGP_API __attribute__((visibility("default")))
+#else
+#define FMTGP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (common.hpp:16-22 exception mapping) */
+#define FMTGP_OK 0
+#define FMTGP_ERR_INVALID 1         /* FastMtgpError: bad sizes / arguments               */
+#define FMTGP_ERR_SCHUR 2           /* SchurBreakdown: non-positive Schur pivot (retryable) */
+#define FMTGP_ERR_NONREAL 3         /* FastMtgpError: non-real Schur complement / residue  */
+#define FMTGP_ERR_CUDA 4            /* CUDA runtime failure                               */
+#define FMTGP_ERR_OOM 5             /* device allocation failed                           */
+#define FMTGP_ERR_UNSUPPORTED 6     /* valid input outside what this build implements     */
+
+#define FMTGP_MAX_D 16
+#define FMTGP_MAX_T 8
+
+/* Design: LdDesign (ld_sequences.hpp:56-77) without materialised points — the kernels
+ * regenerate every coordinate from the generator.  Layout identical to the oracle's
+ * RefDesign (oracle/ref_capi.cpp). */
+typedef struct fmtgp_design {
+    int kind;                  /* 0: shifted rank-1 lattice (SI kernel), 1: digital net (DSI) */
+    int d;                     /* dimension, <= FMTGP_MAX_D                                   */
+    int L;                     /* tasks, <= FMTGP_MAX_T                                       */
+    const int* m;              /* [L] log2 sizes, internal (descending) order                  */
+    const uint64_t* g;         /* lattice: generating vector [d], g[0] == 1                    */
+    uint64_t n_max;            /* lattice: power of two >= 2^m[0]                              */
+    const uint64_t* columns;   /* digital: [d * m_cols] 53-bit msb-aligned direction numbers   */
+    int m_cols;                /* digital: columns per dimension, >= m[0]                      */
+    const uint64_t* shift_bits;/* [L * d] 53-bit per-task shifts (internal order)             */
+} fmtgp_design;
+
+/* Hyperparams (kernels.hpp:21-31), task-indexed fields in INTERNAL order. */
+typedef struct fmtgp_hyper {
+    double gamma;
+    const double* eta;   /* [d] */
+    int si_alpha;        /* lattice: 1 -> B2, 2 -> B4 */
+    double b[4];         /* digital: Walsh order weights */
+    const double* B;     /* [L * s] row-major task factor, R = B B^T + diag(t) */
+    int s;
+    const double* t;     /* [L] > 0 */
+    const double* xi;    /* [L] >= 0 nugget */
+} fmtgp_hyper;
+
+/* One NLL evaluation: loss_value (gp_core.cpp:197-227) plus the analytic gradient that
+ * replaces the reference's central finite differences (gp_core.cpp:341-351). */
+typedef struct fmtgp_result {
+    double nll;                 /* (y - E tau)^T K^-1 (y - E tau) + log|K| (no 1/2, no N log 2pi) */
+    double logdet;
+    double quad;
+    double dgamma;              /* dNLL/dgamma                                          */
+    double deta[FMTGP_MAX_D];   /* dNLL/deta_j                                          */
+    double dR[FMTGP_MAX_T * FMTGP_MAX_T]; /* symmetric G: dNLL = sum_ab G_ab dR_ab (L x L, stride L) */
+    double dB[FMTGP_MAX_T * FMTGP_MAX_T]; /* dNLL/dB = 2 G B   (L x s, row-major)       */
+    double dt[FMTGP_MAX_T];     /* dNLL/dt_l = G_ll                                     */
+    double tau[FMTGP_MAX_T];    /* closed-form NMLL prior means (internal order)        */
+    double xi_scale;            /* nugget escalation factor applied (10^attempts)       */
+    int escalations;            /* SchurBreakdown retries used (gp_core.cpp:98-127)     */
+    int status;                 /* FMTGP_OK or the per-candidate failure code           */
+} fmtgp_result;
+
+typedef struct fmtgp_model* fmtgp_model_t;
+
+FMTGP_API const char* fmtgp_last_error(void);
+FMTGP_API int fmtgp_abi_version(void);
+
+/* ---- model: device-resident design, observations and workspace ------------------- */
+FMTGP_API int fmtgp_model_create(const fmtgp_design* design, int device, int max_candidates, fmtgp_model_t* out);
+FMTGP_API int fmtgp_model_destroy(fmtgp_model_t model);
+/* y: host [N] (internal order).  Uploads, computes yhat = blockdiag(V̄) y once (cached,
+ * BASELINE config 5 "FWHT of y computed once") and the closed-form tau. */
+FMTGP_API int fmtgp_model_set_y(fmtgp_model_t model, const double* y);
+/* same from a device pointer (no host round trip) */
+FMTGP_API int fmtgp_model_set_y_device(fmtgp_model_t model, const double* y_dev);
+/* stream the model's work is ordered on (cudaStream_t as void*) */
+FMTGP_API void* fmtgp_model_stream(fmtgp_model_t model);
+
+/* ---- fast_gram.hpp seam ------------------------------------------------------------ */
+/* build_spectrum (fast_gram.cpp:42-89): Lam_{l,lp} for the hyperparameters. */
+FMTGP_API int fmtgp_build_spectrum(fmtgp_model_t model, const fmtgp_hyper* h);
+/* copy pair (l <= lp) back in natural frequency order, length n_l (tests / small N) */
+FMTGP_API int fmtgp_spectrum_read(fmtgp_model_t model, int l, int lp, double* re, double* im);
+/* invert_and_logdet (fast_gram.cpp:151-263): factorises the current spectrum.
+ * FMTGP_ERR_SCHUR on a non-positive pivot, FMTGP_ERR_NONREAL on a non-real one. */
+FMTGP_API int fmtgp_invert_and_logdet(fmtgp_model_t model, double* logdet);
+/* solve (fast_gram.cpp:265-299): x = K^-1 b, host arrays [N] */
+FMTGP_API int fmtgp_solve(fmtgp_model_t model, const double* b, double* x);
+/* gram_matvec (fast_gram.cpp:91-131): out = K b */
+FMTGP_API int fmtgp_gram_matvec(fmtgp_model_t model, const double* b, double* out);
+/* extract_pi_h (fast_gram.cpp:311-335): Pi = E^T K^-1 E, [L * L] row-major */
+FMTGP_API int fmtgp_extract_pi(fmtgp_model_t model, double* Pi);
+/* trace_inverse (fast_gram.cpp:301-309) */
+FMTGP_API int fmtgp_trace_inverse(fmtgp_model_t model, double* tr);
+
+/* ---- gp_core hot path -------------------------------------------------------------- */
+/* refresh + loss_value (NMLL) [+ analytic gradient] with SchurBreakdown noise escalation
+ * (xi x10, at most 6 retries; zero xi -> 1e-12 * scale, gp_core.cpp:98-127). */
+FMTGP_API int fmtgp_nll(fmtgp_model_t model, const fmtgp_hyper* h, int want_grad, fmtgp_result* out);
+/* ncand independent hyperparameter candidates in one sweep (BASELINE config 5); each
+ * result carries its own status / escalation count. */
+FMTGP_API int fmtgp_nll_batch(fmtgp_model_t model, int ncand, const fmtgp_hyper* h, int want_grad, fmtgp_result* out);
+/* coefficients c = K^-1 (y - E tau) of the last fmtgp_nll call (GpModel::c), host [N] */
+FMTGP_API int fmtgp_coefficients(fmtgp_model_t model, double* c);
+/* posterior_mean_batch (gp_core.cpp:409-421) for the last fmtgp_nll hyperparameters:
+ * X host [count * d], task internal index */
+FMTGP_API int fmtgp_posterior_mean(fmtgp_model_t model, int task, const double* X, int64_t count, double* out);
+/* posterior variance K((t,x),(t,x)) - k^T K^-1 k (posterior_cov, gp_core.cpp:423-445, x = x') */
+FMTGP_API int fmtgp_posterior_var(fmtgp_model_t model, int task, const double* X, int64_t count, double* out);
+/* multitask_cubature (cubature.cpp:52-75): mu [L], Sigma [L * L] (internal order) */
+FMTGP_API int fmtgp_cubature(fmtgp_model_t model, double* mu, double* Sigma);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FASTMTGP_B200_H */

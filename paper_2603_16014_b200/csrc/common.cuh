@@ -1,0 +1,103 @@
+// Shared device helpers for the fastmtgp-b200 kernels (sm_100a, fp64).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+
+namespace fmtgp {
+
+constexpr int MAXD = 16;   // spatial dimensions supported by the register-resident kernels
+constexpr int MAXT = 8;    // tasks (reference make_design: L <= 8, ld_sequences.cpp:167)
+constexpr int MAXP = MAXT * (MAXT + 1) / 2;
+constexpr int DIGITAL_BITS = 53;
+constexpr uint64_t MASK53 = (uint64_t(1) << 53) - 1;
+constexpr int TW_BASE_LOG = 13;  // twiddle tables hold 2^13 entries per level
+
+// ---------------------------------------------------------------- complex fp64
+__host__ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__host__ __device__ __forceinline__ double2 cmulc(double2 a, double2 b) {  // a * conj(b)
+    return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
+__host__ __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__host__ __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__host__ __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__host__ __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+
+// ---------------------------------------------------------------- twiddles
+// tw[L][u] = exp(-2 pi i u / 2^L) for u < min(2^L, 2^13), L = 0..26, built on device
+// with sincospi (see transforms.cu).  exp(-2 pi i t / 2^L) for any t < 2^L is one
+// table read (L <= 13) or the product of two (L > 13): t = hi * 2^(L-13) + lo.
+struct Twiddles {
+    const double2* tab;  // [27][8192]
+};
+
+__device__ __forceinline__ double2 twiddle(const double2* __restrict__ tab, uint64_t t, int L) {
+    // exp(-2 pi i t / 2^L), t taken mod 2^L
+    t &= (uint64_t(1) << L) - 1;
+    if (L <= TW_BASE_LOG) return __ldg(tab + (size_t(L) << TW_BASE_LOG) + t);
+    const int s = L - TW_BASE_LOG;
+    const double2 hi = __ldg(tab + (size_t(TW_BASE_LOG) << TW_BASE_LOG) + (t >> s));
+    const double2 lo = __ldg(tab + (size_t(L) << TW_BASE_LOG) + (t & ((uint64_t(1) << s) - 1)));
+    return cmul(hi, lo);
+}
+
+// ---------------------------------------------------------------- reductions
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* scratch /* >= NT/32 */) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) scratch[w] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (threadIdx.x < 32) {
+        r = (l < NT / 32) ? scratch[l] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    }
+    return r;  // valid in thread 0
+}
+
+__device__ __forceinline__ uint32_t bitrev32(uint32_t x, int m) { return m == 0 ? 0u : (__brev(x) >> (32 - m)); }
+__device__ __forceinline__ uint64_t bitrev64(uint64_t x, int m) { return m == 0 ? 0ull : (__brevll(x) >> (64 - m)); }
+
+// ---------------------------------------------------------------- real / complex scalar ops
+template <bool CX>
+struct Sc;
+template <>
+struct Sc<true> {
+    using T = double2;
+    static __device__ __forceinline__ T zero() { return make_double2(0.0, 0.0); }
+    static __device__ __forceinline__ T one() { return make_double2(1.0, 0.0); }
+    static __device__ __forceinline__ T add(T a, T b) { return cadd(a, b); }
+    static __device__ __forceinline__ T mul(T a, T b) { return cmul(a, b); }
+    static __device__ __forceinline__ T mulc(T a, T b) { return cmulc(a, b); }  // a conj(b)
+    static __device__ __forceinline__ T conj(T a) { return cconj(a); }
+    static __device__ __forceinline__ T sub(T a, T b) { return csub(a, b); }
+    static __device__ __forceinline__ T scale(T a, double s) { return cscale(a, s); }
+    static __device__ __forceinline__ double re(T a) { return a.x; }
+    static __device__ __forceinline__ double im(T a) { return a.y; }
+    static __device__ __forceinline__ double abs2(T a) { return a.x * a.x + a.y * a.y; }
+};
+template <>
+struct Sc<false> {
+    using T = double;
+    static __device__ __forceinline__ T zero() { return 0.0; }
+    static __device__ __forceinline__ T one() { return 1.0; }
+    static __device__ __forceinline__ T add(T a, T b) { return a + b; }
+    static __device__ __forceinline__ T mul(T a, T b) { return a * b; }
+    static __device__ __forceinline__ T mulc(T a, T b) { return a * b; }
+    static __device__ __forceinline__ T conj(T a) { return a; }
+    static __device__ __forceinline__ T sub(T a, T b) { return a - b; }
+    static __device__ __forceinline__ T scale(T a, double s) { return a * s; }
+    static __device__ __forceinline__ double re(T a) { return a; }
+    static __device__ __forceinline__ double im(T) { return 0.0; }
+    static __device__ __forceinline__ double abs2(T a) { return a * a; }
+};
+
+}  // namespace fmtgp

@@ -1,0 +1,810 @@
+// Device kernels of the fast-MTGP fit path (sm_100a, fp64).  See passes.cuh for the
+// transform conventions and kernels.cuh for the launch API.
+#include <climits>
+
+#include "kernels.cuh"
+
+namespace fmtgp {
+
+// ============================================================================ twiddles
+__global__ void k_init_twiddles(double2* tab) {
+    const int L = blockIdx.y;
+    const int cnt = L <= TW_BASE_LOG ? (1 << L) : (1 << TW_BASE_LOG);
+    for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < cnt; u += gridDim.x * blockDim.x) {
+        double s, c;
+        // exp(-2 pi i u / 2^L) = cos(pi x) - i sin(pi x), x = 2u / 2^L (exact)
+        sincospi(ldexp(double(u), 1 - L), &s, &c);
+        tab[(size_t(L) << TW_BASE_LOG) + u] = make_double2(c, -s);
+    }
+}
+
+void init_twiddles(double2* tab, cudaStream_t s) {
+    k_init_twiddles<<<dim3(32, 27), 256, 0, s>>>(tab);
+}
+
+// ============================================================================ generic sink glue
+template <class Snk>
+__device__ __forceinline__ void sink_put(const Snk& s, int v, long long pos, double2 A) { s.put(v, pos, A); }
+template <class Snk>
+__device__ __forceinline__ void sink_put(const Snk& s, int v, long long pos, double A) { s.put(v, pos, A); }
+
+// ============================================================================ forward, single CTA
+template <class Src, class Snk>
+__global__ void __launch_bounds__(NT_T) k_fwd_small_lat(Src src, Snk snk, int m, const double2* __restrict__ tw) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double2* sm = reinterpret_cast<double2*>(smraw);
+    const int v = blockIdx.x;
+    if (m == 0) {
+        if (threadIdx.x == 0) snk.put(v, 0, make_double2(src(v, 0), 0.0));
+        return;
+    }
+    const int lp = m - 1, Np = 1 << lp;
+    for (int e = threadIdx.x; e < Np; e += NT_T) sm[e] = make_double2(src(v, 2ull * e), src(v, 2ull * e + 1));
+    __syncthreads();
+    smem_fft<NT_T>(sm, lp, 1, Np, -1, tw);
+    for (int k = threadIdx.x; k <= Np / 2; k += NT_T) {
+        if (k == 0) {
+            const double2 Z0 = sm[0];
+            snk.put(v, 0, make_double2(Z0.x + Z0.y, Z0.x - Z0.y));
+            continue;
+        }
+        const int kp = Np - k;
+        const double2 Zk = sm[k], Zp = sm[kp];
+        snk.put(v, k, r2c_post(Zk, Zp, twiddle(tw, k, m)));
+        if (kp != k) snk.put(v, kp, r2c_post(Zp, Zk, twiddle(tw, kp, m)));
+    }
+}
+
+template <class Src, class Snk>
+__global__ void __launch_bounds__(NT_T) k_fwd_small_dig(Src src, Snk snk, int m) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double* sm = reinterpret_cast<double*>(smraw);
+    const int v = blockIdx.x, n = 1 << m;
+    for (int e = threadIdx.x; e < n; e += NT_T) sm[e] = src(v, e);
+    __syncthreads();
+    smem_wht<NT_T>(sm, m, 1, n);
+    for (int e = threadIdx.x; e < n; e += NT_T) snk.put(v, e, sm[e]);
+}
+
+// ============================================================================ forward, two pass
+template <class Src>
+__global__ void __launch_bounds__(NT_T) k_fwd_col_lat(Src src, double2* __restrict__ Y, int l1, int l2, int lc,
+                                                      long long vstride, const double2* __restrict__ tw) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double2* sm = reinterpret_cast<double2*>(smraw);
+    const int v = blockIdx.y, C = 1 << lc, N1 = 1 << l1;
+    const long long c0 = (long long)blockIdx.x << lc;
+    for (int e = threadIdx.x; e < (C << l1); e += NT_T) {
+        const int j1 = e >> lc, c = e & (C - 1);
+        const uint64_t j = (uint64_t(j1) << l2) + c0 + c;
+        sm[c * N1 + j1] = make_double2(src(v, 2 * j), src(v, 2 * j + 1));
+    }
+    __syncthreads();
+    smem_fft<NT_T>(sm, l1, C, N1, -1, tw);
+    double2* out = Y + v * vstride;
+    for (int e = threadIdx.x; e < (C << l1); e += NT_T) {
+        const int k1 = e >> lc, c = e & (C - 1);
+        const uint64_t j2 = c0 + c;
+        out[((long long)k1 << l2) + j2] = cmul(sm[c * N1 + k1], twiddle(tw, j2 * uint64_t(k1), l1 + l2));
+    }
+}
+
+template <class Src>
+__global__ void __launch_bounds__(NT_T) k_fwd_col_dig(Src src, double* __restrict__ Y, int l1, int l2, int lc,
+                                                      long long vstride) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double* sm = reinterpret_cast<double*>(smraw);
+    const int v = blockIdx.y, C = 1 << lc, N1 = 1 << l1;
+    const long long c0 = (long long)blockIdx.x << lc;
+    for (int e = threadIdx.x; e < (C << l1); e += NT_T) {
+        const int j1 = e >> lc, c = e & (C - 1);
+        sm[c * N1 + j1] = src(v, (uint64_t(j1) << l2) + c0 + c);
+    }
+    __syncthreads();
+    smem_wht<NT_T>(sm, l1, C, N1);
+    double* out = Y + v * vstride;
+    for (int e = threadIdx.x; e < (C << l1); e += NT_T) {
+        const int k1 = e >> lc, c = e & (C - 1);
+        out[((long long)k1 << l2) + c0 + c] = sm[c * N1 + k1];
+    }
+}
+
+__device__ __forceinline__ int row_of_cluster(int q, int rank, int N1) {
+    if (q == 0) return rank == 0 ? 0 : N1 / 2;
+    return rank == 0 ? q : N1 - q;
+}
+
+template <class Snk>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT_T)
+    k_fwd_row_lat(const double2* __restrict__ Y, Snk snk, int l1, int l2, long long vstride, int m,
+                  const double2* __restrict__ tw) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double2* sm = reinterpret_cast<double2*>(smraw);
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = int(cl.block_rank());
+    const int q = blockIdx.x >> 1, v = blockIdx.y;
+    const int N1 = 1 << l1, N2 = 1 << l2;
+    const int row = row_of_cluster(q, rank, N1);
+    const double2* in = Y + v * vstride + ((long long)row << l2);
+    for (int e = threadIdx.x; e < N2; e += NT_T) sm[e] = in[e];
+    __syncthreads();
+    smem_fft<NT_T>(sm, l2, 1, N2, -1, tw);
+    cl.sync();
+    const bool self = (row == 0) || (row == N1 / 2);
+    const double2* psm = self ? sm : cl.map_shared_rank(sm, rank ^ 1);
+    for (int k2 = threadIdx.x; k2 < N2; k2 += NT_T) {
+        const long long k = row + ((long long)k2 << l1);
+        if (k == 0) {
+            const double2 Z0 = sm[0];
+            snk.put(v, 0, make_double2(Z0.x + Z0.y, Z0.x - Z0.y));
+            continue;
+        }
+        const int kc = (row == 0) ? ((N2 - k2) & (N2 - 1)) : (N2 - 1 - k2);
+        snk.put(v, ((long long)row << l2) + k2, r2c_post(sm[k2], psm[kc], twiddle(tw, uint64_t(k), m)));
+    }
+    cl.sync();
+}
+
+template <class Snk>
+__global__ void __launch_bounds__(NT_T) k_fwd_row_dig(const double* __restrict__ Y, Snk snk, int l2,
+                                                      long long vstride) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double* sm = reinterpret_cast<double*>(smraw);
+    const int row = blockIdx.x, v = blockIdx.y, N2 = 1 << l2;
+    const double* in = Y + v * vstride + ((long long)row << l2);
+    for (int e = threadIdx.x; e < N2; e += NT_T) sm[e] = in[e];
+    __syncthreads();
+    smem_wht<NT_T>(sm, l2, 1, N2);
+    for (int e = threadIdx.x; e < N2; e += NT_T) snk.put(v, ((long long)row << l2) + e, sm[e]);
+}
+
+// ============================================================================ inverse sinks (device side)
+struct GradAcc {
+    double a[MAXD + 1];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int i = 0; i <= MAXD; ++i) a[i] = 0.0;
+    }
+};
+
+__device__ __forceinline__ void grad_add(const GradSink& gs, int v, uint64_t idx, double W, GradAcc& acc) {
+    int p, c;
+    gs.gen.coords(v, p, c);
+    double kappa[MAXD], dq[MAXD];
+    gs.gen.kappa_all(p, idx, kappa);
+    const int d = gs.gen.sp.d;
+    const double q = product_kernel<true>(kappa, gs.gen.eta + size_t(c) * d, d, __ldg(gs.gen.gamma + c), dq);
+#pragma unroll
+    for (int j = 0; j < MAXD; ++j)
+        if (j < d) acc.a[j] = fma(W, dq[j], acc.a[j]);
+    acc.a[MAXD] = fma(W, q, acc.a[MAXD]);
+}
+
+__device__ void grad_flush(const GradSink& gs, int v, int blk, GradAcc& acc) {
+    __shared__ double red[32];
+    const int d = gs.gen.sp.d;
+    double* out = gs.partial + ((size_t)v * gs.nblk + blk) * (MAXD + 1);
+#pragma unroll
+    for (int j = 0; j <= MAXD; ++j) {
+        if (j < d || j == MAXD) {
+            const double s = block_sum<NT_T>(acc.a[j], red);
+            if (threadIdx.x == 0) out[j] = s;
+        }
+    }
+}
+
+struct SinkGrad {  // adapts GradSink to the inverse kernels
+    GradSink gs;
+    int lattice, m;
+    __device__ __forceinline__ void lat(int v, uint64_t j, double2 z, GradAcc& acc) const {
+        if (m == 0) {
+            grad_add(gs, v, 0, z.x, acc);
+            return;
+        }
+        grad_add(gs, v, 2 * j, 2.0 * z.x, acc);
+        grad_add(gs, v, 2 * j + 1, 2.0 * z.y, acc);
+    }
+    __device__ __forceinline__ void dig(int v, uint64_t j, double w, GradAcc& acc) const { grad_add(gs, v, j, w, acc); }
+    __device__ __forceinline__ void flush(int v, int blk, GradAcc& acc) const { grad_flush(gs, v, blk, acc); }
+};
+
+struct SinkCoef {
+    CoefSink cs;
+    int lattice, m;
+    __device__ __forceinline__ void lat(int v, uint64_t j, double2 z, GradAcc&) const {
+        double* o = cs.out + cs.voff[v];
+        if (m == 0) {
+            o[0] = z.x * cs.scale;
+            return;
+        }
+        o[bitrev64(2 * j, m)] = 2.0 * cs.scale * z.x;
+        o[bitrev64(2 * j + 1, m)] = 2.0 * cs.scale * z.y;
+    }
+    __device__ __forceinline__ void dig(int v, uint64_t j, double w, GradAcc&) const {
+        cs.out[cs.voff[v] + j] = w * cs.scale;
+    }
+    __device__ __forceinline__ void flush(int, int, GradAcc&) const {}
+};
+
+// ============================================================================ inverse, single CTA
+template <class Snk>
+__global__ void __launch_bounds__(NT_T) k_inv_small_lat(const double2* __restrict__ in, const long long* in_off,
+                                                        long long cstride, int nvpc, Snk snk, int m,
+                                                        const double2* __restrict__ tw) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double2* sm = reinterpret_cast<double2*>(smraw);
+    const int v = blockIdx.x;
+    const int c = v / nvpc;
+    const double2* x = in + c * cstride + in_off[v - c * nvpc];
+    GradAcc acc;
+    acc.zero();
+    if (m == 0) {
+        if (threadIdx.x == 0) snk.lat(v, 0, x[0], acc);
+        snk.flush(v, 0, acc);
+        return;
+    }
+    const int lp = m - 1, Np = 1 << lp;
+    for (int k = threadIdx.x; k <= Np / 2; k += NT_T) {
+        if (k == 0) {
+            const double2 A = x[0];
+            sm[0] = make_double2(0.5 * (A.x + A.y), 0.5 * (A.x - A.y));
+            continue;
+        }
+        const int kp = Np - k;
+        const double2 Ak = x[k], Ap = x[kp];
+        sm[k] = c2r_pre(Ak, Ap, twiddle(tw, k, m));
+        if (kp != k) sm[kp] = c2r_pre(Ap, Ak, twiddle(tw, kp, m));
+    }
+    __syncthreads();
+    smem_fft<NT_T>(sm, lp, 1, Np, +1, tw);
+    for (int j = threadIdx.x; j < Np; j += NT_T) snk.lat(v, j, sm[j], acc);
+    snk.flush(v, 0, acc);
+}
+
+template <class Snk>
+__global__ void __launch_bounds__(NT_T) k_inv_small_dig(const double* __restrict__ in, const long long* in_off,
+                                                        long long cstride, int nvpc, Snk snk, int m) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double* sm = reinterpret_cast<double*>(smraw);
+    const int v = blockIdx.x, n = 1 << m;
+    const int c = v / nvpc;
+    const double* x = in + c * cstride + in_off[v - c * nvpc];
+    for (int e = threadIdx.x; e < n; e += NT_T) sm[e] = x[e];
+    __syncthreads();
+    smem_wht<NT_T>(sm, m, 1, n);
+    GradAcc acc;
+    acc.zero();
+    for (int e = threadIdx.x; e < n; e += NT_T) snk.dig(v, e, sm[e], acc);
+    snk.flush(v, 0, acc);
+}
+
+// ============================================================================ inverse, two pass
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT_T)
+    k_inv_row_lat(const double2* __restrict__ in, const long long* in_off, long long cstride, int nvpc,
+                  double2* __restrict__ U, long long vstride, int l1, int l2, int m, const double2* __restrict__ tw) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double2* sm = reinterpret_cast<double2*>(smraw);
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = int(cl.block_rank());
+    const int q = blockIdx.x >> 1, v = blockIdx.y;
+    const int N1 = 1 << l1, N2 = 1 << l2;
+    const int row = row_of_cluster(q, rank, N1);
+    const int c = v / nvpc;
+    const double2* x = in + c * cstride + in_off[v - c * nvpc] + ((long long)row << l2);
+    for (int e = threadIdx.x; e < N2; e += NT_T) sm[e] = x[e];
+    cl.sync();
+    const bool self = (row == 0) || (row == N1 / 2);
+    const double2* psm = self ? sm : cl.map_shared_rank(sm, rank ^ 1);
+    double2 zr[EPT];
+#pragma unroll
+    for (int t = 0; t < EPT; ++t) {
+        const int k2 = threadIdx.x + t * NT_T;
+        if (k2 < N2) {
+            const long long k = row + ((long long)k2 << l1);
+            if (k == 0) {
+                const double2 A = sm[0];
+                zr[t] = make_double2(0.5 * (A.x + A.y), 0.5 * (A.x - A.y));
+            } else {
+                const int kc = (row == 0) ? ((N2 - k2) & (N2 - 1)) : (N2 - 1 - k2);
+                zr[t] = c2r_pre(sm[k2], psm[kc], twiddle(tw, uint64_t(k), m));
+            }
+        }
+    }
+    cl.sync();
+#pragma unroll
+    for (int t = 0; t < EPT; ++t) {
+        const int k2 = threadIdx.x + t * NT_T;
+        if (k2 < N2) sm[k2] = zr[t];
+    }
+    __syncthreads();
+    smem_fft<NT_T>(sm, l2, 1, N2, +1, tw);
+    double2* out = U + v * vstride + ((long long)row << l2);
+    for (int j2 = threadIdx.x; j2 < N2; j2 += NT_T)
+        out[j2] = cmulc(sm[j2], twiddle(tw, uint64_t(j2) * uint64_t(row), l1 + l2));
+}
+
+__global__ void __launch_bounds__(NT_T) k_inv_row_dig(const double* __restrict__ in, const long long* in_off,
+                                                      long long cstride, int nvpc, double* __restrict__ U,
+                                                      long long vstride, int l2) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double* sm = reinterpret_cast<double*>(smraw);
+    const int row = blockIdx.x, v = blockIdx.y, N2 = 1 << l2;
+    const int c = v / nvpc;
+    const double* x = in + c * cstride + in_off[v - c * nvpc] + ((long long)row << l2);
+    for (int e = threadIdx.x; e < N2; e += NT_T) sm[e] = x[e];
+    __syncthreads();
+    smem_wht<NT_T>(sm, l2, 1, N2);
+    double* out = U + v * vstride + ((long long)row << l2);
+    for (int e = threadIdx.x; e < N2; e += NT_T) out[e] = sm[e];
+}
+
+template <class Snk>
+__global__ void __launch_bounds__(NT_T) k_inv_col_lat(const double2* __restrict__ U, long long vstride, Snk snk,
+                                                      int l1, int l2, int lc, const double2* __restrict__ tw) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double2* sm = reinterpret_cast<double2*>(smraw);
+    const int v = blockIdx.y, C = 1 << lc, N1 = 1 << l1;
+    const long long c0 = (long long)blockIdx.x << lc;
+    const double2* x = U + v * vstride;
+    for (int e = threadIdx.x; e < (C << l1); e += NT_T) {
+        const int k1 = e >> lc, c = e & (C - 1);
+        sm[c * N1 + k1] = x[((long long)k1 << l2) + c0 + c];
+    }
+    __syncthreads();
+    smem_fft<NT_T>(sm, l1, C, N1, +1, tw);
+    GradAcc acc;
+    acc.zero();
+    for (int e = threadIdx.x; e < (C << l1); e += NT_T) {
+        const int j1 = e >> lc, c = e & (C - 1);
+        const uint64_t j = (uint64_t(j1) << l2) + c0 + c;
+        snk.lat(v, j, sm[c * N1 + j1], acc);
+    }
+    snk.flush(v, blockIdx.x, acc);
+}
+
+template <class Snk>
+__global__ void __launch_bounds__(NT_T) k_inv_col_dig(const double* __restrict__ U, long long vstride, Snk snk,
+                                                      int l1, int l2, int lc) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double* sm = reinterpret_cast<double*>(smraw);
+    const int v = blockIdx.y, C = 1 << lc, N1 = 1 << l1;
+    const long long c0 = (long long)blockIdx.x << lc;
+    const double* x = U + v * vstride;
+    for (int e = threadIdx.x; e < (C << l1); e += NT_T) {
+        const int k1 = e >> lc, c = e & (C - 1);
+        sm[c * N1 + k1] = x[((long long)k1 << l2) + c0 + c];
+    }
+    __syncthreads();
+    smem_wht<NT_T>(sm, l1, C, N1);
+    GradAcc acc;
+    acc.zero();
+    for (int e = threadIdx.x; e < (C << l1); e += NT_T) {
+        const int j1 = e >> lc, c = e & (C - 1);
+        snk.dig(v, (uint64_t(j1) << l2) + c0 + c, sm[c * N1 + j1], acc);
+    }
+    snk.flush(v, blockIdx.x, acc);
+}
+
+// ============================================================================ launchers
+static size_t smem_bytes(int lattice) { return size_t(CAP) * (lattice ? sizeof(double2) : sizeof(double)); }
+
+template <class K>
+static void set_smem(K kern, size_t bytes) {
+    static_assert(sizeof(K) > 0, "");
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+}
+
+template <class Src, class Snk>
+static void fwd_impl(int lattice, const Geo& g, int nvec, const Src& src, const Snk& snk, void* work,
+                     const double2* tw, cudaStream_t s) {
+    const size_t sm = smem_bytes(lattice);
+    if (!g.two) {
+        if (lattice) {
+            auto k = k_fwd_small_lat<Src, Snk>;
+            set_smem(k, sm);
+            k<<<nvec, NT_T, sm, s>>>(src, snk, g.m, tw);
+        } else {
+            auto k = k_fwd_small_dig<Src, Snk>;
+            set_smem(k, sm);
+            k<<<nvec, NT_T, sm, s>>>(src, snk, g.m);
+        }
+        return;
+    }
+    const long long vstride = 1ll << g.lt;
+    const int lc = CAP_LOG - g.l1;
+    const int ncol_blk = (1 << g.l2) >> lc;
+    if (lattice) {
+        auto kc = k_fwd_col_lat<Src>;
+        set_smem(kc, sm);
+        kc<<<dim3(ncol_blk, nvec), NT_T, sm, s>>>(src, static_cast<double2*>(work), g.l1, g.l2, lc, vstride, tw);
+        auto kr = k_fwd_row_lat<Snk>;
+        set_smem(kr, sm);
+        kr<<<dim3(1 << g.l1, nvec), NT_T, sm, s>>>(static_cast<const double2*>(work), snk, g.l1, g.l2, vstride,
+                                                   g.m, tw);
+    } else {
+        auto kc = k_fwd_col_dig<Src>;
+        set_smem(kc, sm);
+        kc<<<dim3(ncol_blk, nvec), NT_T, sm, s>>>(src, static_cast<double*>(work), g.l1, g.l2, lc, vstride);
+        auto kr = k_fwd_row_dig<Snk>;
+        set_smem(kr, sm);
+        kr<<<dim3(1 << g.l1, nvec), NT_T, sm, s>>>(static_cast<const double*>(work), snk, g.l2, vstride);
+    }
+}
+
+void fwd_gen(int lattice, const Geo& g, int nvec, const GenSrc& src, const SpecSink& snk, void* work,
+             const double2* tw, cudaStream_t s) {
+    fwd_impl(lattice, g, nvec, src, snk, work, tw, s);
+}
+void fwd_array(int lattice, const Geo& g, int nvec, const ArraySrc& src, const ScaleSink& snk, void* work,
+               const double2* tw, cudaStream_t s) {
+    fwd_impl(lattice, g, nvec, src, snk, work, tw, s);
+}
+
+int grad_blocks(int lattice, const Geo& g) {
+    (void)lattice;
+    if (!g.two) return 1;
+    const int lc = CAP_LOG - g.l1;
+    return (1 << g.l2) >> lc;
+}
+
+template <class Snk>
+static void inv_impl(int lattice, const Geo& g, int nvec, const void* in, const long long* in_off, long long cstride,
+                     int nvpc, const Snk& snk, void* work, const double2* tw, cudaStream_t s) {
+    const size_t sm = smem_bytes(lattice);
+    if (!g.two) {
+        if (lattice) {
+            auto k = k_inv_small_lat<Snk>;
+            set_smem(k, sm);
+            k<<<nvec, NT_T, sm, s>>>(static_cast<const double2*>(in), in_off, cstride, nvpc, snk, g.m, tw);
+        } else {
+            auto k = k_inv_small_dig<Snk>;
+            set_smem(k, sm);
+            k<<<nvec, NT_T, sm, s>>>(static_cast<const double*>(in), in_off, cstride, nvpc, snk, g.m);
+        }
+        return;
+    }
+    const long long vstride = 1ll << g.lt;
+    const int lc = CAP_LOG - g.l1;
+    const int ncol_blk = (1 << g.l2) >> lc;
+    if (lattice) {
+        set_smem(k_inv_row_lat, sm);
+        k_inv_row_lat<<<dim3(1 << g.l1, nvec), NT_T, sm, s>>>(static_cast<const double2*>(in), in_off, cstride, nvpc,
+                                                              static_cast<double2*>(work), vstride, g.l1, g.l2, g.m,
+                                                              tw);
+        auto kc = k_inv_col_lat<Snk>;
+        set_smem(kc, sm);
+        kc<<<dim3(ncol_blk, nvec), NT_T, sm, s>>>(static_cast<const double2*>(work), vstride, snk, g.l1, g.l2, lc, tw);
+    } else {
+        set_smem(k_inv_row_dig, sm);
+        k_inv_row_dig<<<dim3(1 << g.l1, nvec), NT_T, sm, s>>>(static_cast<const double*>(in), in_off, cstride, nvpc,
+                                                              static_cast<double*>(work), vstride, g.l2);
+        auto kc = k_inv_col_dig<Snk>;
+        set_smem(kc, sm);
+        kc<<<dim3(ncol_blk, nvec), NT_T, sm, s>>>(static_cast<const double*>(work), vstride, snk, g.l1, g.l2, lc);
+    }
+}
+
+void inv_grad(int lattice, const Geo& g, int nvec, const void* in, const long long* in_off, long long cstride,
+              int nvpc, const GradSink& gs, void* work, const double2* tw, cudaStream_t s) {
+    SinkGrad snk{gs, lattice, g.m};
+    inv_impl(lattice, g, nvec, in, in_off, cstride, nvpc, snk, work, tw, s);
+}
+
+void inv_coef(int lattice, const Geo& g, int nvec, const void* in, const long long* in_off, const CoefSink& cs,
+              void* work, const double2* tw, cudaStream_t s) {
+    SinkCoef snk{cs, lattice, g.m};
+    inv_impl(lattice, g, nvec, in, in_off, 0, nvec, snk, work, tw, s);
+}
+
+// ============================================================================ per-frequency T x T solve
+// Hermitian LDL^H of A (upper pairs, row by row), T <= 8.  Pivots are the diagonal Schur
+// complements of Algorithm 1 (fast_gram.cpp:167-178): logdet = sum log d_s.
+// Returns 0 ok, 1 non-positive pivot (SchurBreakdown), 2 non-real diagonal (FastMtgpError).
+template <int T, bool CX>
+__device__ __forceinline__ int ldl_solve(const typename Sc<CX>::T* A, const typename Sc<CX>::T* r, bool want_inv,
+                                         double& logdet, double& quad, typename Sc<CX>::T* chat,
+                                         typename Sc<CX>::T* Ainv) {
+    using S = Sc<CX>;
+    using V = typename S::T;
+    V L[T][T];
+    double dinv[T];
+    int status = 0;
+    // pair index of (a,b), a <= b, row by row (fast_gram.cpp:35-40)
+    auto pidx = [](int a, int b) { return a * T - a * (a - 1) / 2 + (b - a); };
+    logdet = 0.0;
+#pragma unroll
+    for (int s = 0; s < T; ++s) {
+        double dd = S::re(A[pidx(s, s)]);
+        if (fabs(S::im(A[pidx(s, s)])) > 1e-8 * fmax(1.0, fabs(dd))) status = status ? status : 2;
+#pragma unroll
+        for (int k = 0; k < s; ++k) dd -= S::abs2(L[s][k]) / dinv[k];
+        if (!(dd > 0.0)) {
+            status = 1;
+            dd = 1.0;
+        }
+        dinv[s] = 1.0 / dd;
+        logdet += log(dd);
+#pragma unroll
+        for (int i = s + 1; i < T; ++i) {
+            V acc = S::conj(A[pidx(s, i)]);
+#pragma unroll
+            for (int k = 0; k < s; ++k) acc = S::sub(acc, S::scale(S::mulc(L[i][k], L[s][k]), 1.0 / dinv[k]));
+            L[i][s] = S::scale(acc, dinv[s]);
+        }
+    }
+    // z = L^-1 r, quad = sum |z|^2 / d
+    V z[T];
+    quad = 0.0;
+#pragma unroll
+    for (int i = 0; i < T; ++i) {
+        V acc = r[i];
+#pragma unroll
+        for (int k = 0; k < i; ++k) acc = S::sub(acc, S::mul(L[i][k], z[k]));
+        z[i] = acc;
+        quad += S::abs2(acc) * dinv[i];
+    }
+    // chat = L^-H D^-1 z
+#pragma unroll
+    for (int i = T - 1; i >= 0; --i) {
+        V acc = S::scale(z[i], dinv[i]);
+#pragma unroll
+        for (int k = i + 1; k < T; ++k) acc = S::sub(acc, S::mul(S::conj(L[k][i]), chat[k]));
+        chat[i] = acc;
+    }
+    if (want_inv) {
+        // X = L^-1 (unit lower); Ainv_ab = sum_{s >= max(a,b)} conj(X_sa) X_sb / d_s
+        V X[T][T];
+#pragma unroll
+        for (int j = 0; j < T; ++j)
+#pragma unroll
+            for (int i = j + 1; i < T; ++i) {
+                V acc = S::sub(S::zero(), L[i][j]);
+#pragma unroll
+                for (int k = j + 1; k < i; ++k) acc = S::sub(acc, S::mul(L[i][k], X[k][j]));
+                X[i][j] = acc;
+            }
+#pragma unroll
+        for (int a = 0; a < T; ++a)
+#pragma unroll
+            for (int b = a; b < T; ++b) {
+                V acc = S::zero();
+#pragma unroll
+                for (int s = b; s < T; ++s) {
+                    // conj(X_sa) X_sb with X_ss = 1
+                    V term;
+                    if (s == a) term = S::one();  // then b == a == s
+                    else if (s == b) term = S::conj(X[s][a]);
+                    else term = S::mulc(X[s][b], X[s][a]);
+                    acc = S::add(acc, S::scale(term, dinv[s]));
+                }
+                Ainv[pidx(a, b)] = acc;
+            }
+    }
+    return status;
+}
+
+template <int T, bool CX>
+__global__ void __launch_bounds__(256) k_solve_equal(SolveArgs a) {
+    using S = Sc<CX>;
+    using V = typename S::T;
+    constexpr int P = T * (T + 1) / 2;
+    const int c = blockIdx.y;
+    const V* lam = static_cast<const V*>(a.lam) + c * a.cstride;
+    const V* yh = static_cast<const V*>(a.yhat);
+    double ld_acc = 0.0, q_acc = 0.0;
+    int first_bad = INT_MAX, nonreal = 0;
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < a.nslots;
+         p += (long long)gridDim.x * blockDim.x) {
+        V A[P], r[T], ch[T], Ai[P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) A[q] = lam[q * a.nslots + p];
+#pragma unroll
+        for (int t = 0; t < T; ++t) r[t] = yh[t * a.nslots + p];
+        if constexpr (CX) {
+            if (p == 0) {
+                // packed slot 0: frequency 0 (.x) and Nyquist (.y), two real systems, weight 1 each;
+                // tau = yhat(0)/sqrt(n) zeroes the frequency-0 residual (gp_core.cpp:67-88)
+                double A0[P], AN[P], r0[T], rN[T], c0[T], cN[T], I0[P], IN[P], l0, lN, q0, qN;
+#pragma unroll
+                for (int q = 0; q < P; ++q) A0[q] = A[q].x, AN[q] = A[q].y;
+#pragma unroll
+                for (int t = 0; t < T; ++t) r0[t] = 0.0, rN[t] = r[t].y;
+                const bool want = a.M || a.lam_inv;
+                int st0 = ldl_solve<T, false>(A0, r0, want, l0, q0, c0, I0);
+                int stN = 0;
+                if (a.has_nyq) {
+                    stN = ldl_solve<T, false>(AN, rN, want, lN, qN, cN, IN);
+                } else {  // n == 1: no Nyquist frequency
+                    lN = qN = 0.0;
+#pragma unroll
+                    for (int t = 0; t < T; ++t) cN[t] = 0.0;
+#pragma unroll
+                    for (int q = 0; q < P; ++q) IN[q] = 0.0;
+                }
+                if (st0 == 1 || stN == 1) first_bad = 0;
+                ld_acc += l0 + lN;
+                q_acc += q0 + qN;
+                if (a.M) {
+                    V* Mo = static_cast<V*>(a.M) + c * a.cstride;
+                    int q = 0;
+#pragma unroll
+                    for (int x = 0; x < T; ++x)
+#pragma unroll
+                        for (int y = x; y < T; ++y, ++q)
+                            Mo[q * a.nslots] = make_double2(I0[q] - c0[x] * c0[y], IN[q] - cN[x] * cN[y]);
+                }
+                if (a.lam_inv) {
+                    V* Io = static_cast<V*>(a.lam_inv) + c * a.cstride;
+#pragma unroll
+                    for (int q = 0; q < P; ++q) Io[q * a.nslots] = make_double2(I0[q], IN[q]);
+                }
+                if (a.chat) {
+                    V* Co = static_cast<V*>(a.chat) + c * (long long)T * a.nslots;
+#pragma unroll
+                    for (int t = 0; t < T; ++t) Co[t * a.nslots] = make_double2(c0[t], cN[t]);
+                }
+                continue;
+            }
+        } else {
+            if (p == 0) {
+#pragma unroll
+                for (int t = 0; t < T; ++t) r[t] = 0.0;
+            }
+        }
+        double ld, qd;
+        const int st = ldl_solve<T, CX>(A, r, a.M || a.lam_inv, ld, qd, ch, Ai);
+        if (st == 1 && p < first_bad) first_bad = int(p);
+        if (st == 2) nonreal = 1;
+        const double w = CX ? 2.0 : 1.0;  // lattice slot k >= 1 stands for k and n - k
+        ld_acc += w * ld;
+        q_acc += w * qd;
+        if (a.M) {
+            V* Mo = static_cast<V*>(a.M) + c * a.cstride;
+            int q = 0;
+#pragma unroll
+            for (int x = 0; x < T; ++x)
+#pragma unroll
+                for (int y = x; y < T; ++y, ++q) Mo[q * a.nslots + p] = S::sub(Ai[q], S::mulc(ch[x], ch[y]));
+        }
+        if (a.lam_inv) {
+            V* Io = static_cast<V*>(a.lam_inv) + c * a.cstride;
+#pragma unroll
+            for (int q = 0; q < P; ++q) Io[q * a.nslots + p] = Ai[q];
+        }
+        if (a.chat) {
+            V* Co = static_cast<V*>(a.chat) + c * (long long)T * a.nslots;
+#pragma unroll
+            for (int t = 0; t < T; ++t) Co[t * a.nslots + p] = ch[t];
+        }
+    }
+    __shared__ double red[32];
+    const double ls = block_sum<256>(ld_acc, red);
+    const double qs = block_sum<256>(q_acc, red);
+    if (threadIdx.x == 0) {
+        a.partial[((size_t)c * a.nblk + blockIdx.x) * 2 + 0] = ls;
+        a.partial[((size_t)c * a.nblk + blockIdx.x) * 2 + 1] = qs;
+    }
+    if (first_bad != INT_MAX) atomicMin(a.bad + c, first_bad);
+    if (nonreal) atomicOr(a.bad + gridDim.y + c, 1);
+}
+
+template <int T>
+static void solve_t(const SolveArgs& a, int ncand, cudaStream_t s) {
+    dim3 grid(a.nblk, ncand);
+    if (a.lattice) k_solve_equal<T, true><<<grid, 256, 0, s>>>(a);
+    else k_solve_equal<T, false><<<grid, 256, 0, s>>>(a);
+}
+
+void solve_equal(const SolveArgs& a, int ncand, cudaStream_t s) {
+    switch (a.T) {
+        case 1: solve_t<1>(a, ncand, s); break;
+        case 2: solve_t<2>(a, ncand, s); break;
+        case 3: solve_t<3>(a, ncand, s); break;
+        case 4: solve_t<4>(a, ncand, s); break;
+        case 5: solve_t<5>(a, ncand, s); break;
+        case 6: solve_t<6>(a, ncand, s); break;
+        case 7: solve_t<7>(a, ncand, s); break;
+        case 8: solve_t<8>(a, ncand, s); break;
+    }
+}
+
+// ============================================================================ finalize
+__global__ void k_finalize(FinalArgs a) {
+    const int c = blockIdx.x;
+    double* out = a.out + (size_t)c * NOUT;
+    __shared__ double S[MAXP][MAXD + 1];
+    const int d = a.d, P = a.P;
+    if (threadIdx.x == 0) {
+        double ld = 0.0, q = 0.0;
+        for (int b = 0; b < a.nblk_solve; ++b) {
+            ld += a.solve_partial[((size_t)c * a.nblk_solve + b) * 2 + 0];
+            q += a.solve_partial[((size_t)c * a.nblk_solve + b) * 2 + 1];
+        }
+        out[OUT_LOGDET] = ld;
+        out[OUT_QUAD] = q;
+        out[OUT_NLL] = q + ld;  // rT c + logdet (gp_core.cpp:207-211)
+    }
+    if (!a.grad_partial) return;
+    for (int t = threadIdx.x; t < P * (MAXD + 1); t += blockDim.x) {
+        const int p = t / (MAXD + 1), i = t % (MAXD + 1);
+        double acc = 0.0;
+        if (i < d || i == MAXD)
+            for (int b = 0; b < a.nblk_grad; ++b)
+                acc += a.grad_partial[(((size_t)c * P + p) * a.nblk_grad + b) * (MAXD + 1) + i];
+        S[p][i] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double dgam = 0.0;
+        double deta[MAXD];
+        for (int j = 0; j < MAXD; ++j) deta[j] = 0.0;
+        for (int x = 0; x < MAXT * MAXT; ++x) out[OUT_DR + x] = 0.0;
+        for (int p = 0; p < P; ++p) {
+            const int pa = a.pair_a[p], pb = a.pair_b[p];
+            const double w = pa == pb ? 1.0 : 2.0;
+            const double Rp = a.Rpair[(size_t)c * P + p];
+            const double dRp = w * S[p][MAXD];  // dNLL / dR_ab, symmetric pair counted once
+            for (int j = 0; j < d; ++j) deta[j] += w * Rp * S[p][j];
+            dgam += w * Rp * S[p][MAXD];
+            if (pa == pb) out[OUT_DR + pa * MAXT + pb] = dRp;
+            else {
+                out[OUT_DR + pa * MAXT + pb] = 0.5 * dRp;
+                out[OUT_DR + pb * MAXT + pa] = 0.5 * dRp;
+            }
+        }
+        out[OUT_DGAMMA] = dgam / a.gamma[c];
+        for (int j = 0; j < MAXD; ++j) out[OUT_DETA + j] = deta[j];
+    }
+}
+
+void finalize(const FinalArgs& a, cudaStream_t s) { k_finalize<<<a.ncand, 128, 0, s>>>(a); }
+
+// ============================================================================ per-slot Hermitian apply
+template <int T, bool CX>
+__global__ void k_apply_herm(long long nslots, const void* opv, const void* inv, void* outv) {
+    using S = Sc<CX>;
+    using V = typename S::T;
+    const V* op = static_cast<const V*>(opv);
+    const V* in = static_cast<const V*>(inv);
+    V* out = static_cast<V*>(outv);
+    auto pidx = [](int a, int b) { return a * T - a * (a - 1) / 2 + (b - a); };
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < nslots;
+         p += (long long)gridDim.x * blockDim.x) {
+        V x[T];
+#pragma unroll
+        for (int t = 0; t < T; ++t) x[t] = in[t * nslots + p];
+#pragma unroll
+        for (int a = 0; a < T; ++a) {
+            V acc = S::zero();
+#pragma unroll
+            for (int b = 0; b < T; ++b) {
+                const V o = op[pidx(a < b ? a : b, a < b ? b : a) * nslots + p];
+                V e;
+                if constexpr (CX) {
+                    if (p == 0) e = make_double2(o.x * x[b].x, o.y * x[b].y);  // packed real pair
+                    else e = (a <= b) ? S::mul(o, x[b]) : S::mul(S::conj(o), x[b]);
+                    acc = make_double2(acc.x + e.x, acc.y + e.y);
+                } else {
+                    acc += o * x[b];
+                }
+            }
+            out[a * nslots + p] = acc;
+        }
+    }
+}
+
+void apply_hermitian(int lattice, int T, long long nslots, const void* op, const void* in, void* out,
+                     cudaStream_t s) {
+    const int blocks = int((nslots + 255) / 256 < 1184 ? (nslots + 255) / 256 : 1184);
+#define FM_AH(TT)                                                                   \
+    case TT:                                                                        \
+        if (lattice) k_apply_herm<TT, true><<<blocks, 256, 0, s>>>(nslots, op, in, out); \
+        else k_apply_herm<TT, false><<<blocks, 256, 0, s>>>(nslots, op, in, out);        \
+        break;
+    switch (T) {
+        FM_AH(1) FM_AH(2) FM_AH(3) FM_AH(4) FM_AH(5) FM_AH(6) FM_AH(7) FM_AH(8)
+    }
+#undef FM_AH
+}
+
+}  // namespace fmtgp

@@ -1,0 +1,1120 @@
+// Host orchestration + C ABI (include/fastmtgp_b200.h).
+//
+// The C++ here replaces the reference's fast_gram.cpp / gp_core.cpp control flow for the
+// hot path: it owns device memory, plans transforms, launches the kernels of kernels.cu on
+// one stream, and maps failures onto the reference's exception semantics
+// (SchurBreakdown -> FMTGP_ERR_SCHUR, FastMtgpError -> FMTGP_ERR_INVALID / NONREAL).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/fastmtgp_b200.h"
+#include "kernels.cuh"
+#include "posterior.cuh"
+#include "unequal.cuh"
+
+using namespace fmtgp;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Fail {
+    int code;
+    std::string msg;
+};
+
+#define CK(x)                                                                                          \
+    do {                                                                                               \
+        cudaError_t e_ = (x);                                                                          \
+        if (e_ != cudaSuccess)                                                                         \
+            throw Fail{e_ == cudaErrorMemoryAllocation ? FMTGP_ERR_OOM : FMTGP_ERR_CUDA,              \
+                       std::string(#x) + ": " + cudaGetErrorString(e_)};                               \
+    } while (0)
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return FMTGP_OK;
+    } catch (const Fail& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return FMTGP_ERR_INVALID;
+    }
+}
+
+constexpr int BAD_NONE = 0x7f7f7f7f;  // cudaMemset(0x7f) sentinel: no failing slot
+
+[[noreturn]] void invalid(const std::string& m) { throw Fail{FMTGP_ERR_INVALID, m}; }
+
+template <class T>
+T* dalloc(size_t count) {
+    if (count == 0) count = 1;
+    void* p = nullptr;
+    CK(cudaMalloc(&p, count * sizeof(T)));
+    return static_cast<T*>(p);
+}
+
+// twiddle table per device (27 levels x 8192 entries)
+double2* twiddles_for(int dev) {
+    static std::mutex mu;
+    static std::vector<double2*> tabs;
+    std::lock_guard<std::mutex> lock(mu);
+    if (int(tabs.size()) <= dev) tabs.resize(dev + 1, nullptr);
+    if (!tabs[dev]) {
+        double2* t = dalloc<double2>(size_t(27) << TW_BASE_LOG);
+        init_twiddles(t, 0);
+        CK(cudaStreamSynchronize(0));
+        tabs[dev] = t;
+    }
+    return tabs[dev];
+}
+
+struct Group {            // pairs whose generating (row) task has the same length
+    int m;
+    Geo geo;
+    std::vector<int> pairs;  // global pair ids
+    int* d_vec_pair = nullptr;
+    long long* d_voff = nullptr;   // slot offset of each pair's vector
+    double* d_coef = nullptr;      // [max_cand][npairs]
+    double* d_xi = nullptr;
+    int coef_off = 0;              // offset into the host staging coef array
+};
+
+struct TaskGroup {  // tasks of the same length (yhat / solve / coefficient transforms)
+    int m;
+    Geo geo;
+    std::vector<int> tasks;
+    long long* d_yoff = nullptr;   // element offset into y of each task
+    long long* d_soff = nullptr;   // slot offset into yhat-like arrays of each task
+};
+
+}  // namespace
+
+struct fmtgp_model {
+    int dev = 0;
+    cudaStream_t st = nullptr;
+    int kind = 0, lattice = 1, d = 0, T = 0, P = 0, max_cand = 1;
+    int m[MAXT]{};
+    long long n[MAXT]{}, off[MAXT + 1]{}, N = 0;
+    bool equal = true;
+    std::vector<int> pa, pb;  // pair -> (a, b)
+    std::vector<long long> poff, pslots;  // pair slot offset / count
+    long long total_slots = 0;            // per candidate
+    std::vector<long long> toff_slots;    // task slot offsets (yhat layout)
+    long long task_slots = 0;
+    std::vector<Group> groups;
+    std::vector<TaskGroup> tgroups;
+    double2* tw = nullptr;
+    // design tables
+    uint64_t* d_g = nullptr;
+    uint64_t* d_cols = nullptr;
+    int m_cols = 0;
+    uint64_t* d_offs = nullptr;  // [P][MAXD]
+    uint64_t* d_shifts = nullptr;  // [T][d]
+    uint64_t n_max = 0;
+    int mgen = 0;
+    double* d_fit = nullptr;       // last fit: eta [d] | R [T*T]
+    double* d_c = nullptr;         // coefficients of the last fit [N]
+    bool have_c = false;
+    int *d_pa = nullptr, *d_pb = nullptr;
+    std::vector<uint64_t> shifts;  // host [T][d]
+    // data
+    double* d_y = nullptr;
+    void* d_yhat = nullptr;
+    bool have_y = false;
+    double tau[MAXT]{};
+    // per-candidate buffers
+    double *d_eta = nullptr, *d_gamma = nullptr, *d_Rpair = nullptr;
+    void *d_lam = nullptr, *d_M = nullptr, *d_work = nullptr, *d_laminv = nullptr, *d_chat = nullptr;
+    size_t work_elems = 0;
+    double* d_psolve = nullptr;
+    double* d_pgrad = nullptr;
+    int* d_bad = nullptr;
+    double* d_out = nullptr;
+    int nblk_solve = 0, nblk_grad = 0;
+    // scratch vectors for the seam calls
+    double *d_vecA = nullptr, *d_vecB = nullptr;
+    void *d_sA = nullptr, *d_sB = nullptr;
+    // pinned staging
+    double* h_stage = nullptr;
+    size_t stage_len = 0;
+    double* h_out = nullptr;
+    int* h_bad = nullptr;
+    // state of the last spectrum / fit (candidate 0)
+    bool have_spec = false, have_inv = false, have_fit = false;
+    double last_gamma = 1.0;
+    std::vector<double> last_eta, last_R;  // R internal [T*T]
+    int last_alpha = 1;
+    double last_b[4]{};
+    double last_logdet = 0.0;
+    unequal::Plan* uneq = nullptr;
+};
+
+namespace {
+
+int pair_index(int T, int a, int b) { return a * T - a * (a - 1) / 2 + (b - a); }
+
+Spatial spatial_of(const fmtgp_model* M, int si_alpha, const double* b) {
+    Spatial sp{};
+    sp.family = M->lattice ? 0 : 1;
+    sp.d = M->d;
+    sp.si_alpha = si_alpha;
+    for (int i = 0; i < 4; ++i) sp.b[i] = b[i];
+    return sp;
+}
+
+PointGen pointgen_of(const fmtgp_model* M, int m) {
+    PointGen pg{};
+    pg.family = M->lattice ? 0 : 1;
+    pg.m = m;
+    pg.g = M->d_g;
+    pg.cols = M->d_cols;
+    pg.m_cols = M->m_cols;
+    return pg;
+}
+
+void validate_hyper(const fmtgp_model* M, const fmtgp_hyper* h) {
+    if (!h) invalid("null hyperparameters");
+    if (!h->eta || !h->t || !h->xi) invalid("hyperparameters: null eta / t / xi");
+    if (h->s < 0 || (h->s > 0 && !h->B)) invalid("hyperparameters: bad task factor B");
+    for (int l = 0; l < M->T; ++l)
+        if (!(h->t[l] > 0.0)) invalid("task_gram: non-positive diagonal entry");
+    if (M->lattice && h->si_alpha != 1 && h->si_alpha != 2) invalid("si_bernoulli_1d: alpha must be 1 or 2");
+}
+
+// R = B B^T + diag(t) (kernels.cpp:124-135), internal order
+std::vector<double> task_gram(const fmtgp_model* M, const fmtgp_hyper* h) {
+    std::vector<double> R(size_t(M->T) * M->T, 0.0);
+    for (int a = 0; a < M->T; ++a)
+        for (int b = 0; b < M->T; ++b) {
+            double s = 0.0;
+            for (int k = 0; k < h->s; ++k) s += h->B[a * h->s + k] * h->B[b * h->s + k];
+            R[a * M->T + b] = s + (a == b ? h->t[a] : 0.0);
+        }
+    return R;
+}
+
+void ensure_stage(fmtgp_model* M, size_t len) {
+    if (M->stage_len >= len) return;
+    if (M->h_stage) cudaFreeHost(M->h_stage);
+    M->h_stage = nullptr;
+    CK(cudaMallocHost(reinterpret_cast<void**>(&M->h_stage), len * sizeof(double)));
+    M->stage_len = len;
+}
+
+// Upload per-candidate hyperparameter tables (eta, gamma, Rpair, per-group coef and xi).
+// xi_scale[c] is the escalation factor of candidate c.
+void upload_hyper(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, const double* xi_scale) {
+    const int d = M->d, P = M->P;
+    size_t len = size_t(nc) * (d + 1 + P);
+    for (auto& g : M->groups) len += 2 * size_t(nc) * g.pairs.size();
+    ensure_stage(M, len);
+    double* s = M->h_stage;
+    double* eta = s;
+    double* gam = eta + size_t(nc) * d;
+    double* Rp = gam + nc;
+    double* gc = Rp + size_t(nc) * P;
+    for (int c = 0; c < nc; ++c) {
+        const fmtgp_hyper* h = hs[c];
+        for (int j = 0; j < d; ++j) eta[c * d + j] = h->eta[j];
+        gam[c] = h->gamma;
+        const std::vector<double> R = task_gram(M, h);
+        for (int p = 0; p < P; ++p) Rp[c * P + p] = R[M->pa[p] * M->T + M->pb[p]];
+    }
+    double* cur = gc;
+    for (auto& g : M->groups) {
+        const int np = int(g.pairs.size());
+        double* co = cur;
+        double* xi = cur + size_t(nc) * np;
+        for (int c = 0; c < nc; ++c) {
+            const fmtgp_hyper* h = hs[c];
+            for (int q = 0; q < np; ++q) {
+                const int p = g.pairs[q], a = M->pa[p], b = M->pb[p];
+                // sqrt(n_b) * V̄_{m_a} = sqrt(n_b / n_a) * unnormalised transform (fast_gram.cpp:82-83)
+                const double scale = std::sqrt(double(M->n[b]) / double(M->n[a]));
+                co[c * np + q] = Rp[c * P + p] * scale;
+                double x = 0.0;
+                if (a == b) {
+                    x = h->xi[a] * xi_scale[c];
+                    if (xi_scale[c] > 1.0 && h->xi[a] == 0.0) x = 1e-12 * xi_scale[c];  // gp_core.cpp:103-105
+                }
+                xi[c * np + q] = x;
+            }
+        }
+        CK(cudaMemcpyAsync(g.d_coef, co, sizeof(double) * size_t(nc) * np, cudaMemcpyHostToDevice, M->st));
+        CK(cudaMemcpyAsync(g.d_xi, xi, sizeof(double) * size_t(nc) * np, cudaMemcpyHostToDevice, M->st));
+        cur += 2 * size_t(nc) * np;
+    }
+    CK(cudaMemcpyAsync(M->d_eta, eta, sizeof(double) * size_t(nc) * d, cudaMemcpyHostToDevice, M->st));
+    CK(cudaMemcpyAsync(M->d_gamma, gam, sizeof(double) * size_t(nc), cudaMemcpyHostToDevice, M->st));
+    CK(cudaMemcpyAsync(M->d_Rpair, Rp, sizeof(double) * size_t(nc) * P, cudaMemcpyHostToDevice, M->st));
+}
+
+GenSrc gensrc_of(fmtgp_model* M, const Group& g, int si_alpha, const double* b) {
+    GenSrc s{};
+    s.sp = spatial_of(M, si_alpha, b);
+    s.pg = pointgen_of(M, g.m);
+    s.offs = M->d_offs;
+    s.eta = M->d_eta;
+    s.gamma = M->d_gamma;
+    s.vec_pair = g.d_vec_pair;
+    s.nvpc = int(g.pairs.size());
+    return s;
+}
+
+// build_spectrum for nc candidates (fast_gram.cpp:42-89)
+void build_spectra(fmtgp_model* M, int nc, int si_alpha, const double* b) {
+    for (auto& g : M->groups) {
+        const int np = int(g.pairs.size());
+        GenSrc src = gensrc_of(M, g, si_alpha, b);
+        SpecSink snk{};
+        snk.out = M->d_lam;
+        snk.voff = g.d_voff;
+        snk.cstride = M->total_slots;
+        snk.coef = g.d_coef;
+        snk.xi = g.d_xi;
+        snk.nvpc = np;
+        fwd_gen(M->lattice, g.geo, np * nc, src, snk, M->d_work, M->tw, M->st);
+    }
+    CK(cudaGetLastError());
+}
+
+size_t elem_size(const fmtgp_model* M) { return M->lattice ? sizeof(double2) : sizeof(double); }
+
+// forward transform of a length-N vector (device) into task-slot layout
+void forward_vector(fmtgp_model* M, const double* dvec, void* dslots) {
+    for (auto& tg : M->tgroups) {
+        ArraySrc src{dvec, tg.d_yoff, tg.m, M->lattice};
+        ScaleSink snk{dslots, tg.d_soff, 1.0 / std::sqrt(double(1ll << tg.m))};
+        fwd_array(M->lattice, tg.geo, int(tg.tasks.size()), src, snk, M->d_work, M->tw, M->st);
+    }
+    CK(cudaGetLastError());
+}
+
+// inverse transform from task-slot layout into a length-N vector (device)
+void inverse_vector(fmtgp_model* M, const void* dslots, double* dvec) {
+    for (auto& tg : M->tgroups) {
+        CoefSink cs{dvec, tg.d_yoff, tg.m, 1.0 / std::sqrt(double(1ll << tg.m))};
+        inv_coef(M->lattice, tg.geo, int(tg.tasks.size()), dslots, tg.d_soff, cs, M->d_work, M->tw, M->st);
+    }
+    CK(cudaGetLastError());
+}
+
+void compute_yhat_tau(fmtgp_model* M) {
+    forward_vector(M, M->d_y, M->d_yhat);
+    // tau: equal n -> tau_l = yhat_l(0) / sqrt(n) (the sample mean, gp_core.cpp:67-88 with
+    // V̄ 1 = sqrt(n) e_0); unequal n -> class-0 normal equations at fit time.
+    std::vector<double> y0(M->T);
+    for (int t = 0; t < M->T; ++t) {
+        CK(cudaMemcpyAsync(&y0[t], static_cast<char*>(M->d_yhat) + M->toff_slots[t] * elem_size(M), sizeof(double),
+                           cudaMemcpyDeviceToHost, M->st));
+    }
+    CK(cudaStreamSynchronize(M->st));
+    for (int t = 0; t < M->T; ++t) M->tau[t] = y0[t] / std::sqrt(double(M->n[t]));
+    M->have_y = true;
+}
+
+void finish_results(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, bool grad, fmtgp_result* out,
+                    const double* xi_scale, const int* esc) {
+    const int T = M->T;
+    for (int c = 0; c < nc; ++c) {
+        const double* o = M->h_out + size_t(c) * NOUT;
+        fmtgp_result& r = out[c];
+        std::memset(&r, 0, sizeof(r));
+        r.logdet = o[OUT_LOGDET];
+        r.quad = o[OUT_QUAD];
+        r.nll = o[OUT_NLL];
+        r.xi_scale = xi_scale[c];
+        r.escalations = esc[c];
+        for (int t = 0; t < T; ++t) r.tau[t] = M->tau[t];
+        if (grad) {
+            r.dgamma = o[OUT_DGAMMA];
+            for (int j = 0; j < M->d; ++j) r.deta[j] = o[OUT_DETA + j];
+            const fmtgp_hyper* h = hs[c];
+            for (int a = 0; a < T; ++a)
+                for (int b = 0; b < T; ++b) r.dR[a * T + b] = o[OUT_DR + a * MAXT + b];
+            for (int a = 0; a < T; ++a) {
+                r.dt[a] = r.dR[a * T + a];
+                for (int k = 0; k < h->s; ++k) {
+                    double acc = 0.0;
+                    for (int b = 0; b < T; ++b) acc += r.dR[a * T + b] * h->B[b * h->s + k];
+                    r.dB[a * h->s + k] = 2.0 * acc;  // dNLL/dB = 2 G B
+                }
+            }
+        }
+    }
+}
+
+// One batched evaluation attempt (equal n).  Returns per-candidate bad flags in M->h_bad.
+void eval_equal(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, const double* xi_scale, bool grad,
+                bool keep_chat) {
+    const fmtgp_hyper* h0 = hs[0];
+    upload_hyper(M, nc, hs, xi_scale);
+    build_spectra(M, nc, h0->si_alpha, h0->b);
+    CK(cudaMemsetAsync(M->d_bad, 0x7f, sizeof(int) * nc, M->st));
+    CK(cudaMemsetAsync(M->d_bad + nc, 0, sizeof(int) * nc, M->st));
+    SolveArgs sa{};
+    sa.T = M->T;
+    sa.P = M->P;
+    sa.lattice = M->lattice;
+    sa.nslots = M->pslots[0];
+    sa.has_nyq = M->n[0] >= 2;
+    sa.cstride = M->total_slots;
+    sa.lam = M->d_lam;
+    sa.yhat = M->d_yhat;
+    sa.M = grad ? M->d_M : nullptr;
+    sa.lam_inv = nullptr;
+    sa.chat = keep_chat ? M->d_chat : nullptr;
+    sa.partial = M->d_psolve;
+    sa.bad = M->d_bad;
+    sa.nblk = M->nblk_solve;
+    solve_equal(sa, nc, M->st);
+    CK(cudaGetLastError());
+    const Group& g = M->groups[0];
+    if (grad) {
+        GradSink gs{};
+        gs.gen = gensrc_of(M, g, h0->si_alpha, h0->b);
+        gs.partial = M->d_pgrad;
+        gs.nblk = M->nblk_grad;
+        gs.acc_n = M->d + 1;
+        inv_grad(M->lattice, g.geo, M->P * nc, M->d_M, g.d_voff, M->total_slots, M->P, gs, M->d_work, M->tw, M->st);
+        CK(cudaGetLastError());
+    }
+    FinalArgs fa{};
+    fa.T = M->T;
+    fa.P = M->P;
+    fa.d = M->d;
+    fa.ncand = nc;
+    fa.nblk_solve = M->nblk_solve;
+    fa.nblk_grad = M->nblk_grad;
+    fa.solve_partial = M->d_psolve;
+    fa.grad_partial = grad ? M->d_pgrad : nullptr;
+    fa.Rpair = M->d_Rpair;
+    fa.gamma = M->d_gamma;
+    fa.pair_a = M->d_pa;
+    fa.pair_b = M->d_pb;
+    fa.out = M->d_out;
+    finalize(fa, M->st);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(M->h_out, M->d_out, sizeof(double) * NOUT * nc, cudaMemcpyDeviceToHost, M->st));
+    CK(cudaMemcpyAsync(M->h_bad, M->d_bad, sizeof(int) * 2 * nc, cudaMemcpyDeviceToHost, M->st));
+    CK(cudaStreamSynchronize(M->st));
+}
+
+void remember_hyper(fmtgp_model* M, const fmtgp_hyper* h) {
+    M->last_gamma = h->gamma;
+    M->last_eta.assign(h->eta, h->eta + M->d);
+    M->last_R = task_gram(M, h);
+    M->last_alpha = h->si_alpha;
+    for (int i = 0; i < 4; ++i) M->last_b[i] = h->b[i];
+    std::vector<double> buf(MAXD + MAXT * MAXT, 0.0);
+    for (int j = 0; j < M->d; ++j) buf[j] = M->last_eta[j];
+    for (size_t k = 0; k < M->last_R.size(); ++k) buf[MAXD + k] = M->last_R[k];
+    CK(cudaMemcpyAsync(M->d_fit, buf.data(), buf.size() * sizeof(double), cudaMemcpyHostToDevice, M->st));
+    CK(cudaStreamSynchronize(M->st));
+}
+
+// nll over a batch with the reference's escalation schedule per candidate
+void nll_batch_impl(fmtgp_model* M, int nc, const fmtgp_hyper* hin, bool grad, fmtgp_result* out, bool keep_chat) {
+    if (!M->have_y) invalid("nll: observations not set (fmtgp_model_set_y)");
+    for (int c = 0; c < nc; ++c) validate_hyper(M, hin + c);
+    if (!M->equal) {
+        if (nc != 1) throw Fail{FMTGP_ERR_UNSUPPORTED, "nll_batch: unequal sample sizes support one candidate"};
+        unequal::nll(M->uneq, M, hin, grad, out);
+        return;
+    }
+    std::vector<int> todo(nc);
+    for (int c = 0; c < nc; ++c) todo[c] = c;
+    std::vector<double> scale(nc, 1.0);
+    std::vector<int> esc(nc, 0);
+    std::vector<int> status(nc, FMTGP_OK);
+    for (int attempt = 0; !todo.empty(); ++attempt) {
+        for (size_t base = 0; base < todo.size(); base += M->max_cand) {
+            const int cnt = int(std::min<size_t>(M->max_cand, todo.size() - base));
+            std::vector<const fmtgp_hyper*> hs(cnt);
+            std::vector<double> sc(cnt);
+            std::vector<int> es(cnt);
+            for (int i = 0; i < cnt; ++i) {
+                hs[i] = hin + todo[base + i];
+                sc[i] = scale[todo[base + i]];
+                es[i] = attempt;
+            }
+            eval_equal(M, cnt, hs.data(), sc.data(), grad, keep_chat && todo[base] == 0 && cnt == 1);
+            std::vector<fmtgp_result> tmp(cnt);
+            finish_results(M, cnt, hs.data(), grad, tmp.data(), sc.data(), es.data());
+            for (int i = 0; i < cnt; ++i) {
+                const int c = todo[base + i];
+                out[c] = tmp[i];
+                if (M->h_bad[cnt + i]) status[c] = FMTGP_ERR_NONREAL;
+                else if (M->h_bad[i] != BAD_NONE) status[c] = FMTGP_ERR_SCHUR;
+                else status[c] = FMTGP_OK;
+            }
+        }
+        std::vector<int> next;
+        for (int c : todo)
+            if (status[c] == FMTGP_ERR_SCHUR) {
+                if (attempt + 1 > 6) continue;  // schedule exhausted (gp_core.cpp:100)
+                scale[c] *= 10.0;
+                next.push_back(c);
+            }
+        todo.swap(next);
+    }
+    for (int c = 0; c < nc; ++c) out[c].status = status[c];
+}
+
+long long slots_of(const fmtgp_model* M, int m) { return M->lattice ? (m > 0 ? (1ll << (m - 1)) : 1) : (1ll << m); }
+
+void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_model** out) {
+    if (!dz || !out) invalid("model_create: null argument");
+    if (dz->kind != 0 && dz->kind != 1) invalid("design: kind must be 0 (lattice) or 1 (digital)");
+    if (dz->d < 1 || dz->d > MAXD) throw Fail{FMTGP_ERR_UNSUPPORTED, "design: d must be in [1, 16]"};
+    if (dz->L < 1 || dz->L > MAXT) invalid("make_design: at most 8 tasks supported");
+    if (!dz->m || !dz->shift_bits) invalid("design: null m / shift_bits");
+    for (int l = 0; l < dz->L; ++l) {
+        if (dz->m[l] < 0 || dz->m[l] > 27) invalid("design: log2 size out of range");
+        if (l + 1 < dz->L && dz->m[l] < dz->m[l + 1]) invalid("build_spectrum: task sizes must be descending");
+    }
+    if (dz->kind == 0) {
+        if (!dz->g || dz->n_max == 0 || (dz->n_max & (dz->n_max - 1)) || dz->n_max < (1ull << dz->m[0]))
+            invalid("lattice design: bad generating vector / n_max");
+    } else {
+        if (!dz->columns || dz->m_cols < dz->m[0] || dz->m_cols > 64) invalid("digital design: bad columns");
+    }
+    if (max_cand < 1) max_cand = 1;
+    CK(cudaSetDevice(device));
+    auto* M = new fmtgp_model;
+    try {
+        M->dev = device;
+        CK(cudaStreamCreateWithFlags(&M->st, cudaStreamNonBlocking));
+        M->kind = dz->kind;
+        M->lattice = dz->kind == 0;
+        M->d = dz->d;
+        M->T = dz->L;
+        M->max_cand = max_cand;
+        M->off[0] = 0;
+        for (int l = 0; l < M->T; ++l) {
+            M->m[l] = dz->m[l];
+            M->n[l] = 1ll << dz->m[l];
+            M->off[l + 1] = M->off[l] + M->n[l];
+            if (M->m[l] != M->m[0]) M->equal = false;
+        }
+        M->N = M->off[M->T];
+        M->tw = twiddles_for(device);
+        // pairs, row by row
+        for (int a = 0; a < M->T; ++a)
+            for (int b = a; b < M->T; ++b) {
+                M->pa.push_back(a);
+                M->pb.push_back(b);
+            }
+        M->P = int(M->pa.size());
+        M->poff.resize(M->P);
+        M->pslots.resize(M->P);
+        long long acc = 0;
+        for (int p = 0; p < M->P; ++p) {
+            M->poff[p] = acc;
+            M->pslots[p] = slots_of(M, M->m[M->pa[p]]);
+            acc += M->pslots[p];
+        }
+        M->total_slots = acc;
+        M->toff_slots.resize(M->T);
+        acc = 0;
+        for (int t = 0; t < M->T; ++t) {
+            M->toff_slots[t] = acc;
+            acc += slots_of(M, M->m[t]);
+        }
+        M->task_slots = acc;
+        // design tables
+        M->shifts.assign(dz->shift_bits, dz->shift_bits + size_t(M->T) * M->d);
+        std::vector<uint64_t> offs(size_t(M->P) * MAXD, 0);
+        for (int p = 0; p < M->P; ++p)
+            for (int j = 0; j < M->d; ++j) {
+                const uint64_t sa = dz->shift_bits[M->pa[p] * M->d + j] & MASK53;
+                const uint64_t sb = dz->shift_bits[M->pb[p] * M->d + j] & MASK53;
+                offs[size_t(p) * MAXD + j] = M->lattice ? ((sa - sb) & MASK53) : (sa ^ sb);
+            }
+        M->d_shifts = dalloc<uint64_t>(M->shifts.size());
+        CK(cudaMemcpy(M->d_shifts, M->shifts.data(), M->shifts.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
+        M->d_fit = dalloc<double>(MAXD + MAXT * MAXT);
+        M->d_c = dalloc<double>(M->N);
+        if (dz->kind == 0) {
+            M->n_max = dz->n_max;
+            while ((1ull << M->mgen) < M->n_max) ++M->mgen;
+        }
+        M->d_offs = dalloc<uint64_t>(offs.size());
+        CK(cudaMemcpy(M->d_offs, offs.data(), offs.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
+        if (M->lattice) {
+            M->d_g = dalloc<uint64_t>(M->d);
+            CK(cudaMemcpy(M->d_g, dz->g, M->d * sizeof(uint64_t), cudaMemcpyHostToDevice));
+        } else {
+            M->m_cols = dz->m_cols;
+            M->d_cols = dalloc<uint64_t>(size_t(M->d) * M->m_cols);
+            CK(cudaMemcpy(M->d_cols, dz->columns, size_t(M->d) * M->m_cols * sizeof(uint64_t),
+                          cudaMemcpyHostToDevice));
+        }
+        M->d_pa = dalloc<int>(M->P);
+        M->d_pb = dalloc<int>(M->P);
+        CK(cudaMemcpy(M->d_pa, M->pa.data(), M->P * sizeof(int), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(M->d_pb, M->pb.data(), M->P * sizeof(int), cudaMemcpyHostToDevice));
+        // groups of pairs by generating-task length
+        size_t work = 0;
+        for (int p = 0; p < M->P; ++p) {
+            const int mm = M->m[M->pa[p]];
+            auto it = std::find_if(M->groups.begin(), M->groups.end(), [&](const Group& g) { return g.m == mm; });
+            if (it == M->groups.end()) {
+                M->groups.push_back(Group{});
+                M->groups.back().m = mm;
+                M->groups.back().geo = Geo::make(mm, M->lattice);
+                it = M->groups.end() - 1;
+            }
+            it->pairs.push_back(p);
+        }
+        for (auto& g : M->groups) {
+            const int np = int(g.pairs.size());
+            std::vector<long long> vo(np);
+            for (int q = 0; q < np; ++q) vo[q] = M->poff[g.pairs[q]];
+            g.d_vec_pair = dalloc<int>(np);
+            g.d_voff = dalloc<long long>(np);
+            g.d_coef = dalloc<double>(size_t(np) * max_cand);
+            g.d_xi = dalloc<double>(size_t(np) * max_cand);
+            CK(cudaMemcpy(g.d_vec_pair, g.pairs.data(), np * sizeof(int), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(g.d_voff, vo.data(), np * sizeof(long long), cudaMemcpyHostToDevice));
+            if (g.geo.two) work = std::max(work, size_t(np) * max_cand * (size_t(1) << g.geo.lt));
+        }
+        for (int t = 0; t < M->T; ++t) {
+            const int mm = M->m[t];
+            auto it = std::find_if(M->tgroups.begin(), M->tgroups.end(), [&](const TaskGroup& g) { return g.m == mm; });
+            if (it == M->tgroups.end()) {
+                M->tgroups.push_back(TaskGroup{});
+                M->tgroups.back().m = mm;
+                M->tgroups.back().geo = Geo::make(mm, M->lattice);
+                it = M->tgroups.end() - 1;
+            }
+            it->tasks.push_back(t);
+        }
+        for (auto& tg : M->tgroups) {
+            const int nt = int(tg.tasks.size());
+            std::vector<long long> yo(nt), so(nt);
+            for (int q = 0; q < nt; ++q) {
+                yo[q] = M->off[tg.tasks[q]];
+                so[q] = M->toff_slots[tg.tasks[q]];
+            }
+            tg.d_yoff = dalloc<long long>(nt);
+            tg.d_soff = dalloc<long long>(nt);
+            CK(cudaMemcpy(tg.d_yoff, yo.data(), nt * sizeof(long long), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(tg.d_soff, so.data(), nt * sizeof(long long), cudaMemcpyHostToDevice));
+            if (tg.geo.two) work = std::max(work, size_t(nt) * (size_t(1) << tg.geo.lt));
+        }
+        const size_t es = elem_size(M);
+        M->work_elems = work;
+        M->d_work = dalloc<char>(std::max<size_t>(work, 1) * es);
+        M->d_y = dalloc<double>(M->N);
+        M->d_yhat = dalloc<char>(M->task_slots * es);
+        // hyper block: eta [mc*d] | gamma [mc] | Rpair [mc*P]
+        M->d_eta = dalloc<double>(size_t(max_cand) * (M->d + 1 + M->P));
+        M->d_gamma = M->d_eta + size_t(max_cand) * M->d;
+        M->d_Rpair = M->d_gamma + max_cand;
+        M->d_lam = dalloc<char>(size_t(max_cand) * M->total_slots * es);
+        M->d_laminv = dalloc<char>(size_t(M->total_slots) * es);
+        M->d_chat = dalloc<char>(size_t(M->task_slots) * es);
+        if (M->equal) {
+            M->d_M = dalloc<char>(size_t(max_cand) * M->total_slots * es);
+            const long long ns = M->pslots[0];
+            M->nblk_solve = int(std::min<long long>((ns + 255) / 256, 148 * 8));
+            M->nblk_grad = grad_blocks(M->lattice, M->groups[0].geo);
+            M->d_pgrad = dalloc<double>(size_t(max_cand) * M->P * M->nblk_grad * (MAXD + 1));
+        } else {
+            M->nblk_solve = 1;
+        }
+        M->d_psolve = dalloc<double>(size_t(max_cand) * std::max(M->nblk_solve, 1) * 3);
+        M->d_bad = dalloc<int>(2 * size_t(max_cand));
+        M->d_out = dalloc<double>(size_t(max_cand) * NOUT);
+        M->d_vecA = dalloc<double>(M->N);
+        M->d_vecB = dalloc<double>(M->N);
+        M->d_sA = dalloc<char>(M->task_slots * es);
+        M->d_sB = dalloc<char>(M->task_slots * es);
+        CK(cudaMallocHost(reinterpret_cast<void**>(&M->h_out), sizeof(double) * NOUT * max_cand));
+        CK(cudaMallocHost(reinterpret_cast<void**>(&M->h_bad), sizeof(int) * 2 * max_cand));
+        CK(cudaMemsetAsync(M->d_yhat, 0, M->task_slots * es, M->st));
+        if (!M->equal) M->uneq = unequal::create(M);
+        CK(cudaStreamSynchronize(M->st));
+    } catch (...) {
+        fmtgp_model_destroy(M);
+        throw;
+    }
+    *out = M;
+}
+
+}  // namespace
+
+void ensure_coefficients(fmtgp_model* M) {
+    if (M->have_c) return;
+    if (M->equal) inverse_vector(M, M->d_chat, M->d_c);
+    else unequal::coefficients(M->uneq, M, M->d_c);
+    M->have_c = true;
+}
+
+// ===================================================================== accessors for unequal.cu
+namespace fmtgp::hostapi {
+cudaStream_t stream(fmtgp_model* M) { return M->st; }
+}  // namespace fmtgp::hostapi
+
+#include "unequal_impl.inc"
+
+// ===================================================================== C ABI
+extern "C" {
+
+const char* fmtgp_last_error(void) { return g_err.c_str(); }
+int fmtgp_abi_version(void) { return 1; }
+
+int fmtgp_model_create(const fmtgp_design* design, int device, int max_candidates, fmtgp_model_t* out) {
+    return guarded([&] { model_create_impl(design, device, max_candidates, out); });
+}
+
+int fmtgp_model_destroy(fmtgp_model_t M) {
+    if (!M) return FMTGP_OK;
+    cudaSetDevice(M->dev);
+    if (M->st) cudaStreamSynchronize(M->st);
+    auto F = [](void* p) {
+        if (p) cudaFree(p);
+    };
+    for (auto& g : M->groups) {
+        F(g.d_vec_pair);
+        F(g.d_voff);
+        F(g.d_coef);
+        F(g.d_xi);
+    }
+    for (auto& tg : M->tgroups) {
+        F(tg.d_yoff);
+        F(tg.d_soff);
+    }
+    F(M->d_g);
+    F(M->d_cols);
+    F(M->d_offs);
+    F(M->d_shifts);
+    F(M->d_fit);
+    F(M->d_c);
+    F(M->d_pa);
+    F(M->d_pb);
+    F(M->d_y);
+    F(M->d_yhat);
+    F(M->d_eta);
+    F(M->d_lam);
+    F(M->d_M);
+    F(M->d_work);
+    F(M->d_laminv);
+    F(M->d_chat);
+    F(M->d_psolve);
+    F(M->d_pgrad);
+    F(M->d_bad);
+    F(M->d_out);
+    F(M->d_vecA);
+    F(M->d_vecB);
+    F(M->d_sA);
+    F(M->d_sB);
+    if (M->uneq) unequal::destroy(M->uneq);
+    if (M->h_stage) cudaFreeHost(M->h_stage);
+    if (M->h_out) cudaFreeHost(M->h_out);
+    if (M->h_bad) cudaFreeHost(M->h_bad);
+    if (M->st) cudaStreamDestroy(M->st);
+    delete M;
+    return FMTGP_OK;
+}
+
+void* fmtgp_model_stream(fmtgp_model_t M) { return M ? static_cast<void*>(M->st) : nullptr; }
+
+int fmtgp_model_set_y(fmtgp_model_t M, const double* y) {
+    return guarded([&] {
+        if (!M || !y) invalid("set_y: null argument");
+        CK(cudaSetDevice(M->dev));
+        CK(cudaMemcpyAsync(M->d_y, y, sizeof(double) * M->N, cudaMemcpyHostToDevice, M->st));
+        compute_yhat_tau(M);
+        M->have_fit = false;
+    });
+}
+
+int fmtgp_model_set_y_device(fmtgp_model_t M, const double* y) {
+    return guarded([&] {
+        if (!M || !y) invalid("set_y_device: null argument");
+        CK(cudaSetDevice(M->dev));
+        CK(cudaMemcpyAsync(M->d_y, y, sizeof(double) * M->N, cudaMemcpyDeviceToDevice, M->st));
+        compute_yhat_tau(M);
+        M->have_fit = false;
+    });
+}
+
+int fmtgp_build_spectrum(fmtgp_model_t M, const fmtgp_hyper* h) {
+    return guarded([&] {
+        if (!M) invalid("build_spectrum: null model");
+        CK(cudaSetDevice(M->dev));
+        validate_hyper(M, h);
+        const double one = 1.0;
+        const fmtgp_hyper* hs[1] = {h};
+        upload_hyper(M, 1, hs, &one);
+        build_spectra(M, 1, h->si_alpha, h->b);
+        CK(cudaStreamSynchronize(M->st));
+        remember_hyper(M, h);
+        M->have_spec = true;
+        M->have_inv = false;
+    });
+}
+
+int fmtgp_spectrum_read(fmtgp_model_t M, int l, int lp, double* re, double* im) {
+    return guarded([&] {
+        if (!M || !re || !im) invalid("spectrum_read: null argument");
+        if (!M->have_spec) invalid("spectrum_read: no spectrum built");
+        if (l < 0 || lp < l || lp >= M->T) invalid("pair_index: need 0 <= l <= lp < L");
+        const int p = pair_index(M->T, l, lp);
+        const long long ns = M->pslots[p], n = M->n[l];
+        std::vector<double> buf(size_t(ns) * (M->lattice ? 2 : 1));
+        CK(cudaMemcpy(buf.data(), static_cast<char*>(M->d_lam) + M->poff[p] * elem_size(M), buf.size() * sizeof(double),
+                      cudaMemcpyDeviceToHost));
+        if (!M->lattice) {
+            for (long long k = 0; k < n; ++k) {
+                re[k] = buf[k];
+                im[k] = 0.0;
+            }
+            return;
+        }
+        const Geo g = Geo::make(M->m[l], 1);
+        for (long long k = 0; k < n; ++k) {
+            if (n == 1) {
+                re[0] = buf[0];
+                im[0] = 0.0;
+                break;
+            }
+            const long long half = n / 2;
+            if (k == 0) {
+                re[k] = buf[0];
+                im[k] = 0.0;
+            } else if (k == half) {
+                re[k] = buf[1];
+                im[k] = 0.0;
+            } else if (k < half) {
+                const long long q = g.pos_of(k);
+                re[k] = buf[2 * q];
+                im[k] = buf[2 * q + 1];
+            } else {
+                const long long q = g.pos_of(n - k);
+                re[k] = buf[2 * q];
+                im[k] = -buf[2 * q + 1];
+            }
+        }
+    });
+}
+
+int fmtgp_invert_and_logdet(fmtgp_model_t M, double* logdet) {
+    return guarded([&] {
+        if (!M || !logdet) invalid("invert_and_logdet: null argument");
+        if (!M->have_spec) invalid("invert_and_logdet: no spectrum built");
+        CK(cudaSetDevice(M->dev));
+        if (!M->equal) {
+            unequal::invert(M->uneq, M, logdet);
+            M->have_inv = true;
+            return;
+        }
+        CK(cudaMemsetAsync(M->d_bad, 0x7f, sizeof(int), M->st));
+        CK(cudaMemsetAsync(M->d_bad + 1, 0, sizeof(int), M->st));
+        SolveArgs sa{};
+        sa.T = M->T;
+        sa.P = M->P;
+        sa.lattice = M->lattice;
+        sa.nslots = M->pslots[0];
+    sa.has_nyq = M->n[0] >= 2;
+        sa.cstride = M->total_slots;
+        sa.lam = M->d_lam;
+        sa.yhat = M->d_sA;  // zero right-hand side: logdet and the inverse only
+        CK(cudaMemsetAsync(M->d_sA, 0, M->task_slots * elem_size(M), M->st));
+        sa.lam_inv = M->d_laminv;
+        sa.partial = M->d_psolve;
+        sa.bad = M->d_bad;
+        sa.nblk = M->nblk_solve;
+        solve_equal(sa, 1, M->st);
+        FinalArgs fa{};
+        fa.T = M->T;
+        fa.P = M->P;
+        fa.d = M->d;
+        fa.ncand = 1;
+        fa.nblk_solve = M->nblk_solve;
+        fa.solve_partial = M->d_psolve;
+        fa.out = M->d_out;
+        finalize(fa, M->st);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(M->h_out, M->d_out, sizeof(double) * NOUT, cudaMemcpyDeviceToHost, M->st));
+        CK(cudaMemcpyAsync(M->h_bad, M->d_bad, sizeof(int) * 2, cudaMemcpyDeviceToHost, M->st));
+        CK(cudaStreamSynchronize(M->st));
+        if (M->h_bad[1]) throw Fail{FMTGP_ERR_NONREAL, "invert_and_logdet: non-real Schur complement"};
+        if (M->h_bad[0] != BAD_NONE)
+            throw Fail{FMTGP_ERR_SCHUR, "non-positive Schur entry at slot " + std::to_string(M->h_bad[0])};
+        M->last_logdet = M->h_out[OUT_LOGDET];
+        *logdet = M->last_logdet;
+        M->have_inv = true;
+    });
+}
+
+int fmtgp_solve(fmtgp_model_t M, const double* b, double* x) {
+    return guarded([&] {
+        if (!M || !b || !x) invalid("solve: null argument");
+        if (!M->have_inv) invalid("solve: no factorisation (invert_and_logdet)");
+        CK(cudaSetDevice(M->dev));
+        CK(cudaMemcpyAsync(M->d_vecA, b, sizeof(double) * M->N, cudaMemcpyHostToDevice, M->st));
+        forward_vector(M, M->d_vecA, M->d_sA);
+        if (M->equal) apply_hermitian(M->lattice, M->T, M->pslots[0], M->d_laminv, M->d_sA, M->d_sB, M->st);
+        else unequal::apply_inverse(M->uneq, M, M->d_sA, M->d_sB);
+        inverse_vector(M, M->d_sB, M->d_vecB);
+        CK(cudaMemcpyAsync(x, M->d_vecB, sizeof(double) * M->N, cudaMemcpyDeviceToHost, M->st));
+        CK(cudaStreamSynchronize(M->st));
+    });
+}
+
+int fmtgp_gram_matvec(fmtgp_model_t M, const double* b, double* out) {
+    return guarded([&] {
+        if (!M || !b || !out) invalid("gram_matvec: null argument");
+        if (!M->have_spec) invalid("gram_matvec: no spectrum built");
+        CK(cudaSetDevice(M->dev));
+        CK(cudaMemcpyAsync(M->d_vecA, b, sizeof(double) * M->N, cudaMemcpyHostToDevice, M->st));
+        forward_vector(M, M->d_vecA, M->d_sA);
+        if (M->equal) apply_hermitian(M->lattice, M->T, M->pslots[0], M->d_lam, M->d_sA, M->d_sB, M->st);
+        else unequal::apply_gram(M->uneq, M, M->d_sA, M->d_sB);
+        inverse_vector(M, M->d_sB, M->d_vecB);
+        CK(cudaMemcpyAsync(out, M->d_vecB, sizeof(double) * M->N, cudaMemcpyDeviceToHost, M->st));
+        CK(cudaStreamSynchronize(M->st));
+    });
+}
+
+int fmtgp_extract_pi(fmtgp_model_t M, double* Pi) {
+    return guarded([&] {
+        if (!M || !Pi) invalid("extract_pi: null argument");
+        if (!M->have_inv) invalid("extract_pi: no factorisation");
+        CK(cudaSetDevice(M->dev));
+        if (!M->equal) {
+            unequal::extract_pi(M->uneq, M, Pi);
+            return;
+        }
+        // Pi = n Lam(0)^-1 (fast_gram.cpp:311-335 with V̄ 1 = sqrt(n) e_0)
+        const int T = M->T;
+        for (int a = 0; a < T; ++a)
+            for (int b = a; b < T; ++b) {
+                const int p = pair_index(T, a, b);
+                double v = 0.0;
+                CK(cudaMemcpy(&v, static_cast<char*>(M->d_laminv) + M->poff[p] * elem_size(M), sizeof(double),
+                              cudaMemcpyDeviceToHost));
+                Pi[a * T + b] = Pi[b * T + a] = double(M->n[a]) * v;
+            }
+    });
+}
+
+int fmtgp_trace_inverse(fmtgp_model_t M, double* tr) {
+    return guarded([&] {
+        if (!M || !tr) invalid("trace_inverse: null argument");
+        if (!M->have_inv) invalid("trace_inverse: no factorisation");
+        if (!M->equal) throw Fail{FMTGP_ERR_UNSUPPORTED, "trace_inverse: unequal sample sizes not implemented"};
+        CK(cudaSetDevice(M->dev));
+        const long long ns = M->pslots[0];
+        const int T = M->T;
+        double acc = 0.0;
+        std::vector<double> buf(size_t(ns) * (M->lattice ? 2 : 1));
+        for (int a = 0; a < T; ++a) {
+            const int p = pair_index(T, a, a);
+            CK(cudaMemcpy(buf.data(), static_cast<char*>(M->d_laminv) + M->poff[p] * elem_size(M),
+                          buf.size() * sizeof(double), cudaMemcpyDeviceToHost));
+            if (M->lattice) {
+                acc += buf[0] + (M->n[a] > 1 ? buf[1] : 0.0);
+                for (long long q = 1; q < ns; ++q) acc += 2.0 * buf[2 * q];
+            } else {
+                for (long long q = 0; q < ns; ++q) acc += buf[q];
+            }
+        }
+        *tr = acc;
+    });
+}
+
+int fmtgp_nll(fmtgp_model_t M, const fmtgp_hyper* h, int want_grad, fmtgp_result* out) {
+    return guarded([&] {
+        if (!M || !h || !out) invalid("nll: null argument");
+        CK(cudaSetDevice(M->dev));
+        nll_batch_impl(M, 1, h, want_grad != 0, out, true);
+        if (out->status != FMTGP_OK) {
+            if (out->status == FMTGP_ERR_SCHUR) throw Fail{FMTGP_ERR_SCHUR, "noise escalation schedule exhausted"};
+            throw Fail{out->status, "invert_and_logdet: non-real Schur complement"};
+        }
+        remember_hyper(M, h);
+        M->have_fit = true;
+        M->have_c = false;
+        M->have_spec = true;
+        M->have_inv = false;
+    });
+}
+
+int fmtgp_nll_batch(fmtgp_model_t M, int ncand, const fmtgp_hyper* h, int want_grad, fmtgp_result* out) {
+    return guarded([&] {
+        if (!M || !h || !out || ncand < 1) invalid("nll_batch: bad argument");
+        CK(cudaSetDevice(M->dev));
+        nll_batch_impl(M, ncand, h, want_grad != 0, out, false);
+        M->have_fit = false;
+        M->have_spec = false;
+        M->have_inv = false;
+    });
+}
+
+int fmtgp_coefficients(fmtgp_model_t M, double* c) {
+    return guarded([&] {
+        if (!M || !c) invalid("coefficients: null argument");
+        if (!M->have_fit) invalid("coefficients: model not refreshed (call fmtgp_nll)");
+        CK(cudaSetDevice(M->dev));
+        ensure_coefficients(M);
+        CK(cudaMemcpyAsync(c, M->d_c, sizeof(double) * M->N, cudaMemcpyDeviceToHost, M->st));
+        CK(cudaStreamSynchronize(M->st));
+    });
+}
+
+int fmtgp_posterior_mean(fmtgp_model_t M, int task, const double* X, int64_t count, double* out) {
+    return guarded([&] {
+        if (!M || (!X && count > 0) || (!out && count > 0)) invalid("posterior_mean: null argument");
+        if (!M->have_fit) invalid("posterior_mean: model not refreshed");
+        if (task < 0 || task >= M->T) invalid("posterior_mean: task out of range");
+        if (count <= 0) return;
+        CK(cudaSetDevice(M->dev));
+        ensure_coefficients(M);
+        double* dX = dalloc<double>(size_t(count) * M->d);
+        double* dO = dalloc<double>(size_t(count));
+        try {
+            CK(cudaMemcpyAsync(dX, X, sizeof(double) * count * M->d, cudaMemcpyHostToDevice, M->st));
+            PostArgs a{};
+            a.lattice = M->lattice;
+            a.d = M->d;
+            a.T = M->T;
+            a.task = task;
+            a.si_alpha = M->last_alpha;
+            a.mgen = M->mgen;
+            a.m_cols = M->m_cols;
+            a.n_max = M->n_max;
+            a.g = M->d_g;
+            a.cols = M->d_cols;
+            a.shifts = M->d_shifts;
+            for (int i = 0; i < 4; ++i) a.b[i] = M->last_b[i];
+            a.eta = M->d_fit;
+            a.R = M->d_fit + MAXD;
+            a.gamma = M->last_gamma;
+            a.tau = M->tau[task];
+            for (int l = 0; l < M->T; ++l) {
+                a.n[l] = M->n[l];
+                a.off[l] = M->off[l];
+            }
+            a.c = M->d_c;
+            a.X = dX;
+            a.count = count;
+            a.out = dO;
+            posterior_mean(a, M->st);
+            CK(cudaGetLastError());
+            CK(cudaMemcpyAsync(out, dO, sizeof(double) * count, cudaMemcpyDeviceToHost, M->st));
+            CK(cudaStreamSynchronize(M->st));
+        } catch (...) {
+            cudaFree(dX);
+            cudaFree(dO);
+            throw;
+        }
+        cudaFree(dX);
+        cudaFree(dO);
+    });
+}
+
+int fmtgp_posterior_var(fmtgp_model_t M, int task, const double* X, int64_t count, double* out) {
+    return guarded([&] {
+        if (!M || (!X && count > 0) || (!out && count > 0)) invalid("posterior_var: null argument");
+        if (!M->have_fit) invalid("posterior_var: model not refreshed");
+        if (task < 0 || task >= M->T) invalid("posterior_var: task out of range");
+        CK(cudaSetDevice(M->dev));
+        if (!M->uneq) throw Fail{FMTGP_ERR_UNSUPPORTED, "posterior_var: needs the fold plan"};
+        unequal::posterior_var(M->uneq, M, task, X, count, out);
+    });
+}
+
+// multitask_cubature (cubature.cpp:52-75): mu = tau + gamma R (E^T c), Sigma = gamma R - gamma^2 R Pi R
+int fmtgp_cubature(fmtgp_model_t M, double* mu, double* Sigma) {
+    return guarded([&] {
+        if (!M || !mu || !Sigma) invalid("cubature: null argument");
+        if (!M->have_fit) invalid("cubature: model not refreshed");
+        CK(cudaSetDevice(M->dev));
+        const int T = M->T;
+        std::vector<double> Pi(size_t(T) * T), etc(T, 0.0);
+        if (M->equal) {
+            // Pi = n Lam(0)^-1 from the fitted spectrum's frequency-0 entries; E^T c = sqrt(n) chat(0)
+            std::vector<double> A(size_t(T) * T);
+            for (int a = 0; a < T; ++a)
+                for (int b = a; b < T; ++b) {
+                    double v = 0.0;
+                    CK(cudaMemcpy(&v, static_cast<char*>(M->d_lam) + M->poff[pair_index(T, a, b)] * elem_size(M),
+                                  sizeof(double), cudaMemcpyDeviceToHost));
+                    A[a * T + b] = A[b * T + a] = v;
+                }
+            // Gauss-Jordan inverse (T <= 8)
+            std::vector<double> I(size_t(T) * T, 0.0);
+            for (int a = 0; a < T; ++a) I[a * T + a] = 1.0;
+            for (int k = 0; k < T; ++k) {
+                int piv = k;
+                for (int i = k + 1; i < T; ++i)
+                    if (std::fabs(A[i * T + k]) > std::fabs(A[piv * T + k])) piv = i;
+                for (int j = 0; j < T; ++j) {
+                    std::swap(A[k * T + j], A[piv * T + j]);
+                    std::swap(I[k * T + j], I[piv * T + j]);
+                }
+                const double dk = A[k * T + k];
+                for (int j = 0; j < T; ++j) {
+                    A[k * T + j] /= dk;
+                    I[k * T + j] /= dk;
+                }
+                for (int i = 0; i < T; ++i)
+                    if (i != k) {
+                        const double f = A[i * T + k];
+                        for (int j = 0; j < T; ++j) {
+                            A[i * T + j] -= f * A[k * T + j];
+                            I[i * T + j] -= f * I[k * T + j];
+                        }
+                    }
+            }
+            for (int a = 0; a < T; ++a)
+                for (int b = 0; b < T; ++b) Pi[a * T + b] = double(M->n[0]) * I[a * T + b];
+            ensure_coefficients(M);
+            std::vector<double> c(M->N);
+            CK(cudaMemcpy(c.data(), M->d_c, sizeof(double) * M->N, cudaMemcpyDeviceToHost));
+            for (int l = 0; l < T; ++l)
+                for (long long k = M->off[l]; k < M->off[l + 1]; ++k) etc[l] += c[k];
+        } else {
+            unequal::cubature_terms(M->uneq, M, Pi.data(), etc.data());
+        }
+        const std::vector<double>& R = M->last_R;
+        const double g = M->last_gamma;
+        for (int a = 0; a < T; ++a) {
+            double s = 0.0;
+            for (int b = 0; b < T; ++b) s += R[a * T + b] * etc[b];
+            mu[a] = M->tau[a] + g * s;
+        }
+        std::vector<double> RP(size_t(T) * T, 0.0);
+        for (int a = 0; a < T; ++a)
+            for (int b = 0; b < T; ++b)
+                for (int k = 0; k < T; ++k) RP[a * T + b] += R[a * T + k] * Pi[k * T + b];
+        for (int a = 0; a < T; ++a)
+            for (int b = 0; b < T; ++b) {
+                double s = 0.0;
+                for (int k = 0; k < T; ++k) s += RP[a * T + k] * R[k * T + b];
+                Sigma[a * T + b] = g * R[a * T + b] - g * g * s;
+            }
+        for (int a = 0; a < T; ++a)
+            for (int b = a + 1; b < T; ++b) Sigma[a * T + b] = Sigma[b * T + a] = 0.5 * (Sigma[a * T + b] + Sigma[b * T + a]);
+        for (int a = 0; a < T; ++a)
+            if (Sigma[a * T + a] < 0.0 && Sigma[a * T + a] > -1e-12) Sigma[a * T + a] = 0.0;
+    });
+}
+
+}  // extern "C"

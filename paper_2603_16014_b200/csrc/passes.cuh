@@ -1,0 +1,188 @@
+// Transform passes with fused sources (generator / gathered data) and sinks
+// (spectrum epilogue, gradient dot, coefficient scatter).
+//
+// Length-n real transforms:
+//   lattice (SI):  V̄ a = DFT(bitrev a) (transforms.cpp:58-77) of a REAL column, computed as
+//                  a half-length complex FFT of z(j) = a(2j) + i a(2j+1) plus the standard
+//                  real-FFT post-processing; only the Hermitian half is stored: slot k holds
+//                  A(k) for 1 <= k < n/2 and slot 0 packs (A(0), A(n/2)), both real.
+//   digital (DSI): FWHT (transforms.cpp:19-30), real, natural order, n slots.
+// One CTA transforms up to CAP = 2^13 elements; longer vectors use a two-pass four-step
+// decomposition n' = N1 * N2 (column pass then row pass, intermediate through L2/HBM).
+// Lattice slot layout of a two-pass transform: position k1*N2 + k2 <-> frequency
+// k = k1 + N1*k2 (the row pass's natural output), identical for every vector of that length,
+// which is all the per-frequency solve needs.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "generator.cuh"
+#include "transform.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace fmtgp {
+
+constexpr int NT_T = 512;        // threads per transform CTA
+constexpr int CAP_LOG = 13;      // elements per transform CTA = NT_T * EPT
+constexpr int CAP = 1 << CAP_LOG;
+
+// --------------------------------------------------------------------- geometry
+struct Geo {
+    int m;        // log2 n (task length)
+    int lt;       // log2 of the transformed length: m-1 (lattice) or m (digital)
+    int two;      // two-pass?
+    int l1, l2;   // two-pass split lt = l1 + l2
+    int C;        // columns per CTA in the column pass
+    __host__ __device__ static Geo make(int m, int lattice) {
+        Geo g{};
+        g.m = m;
+        g.lt = lattice ? (m > 0 ? m - 1 : 0) : m;
+        g.two = g.lt > CAP_LOG;
+        if (g.two) {
+            g.l2 = CAP_LOG;
+            g.l1 = g.lt - CAP_LOG;
+            g.C = CAP >> g.l1;
+        } else {
+            g.l1 = 0;
+            g.l2 = g.lt;
+            g.C = 1;
+        }
+        return g;
+    }
+    __host__ __device__ long long slots(int lattice) const {
+        return lattice ? (m > 0 ? (1ll << (m - 1)) : 1) : (1ll << m);
+    }
+    // position of lattice frequency k (0 <= k < n/2) in the slot layout
+    __host__ __device__ long long pos_of(long long k) const {
+        if (!two) return k;
+        const long long N1 = 1ll << l1;
+        return (k & (N1 - 1)) * (1ll << l2) + (k >> l1);
+    }
+};
+
+// --------------------------------------------------------------------- sources
+// Generator column of (pair, candidate) at transform-input index idx (lattice: DFT order,
+// digital: natural order), WITHOUT R and scale (those go to the spectrum epilogue).
+struct GenSrc {
+    Spatial sp;
+    PointGen pg;
+    const uint64_t* offs;   // [P][MAXD] pair offsets
+    const double* eta;      // [ncand][d]
+    const double* gamma;    // [ncand]
+    const int* vec_pair;    // [nvec_per_cand] -> global pair id
+    int nvpc;               // vectors per candidate in this launch
+
+    __device__ __forceinline__ void coords(int v, int& p, int& c) const {
+        c = v / nvpc;
+        p = vec_pair[v - c * nvpc];
+    }
+    __device__ __forceinline__ double kappa_all(int p, uint64_t idx, double* kappa) const {
+        const uint64_t* off = offs + size_t(p) * MAXD;
+        if (sp.family == 0) {
+#pragma unroll
+            for (int j = 0; j < MAXD; ++j)
+                if (j < sp.d) kappa[j] = si_base(pg.lattice_word(idx, j, __ldg(off + j)), sp.si_alpha);
+        } else {
+#pragma unroll
+            for (int j = 0; j < MAXD; ++j)
+                if (j < sp.d) kappa[j] = dsi_walsh(pg.digital_z(idx, j) ^ __ldg(off + j), sp.b);
+        }
+        return 0.0;
+    }
+    __device__ __forceinline__ double operator()(int v, uint64_t idx) const {
+        int p, c;
+        coords(v, p, c);
+        double kappa[MAXD];
+        kappa_all(p, idx, kappa);
+        return product_kernel<false>(kappa, eta + size_t(c) * sp.d, sp.d, __ldg(gamma + c), nullptr);
+    }
+};
+
+// Data vector gathered into transform order: lattice y(bitrev_m(j)) (V̄ = DFT o bitrev),
+// digital y(i).  src + vec_off[v] is the task's block.
+struct ArraySrc {
+    const double* src;
+    const long long* vec_off;  // [nvec]
+    int m;
+    int bitrev;
+    __device__ __forceinline__ double operator()(int v, uint64_t idx) const {
+        const uint64_t i = bitrev ? bitrev64(idx, m) : idx;
+        return __ldg(src + vec_off[v] + i);
+    }
+};
+
+// --------------------------------------------------------------------- forward sinks
+// lam = coef * A + xi, coef = R_ab * sqrt(n_b / n_a) (fast_gram.cpp:82-85).
+// Lattice slot 0 packs (A(0), A(n/2)): both real, both get + xi.
+struct SpecSink {
+    void* out;              // double2 (lattice) or double (digital)
+    const long long* voff;  // [nvec_per_cand] slot offset of each vector
+    long long cstride;      // slots per candidate
+    const double* coef;     // [ncand][nvpc]
+    const double* xi;       // [ncand][nvpc]
+    int nvpc;
+    __device__ __forceinline__ void put(int v, long long pos, double2 A) const {
+        const int c = v / nvpc, q = v - c * nvpc;
+        const double s = __ldg(coef + v), x = __ldg(xi + v);
+        double2* o = static_cast<double2*>(out) + c * cstride + voff[q] + pos;
+        *o = make_double2(fma(s, A.x, x), pos == 0 ? fma(s, A.y, x) : s * A.y);
+    }
+    __device__ __forceinline__ void put(int v, long long pos, double A) const {
+        const int c = v / nvpc, q = v - c * nvpc;
+        double* o = static_cast<double*>(out) + c * cstride + voff[q] + pos;
+        *o = fma(__ldg(coef + v), A, __ldg(xi + v));
+    }
+};
+
+struct ScaleSink {  // yhat = n^{-1/2} * transform
+    void* out;
+    const long long* voff;
+    double scale;
+    __device__ __forceinline__ void put(int v, long long pos, double2 A) const {
+        static_cast<double2*>(out)[voff[v] + pos] = cscale(A, scale);
+    }
+    __device__ __forceinline__ void put(int v, long long pos, double A) const {
+        static_cast<double*>(out)[voff[v] + pos] = A * scale;
+    }
+};
+
+// --------------------------------------------------------------------- inverse sinks
+// Gradient dot: for W = unnormalised inverse transform of M_ab (real), accumulate
+// sum_j W(j) * dq(j)/deta_k (k < d) and sum_j W(j) q(j) (slot d).  Lattice receives the
+// half-length complex z'(j): W(2j) = 2 Re z', W(2j+1) = 2 Im z'.
+struct GradSink {
+    GenSrc gen;
+    double* partial;  // [nvec][nblk][MAXD+1]
+    int nblk;
+    int acc_n;        // d + 1
+};
+
+// Coefficients c = V chat scattered to natural point order:
+//   lattice c(bitrev_m(j)) = sqrt(n) * IDFT_n(chat)(j):  c(bitrev(2j)) = s Re z'(j), ... with
+//   s = sqrt(n) / (n/2);  digital c = n^{-1/2} H chat.
+struct CoefSink {
+    double* out;
+    const long long* voff;  // [nvec] element offset of the task block
+    int m;
+    double scale;
+};
+
+// --------------------------------------------------------------------- helpers
+// Real-FFT post-processing: A(k) from Z(k), Z(N'-k); wk = exp(-2 pi i k / n).
+__device__ __forceinline__ double2 r2c_post(double2 Zk, double2 Zp, double2 wk) {
+    const double2 E = make_double2(0.5 * (Zk.x + Zp.x), 0.5 * (Zk.y - Zp.y));
+    const double2 D = make_double2(Zk.x - Zp.x, Zk.y + Zp.y);  // Zk - conj(Zp)
+    const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);     // -i D / 2
+    return cadd(E, cmul(wk, O));
+}
+// Inverse pre-processing: Z(k) from A(k), A(N'-k); wk = exp(-2 pi i k / n) (conjugated inside).
+__device__ __forceinline__ double2 c2r_pre(double2 Ak, double2 Ap, double2 wk) {
+    const double2 E = make_double2(0.5 * (Ak.x + Ap.x), 0.5 * (Ak.y - Ap.y));
+    const double2 D = make_double2(0.5 * (Ak.x - Ap.x), 0.5 * (Ak.y + Ap.y));
+    const double2 O = cmulc(D, wk);  // D * exp(+2 pi i k/n)
+    return make_double2(E.x - O.y, E.y + O.x);  // E + i O
+}
+
+}  // namespace fmtgp

@@ -1,0 +1,212 @@
+"""Host-side mirror of the reference's fast-Gram seam and GpModel hot path, on the B200
+C ABI (include/fastmtgp_b200.h).
+
+Reference interface followed (names, argument meaning, error behaviour):
+  fast_gram.hpp:34-70  build_spectrum / invert_and_logdet / solve / extract_pi_h /
+                       trace_inverse / gram_matvec  (SchurBreakdown vs FastMtgpError)
+  gp_core.hpp:46-83    refresh + loss_value (NMLL), posterior_mean_batch,
+                       posterior_cov (variance), multitask_cubature
+plus ``nll_grad``: the analytic hyperparameter gradient replacing the reference's
+central finite differences (gp_core.cpp:341-351).
+
+Inputs are in the reference's INTERNAL task order (descending n) — what the fast_gram
+functions take; GpModel's user<->internal mapping is the caller's (gp_core.cpp:19-32).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import CDesign, CHyper, CResult, FastMtgpError, SchurBreakdown, Unsupported, check, dptr  # noqa: F401
+from .designs import LATTICE, Design, Hyper
+
+
+def _cdesign(dz: Design):
+    keep = [np.ascontiguousarray(dz.m, dtype=np.int32), np.ascontiguousarray(dz.shift_bits, dtype=np.uint64)]
+    cd = CDesign(kind=dz.kind, d=dz.d, L=dz.L, m=keep[0].ctypes.data_as(_lib._ip),
+                 shift_bits=keep[1].ctypes.data_as(_lib._u64p))
+    if dz.kind == LATTICE:
+        g = np.ascontiguousarray(dz.g, dtype=np.uint64)
+        keep.append(g)
+        cd.g = g.ctypes.data_as(_lib._u64p)
+        cd.n_max = int(dz.n_max)
+    else:
+        cols = np.ascontiguousarray(dz.columns, dtype=np.uint64)
+        keep.append(cols)
+        cd.columns = cols.ctypes.data_as(_lib._u64p)
+        cd.m_cols = int(cols.shape[1])
+    return cd, keep
+
+
+def _chyper(hp: Hyper):
+    eta = np.ascontiguousarray(hp.eta, dtype=np.float64)
+    B = np.ascontiguousarray(hp.B, dtype=np.float64)
+    t = np.ascontiguousarray(hp.t, dtype=np.float64)
+    xi = np.ascontiguousarray(hp.xi, dtype=np.float64)
+    ch = CHyper(gamma=float(hp.gamma), eta=dptr(eta), si_alpha=int(hp.si_alpha), b=(C.c_double * 4)(*hp.b),
+                B=dptr(B), s=int(B.shape[1]), t=dptr(t), xi=dptr(xi))
+    return ch, (eta, B, t, xi)
+
+
+def _result(r: CResult, dz: Design, hp: Hyper) -> Dict:
+    L, d, s = dz.L, dz.d, hp.B.shape[1]
+    return dict(nll=r.nll, logdet=r.logdet, quad=r.quad, dgamma=r.dgamma,
+                deta=np.array(r.deta[:d]), dR=np.array(r.dR[:L * L]).reshape(L, L),
+                dB=np.array(r.dB[:L * s]).reshape(L, s), dt=np.array(r.dt[:L]), tau=np.array(r.tau[:L]),
+                xi_scale=r.xi_scale, escalations=r.escalations, status=r.status)
+
+
+class Model:
+    """Device-resident design + observations + workspace (one per GPU / dataset)."""
+
+    def __init__(self, design: Design, device: int = 0, max_candidates: int = 1):
+        self.lib = _lib.load()
+        self.design = design
+        self._cd, self._keep = _cdesign(design)
+        h = C.c_void_p()
+        check(self.lib.fmtgp_model_create(C.byref(self._cd), device, max_candidates, C.byref(h)))
+        self.h = h
+        self.hyper: Optional[Hyper] = None
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.fmtgp_model_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- data
+    def set_y(self, y: np.ndarray):
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        if y.shape != (self.design.N,):
+            raise FastMtgpError("make_model: observation size mismatch")
+        check(self.lib.fmtgp_model_set_y(self.h, dptr(y)))
+
+    def set_y_device(self, ptr: int):
+        check(self.lib.fmtgp_model_set_y_device(self.h, C.c_void_p(ptr)))
+
+    @property
+    def stream(self) -> int:
+        return self.lib.fmtgp_model_stream(self.h) or 0
+
+    # -- fast_gram.hpp seam
+    def build_spectrum(self, hp: Hyper):
+        ch, keep = _chyper(hp)
+        check(self.lib.fmtgp_build_spectrum(self.h, C.byref(ch)))
+        self.hyper = hp
+
+    def spectrum(self, l: int, lp: int) -> np.ndarray:
+        n = self.design.n[l]
+        re, im = np.empty(n), np.empty(n)
+        check(self.lib.fmtgp_spectrum_read(self.h, l, lp, dptr(re), dptr(im)))
+        return re + 1j * im
+
+    def invert_and_logdet(self) -> float:
+        v = C.c_double()
+        check(self.lib.fmtgp_invert_and_logdet(self.h, C.byref(v)))
+        return v.value
+
+    def solve(self, b: np.ndarray) -> np.ndarray:
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        if b.shape != (self.design.N,):
+            raise FastMtgpError("solve: length mismatch")
+        x = np.empty_like(b)
+        check(self.lib.fmtgp_solve(self.h, dptr(b), dptr(x)))
+        return x
+
+    def gram_matvec(self, b: np.ndarray) -> np.ndarray:
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        if b.shape != (self.design.N,):
+            raise FastMtgpError("gram_matvec: length mismatch")
+        x = np.empty_like(b)
+        check(self.lib.fmtgp_gram_matvec(self.h, dptr(b), dptr(x)))
+        return x
+
+    def extract_pi(self) -> np.ndarray:
+        L = self.design.L
+        Pi = np.empty((L, L))
+        check(self.lib.fmtgp_extract_pi(self.h, dptr(Pi)))
+        return Pi
+
+    def trace_inverse(self) -> float:
+        v = C.c_double()
+        check(self.lib.fmtgp_trace_inverse(self.h, C.byref(v)))
+        return v.value
+
+    # -- gp_core hot path
+    def nll(self, hp: Hyper, grad: bool = True) -> Dict:
+        """refresh + loss_value (NMLL) with escalation, plus the analytic gradient."""
+        ch, keep = _chyper(hp)
+        r = CResult()
+        check(self.lib.fmtgp_nll(self.h, C.byref(ch), int(grad), C.byref(r)))
+        self.hyper = hp
+        return _result(r, self.design, hp)
+
+    def nll_batch(self, hps: Sequence[Hyper], grad: bool = True) -> List[Dict]:
+        n = len(hps)
+        arr = (CHyper * n)()
+        keeps = []
+        for i, hp in enumerate(hps):
+            ch, keep = _chyper(hp)
+            arr[i] = ch
+            keeps.append(keep)
+        res = (CResult * n)()
+        check(self.lib.fmtgp_nll_batch(self.h, n, arr, int(grad), res))
+        return [_result(res[i], self.design, hps[i]) for i in range(n)]
+
+    def coefficients(self) -> np.ndarray:
+        c = np.empty(self.design.N)
+        check(self.lib.fmtgp_coefficients(self.h, dptr(c)))
+        return c
+
+    def posterior_mean(self, task: int, X: np.ndarray) -> np.ndarray:
+        X = np.ascontiguousarray(X, dtype=np.float64).reshape(-1, self.design.d)
+        out = np.empty(X.shape[0])
+        check(self.lib.fmtgp_posterior_mean(self.h, task, dptr(X), X.shape[0], dptr(out)))
+        return out
+
+    def posterior_var(self, task: int, X: np.ndarray) -> np.ndarray:
+        X = np.ascontiguousarray(X, dtype=np.float64).reshape(-1, self.design.d)
+        out = np.empty(X.shape[0])
+        check(self.lib.fmtgp_posterior_var(self.h, task, dptr(X), X.shape[0], dptr(out)))
+        return out
+
+    def cubature(self):
+        L = self.design.L
+        mu, S = np.empty(L), np.empty((L, L))
+        check(self.lib.fmtgp_cubature(self.h, dptr(mu), dptr(S)))
+        return mu, S
+
+
+# ---- free-function spelling of the seam (fast_gram.hpp:34-70) ---------------------------
+
+def build_spectrum(model: Model, hp: Hyper) -> Model:
+    model.build_spectrum(hp)
+    return model
+
+
+def invert_and_logdet(model: Model) -> float:
+    return model.invert_and_logdet()
+
+
+def solve(model: Model, y: np.ndarray) -> np.ndarray:
+    return model.solve(y)
+
+
+def extract_pi_h(model: Model) -> np.ndarray:
+    return model.extract_pi()
+
+
+def trace_inverse(model: Model) -> float:
+    return model.trace_inverse()
+
+
+def gram_matvec(model: Model, y: np.ndarray) -> np.ndarray:
+    return model.gram_matvec(y)
