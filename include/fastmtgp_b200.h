@@ -135,6 +135,13 @@ FMTGP_API int fmtgp_posterior_var(fmtgp_model_t model, int task, const double* X
 /* multitask_cubature (cubature.cpp:52-75): mu [L], Sigma [L * L] (internal order) */
 FMTGP_API int fmtgp_cubature(fmtgp_model_t model, double* mu, double* Sigma);
 
+/* ---- measurement: per-kernel CUDA-event timing on the model's stream ---------------- */
+FMTGP_API int fmtgp_profile_enable(fmtgp_model_t model, int on);  /* also resets the tallies */
+/* idx-th kernel name seen since enable, its summed device ms and launch count;
+ * FMTGP_ERR_INVALID past the last entry */
+FMTGP_API int fmtgp_profile_read(fmtgp_model_t model, int idx, char* name, int name_len, double* total_ms,
+                                 int* launches);
+
 #ifdef __cplusplus
 }
 #endif

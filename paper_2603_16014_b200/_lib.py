@@ -80,6 +80,8 @@ _SIGS = {
     "fmtgp_posterior_mean": (C.c_int, [C.c_void_p, C.c_int, _dp, C.c_int64, _dp]),
     "fmtgp_posterior_var": (C.c_int, [C.c_void_p, C.c_int, _dp, C.c_int64, _dp]),
     "fmtgp_cubature": (C.c_int, [C.c_void_p, _dp, _dp]),
+    "fmtgp_profile_enable": (C.c_int, [C.c_void_p, C.c_int]),
+    "fmtgp_profile_read": (C.c_int, [C.c_void_p, C.c_int, C.c_char_p, C.c_int, _dp, _ip]),
 }
 
 EXPORTED = sorted(_SIGS)

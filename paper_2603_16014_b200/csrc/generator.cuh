@@ -86,6 +86,25 @@ __device__ __forceinline__ double dsi_order(uint64_t w, int alpha) {
     }
 }
 
+// Order-4 with X3 from an 8-bit table T8[b] = sum_i bit(7-i of b) 8^-i (exact 24-bit values):
+// X3 = 2^(-3 beta) (T8[b0] + 2^-24 (T8[b1] + 2^-24 T8[b2])) over the three leading bytes of
+// the normalised word — same value as the set-bit loop of kernels.cpp:69-75 to ~1 ulp.
+__device__ __forceinline__ double dsi_order4_t8(uint64_t w, const double* __restrict__ T8) {
+    w &= MASK53;
+    if (w == 0) return 407.0 / 294.0;
+    const int clz = __clzll((long long)w);
+    const int beta = clz - 10;  // 53 - (63 - clz)
+    const double u = double(w) * 0x1p-53;
+    const double t1 = pow2i(-beta);
+    const double t2 = t1 * t1, t3 = t2 * t1;
+    const double db = double(beta);
+    const uint64_t top = w << clz;
+    const double x3s = fma(fma(T8[(top >> 40) & 255], 0x1p-24, T8[(top >> 48) & 255]), 0x1p-24, T8[top >> 56]);
+    const double x3 = x3s * pow2i(-3 * beta);
+    return -1.0 - (2.0 / 3.0) * db * u * u * u + 5.0 * (1.0 - t1) * u * u - (43.0 / 9.0) * (1.0 - t2) * u +
+           (701.0 / 294.0) * (1.0 - t3) - db * x3 / 3.0;
+}
+
 __device__ __forceinline__ double dsi_walsh(uint64_t w, const double* b) {
     double acc = 0.0;
 #pragma unroll
@@ -149,6 +168,34 @@ __device__ __forceinline__ double product_kernel(const double* kappa, const doub
                 dq_deta[j] *= suf;
                 suf *= f[j];
             }
+    }
+    return prod;
+}
+
+// Compile-time-dimension product kernel (register-resident, no MAXD padding).
+template <int D, bool GRAD>
+__device__ __forceinline__ double product_kernel_d(const double* kappa, const double* eta, double gamma,
+                                                   double* dq_deta) {
+    double f[D];
+    double prod = gamma;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        f[j] = 1.0 + eta[j] * kappa[j];
+        prod *= f[j];
+    }
+    if (GRAD) {
+        double pre = gamma;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            dq_deta[j] = pre * kappa[j];
+            pre *= f[j];
+        }
+        double suf = 1.0;
+#pragma unroll
+        for (int j = D - 1; j >= 0; --j) {
+            dq_deta[j] *= suf;
+            suf *= f[j];
+        }
     }
     return prod;
 }

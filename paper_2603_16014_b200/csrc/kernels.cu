@@ -1,10 +1,15 @@
 // Device kernels of the fast-MTGP fit path (sm_100a, fp64).  See passes.cuh for the
 // transform conventions and kernels.cuh for the launch API.
 #include <climits>
+#include <mutex>
+#include <utility>
+#include <vector>
 
 #include "kernels.cuh"
 
 namespace fmtgp {
+
+thread_local Profiler* g_prof = nullptr;
 
 // ============================================================================ twiddles
 __global__ void k_init_twiddles(double2* tab) {
@@ -22,15 +27,9 @@ void init_twiddles(double2* tab, cudaStream_t s) {
     k_init_twiddles<<<dim3(32, 27), 256, 0, s>>>(tab);
 }
 
-// ============================================================================ generic sink glue
-template <class Snk>
-__device__ __forceinline__ void sink_put(const Snk& s, int v, long long pos, double2 A) { s.put(v, pos, A); }
-template <class Snk>
-__device__ __forceinline__ void sink_put(const Snk& s, int v, long long pos, double A) { s.put(v, pos, A); }
-
 // ============================================================================ forward, single CTA
-template <class Src, class Snk>
-__global__ void __launch_bounds__(NT_T) k_fwd_small_lat(Src src, Snk snk, int m, const double2* __restrict__ tw) {
+template <int NT, class Src, class Snk>
+__global__ void __launch_bounds__(NT) k_fwd_small_lat(Src src, Snk snk, int m, const double2* __restrict__ tw) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double2* sm = reinterpret_cast<double2*>(smraw);
     const int v = blockIdx.x;
@@ -39,10 +38,10 @@ __global__ void __launch_bounds__(NT_T) k_fwd_small_lat(Src src, Snk snk, int m,
         return;
     }
     const int lp = m - 1, Np = 1 << lp;
-    for (int e = threadIdx.x; e < Np; e += NT_T) sm[e] = make_double2(src(v, 2ull * e), src(v, 2ull * e + 1));
+    for (int e = threadIdx.x; e < Np; e += NT) sm[e] = make_double2(src(v, 2ull * e), src(v, 2ull * e + 1));
     __syncthreads();
-    smem_fft<NT_T>(sm, lp, 1, Np, -1, tw);
-    for (int k = threadIdx.x; k <= Np / 2; k += NT_T) {
+    smem_fft<NT>(sm, lp, 1, Np, -1, tw);
+    for (int k = threadIdx.x; k <= Np / 2; k += NT) {
         if (k == 0) {
             const double2 Z0 = sm[0];
             snk.put(v, 0, make_double2(Z0.x + Z0.y, Z0.x - Z0.y));
@@ -55,55 +54,55 @@ __global__ void __launch_bounds__(NT_T) k_fwd_small_lat(Src src, Snk snk, int m,
     }
 }
 
-template <class Src, class Snk>
-__global__ void __launch_bounds__(NT_T) k_fwd_small_dig(Src src, Snk snk, int m) {
+template <int NT, class Src, class Snk>
+__global__ void __launch_bounds__(NT) k_fwd_small_dig(Src src, Snk snk, int m) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double* sm = reinterpret_cast<double*>(smraw);
     const int v = blockIdx.x, n = 1 << m;
-    for (int e = threadIdx.x; e < n; e += NT_T) sm[e] = src(v, e);
+    for (int e = threadIdx.x; e < n; e += NT) sm[e] = src(v, e);
     __syncthreads();
-    smem_wht<NT_T>(sm, m, 1, n);
-    for (int e = threadIdx.x; e < n; e += NT_T) snk.put(v, e, sm[e]);
+    smem_wht<NT>(sm, m, 1, n);
+    for (int e = threadIdx.x; e < n; e += NT) snk.put(v, e, sm[e]);
 }
 
 // ============================================================================ forward, two pass
-template <class Src>
-__global__ void __launch_bounds__(NT_T) k_fwd_col_lat(Src src, double2* __restrict__ Y, int l1, int l2, int lc,
-                                                      long long vstride, const double2* __restrict__ tw) {
+template <int NT, class Src>
+__global__ void __launch_bounds__(NT) k_fwd_col_lat(Src src, double2* __restrict__ Y, int l1, int l2, int lc,
+                                                    long long vstride, const double2* __restrict__ tw) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double2* sm = reinterpret_cast<double2*>(smraw);
     const int v = blockIdx.y, C = 1 << lc, N1 = 1 << l1;
     const long long c0 = (long long)blockIdx.x << lc;
-    for (int e = threadIdx.x; e < (C << l1); e += NT_T) {
+    for (int e = threadIdx.x; e < (C << l1); e += NT) {
         const int j1 = e >> lc, c = e & (C - 1);
         const uint64_t j = (uint64_t(j1) << l2) + c0 + c;
         sm[c * N1 + j1] = make_double2(src(v, 2 * j), src(v, 2 * j + 1));
     }
     __syncthreads();
-    smem_fft<NT_T>(sm, l1, C, N1, -1, tw);
+    smem_fft<NT>(sm, l1, C, N1, -1, tw);
     double2* out = Y + v * vstride;
-    for (int e = threadIdx.x; e < (C << l1); e += NT_T) {
+    for (int e = threadIdx.x; e < (C << l1); e += NT) {
         const int k1 = e >> lc, c = e & (C - 1);
         const uint64_t j2 = c0 + c;
         out[((long long)k1 << l2) + j2] = cmul(sm[c * N1 + k1], twiddle(tw, j2 * uint64_t(k1), l1 + l2));
     }
 }
 
-template <class Src>
-__global__ void __launch_bounds__(NT_T) k_fwd_col_dig(Src src, double* __restrict__ Y, int l1, int l2, int lc,
-                                                      long long vstride) {
+template <int NT, class Src>
+__global__ void __launch_bounds__(NT) k_fwd_col_dig(Src src, double* __restrict__ Y, int l1, int l2, int lc,
+                                                    long long vstride) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double* sm = reinterpret_cast<double*>(smraw);
     const int v = blockIdx.y, C = 1 << lc, N1 = 1 << l1;
     const long long c0 = (long long)blockIdx.x << lc;
-    for (int e = threadIdx.x; e < (C << l1); e += NT_T) {
+    for (int e = threadIdx.x; e < (C << l1); e += NT) {
         const int j1 = e >> lc, c = e & (C - 1);
         sm[c * N1 + j1] = src(v, (uint64_t(j1) << l2) + c0 + c);
     }
     __syncthreads();
-    smem_wht<NT_T>(sm, l1, C, N1);
+    smem_wht<NT>(sm, l1, C, N1);
     double* out = Y + v * vstride;
-    for (int e = threadIdx.x; e < (C << l1); e += NT_T) {
+    for (int e = threadIdx.x; e < (C << l1); e += NT) {
         const int k1 = e >> lc, c = e & (C - 1);
         out[((long long)k1 << l2) + c0 + c] = sm[c * N1 + k1];
     }
@@ -114,8 +113,8 @@ __device__ __forceinline__ int row_of_cluster(int q, int rank, int N1) {
     return rank == 0 ? q : N1 - q;
 }
 
-template <class Snk>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT_T)
+template <int NT, class Snk>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT)
     k_fwd_row_lat(const double2* __restrict__ Y, Snk snk, int l1, int l2, long long vstride, int m,
                   const double2* __restrict__ tw) {
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -126,13 +125,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT_T)
     const int N1 = 1 << l1, N2 = 1 << l2;
     const int row = row_of_cluster(q, rank, N1);
     const double2* in = Y + v * vstride + ((long long)row << l2);
-    for (int e = threadIdx.x; e < N2; e += NT_T) sm[e] = in[e];
+    for (int e = threadIdx.x; e < N2; e += NT) sm[e] = in[e];
     __syncthreads();
-    smem_fft<NT_T>(sm, l2, 1, N2, -1, tw);
+    smem_fft<NT>(sm, l2, 1, N2, -1, tw);
     cl.sync();
     const bool self = (row == 0) || (row == N1 / 2);
     const double2* psm = self ? sm : cl.map_shared_rank(sm, rank ^ 1);
-    for (int k2 = threadIdx.x; k2 < N2; k2 += NT_T) {
+    for (int k2 = threadIdx.x; k2 < N2; k2 += NT) {
         const long long k = row + ((long long)k2 << l1);
         if (k == 0) {
             const double2 Z0 = sm[0];
@@ -145,18 +144,150 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT_T)
     cl.sync();
 }
 
-template <class Snk>
-__global__ void __launch_bounds__(NT_T) k_fwd_row_dig(const double* __restrict__ Y, Snk snk, int l2,
-                                                      long long vstride) {
+template <int NT, class Snk>
+__global__ void __launch_bounds__(NT) k_fwd_row_dig(const double* __restrict__ Y, Snk snk, int l2, long long vstride) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double* sm = reinterpret_cast<double*>(smraw);
     const int row = blockIdx.x, v = blockIdx.y, N2 = 1 << l2;
     const double* in = Y + v * vstride + ((long long)row << l2);
-    for (int e = threadIdx.x; e < N2; e += NT_T) sm[e] = in[e];
+    for (int e = threadIdx.x; e < N2; e += NT) sm[e] = in[e];
     __syncthreads();
-    smem_wht<NT_T>(sm, l2, 1, N2);
-    for (int e = threadIdx.x; e < N2; e += NT_T) snk.put(v, ((long long)row << l2) + e, sm[e]);
+    smem_wht<NT>(sm, l2, 1, N2);
+    for (int e = threadIdx.x; e < N2; e += NT) snk.put(v, ((long long)row << l2) + e, sm[e]);
 }
+
+// ============================================================================ generator / gradient-dot (split mode)
+// One element per thread per sweep: for small problems the generator, not the transform,
+// sets the parallelism.  Compile-time dimension D keeps kappa / dq / accumulators in
+// registers.  Digital z_i comes from two 32-entry XOR tables per dimension in smem, X3 of
+// the order-4 Walsh kernel from an 8-bit table.
+template <int D>
+struct GenSmem {
+    uint64_t lo[D][32], mid[D][32];
+    double T8[256];
+    double eta[D];
+};
+
+template <int D>
+__device__ __forceinline__ void gen_smem_init(GenSmem<D>& t, const GenSrc& g, int c) {
+    if (g.sp.family == 1) {
+        for (int e = threadIdx.x; e < D * 64; e += blockDim.x) {
+            const int j = e >> 6, r = e & 63;
+            const int shift = r < 32 ? 0 : 5;
+            const int val = r & 31;
+            uint64_t z = 0;
+            const uint64_t* col = g.pg.cols + size_t(j) * g.pg.m_cols;
+            for (int p = 0; p < 5; ++p)
+                if (((val >> p) & 1) && p + shift < g.pg.m_cols) z ^= __ldg(col + p + shift);
+            if (r < 32) t.lo[j][val] = z;
+            else t.mid[j][val] = z;
+        }
+        for (int b = threadIdx.x; b < 256; b += blockDim.x) {
+            double acc = 0.0;
+            for (int i = 7; i >= 0; --i)  // smallest terms first
+                if ((b >> (7 - i)) & 1) acc += pow2i(-3 * i);
+            t.T8[b] = acc;
+        }
+    }
+    for (int j = threadIdx.x; j < D; j += blockDim.x) t.eta[j] = g.eta[size_t(c) * D + j];
+}
+
+template <int D>
+__device__ __forceinline__ void kappa_d(const GenSrc& g, const GenSmem<D>& t, const uint64_t* off, uint64_t idx,
+                                        double* kappa) {
+    if (g.sp.family == 0) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) kappa[j] = si_base(g.pg.lattice_word(idx, j, off[j]), g.sp.si_alpha);
+        return;
+    }
+    const uint64_t hi = idx >> 10;
+    const bool only4 = g.sp.b[0] == 0.0 && g.sp.b[1] == 0.0 && g.sp.b[2] == 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        uint64_t z = t.lo[j][idx & 31] ^ t.mid[j][(idx >> 5) & 31];
+        if (hi) {
+            const uint64_t* col = g.pg.cols + size_t(j) * g.pg.m_cols + 10;
+            uint64_t h = hi;
+            for (int q = 0; h; ++q, h >>= 1)
+                if (h & 1) z ^= __ldg(col + q);
+        }
+        const uint64_t w = z ^ off[j];
+        kappa[j] = only4 ? g.sp.b[3] * dsi_order4_t8(w, t.T8) : dsi_walsh(w, g.sp.b);
+    }
+}
+
+constexpr int GEN_NT = 256;
+constexpr int GEN_EPT = 4;  // elements per thread per block (dot kernel partial count)
+
+// out[v][idx] = gamma prod_j (1 + eta_j kappa_j) in transform-input order
+template <int D>
+__global__ void __launch_bounds__(GEN_NT) k_gen_fill(GenSrc g, double* __restrict__ out, long long n) {
+    __shared__ GenSmem<D> t;
+    const int v = blockIdx.y;
+    int p, c;
+    g.coords(v, p, c);
+    gen_smem_init<D>(t, g, c);
+    uint64_t off[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) off[j] = __ldg(g.offs + size_t(p) * MAXD + j);
+    const double gam = __ldg(g.gamma + c);
+    __syncthreads();
+    for (long long idx = blockIdx.x * (long long)GEN_NT + threadIdx.x; idx < n; idx += (long long)gridDim.x * GEN_NT) {
+        double kappa[D];
+        kappa_d<D>(g, t, off, idx, kappa);
+        out[v * n + idx] = product_kernel_d<D, false>(kappa, t.eta, gam, nullptr);
+    }
+}
+
+// partial[v][blk][.] = sum_idx W(idx) * (dq/deta_j, q)  (W already in transform-input order)
+template <int D>
+__global__ void __launch_bounds__(GEN_NT) k_gen_dot(GradSink gs, const double* __restrict__ W, long long n) {
+    __shared__ GenSmem<D> t;
+    __shared__ double red[32];
+    const GenSrc& g = gs.gen;
+    const int v = blockIdx.y;
+    int p, c;
+    g.coords(v, p, c);
+    gen_smem_init<D>(t, g, c);
+    uint64_t off[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) off[j] = __ldg(g.offs + size_t(p) * MAXD + j);
+    const double gam = __ldg(g.gamma + c);
+    __syncthreads();
+    double acc[D + 1];
+#pragma unroll
+    for (int j = 0; j <= D; ++j) acc[j] = 0.0;
+    for (long long idx = blockIdx.x * (long long)GEN_NT + threadIdx.x; idx < n; idx += (long long)gridDim.x * GEN_NT) {
+        double kappa[D], dq[D];
+        kappa_d<D>(g, t, off, idx, kappa);
+        const double q = product_kernel_d<D, true>(kappa, t.eta, gam, dq);
+        const double w = W[v * n + idx];
+#pragma unroll
+        for (int j = 0; j < D; ++j) acc[j] = fma(w, dq[j], acc[j]);
+        acc[D] = fma(w, q, acc[D]);
+    }
+    double* out = gs.partial + ((size_t)v * gs.nblk + blockIdx.x) * (MAXD + 1);
+#pragma unroll
+    for (int j = 0; j <= D; ++j) {
+        const double s = block_sum<GEN_NT>(acc[j], red);
+        if (threadIdx.x == 0) out[j == D ? MAXD : j] = s;
+    }
+}
+
+#define FM_D_DISPATCH(d, ...)                                                                          \
+    switch (d) {                                                                                       \
+        FM_D_CASE(1, __VA_ARGS__) FM_D_CASE(2, __VA_ARGS__) FM_D_CASE(3, __VA_ARGS__)                  \
+        FM_D_CASE(4, __VA_ARGS__) FM_D_CASE(5, __VA_ARGS__) FM_D_CASE(6, __VA_ARGS__)                  \
+        FM_D_CASE(7, __VA_ARGS__) FM_D_CASE(8, __VA_ARGS__) FM_D_CASE(9, __VA_ARGS__)                  \
+        FM_D_CASE(10, __VA_ARGS__) FM_D_CASE(11, __VA_ARGS__) FM_D_CASE(12, __VA_ARGS__)               \
+        FM_D_CASE(13, __VA_ARGS__) FM_D_CASE(14, __VA_ARGS__) FM_D_CASE(15, __VA_ARGS__)               \
+        FM_D_CASE(16, __VA_ARGS__) default : break;                                                    \
+    }
+#define FM_D_CASE(V, ...)    \
+    case V: {                \
+        constexpr int D = V; \
+        __VA_ARGS__;         \
+    } break;
 
 // ============================================================================ inverse sinks (device side)
 struct GradAcc {
@@ -180,6 +311,7 @@ __device__ __forceinline__ void grad_add(const GradSink& gs, int v, uint64_t idx
     acc.a[MAXD] = fma(W, q, acc.a[MAXD]);
 }
 
+template <int NT>
 __device__ void grad_flush(const GradSink& gs, int v, int blk, GradAcc& acc) {
     __shared__ double red[32];
     const int d = gs.gen.sp.d;
@@ -187,13 +319,13 @@ __device__ void grad_flush(const GradSink& gs, int v, int blk, GradAcc& acc) {
 #pragma unroll
     for (int j = 0; j <= MAXD; ++j) {
         if (j < d || j == MAXD) {
-            const double s = block_sum<NT_T>(acc.a[j], red);
+            const double s = block_sum<NT>(acc.a[j], red);
             if (threadIdx.x == 0) out[j] = s;
         }
     }
 }
 
-struct SinkGrad {  // adapts GradSink to the inverse kernels
+struct SinkGrad {  // fused dot (large problems)
     GradSink gs;
     int lattice, m;
     __device__ __forceinline__ void lat(int v, uint64_t j, double2 z, GradAcc& acc) const {
@@ -205,7 +337,28 @@ struct SinkGrad {  // adapts GradSink to the inverse kernels
         grad_add(gs, v, 2 * j + 1, 2.0 * z.y, acc);
     }
     __device__ __forceinline__ void dig(int v, uint64_t j, double w, GradAcc& acc) const { grad_add(gs, v, j, w, acc); }
-    __device__ __forceinline__ void flush(int v, int blk, GradAcc& acc) const { grad_flush(gs, v, blk, acc); }
+    template <int NT>
+    __device__ __forceinline__ void flush(int v, int blk, GradAcc& acc) const {
+        grad_flush<NT>(gs, v, blk, acc);
+    }
+};
+
+struct SinkStoreW {  // W in transform-input order for k_gen_dot (small problems)
+    double* W;
+    long long n;
+    int m;
+    __device__ __forceinline__ void lat(int v, uint64_t j, double2 z, GradAcc&) const {
+        double* o = W + v * n;
+        if (m == 0) {
+            o[0] = z.x;
+            return;
+        }
+        o[2 * j] = 2.0 * z.x;
+        o[2 * j + 1] = 2.0 * z.y;
+    }
+    __device__ __forceinline__ void dig(int v, uint64_t j, double w, GradAcc&) const { W[v * n + j] = w; }
+    template <int NT>
+    __device__ __forceinline__ void flush(int, int, GradAcc&) const {}
 };
 
 struct SinkCoef {
@@ -223,14 +376,15 @@ struct SinkCoef {
     __device__ __forceinline__ void dig(int v, uint64_t j, double w, GradAcc&) const {
         cs.out[cs.voff[v] + j] = w * cs.scale;
     }
+    template <int NT>
     __device__ __forceinline__ void flush(int, int, GradAcc&) const {}
 };
 
 // ============================================================================ inverse, single CTA
-template <class Snk>
-__global__ void __launch_bounds__(NT_T) k_inv_small_lat(const double2* __restrict__ in, const long long* in_off,
-                                                        long long cstride, int nvpc, Snk snk, int m,
-                                                        const double2* __restrict__ tw) {
+template <int NT, class Snk>
+__global__ void __launch_bounds__(NT) k_inv_small_lat(const double2* __restrict__ in, const long long* in_off,
+                                                      long long cstride, int nvpc, Snk snk, int m,
+                                                      const double2* __restrict__ tw) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double2* sm = reinterpret_cast<double2*>(smraw);
     const int v = blockIdx.x;
@@ -240,11 +394,11 @@ __global__ void __launch_bounds__(NT_T) k_inv_small_lat(const double2* __restric
     acc.zero();
     if (m == 0) {
         if (threadIdx.x == 0) snk.lat(v, 0, x[0], acc);
-        snk.flush(v, 0, acc);
+        snk.template flush<NT>(v, 0, acc);
         return;
     }
     const int lp = m - 1, Np = 1 << lp;
-    for (int k = threadIdx.x; k <= Np / 2; k += NT_T) {
+    for (int k = threadIdx.x; k <= Np / 2; k += NT) {
         if (k == 0) {
             const double2 A = x[0];
             sm[0] = make_double2(0.5 * (A.x + A.y), 0.5 * (A.x - A.y));
@@ -256,30 +410,31 @@ __global__ void __launch_bounds__(NT_T) k_inv_small_lat(const double2* __restric
         if (kp != k) sm[kp] = c2r_pre(Ap, Ak, twiddle(tw, kp, m));
     }
     __syncthreads();
-    smem_fft<NT_T>(sm, lp, 1, Np, +1, tw);
-    for (int j = threadIdx.x; j < Np; j += NT_T) snk.lat(v, j, sm[j], acc);
-    snk.flush(v, 0, acc);
+    smem_fft<NT>(sm, lp, 1, Np, +1, tw);
+    for (int j = threadIdx.x; j < Np; j += NT) snk.lat(v, j, sm[j], acc);
+    snk.template flush<NT>(v, 0, acc);
 }
 
-template <class Snk>
-__global__ void __launch_bounds__(NT_T) k_inv_small_dig(const double* __restrict__ in, const long long* in_off,
-                                                        long long cstride, int nvpc, Snk snk, int m) {
+template <int NT, class Snk>
+__global__ void __launch_bounds__(NT) k_inv_small_dig(const double* __restrict__ in, const long long* in_off,
+                                                      long long cstride, int nvpc, Snk snk, int m) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double* sm = reinterpret_cast<double*>(smraw);
     const int v = blockIdx.x, n = 1 << m;
     const int c = v / nvpc;
     const double* x = in + c * cstride + in_off[v - c * nvpc];
-    for (int e = threadIdx.x; e < n; e += NT_T) sm[e] = x[e];
+    for (int e = threadIdx.x; e < n; e += NT) sm[e] = x[e];
     __syncthreads();
-    smem_wht<NT_T>(sm, m, 1, n);
+    smem_wht<NT>(sm, m, 1, n);
     GradAcc acc;
     acc.zero();
-    for (int e = threadIdx.x; e < n; e += NT_T) snk.dig(v, e, sm[e], acc);
-    snk.flush(v, 0, acc);
+    for (int e = threadIdx.x; e < n; e += NT) snk.dig(v, e, sm[e], acc);
+    snk.template flush<NT>(v, 0, acc);
 }
 
 // ============================================================================ inverse, two pass
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT_T)
+template <int NT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT)
     k_inv_row_lat(const double2* __restrict__ in, const long long* in_off, long long cstride, int nvpc,
                   double2* __restrict__ U, long long vstride, int l1, int l2, int m, const double2* __restrict__ tw) {
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -291,14 +446,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT_T)
     const int row = row_of_cluster(q, rank, N1);
     const int c = v / nvpc;
     const double2* x = in + c * cstride + in_off[v - c * nvpc] + ((long long)row << l2);
-    for (int e = threadIdx.x; e < N2; e += NT_T) sm[e] = x[e];
+    for (int e = threadIdx.x; e < N2; e += NT) sm[e] = x[e];
     cl.sync();
     const bool self = (row == 0) || (row == N1 / 2);
     const double2* psm = self ? sm : cl.map_shared_rank(sm, rank ^ 1);
     double2 zr[EPT];
 #pragma unroll
     for (int t = 0; t < EPT; ++t) {
-        const int k2 = threadIdx.x + t * NT_T;
+        const int k2 = threadIdx.x + t * NT;
         if (k2 < N2) {
             const long long k = row + ((long long)k2 << l1);
             if (k == 0) {
@@ -313,179 +468,274 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT_T)
     cl.sync();
 #pragma unroll
     for (int t = 0; t < EPT; ++t) {
-        const int k2 = threadIdx.x + t * NT_T;
+        const int k2 = threadIdx.x + t * NT;
         if (k2 < N2) sm[k2] = zr[t];
     }
     __syncthreads();
-    smem_fft<NT_T>(sm, l2, 1, N2, +1, tw);
+    smem_fft<NT>(sm, l2, 1, N2, +1, tw);
     double2* out = U + v * vstride + ((long long)row << l2);
-    for (int j2 = threadIdx.x; j2 < N2; j2 += NT_T)
+    for (int j2 = threadIdx.x; j2 < N2; j2 += NT)
         out[j2] = cmulc(sm[j2], twiddle(tw, uint64_t(j2) * uint64_t(row), l1 + l2));
 }
 
-__global__ void __launch_bounds__(NT_T) k_inv_row_dig(const double* __restrict__ in, const long long* in_off,
-                                                      long long cstride, int nvpc, double* __restrict__ U,
-                                                      long long vstride, int l2) {
+template <int NT>
+__global__ void __launch_bounds__(NT) k_inv_row_dig(const double* __restrict__ in, const long long* in_off,
+                                                    long long cstride, int nvpc, double* __restrict__ U,
+                                                    long long vstride, int l2) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double* sm = reinterpret_cast<double*>(smraw);
     const int row = blockIdx.x, v = blockIdx.y, N2 = 1 << l2;
     const int c = v / nvpc;
     const double* x = in + c * cstride + in_off[v - c * nvpc] + ((long long)row << l2);
-    for (int e = threadIdx.x; e < N2; e += NT_T) sm[e] = x[e];
+    for (int e = threadIdx.x; e < N2; e += NT) sm[e] = x[e];
     __syncthreads();
-    smem_wht<NT_T>(sm, l2, 1, N2);
+    smem_wht<NT>(sm, l2, 1, N2);
     double* out = U + v * vstride + ((long long)row << l2);
-    for (int e = threadIdx.x; e < N2; e += NT_T) out[e] = sm[e];
+    for (int e = threadIdx.x; e < N2; e += NT) out[e] = sm[e];
 }
 
-template <class Snk>
-__global__ void __launch_bounds__(NT_T) k_inv_col_lat(const double2* __restrict__ U, long long vstride, Snk snk,
-                                                      int l1, int l2, int lc, const double2* __restrict__ tw) {
+template <int NT, class Snk>
+__global__ void __launch_bounds__(NT) k_inv_col_lat(const double2* __restrict__ U, long long vstride, Snk snk, int l1,
+                                                    int l2, int lc, const double2* __restrict__ tw) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double2* sm = reinterpret_cast<double2*>(smraw);
     const int v = blockIdx.y, C = 1 << lc, N1 = 1 << l1;
     const long long c0 = (long long)blockIdx.x << lc;
     const double2* x = U + v * vstride;
-    for (int e = threadIdx.x; e < (C << l1); e += NT_T) {
+    for (int e = threadIdx.x; e < (C << l1); e += NT) {
         const int k1 = e >> lc, c = e & (C - 1);
         sm[c * N1 + k1] = x[((long long)k1 << l2) + c0 + c];
     }
     __syncthreads();
-    smem_fft<NT_T>(sm, l1, C, N1, +1, tw);
+    smem_fft<NT>(sm, l1, C, N1, +1, tw);
     GradAcc acc;
     acc.zero();
-    for (int e = threadIdx.x; e < (C << l1); e += NT_T) {
+    for (int e = threadIdx.x; e < (C << l1); e += NT) {
         const int j1 = e >> lc, c = e & (C - 1);
         const uint64_t j = (uint64_t(j1) << l2) + c0 + c;
         snk.lat(v, j, sm[c * N1 + j1], acc);
     }
-    snk.flush(v, blockIdx.x, acc);
+    snk.template flush<NT>(v, blockIdx.x, acc);
 }
 
-template <class Snk>
-__global__ void __launch_bounds__(NT_T) k_inv_col_dig(const double* __restrict__ U, long long vstride, Snk snk,
-                                                      int l1, int l2, int lc) {
+template <int NT, class Snk>
+__global__ void __launch_bounds__(NT) k_inv_col_dig(const double* __restrict__ U, long long vstride, Snk snk, int l1,
+                                                    int l2, int lc) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double* sm = reinterpret_cast<double*>(smraw);
     const int v = blockIdx.y, C = 1 << lc, N1 = 1 << l1;
     const long long c0 = (long long)blockIdx.x << lc;
     const double* x = U + v * vstride;
-    for (int e = threadIdx.x; e < (C << l1); e += NT_T) {
+    for (int e = threadIdx.x; e < (C << l1); e += NT) {
         const int k1 = e >> lc, c = e & (C - 1);
         sm[c * N1 + k1] = x[((long long)k1 << l2) + c0 + c];
     }
     __syncthreads();
-    smem_wht<NT_T>(sm, l1, C, N1);
+    smem_wht<NT>(sm, l1, C, N1);
     GradAcc acc;
     acc.zero();
-    for (int e = threadIdx.x; e < (C << l1); e += NT_T) {
+    for (int e = threadIdx.x; e < (C << l1); e += NT) {
         const int j1 = e >> lc, c = e & (C - 1);
         snk.dig(v, (uint64_t(j1) << l2) + c0 + c, sm[c * N1 + j1], acc);
     }
-    snk.flush(v, blockIdx.x, acc);
+    snk.template flush<NT>(v, blockIdx.x, acc);
 }
 
 // ============================================================================ launchers
-static size_t smem_bytes(int lattice) { return size_t(CAP) * (lattice ? sizeof(double2) : sizeof(double)); }
-
+// Opt a kernel into > 48 KB dynamic smem once (host call; kept out of graph captures).
 template <class K>
 static void set_smem(K kern, size_t bytes) {
-    static_assert(sizeof(K) > 0, "");
+    static std::mutex mu;
+    static std::vector<std::pair<const void*, size_t>> done;
+    std::lock_guard<std::mutex> lock(mu);
+    const void* key = reinterpret_cast<const void*>(kern);
+    for (auto& e : done)
+        if (e.first == key && e.second >= bytes) return;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+    done.push_back({key, bytes});
 }
+
+// threads for a tile of 2^tl elements (EPT per thread), 32..512
+static int nt_for(int tl) {
+    int nt = 1 << (tl > 4 ? tl - 4 : 0);
+    return nt < 32 ? 32 : (nt > 512 ? 512 : nt);
+}
+
+#define FM_NT_CASE(V, ...)     \
+    case V: {                  \
+        constexpr int NT = V;  \
+        __VA_ARGS__;           \
+    } break;
+#define FM_NT_DISPATCH(nt, ...)                                                                      \
+    switch (nt) {                                                                                    \
+        FM_NT_CASE(32, __VA_ARGS__) FM_NT_CASE(64, __VA_ARGS__) FM_NT_CASE(128, __VA_ARGS__)         \
+        FM_NT_CASE(256, __VA_ARGS__) default : {                                                      \
+            constexpr int NT = 512;                                                                  \
+            __VA_ARGS__;                                                                             \
+        }                                                                                            \
+        break;                                                                                       \
+    }
 
 template <class Src, class Snk>
 static void fwd_impl(int lattice, const Geo& g, int nvec, const Src& src, const Snk& snk, void* work,
                      const double2* tw, cudaStream_t s) {
-    const size_t sm = smem_bytes(lattice);
+    const size_t es = lattice ? sizeof(double2) : sizeof(double);
     if (!g.two) {
+        const size_t sm = (size_t(1) << g.lt) * es;
+        const int nt = nt_for(g.lt);
         if (lattice) {
-            auto k = k_fwd_small_lat<Src, Snk>;
-            set_smem(k, sm);
-            k<<<nvec, NT_T, sm, s>>>(src, snk, g.m, tw);
+            FM_NT_DISPATCH(nt, {
+                auto k = k_fwd_small_lat<NT, Src, Snk>;
+                set_smem(k, sm);
+                ProfScope ps("fwd_small_lat", s);
+                k<<<nvec, NT, sm, s>>>(src, snk, g.m, tw);
+            })
         } else {
-            auto k = k_fwd_small_dig<Src, Snk>;
-            set_smem(k, sm);
-            k<<<nvec, NT_T, sm, s>>>(src, snk, g.m);
+            FM_NT_DISPATCH(nt, {
+                auto k = k_fwd_small_dig<NT, Src, Snk>;
+                set_smem(k, sm);
+                ProfScope ps("fwd_small_dig", s);
+                k<<<nvec, NT, sm, s>>>(src, snk, g.m);
+            })
         }
         return;
     }
+    const size_t sm = (size_t(1) << g.cap) * es;
     const long long vstride = 1ll << g.lt;
-    const int lc = CAP_LOG - g.l1;
+    const int lc = g.cap - g.l1;
     const int ncol_blk = (1 << g.l2) >> lc;
-    if (lattice) {
-        auto kc = k_fwd_col_lat<Src>;
-        set_smem(kc, sm);
-        kc<<<dim3(ncol_blk, nvec), NT_T, sm, s>>>(src, static_cast<double2*>(work), g.l1, g.l2, lc, vstride, tw);
-        auto kr = k_fwd_row_lat<Snk>;
-        set_smem(kr, sm);
-        kr<<<dim3(1 << g.l1, nvec), NT_T, sm, s>>>(static_cast<const double2*>(work), snk, g.l1, g.l2, vstride,
-                                                   g.m, tw);
-    } else {
-        auto kc = k_fwd_col_dig<Src>;
-        set_smem(kc, sm);
-        kc<<<dim3(ncol_blk, nvec), NT_T, sm, s>>>(src, static_cast<double*>(work), g.l1, g.l2, lc, vstride);
-        auto kr = k_fwd_row_dig<Snk>;
-        set_smem(kr, sm);
-        kr<<<dim3(1 << g.l1, nvec), NT_T, sm, s>>>(static_cast<const double*>(work), snk, g.l2, vstride);
-    }
+    const int nt = nt_for(g.cap);
+    FM_NT_DISPATCH(nt, {
+        if (lattice) {
+            auto kc = k_fwd_col_lat<NT, Src>;
+            set_smem(kc, sm);
+            {
+                ProfScope ps("fwd_col_lat", s);
+                kc<<<dim3(ncol_blk, nvec), NT, sm, s>>>(src, static_cast<double2*>(work), g.l1, g.l2, lc, vstride, tw);
+            }
+            auto kr = k_fwd_row_lat<NT, Snk>;
+            set_smem(kr, sm);
+            ProfScope ps("fwd_row_lat", s);
+            kr<<<dim3(1 << g.l1, nvec), NT, sm, s>>>(static_cast<const double2*>(work), snk, g.l1, g.l2, vstride, g.m,
+                                                     tw);
+        } else {
+            auto kc = k_fwd_col_dig<NT, Src>;
+            set_smem(kc, sm);
+            {
+                ProfScope ps("fwd_col_dig", s);
+                kc<<<dim3(ncol_blk, nvec), NT, sm, s>>>(src, static_cast<double*>(work), g.l1, g.l2, lc, vstride);
+            }
+            auto kr = k_fwd_row_dig<NT, Snk>;
+            set_smem(kr, sm);
+            ProfScope ps("fwd_row_dig", s);
+            kr<<<dim3(1 << g.l1, nvec), NT, sm, s>>>(static_cast<const double*>(work), snk, g.l2, vstride);
+        }
+    })
 }
 
-void fwd_gen(int lattice, const Geo& g, int nvec, const GenSrc& src, const SpecSink& snk, void* work,
+static int gen_blocks(long long n, int ept = 1) {
+    long long b = (n + GEN_NT * ept - 1) / (GEN_NT * ept);
+    return int(b > 4096 ? 4096 : b);
+}
+
+void fwd_gen(int lattice, const Geo& g, int nvec, const GenSrc& src, const SpecSink& snk, void* work, void* genbuf,
              const double2* tw, cudaStream_t s) {
+    if (genbuf) {  // split: generator at full parallelism, then transform the buffer
+        const long long n = 1ll << g.m;
+        {
+            ProfScope ps("gen_fill", s);
+            FM_D_DISPATCH(src.sp.d, k_gen_fill<D><<<dim3(gen_blocks(n), nvec), GEN_NT, 0, s>>>(
+                                        src, static_cast<double*>(genbuf), n))
+        }
+        fwd_impl(lattice, g, nvec, BufSrc{static_cast<const double*>(genbuf), n}, snk, work, tw, s);
+        return;
+    }
     fwd_impl(lattice, g, nvec, src, snk, work, tw, s);
 }
+
 void fwd_array(int lattice, const Geo& g, int nvec, const ArraySrc& src, const ScaleSink& snk, void* work,
                const double2* tw, cudaStream_t s) {
     fwd_impl(lattice, g, nvec, src, snk, work, tw, s);
 }
 
-int grad_blocks(int lattice, const Geo& g) {
+int grad_blocks(int lattice, const Geo& g, bool split) {
     (void)lattice;
+    if (split) return gen_blocks(1ll << g.m, GEN_EPT);
     if (!g.two) return 1;
-    const int lc = CAP_LOG - g.l1;
+    const int lc = g.cap - g.l1;
     return (1 << g.l2) >> lc;
 }
 
 template <class Snk>
 static void inv_impl(int lattice, const Geo& g, int nvec, const void* in, const long long* in_off, long long cstride,
                      int nvpc, const Snk& snk, void* work, const double2* tw, cudaStream_t s) {
-    const size_t sm = smem_bytes(lattice);
+    const size_t es = lattice ? sizeof(double2) : sizeof(double);
     if (!g.two) {
+        const size_t sm = (size_t(1) << g.lt) * es;
+        const int nt = nt_for(g.lt);
         if (lattice) {
-            auto k = k_inv_small_lat<Snk>;
-            set_smem(k, sm);
-            k<<<nvec, NT_T, sm, s>>>(static_cast<const double2*>(in), in_off, cstride, nvpc, snk, g.m, tw);
+            FM_NT_DISPATCH(nt, {
+                auto k = k_inv_small_lat<NT, Snk>;
+                set_smem(k, sm);
+                ProfScope ps("inv_small_lat", s);
+                k<<<nvec, NT, sm, s>>>(static_cast<const double2*>(in), in_off, cstride, nvpc, snk, g.m, tw);
+            })
         } else {
-            auto k = k_inv_small_dig<Snk>;
-            set_smem(k, sm);
-            k<<<nvec, NT_T, sm, s>>>(static_cast<const double*>(in), in_off, cstride, nvpc, snk, g.m);
+            FM_NT_DISPATCH(nt, {
+                auto k = k_inv_small_dig<NT, Snk>;
+                set_smem(k, sm);
+                ProfScope ps("inv_small_dig", s);
+                k<<<nvec, NT, sm, s>>>(static_cast<const double*>(in), in_off, cstride, nvpc, snk, g.m);
+            })
         }
         return;
     }
+    const size_t sm = (size_t(1) << g.cap) * es;
     const long long vstride = 1ll << g.lt;
-    const int lc = CAP_LOG - g.l1;
+    const int lc = g.cap - g.l1;
     const int ncol_blk = (1 << g.l2) >> lc;
-    if (lattice) {
-        set_smem(k_inv_row_lat, sm);
-        k_inv_row_lat<<<dim3(1 << g.l1, nvec), NT_T, sm, s>>>(static_cast<const double2*>(in), in_off, cstride, nvpc,
-                                                              static_cast<double2*>(work), vstride, g.l1, g.l2, g.m,
-                                                              tw);
-        auto kc = k_inv_col_lat<Snk>;
-        set_smem(kc, sm);
-        kc<<<dim3(ncol_blk, nvec), NT_T, sm, s>>>(static_cast<const double2*>(work), vstride, snk, g.l1, g.l2, lc, tw);
-    } else {
-        set_smem(k_inv_row_dig, sm);
-        k_inv_row_dig<<<dim3(1 << g.l1, nvec), NT_T, sm, s>>>(static_cast<const double*>(in), in_off, cstride, nvpc,
-                                                              static_cast<double*>(work), vstride, g.l2);
-        auto kc = k_inv_col_dig<Snk>;
-        set_smem(kc, sm);
-        kc<<<dim3(ncol_blk, nvec), NT_T, sm, s>>>(static_cast<const double*>(work), vstride, snk, g.l1, g.l2, lc);
-    }
+    const int nt = nt_for(g.cap);
+    FM_NT_DISPATCH(nt, {
+        if (lattice) {
+            set_smem(k_inv_row_lat<NT>, sm);
+            {
+                ProfScope ps("inv_row_lat", s);
+                k_inv_row_lat<NT><<<dim3(1 << g.l1, nvec), NT, sm, s>>>(static_cast<const double2*>(in), in_off, cstride,
+                                                                        nvpc, static_cast<double2*>(work), vstride,
+                                                                        g.l1, g.l2, g.m, tw);
+            }
+            auto kc = k_inv_col_lat<NT, Snk>;
+            set_smem(kc, sm);
+            ProfScope ps("inv_col_lat", s);
+            kc<<<dim3(ncol_blk, nvec), NT, sm, s>>>(static_cast<const double2*>(work), vstride, snk, g.l1, g.l2, lc,
+                                                    tw);
+        } else {
+            set_smem(k_inv_row_dig<NT>, sm);
+            {
+                ProfScope ps("inv_row_dig", s);
+                k_inv_row_dig<NT><<<dim3(1 << g.l1, nvec), NT, sm, s>>>(static_cast<const double*>(in), in_off, cstride,
+                                                                        nvpc, static_cast<double*>(work), vstride,
+                                                                        g.l2);
+            }
+            auto kc = k_inv_col_dig<NT, Snk>;
+            set_smem(kc, sm);
+            ProfScope ps("inv_col_dig", s);
+            kc<<<dim3(ncol_blk, nvec), NT, sm, s>>>(static_cast<const double*>(work), vstride, snk, g.l1, g.l2, lc);
+        }
+    })
 }
 
 void inv_grad(int lattice, const Geo& g, int nvec, const void* in, const long long* in_off, long long cstride,
-              int nvpc, const GradSink& gs, void* work, const double2* tw, cudaStream_t s) {
+              int nvpc, const GradSink& gs, void* work, void* genbuf, const double2* tw, cudaStream_t s) {
+    if (genbuf) {  // split: inverse transform -> W buffer -> full-parallelism dot
+        const long long n = 1ll << g.m;
+        SinkStoreW snk{static_cast<double*>(genbuf), n, g.m};
+        inv_impl(lattice, g, nvec, in, in_off, cstride, nvpc, snk, work, tw, s);
+        ProfScope ps("gen_dot", s);
+        FM_D_DISPATCH(gs.gen.sp.d, k_gen_dot<D><<<dim3(gs.nblk, nvec), GEN_NT, 0, s>>>(
+                                       gs, static_cast<const double*>(genbuf), n))
+        return;
+    }
     SinkGrad snk{gs, lattice, g.m};
     inv_impl(lattice, g, nvec, in, in_off, cstride, nvpc, snk, work, tw, s);
 }
@@ -691,6 +941,7 @@ __global__ void __launch_bounds__(256) k_solve_equal(SolveArgs a) {
 template <int T>
 static void solve_t(const SolveArgs& a, int ncand, cudaStream_t s) {
     dim3 grid(a.nblk, ncand);
+    ProfScope ps("solve_equal", s);
     if (a.lattice) k_solve_equal<T, true><<<grid, 256, 0, s>>>(a);
     else k_solve_equal<T, false><<<grid, 256, 0, s>>>(a);
 }
@@ -709,29 +960,38 @@ void solve_equal(const SolveArgs& a, int ncand, cudaStream_t s) {
 }
 
 // ============================================================================ finalize
-__global__ void k_finalize(FinalArgs a) {
+// Deterministic fixed-order reductions of the per-block partials into the per-candidate
+// result record (NLL = r^T c + logdet, gp_core.cpp:207-211; gradient chain to R, eta, gamma).
+__global__ void __launch_bounds__(256) k_finalize(FinalArgs a) {
     const int c = blockIdx.x;
     double* out = a.out + (size_t)c * NOUT;
+    __shared__ double red[32];
     __shared__ double S[MAXP][MAXD + 1];
     const int d = a.d, P = a.P;
+    double ld = 0.0, q = 0.0;
+    for (int b = threadIdx.x; b < a.nblk_solve; b += 256) {
+        ld += a.solve_partial[((size_t)c * a.nblk_solve + b) * 2 + 0];
+        q += a.solve_partial[((size_t)c * a.nblk_solve + b) * 2 + 1];
+    }
+    ld = block_sum<256>(ld, red);
+    q = block_sum<256>(q, red);
     if (threadIdx.x == 0) {
-        double ld = 0.0, q = 0.0;
-        for (int b = 0; b < a.nblk_solve; ++b) {
-            ld += a.solve_partial[((size_t)c * a.nblk_solve + b) * 2 + 0];
-            q += a.solve_partial[((size_t)c * a.nblk_solve + b) * 2 + 1];
-        }
         out[OUT_LOGDET] = ld;
         out[OUT_QUAD] = q;
         out[OUT_NLL] = q + ld;  // rT c + logdet (gp_core.cpp:207-211)
     }
     if (!a.grad_partial) return;
-    for (int t = threadIdx.x; t < P * (MAXD + 1); t += blockDim.x) {
+    // one warp per (pair, component): fixed-order strided sums + warp tree (deterministic)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int t = warp; t < P * (MAXD + 1); t += 256 / 32) {
         const int p = t / (MAXD + 1), i = t % (MAXD + 1);
         double acc = 0.0;
         if (i < d || i == MAXD)
-            for (int b = 0; b < a.nblk_grad; ++b)
+            for (int b = lane; b < a.nblk_grad; b += 32)
                 acc += a.grad_partial[(((size_t)c * P + p) * a.nblk_grad + b) * (MAXD + 1) + i];
-        S[p][i] = acc;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) S[p][i] = acc;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -757,7 +1017,10 @@ __global__ void k_finalize(FinalArgs a) {
     }
 }
 
-void finalize(const FinalArgs& a, cudaStream_t s) { k_finalize<<<a.ncand, 128, 0, s>>>(a); }
+void finalize(const FinalArgs& a, cudaStream_t s) {
+    ProfScope ps("finalize", s);
+    k_finalize<<<a.ncand, 256, 0, s>>>(a);
+}
 
 // ============================================================================ per-slot Hermitian apply
 template <int T, bool CX>
@@ -796,6 +1059,7 @@ __global__ void k_apply_herm(long long nslots, const void* opv, const void* inv,
 void apply_hermitian(int lattice, int T, long long nslots, const void* op, const void* in, void* out,
                      cudaStream_t s) {
     const int blocks = int((nslots + 255) / 256 < 1184 ? (nslots + 255) / 256 : 1184);
+    ProfScope ps("apply_hermitian", s);
 #define FM_AH(TT)                                                                   \
     case TT:                                                                        \
         if (lattice) k_apply_herm<TT, true><<<blocks, 256, 0, s>>>(nslots, op, in, out); \

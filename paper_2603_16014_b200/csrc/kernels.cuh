@@ -5,21 +5,41 @@
 
 namespace fmtgp {
 
+// ---------------------------------------------------------------- optional per-launch timing
+// When a model enables profiling, every kernel launch is bracketed by CUDA events on its
+// stream (bench.py's live roofline denominators).  Off by default: zero overhead.
+struct Profiler {
+    virtual void begin(const char* name, cudaStream_t s) = 0;
+    virtual void end(cudaStream_t s) = 0;
+    virtual ~Profiler() = default;
+};
+extern thread_local Profiler* g_prof;
+struct ProfScope {
+    cudaStream_t s;
+    ProfScope(const char* name, cudaStream_t st) : s(st) {
+        if (g_prof) g_prof->begin(name, s);
+    }
+    ~ProfScope() {
+        if (g_prof) g_prof->end(s);
+    }
+};
+
 // ---------------------------------------------------------------- launch helpers
 void init_twiddles(double2* tab, cudaStream_t s);
 
 // forward transforms of nvec vectors of log2-length m into slot arrays
-void fwd_gen(int lattice, const Geo& g, int nvec, const GenSrc& src, const SpecSink& snk, void* work,
+// genbuf != nullptr selects the split mode (separate full-parallelism generator kernel)
+void fwd_gen(int lattice, const Geo& g, int nvec, const GenSrc& src, const SpecSink& snk, void* work, void* genbuf,
              const double2* tw, cudaStream_t s);
 void fwd_array(int lattice, const Geo& g, int nvec, const ArraySrc& src, const ScaleSink& snk, void* work,
                const double2* tw, cudaStream_t s);
 
 // inverse transforms of slot arrays (vector v at in + in_off[v]) into a sink
 void inv_grad(int lattice, const Geo& g, int nvec, const void* in, const long long* in_off, long long cstride,
-              int nvpc, const GradSink& snk, void* work, const double2* tw, cudaStream_t s);
+              int nvpc, const GradSink& snk, void* work, void* genbuf, const double2* tw, cudaStream_t s);
 void inv_coef(int lattice, const Geo& g, int nvec, const void* in, const long long* in_off, const CoefSink& snk,
               void* work, const double2* tw, cudaStream_t s);
-int grad_blocks(int lattice, const Geo& g);
+int grad_blocks(int lattice, const Geo& g, bool split);
 
 // ---------------------------------------------------------------- equal-n per-frequency solve
 struct SolveArgs {

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
@@ -99,9 +100,94 @@ struct TaskGroup {  // tasks of the same length (yhat / solve / coefficient tran
     long long* d_soff = nullptr;   // slot offset into yhat-like arrays of each task
 };
 
+// Per-launch event pairs, aggregated per kernel name (see kernels.cuh Profiler).
+struct EventProfiler : Profiler {
+    struct Rec {
+        const char* name;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> open, done;
+    std::vector<cudaEvent_t> pool;
+    cudaEvent_t get() {
+        if (pool.empty()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            return e;
+        }
+        cudaEvent_t e = pool.back();
+        pool.pop_back();
+        return e;
+    }
+    std::vector<Rec>* capture_list = nullptr;  // set while a graph is being captured
+    static bool capturing(cudaStream_t s) {
+        cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(s, &st);
+        return st == cudaStreamCaptureStatusActive;
+    }
+    void begin(const char* name, cudaStream_t s) override {
+        Rec r{name, get(), get()};
+        if (capturing(s)) cudaEventRecordWithFlags(r.a, s, cudaEventRecordExternal);
+        else cudaEventRecord(r.a, s);
+        open.push_back(r);
+    }
+    void end(cudaStream_t s) override {
+        Rec r = open.back();
+        open.pop_back();
+        if (capturing(s)) {
+            cudaEventRecordWithFlags(r.b, s, cudaEventRecordExternal);
+            if (capture_list) capture_list->push_back(r);  // owned by the graph, re-recorded per replay
+        } else {
+            cudaEventRecord(r.b, s);
+            done.push_back(r);
+        }
+    }
+    void add(const char* name, float ms) {
+        auto it = std::find_if(agg.begin(), agg.end(), [&](auto& x) { return x.first == name; });
+        if (it == agg.end()) {
+            agg.push_back({name, {0.0, 0}});
+            it = agg.end() - 1;
+        }
+        it->second.first += ms;
+        it->second.second += 1;
+    }
+    void add_graph(const std::vector<Rec>& recs) {
+        for (const auto& r : recs) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, r.a, r.b);
+            add(r.name, ms);
+        }
+    }
+    // name -> (total ms, launches)
+    std::vector<std::pair<std::string, std::pair<double, int>>> agg;
+    void collect() {
+        for (auto& r : done) {
+            cudaEventSynchronize(r.b);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, r.a, r.b);
+            add(r.name, ms);
+            pool.push_back(r.a);
+            pool.push_back(r.b);
+        }
+        done.clear();
+    }
+    void reset() {
+        collect();
+        agg.clear();
+    }
+    ~EventProfiler() override {
+        for (auto& r : done) {
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+        for (auto e : pool) cudaEventDestroy(e);
+    }
+};
+
 }  // namespace
 
 struct fmtgp_model {
+    EventProfiler prof;
+    bool profiling = false;
     int dev = 0;
     cudaStream_t st = nullptr;
     int kind = 0, lattice = 1, d = 0, T = 0, P = 0, max_cand = 1;
@@ -159,6 +245,23 @@ struct fmtgp_model {
     double last_b[4]{};
     double last_logdet = 0.0;
     unequal::Plan* uneq = nullptr;
+    Geo geo_m[28]{};           // transform geometry per log2 length (shared by pairs and tasks)
+    bool split = false;        // small problem: separate full-parallelism generator / dot kernels
+    void* d_gen = nullptr;     // split-mode generator / W buffer
+    // packed per-candidate hyperparameter block (fixed layout, one H2D copy per evaluation)
+    double* d_hyp = nullptr;
+    double* h_hyp = nullptr;
+    size_t hyp_len = 0;
+    // CUDA graphs of the equal-n evaluation, keyed on everything baked into kernel params
+    struct GraphEntry {
+        int nc, grad, keep_chat, si_alpha, prof;
+        double b[4];
+        int runs = 0;
+        cudaGraphExec_t exec = nullptr;
+        std::vector<EventProfiler::Rec> recs;
+    };
+    std::vector<GraphEntry> graphs;
+    bool use_graphs = true;
 };
 
 namespace {
@@ -213,18 +316,14 @@ void ensure_stage(fmtgp_model* M, size_t len) {
     M->stage_len = len;
 }
 
-// Upload per-candidate hyperparameter tables (eta, gamma, Rpair, per-group coef and xi).
-// xi_scale[c] is the escalation factor of candidate c.
-void upload_hyper(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, const double* xi_scale) {
-    const int d = M->d, P = M->P;
-    size_t len = size_t(nc) * (d + 1 + P);
-    for (auto& g : M->groups) len += 2 * size_t(nc) * g.pairs.size();
-    ensure_stage(M, len);
-    double* s = M->h_stage;
-    double* eta = s;
-    double* gam = eta + size_t(nc) * d;
-    double* Rp = gam + nc;
-    double* gc = Rp + size_t(nc) * P;
+// Fill the pinned hyperparameter block (eta, gamma, Rpair, per-group coef and xi) for nc
+// candidates; xi_scale[c] is the escalation factor of candidate c.  Host-only: the H2D copy
+// is issued by copy_hyper (inside the captured graph).
+void fill_hyper(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, const double* xi_scale) {
+    const int d = M->d, P = M->P, mc = M->max_cand;
+    double* eta = M->h_hyp;
+    double* gam = eta + size_t(mc) * d;
+    double* Rp = gam + mc;
     for (int c = 0; c < nc; ++c) {
         const fmtgp_hyper* h = hs[c];
         for (int j = 0; j < d; ++j) eta[c * d + j] = h->eta[j];
@@ -232,11 +331,11 @@ void upload_hyper(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, const do
         const std::vector<double> R = task_gram(M, h);
         for (int p = 0; p < P; ++p) Rp[c * P + p] = R[M->pa[p] * M->T + M->pb[p]];
     }
-    double* cur = gc;
+    double* cur = Rp + size_t(mc) * P;
     for (auto& g : M->groups) {
         const int np = int(g.pairs.size());
         double* co = cur;
-        double* xi = cur + size_t(nc) * np;
+        double* xi = cur + size_t(mc) * np;
         for (int c = 0; c < nc; ++c) {
             const fmtgp_hyper* h = hs[c];
             for (int q = 0; q < np; ++q) {
@@ -252,13 +351,17 @@ void upload_hyper(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, const do
                 xi[c * np + q] = x;
             }
         }
-        CK(cudaMemcpyAsync(g.d_coef, co, sizeof(double) * size_t(nc) * np, cudaMemcpyHostToDevice, M->st));
-        CK(cudaMemcpyAsync(g.d_xi, xi, sizeof(double) * size_t(nc) * np, cudaMemcpyHostToDevice, M->st));
-        cur += 2 * size_t(nc) * np;
+        cur += 2 * size_t(mc) * np;
     }
-    CK(cudaMemcpyAsync(M->d_eta, eta, sizeof(double) * size_t(nc) * d, cudaMemcpyHostToDevice, M->st));
-    CK(cudaMemcpyAsync(M->d_gamma, gam, sizeof(double) * size_t(nc), cudaMemcpyHostToDevice, M->st));
-    CK(cudaMemcpyAsync(M->d_Rpair, Rp, sizeof(double) * size_t(nc) * P, cudaMemcpyHostToDevice, M->st));
+}
+
+void copy_hyper(fmtgp_model* M) {
+    CK(cudaMemcpyAsync(M->d_hyp, M->h_hyp, M->hyp_len * sizeof(double), cudaMemcpyHostToDevice, M->st));
+}
+
+void upload_hyper(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, const double* xi_scale) {
+    fill_hyper(M, nc, hs, xi_scale);
+    copy_hyper(M);
 }
 
 GenSrc gensrc_of(fmtgp_model* M, const Group& g, int si_alpha, const double* b) {
@@ -285,7 +388,7 @@ void build_spectra(fmtgp_model* M, int nc, int si_alpha, const double* b) {
         snk.coef = g.d_coef;
         snk.xi = g.d_xi;
         snk.nvpc = np;
-        fwd_gen(M->lattice, g.geo, np * nc, src, snk, M->d_work, M->tw, M->st);
+        fwd_gen(M->lattice, g.geo, np * nc, src, snk, M->d_work, M->split ? M->d_gen : nullptr, M->tw, M->st);
     }
     CK(cudaGetLastError());
 }
@@ -356,12 +459,10 @@ void finish_results(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, bool g
     }
 }
 
-// One batched evaluation attempt (equal n).  Returns per-candidate bad flags in M->h_bad.
-void eval_equal(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, const double* xi_scale, bool grad,
-                bool keep_chat) {
-    const fmtgp_hyper* h0 = hs[0];
-    upload_hyper(M, nc, hs, xi_scale);
-    build_spectra(M, nc, h0->si_alpha, h0->b);
+// Stream-ordered body of one equal-n evaluation (captured into a CUDA graph).
+void eval_equal_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, bool grad, bool keep_chat) {
+    copy_hyper(M);
+    build_spectra(M, nc, si_alpha, bw);
     CK(cudaMemsetAsync(M->d_bad, 0x7f, sizeof(int) * nc, M->st));
     CK(cudaMemsetAsync(M->d_bad + nc, 0, sizeof(int) * nc, M->st));
     SolveArgs sa{};
@@ -384,11 +485,12 @@ void eval_equal(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, const doub
     const Group& g = M->groups[0];
     if (grad) {
         GradSink gs{};
-        gs.gen = gensrc_of(M, g, h0->si_alpha, h0->b);
+        gs.gen = gensrc_of(M, g, si_alpha, bw);
         gs.partial = M->d_pgrad;
         gs.nblk = M->nblk_grad;
         gs.acc_n = M->d + 1;
-        inv_grad(M->lattice, g.geo, M->P * nc, M->d_M, g.d_voff, M->total_slots, M->P, gs, M->d_work, M->tw, M->st);
+        inv_grad(M->lattice, g.geo, M->P * nc, M->d_M, g.d_voff, M->total_slots, M->P, gs, M->d_work,
+                 M->split ? M->d_gen : nullptr, M->tw, M->st);
         CK(cudaGetLastError());
     }
     FinalArgs fa{};
@@ -409,7 +511,60 @@ void eval_equal(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, const doub
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(M->h_out, M->d_out, sizeof(double) * NOUT * nc, cudaMemcpyDeviceToHost, M->st));
     CK(cudaMemcpyAsync(M->h_bad, M->d_bad, sizeof(int) * 2 * nc, cudaMemcpyDeviceToHost, M->st));
+}
+
+// One batched evaluation attempt (equal n).  Results land in M->h_out / M->h_bad.  The first
+// run of a configuration executes eagerly; later runs replay a captured CUDA graph (one
+// launch per fit instead of ~10 kernel launches + copies).
+void eval_equal(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, const double* xi_scale, bool grad,
+                bool keep_chat) {
+    const fmtgp_hyper* h0 = hs[0];
+    fill_hyper(M, nc, hs, xi_scale);
+    const int prof = M->profiling ? 1 : 0;
+    fmtgp_model::GraphEntry* ge = nullptr;
+    for (auto& e : M->graphs)
+        if (e.nc == nc && e.grad == int(grad) && e.keep_chat == int(keep_chat) && e.si_alpha == h0->si_alpha &&
+            e.prof == prof && std::memcmp(e.b, h0->b, sizeof(e.b)) == 0)
+            ge = &e;
+    if (!M->use_graphs || !ge || ge->runs == 0) {
+        eval_equal_body(M, nc, h0->si_alpha, h0->b, grad, keep_chat);
+        CK(cudaStreamSynchronize(M->st));
+        if (M->use_graphs) {
+            if (!ge) {
+                M->graphs.push_back(fmtgp_model::GraphEntry{});
+                ge = &M->graphs.back();
+                ge->nc = nc;
+                ge->grad = grad;
+                ge->keep_chat = keep_chat;
+                ge->si_alpha = h0->si_alpha;
+                ge->prof = prof;
+                std::memcpy(ge->b, h0->b, sizeof(ge->b));
+            }
+            ge->runs = 1;
+        }
+        return;
+    }
+    if (!ge->exec) {
+        cudaGraph_t graph = nullptr;
+        M->prof.capture_list = &ge->recs;
+        CK(cudaStreamBeginCapture(M->st, cudaStreamCaptureModeThreadLocal));
+        try {
+            eval_equal_body(M, nc, h0->si_alpha, h0->b, grad, keep_chat);
+        } catch (...) {
+            cudaStreamEndCapture(M->st, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            M->prof.capture_list = nullptr;
+            throw;
+        }
+        CK(cudaStreamEndCapture(M->st, &graph));
+        M->prof.capture_list = nullptr;
+        CK(cudaGraphInstantiate(&ge->exec, graph, 0));
+        cudaGraphDestroy(graph);
+    }
+    CK(cudaGraphLaunch(ge->exec, M->st));
     CK(cudaStreamSynchronize(M->st));
+    if (prof) M->prof.add_graph(ge->recs);
+    ge->runs++;
 }
 
 void remember_hyper(fmtgp_model* M, const fmtgp_hyper* h) {
@@ -566,6 +721,17 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
         M->d_pb = dalloc<int>(M->P);
         CK(cudaMemcpy(M->d_pa, M->pa.data(), M->P * sizeof(int), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(M->d_pb, M->pb.data(), M->P * sizeof(int), cudaMemcpyHostToDevice));
+        // transform geometry per length: tiles sized from all vectors of that length
+        {
+            long long tot[28] = {0};
+            long long all = 0;
+            for (int p = 0; p < M->P; ++p) {
+                tot[M->m[M->pa[p]]] += (1ll << M->m[M->pa[p]]) * max_cand;
+                all += (1ll << M->m[M->pa[p]]) * max_cand;
+            }
+            for (int mm = 0; mm < 28; ++mm) M->geo_m[mm] = Geo::make(mm, M->lattice, tot[mm]);
+            M->split = all <= (1ll << 22);
+        }
         // groups of pairs by generating-task length
         size_t work = 0;
         for (int p = 0; p < M->P; ++p) {
@@ -574,7 +740,7 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
             if (it == M->groups.end()) {
                 M->groups.push_back(Group{});
                 M->groups.back().m = mm;
-                M->groups.back().geo = Geo::make(mm, M->lattice);
+                M->groups.back().geo = M->geo_m[mm];
                 it = M->groups.end() - 1;
             }
             it->pairs.push_back(p);
@@ -585,8 +751,6 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
             for (int q = 0; q < np; ++q) vo[q] = M->poff[g.pairs[q]];
             g.d_vec_pair = dalloc<int>(np);
             g.d_voff = dalloc<long long>(np);
-            g.d_coef = dalloc<double>(size_t(np) * max_cand);
-            g.d_xi = dalloc<double>(size_t(np) * max_cand);
             CK(cudaMemcpy(g.d_vec_pair, g.pairs.data(), np * sizeof(int), cudaMemcpyHostToDevice));
             CK(cudaMemcpy(g.d_voff, vo.data(), np * sizeof(long long), cudaMemcpyHostToDevice));
             if (g.geo.two) work = std::max(work, size_t(np) * max_cand * (size_t(1) << g.geo.lt));
@@ -597,7 +761,7 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
             if (it == M->tgroups.end()) {
                 M->tgroups.push_back(TaskGroup{});
                 M->tgroups.back().m = mm;
-                M->tgroups.back().geo = Geo::make(mm, M->lattice);
+                M->tgroups.back().geo = M->geo_m[mm];
                 it = M->tgroups.end() - 1;
             }
             it->tasks.push_back(t);
@@ -618,12 +782,31 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
         const size_t es = elem_size(M);
         M->work_elems = work;
         M->d_work = dalloc<char>(std::max<size_t>(work, 1) * es);
+        if (M->split) {
+            size_t gen = 0;
+            for (auto& g : M->groups) gen = std::max(gen, g.pairs.size() * size_t(max_cand) * (size_t(1) << g.m));
+            M->d_gen = dalloc<double>(gen);
+        }
         M->d_y = dalloc<double>(M->N);
         M->d_yhat = dalloc<char>(M->task_slots * es);
-        // hyper block: eta [mc*d] | gamma [mc] | Rpair [mc*P]
-        M->d_eta = dalloc<double>(size_t(max_cand) * (M->d + 1 + M->P));
-        M->d_gamma = M->d_eta + size_t(max_cand) * M->d;
-        M->d_Rpair = M->d_gamma + max_cand;
+        // hyper block: eta [mc*d] | gamma [mc] | Rpair [mc*P] | per group: coef [mc*np] | xi [mc*np]
+        {
+            size_t len = size_t(max_cand) * (M->d + 1 + M->P);
+            for (auto& g : M->groups) len += 2 * size_t(max_cand) * g.pairs.size();
+            M->hyp_len = len;
+            M->d_hyp = dalloc<double>(len);
+            CK(cudaMallocHost(reinterpret_cast<void**>(&M->h_hyp), len * sizeof(double)));
+            std::memset(M->h_hyp, 0, len * sizeof(double));
+            M->d_eta = M->d_hyp;
+            M->d_gamma = M->d_eta + size_t(max_cand) * M->d;
+            M->d_Rpair = M->d_gamma + max_cand;
+            double* cur = M->d_Rpair + size_t(max_cand) * M->P;
+            for (auto& g : M->groups) {
+                g.d_coef = cur;
+                g.d_xi = cur + size_t(max_cand) * g.pairs.size();
+                cur += 2 * size_t(max_cand) * g.pairs.size();
+            }
+        }
         M->d_lam = dalloc<char>(size_t(max_cand) * M->total_slots * es);
         M->d_laminv = dalloc<char>(size_t(M->total_slots) * es);
         M->d_chat = dalloc<char>(size_t(M->task_slots) * es);
@@ -631,7 +814,7 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
             M->d_M = dalloc<char>(size_t(max_cand) * M->total_slots * es);
             const long long ns = M->pslots[0];
             M->nblk_solve = int(std::min<long long>((ns + 255) / 256, 148 * 8));
-            M->nblk_grad = grad_blocks(M->lattice, M->groups[0].geo);
+            M->nblk_grad = grad_blocks(M->lattice, M->groups[0].geo, M->split);
             M->d_pgrad = dalloc<double>(size_t(max_cand) * M->P * M->nblk_grad * (MAXD + 1));
         } else {
             M->nblk_solve = 1;
@@ -671,6 +854,13 @@ cudaStream_t stream(fmtgp_model* M) { return M->st; }
 
 #include "unequal_impl.inc"
 
+// Routes the kernels.cu launch brackets to the model's profiler for one API call.
+struct ProfGuard {
+    Profiler* prev;
+    explicit ProfGuard(fmtgp_model* M) : prev(g_prof) { g_prof = (M && M->profiling) ? &M->prof : nullptr; }
+    ~ProfGuard() { g_prof = prev; }
+};
+
 // ===================================================================== C ABI
 extern "C" {
 
@@ -691,8 +881,6 @@ int fmtgp_model_destroy(fmtgp_model_t M) {
     for (auto& g : M->groups) {
         F(g.d_vec_pair);
         F(g.d_voff);
-        F(g.d_coef);
-        F(g.d_xi);
     }
     for (auto& tg : M->tgroups) {
         F(tg.d_yoff);
@@ -708,10 +896,14 @@ int fmtgp_model_destroy(fmtgp_model_t M) {
     F(M->d_pb);
     F(M->d_y);
     F(M->d_yhat);
-    F(M->d_eta);
+    F(M->d_hyp);
+    for (auto& ge : M->graphs)
+        if (ge.exec) cudaGraphExecDestroy(ge.exec);
+    if (M->h_hyp) cudaFreeHost(M->h_hyp);
     F(M->d_lam);
     F(M->d_M);
     F(M->d_work);
+    F(M->d_gen);
     F(M->d_laminv);
     F(M->d_chat);
     F(M->d_psolve);
@@ -735,6 +927,7 @@ void* fmtgp_model_stream(fmtgp_model_t M) { return M ? static_cast<void*>(M->st)
 
 int fmtgp_model_set_y(fmtgp_model_t M, const double* y) {
     return guarded([&] {
+        ProfGuard pg_(M);
         if (!M || !y) invalid("set_y: null argument");
         CK(cudaSetDevice(M->dev));
         CK(cudaMemcpyAsync(M->d_y, y, sizeof(double) * M->N, cudaMemcpyHostToDevice, M->st));
@@ -745,6 +938,7 @@ int fmtgp_model_set_y(fmtgp_model_t M, const double* y) {
 
 int fmtgp_model_set_y_device(fmtgp_model_t M, const double* y) {
     return guarded([&] {
+        ProfGuard pg_(M);
         if (!M || !y) invalid("set_y_device: null argument");
         CK(cudaSetDevice(M->dev));
         CK(cudaMemcpyAsync(M->d_y, y, sizeof(double) * M->N, cudaMemcpyDeviceToDevice, M->st));
@@ -755,6 +949,7 @@ int fmtgp_model_set_y_device(fmtgp_model_t M, const double* y) {
 
 int fmtgp_build_spectrum(fmtgp_model_t M, const fmtgp_hyper* h) {
     return guarded([&] {
+        ProfGuard pg_(M);
         if (!M) invalid("build_spectrum: null model");
         CK(cudaSetDevice(M->dev));
         validate_hyper(M, h);
@@ -786,7 +981,7 @@ int fmtgp_spectrum_read(fmtgp_model_t M, int l, int lp, double* re, double* im) 
             }
             return;
         }
-        const Geo g = Geo::make(M->m[l], 1);
+        const Geo g = M->geo_m[M->m[l]];
         for (long long k = 0; k < n; ++k) {
             if (n == 1) {
                 re[0] = buf[0];
@@ -815,6 +1010,7 @@ int fmtgp_spectrum_read(fmtgp_model_t M, int l, int lp, double* re, double* im) 
 
 int fmtgp_invert_and_logdet(fmtgp_model_t M, double* logdet) {
     return guarded([&] {
+        ProfGuard pg_(M);
         if (!M || !logdet) invalid("invert_and_logdet: null argument");
         if (!M->have_spec) invalid("invert_and_logdet: no spectrum built");
         CK(cudaSetDevice(M->dev));
@@ -864,6 +1060,7 @@ int fmtgp_invert_and_logdet(fmtgp_model_t M, double* logdet) {
 
 int fmtgp_solve(fmtgp_model_t M, const double* b, double* x) {
     return guarded([&] {
+        ProfGuard pg_(M);
         if (!M || !b || !x) invalid("solve: null argument");
         if (!M->have_inv) invalid("solve: no factorisation (invert_and_logdet)");
         CK(cudaSetDevice(M->dev));
@@ -879,6 +1076,7 @@ int fmtgp_solve(fmtgp_model_t M, const double* b, double* x) {
 
 int fmtgp_gram_matvec(fmtgp_model_t M, const double* b, double* out) {
     return guarded([&] {
+        ProfGuard pg_(M);
         if (!M || !b || !out) invalid("gram_matvec: null argument");
         if (!M->have_spec) invalid("gram_matvec: no spectrum built");
         CK(cudaSetDevice(M->dev));
@@ -941,6 +1139,7 @@ int fmtgp_trace_inverse(fmtgp_model_t M, double* tr) {
 
 int fmtgp_nll(fmtgp_model_t M, const fmtgp_hyper* h, int want_grad, fmtgp_result* out) {
     return guarded([&] {
+        ProfGuard pg_(M);
         if (!M || !h || !out) invalid("nll: null argument");
         CK(cudaSetDevice(M->dev));
         nll_batch_impl(M, 1, h, want_grad != 0, out, true);
@@ -958,6 +1157,7 @@ int fmtgp_nll(fmtgp_model_t M, const fmtgp_hyper* h, int want_grad, fmtgp_result
 
 int fmtgp_nll_batch(fmtgp_model_t M, int ncand, const fmtgp_hyper* h, int want_grad, fmtgp_result* out) {
     return guarded([&] {
+        ProfGuard pg_(M);
         if (!M || !h || !out || ncand < 1) invalid("nll_batch: bad argument");
         CK(cudaSetDevice(M->dev));
         nll_batch_impl(M, ncand, h, want_grad != 0, out, false);
@@ -969,6 +1169,7 @@ int fmtgp_nll_batch(fmtgp_model_t M, int ncand, const fmtgp_hyper* h, int want_g
 
 int fmtgp_coefficients(fmtgp_model_t M, double* c) {
     return guarded([&] {
+        ProfGuard pg_(M);
         if (!M || !c) invalid("coefficients: null argument");
         if (!M->have_fit) invalid("coefficients: model not refreshed (call fmtgp_nll)");
         CK(cudaSetDevice(M->dev));
@@ -980,6 +1181,7 @@ int fmtgp_coefficients(fmtgp_model_t M, double* c) {
 
 int fmtgp_posterior_mean(fmtgp_model_t M, int task, const double* X, int64_t count, double* out) {
     return guarded([&] {
+        ProfGuard pg_(M);
         if (!M || (!X && count > 0) || (!out && count > 0)) invalid("posterior_mean: null argument");
         if (!M->have_fit) invalid("posterior_mean: model not refreshed");
         if (task < 0 || task >= M->T) invalid("posterior_mean: task out of range");
@@ -1031,6 +1233,7 @@ int fmtgp_posterior_mean(fmtgp_model_t M, int task, const double* X, int64_t cou
 
 int fmtgp_posterior_var(fmtgp_model_t M, int task, const double* X, int64_t count, double* out) {
     return guarded([&] {
+        ProfGuard pg_(M);
         if (!M || (!X && count > 0) || (!out && count > 0)) invalid("posterior_var: null argument");
         if (!M->have_fit) invalid("posterior_var: model not refreshed");
         if (task < 0 || task >= M->T) invalid("posterior_var: task out of range");
@@ -1043,6 +1246,7 @@ int fmtgp_posterior_var(fmtgp_model_t M, int task, const double* X, int64_t coun
 // multitask_cubature (cubature.cpp:52-75): mu = tau + gamma R (E^T c), Sigma = gamma R - gamma^2 R Pi R
 int fmtgp_cubature(fmtgp_model_t M, double* mu, double* Sigma) {
     return guarded([&] {
+        ProfGuard pg_(M);
         if (!M || !mu || !Sigma) invalid("cubature: null argument");
         if (!M->have_fit) invalid("cubature: model not refreshed");
         CK(cudaSetDevice(M->dev));
@@ -1114,6 +1318,26 @@ int fmtgp_cubature(fmtgp_model_t M, double* mu, double* Sigma) {
             for (int b = a + 1; b < T; ++b) Sigma[a * T + b] = Sigma[b * T + a] = 0.5 * (Sigma[a * T + b] + Sigma[b * T + a]);
         for (int a = 0; a < T; ++a)
             if (Sigma[a * T + a] < 0.0 && Sigma[a * T + a] > -1e-12) Sigma[a * T + a] = 0.0;
+    });
+}
+
+int fmtgp_profile_enable(fmtgp_model_t M, int on) {
+    return guarded([&] {
+        if (!M) invalid("profile_enable: null model");
+        M->prof.reset();
+        M->profiling = on != 0;
+    });
+}
+
+int fmtgp_profile_read(fmtgp_model_t M, int idx, char* name, int name_len, double* total_ms, int* launches) {
+    return guarded([&] {
+        if (!M || !name || name_len < 1 || !total_ms || !launches) invalid("profile_read: bad argument");
+        M->prof.collect();
+        if (idx < 0 || idx >= int(M->prof.agg.size())) invalid("profile_read: index out of range");
+        const auto& e = M->prof.agg[idx];
+        std::snprintf(name, size_t(name_len), "%s", e.first.c_str());
+        *total_ms = e.second.first;
+        *launches = e.second.second;
     });
 }
 

@@ -7,7 +7,7 @@
 //                  real-FFT post-processing; only the Hermitian half is stored: slot k holds
 //                  A(k) for 1 <= k < n/2 and slot 0 packs (A(0), A(n/2)), both real.
 //   digital (DSI): FWHT (transforms.cpp:19-30), real, natural order, n slots.
-// One CTA transforms up to CAP = 2^13 elements; longer vectors use a two-pass four-step
+// One CTA transforms a tile of 2^11..2^13 elements; longer vectors use a two-pass four-step
 // decomposition n' = N1 * N2 (column pass then row pass, intermediate through L2/HBM).
 // Lattice slot layout of a two-pass transform: position k1*N2 + k2 <-> frequency
 // k = k1 + N1*k2 (the row pass's natural output), identical for every vector of that length,
@@ -24,26 +24,31 @@ namespace cg = cooperative_groups;
 
 namespace fmtgp {
 
-constexpr int NT_T = 512;        // threads per transform CTA
-constexpr int CAP_LOG = 13;      // elements per transform CTA = NT_T * EPT
-constexpr int CAP = 1 << CAP_LOG;
+constexpr int MAX_CAP_LOG = 13;  // elements per transform CTA <= 2^13 (NT = tile / EPT <= 512 threads)
 
 // --------------------------------------------------------------------- geometry
 struct Geo {
     int m;        // log2 n (task length)
     int lt;       // log2 of the transformed length: m-1 (lattice) or m (digital)
+    int cap;      // log2 elements per CTA tile (11..13)
     int two;      // two-pass?
-    int l1, l2;   // two-pass split lt = l1 + l2
+    int l1, l2;   // two-pass split lt = l1 + l2 (l2 = cap: a row fills one tile)
     int C;        // columns per CTA in the column pass
-    __host__ __device__ static Geo make(int m, int lattice) {
+    // `total` = elements of all vectors transformed together; tiles shrink (down to 2^11) so
+    // that small problems still launch >= ~2 CTAs per SM.
+    __host__ __device__ static Geo make(int m, int lattice, long long total = 0) {
         Geo g{};
         g.m = m;
         g.lt = lattice ? (m > 0 ? m - 1 : 0) : m;
-        g.two = g.lt > CAP_LOG;
+        int cap = MAX_CAP_LOG;
+        while (cap > 11 && total > 0 && (total >> cap) < 296) --cap;
+        while (g.lt > 2 * cap && cap < MAX_CAP_LOG) ++cap;
+        g.cap = cap;
+        g.two = g.lt > cap;
         if (g.two) {
-            g.l2 = CAP_LOG;
-            g.l1 = g.lt - CAP_LOG;
-            g.C = CAP >> g.l1;
+            g.l2 = cap;
+            g.l1 = g.lt - cap;
+            g.C = 1 << (cap - g.l1);
         } else {
             g.l1 = 0;
             g.l2 = g.lt;
@@ -111,6 +116,13 @@ struct ArraySrc {
         const uint64_t i = bitrev ? bitrev64(idx, m) : idx;
         return __ldg(src + vec_off[v] + i);
     }
+};
+
+// Plain buffer already in transform-input order (the split generator's output).
+struct BufSrc {
+    const double* buf;  // [nvec][n]
+    long long n;
+    __device__ __forceinline__ double operator()(int v, uint64_t idx) const { return buf[v * n + idx]; }
 };
 
 // --------------------------------------------------------------------- forward sinks

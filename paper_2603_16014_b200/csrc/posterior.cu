@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(PM_NT) k_post_mean(PostArgs a) {
 
 void posterior_mean(const PostArgs& a, cudaStream_t s) {
     const long long blocks = (a.count + PM_NT - 1) / PM_NT;
+    ProfScope ps("posterior_mean", s);
     if (blocks > 0) k_post_mean<<<unsigned(blocks), PM_NT, 0, s>>>(a);
 }
 

@@ -16,7 +16,7 @@ namespace fmtgp {
 
 constexpr int EPT = 16;
 
-// In-register DFT of R points (natural order in and out), dir = -1 / +1.
+// In-register DFT of R points (natural order in, bit-reversed order out), dir = -1 / +1.
 template <int R>
 __device__ __forceinline__ void reg_dft(double2* v, int dir) {
     // cos / sin (2 pi t / 16), t = 0..15
@@ -74,17 +74,14 @@ __device__ __forceinline__ void reg_dft(double2* v, int dir) {
                 v[i + j + half] = d;
             }
     }
-    // undo the bit reversal
-    double2 tmp[R];
-#pragma unroll
-    for (int k = 0; k < R; ++k) tmp[k] = v[k];
-#pragma unroll
-    for (int k = 0; k < R; ++k) {
-        int r = 0;
-#pragma unroll
-        for (int b = 0, kk = k; (1 << b) < R; ++b, kk >>= 1) r = (r << 1) | (kk & 1);
-        v[k] = tmp[r];
-    }
+    // output left in bit-reversed order: v[r] = X[bitrev_R(r)]; callers index accordingly
+}
+
+template <int R>
+__host__ __device__ constexpr int brev_c(int k) {
+    int r = 0;
+    for (int b = 1; b < R; b <<= 1, k >>= 1) r = (r << 1) | (k & 1);
+    return r;
 }
 
 template <int R>
@@ -143,7 +140,7 @@ __device__ __forceinline__ void fft_stage(double2* buf, int logN, int ns_log, in
             const int k = j & ((1 << ns_log) - 1);
             const int o = ((j >> ns_log) << (ns_log + RL)) + k;
 #pragma unroll
-            for (int r = 0; r < R; ++r) x[o + (r << ns_log)] = v[q][r];
+            for (int r = 0; r < R; ++r) x[o + (brev_c<R>(r) << ns_log)] = v[q][r];
         }
     }
     __syncthreads();

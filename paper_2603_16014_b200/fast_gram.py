@@ -185,6 +185,25 @@ class Model:
         return mu, S
 
 
+    # -- measurement
+    def profile(self, on: bool = True):
+        check(self.lib.fmtgp_profile_enable(self.h, int(on)))
+
+    def profile_read(self) -> Dict[str, tuple]:
+        """kernel name -> (total device ms, launches) since profile(True)."""
+        out = {}
+        i = 0
+        buf = C.create_string_buffer(64)
+        while True:
+            ms, cnt = C.c_double(), C.c_int()
+            rc = self.lib.fmtgp_profile_read(self.h, i, buf, 64, C.byref(ms), C.byref(cnt))
+            if rc != _lib.OK:
+                break
+            out[buf.value.decode()] = (ms.value, cnt.value)
+            i += 1
+        return out
+
+
 # ---- free-function spelling of the seam (fast_gram.hpp:34-70) ---------------------------
 
 def build_spectrum(model: Model, hp: Hyper) -> Model:
