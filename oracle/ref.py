@@ -44,6 +44,10 @@ def lib():
         P, D = C.POINTER(CDesign), C.POINTER(CHyper)
         dp = C.POINTER(C.c_double)
         L.ref_last_error.restype = C.c_char_p
+        L.ref_rand_u64.restype = C.c_uint64
+        L.ref_rand_u64.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
+        L.ref_normal.restype = C.c_double
+        L.ref_normal.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
         L.ref_bit_reverse.restype = C.c_uint64
         L.ref_bit_reverse.argtypes = [C.c_uint64, C.c_int]
         L.ref_fwht.argtypes = [dp, C.c_size_t]

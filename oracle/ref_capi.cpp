@@ -24,6 +24,7 @@
 #include "fastmtgp/gp_core.hpp"
 #include "fastmtgp/kernels.hpp"
 #include "fastmtgp/ld_sequences.hpp"
+#include "fastmtgp/rng.hpp"
 #include "fastmtgp/transforms.hpp"
 
 // The shipped generator tables are only reached through default_lattice /
@@ -160,6 +161,12 @@ struct RefModel {
 extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
+
+// ---- rng.hpp (counter RNG: every seeded input in the reference's tests)
+std::uint64_t ref_rand_u64(std::uint64_t seed, std::uint64_t stream, std::uint64_t counter) {
+    return rng::rand_u64(seed, stream, counter);
+}
+double ref_normal(std::uint64_t seed, std::uint64_t stream, std::uint64_t k) { return rng::normal(seed, stream, k); }
 
 // ---- transforms / kernels / points (transforms.cpp, kernels.cpp, ld_sequences.cpp)
 std::uint64_t ref_bit_reverse(std::uint64_t i, int m) { return bit_reverse(i, m); }

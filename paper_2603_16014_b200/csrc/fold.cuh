@@ -2,7 +2,7 @@
 //
 // Reference: invert_and_logdet builds the dense r x r grid of Lam^-1 (Algorithm 1,
 // /root/reference/proj/src/fast_gram.cpp:151-263), O(N^2/n_L) storage.
-// Same pivots (the diagonal Schur complements S of each stage, so the same logdet),
+// Same pivots (the diagonal Schur complements S of each stage, hence the same logdet),
 // factored instead of inverted: stage s eliminates task s (largest first) and updates
 //   lam_ab[k] -= sum_c conj(lam_sa[c n_a + k]) lam_sb[c n_a + k] / d_s[c n_a + k],  s < a <= b,
 // in place, so storage stays the spectrum's own sum_l (T-l+1) n_l entries.  Solves are
@@ -13,22 +13,42 @@
 // Digital vectors are real, stored in full (n entries).
 #pragma once
 
-#include "common.cuh"
+#include "passes.cuh"
 
 namespace fmtgp {
 
-struct FoldDims {
-    int T, P, lattice;
-    long long n[MAXT];
-    long long H[MAXT];        // stored length per task-length vector
-    long long poff[MAXP];     // pair (a<=b) natural offsets
-    long long toff[MAXT];     // task natural offsets (right-hand-side layout)
-    long long tot_pair, tot_task;
-    int pid[MAXT][MAXT];      // pair id of (a<=b)
+struct VecMap {          // one vector: slot layout <-> natural layout
+    long long soff, noff;  // slot offset, natural offset
+    int m, two, l1, l2;
 };
 
-// spectra slot layout (transform output) <-> natural half layout, per vector
-void slots_to_nat(int lattice, int m, const Geo_* geo_unused, int nvec, const void* slots, const long long* soff,
-                  void* nat, const long long* noff, cudaStream_t s);
+struct FoldDims {
+    int T, lattice;
+    long long n[MAXT];
+    long long H[MAXT];      // stored (natural) length of a vector of task length n[t]
+    long long poff[MAXP];   // natural offset of pair (a <= b), row by row
+    long long toff[MAXT];   // natural offset of task t in a right-hand-side block
+    long long tot_pair, tot_task;
+    int pid[MAXT][MAXT];
+};
+
+__host__ __device__ inline long long fold_H(int lattice, long long n) { return lattice ? (n > 1 ? n / 2 + 1 : 1) : n; }
+
+// slot layout -> natural layout for nvec vectors (maps[v]); vector v of candidate/query block
+// `blk` lives at slots + blk * sstride + soff, nat + blk * nstride + noff
+void slots_to_nat(int lattice, int nvec, int nblk, const VecMap* maps, const void* slots, long long sstride,
+                  void* nat, long long nstride, cudaStream_t s);
+void nat_to_slots(int lattice, int nvec, int nblk, const VecMap* maps, const void* nat, long long nstride,
+                  void* slots, long long sstride, cudaStream_t s);
+
+// factor in place; per-stage pivot partials: partial[s][blk] (logdet), bad[0] first failing
+// natural index (0x7f7f7f7f none), bad[1] non-real flag
+void fold_factor(const FoldDims& D, void* lam, double* partial, int nblk, int* bad, cudaStream_t s);
+// nrhs right-hand sides [nrhs][tot_task] in place: forward substitution (+ quad partials
+// qpart[r][s][blk]) and optionally back substitution (-> Lam^-1 rhs)
+void fold_solve(const FoldDims& D, const void* lam, void* rhs, int nrhs, double* qpart, int nblk, bool back,
+                cudaStream_t s);
+// out = Lam v (unfolded spectrum, natural layout), one right-hand side
+void fold_gram_apply(const FoldDims& D, const void* lam, const void* v, void* out, cudaStream_t s);
 
 }  // namespace fmtgp

@@ -658,6 +658,11 @@ void fwd_array(int lattice, const Geo& g, int nvec, const ArraySrc& src, const S
     fwd_impl(lattice, g, nvec, src, snk, work, tw, s);
 }
 
+void fwd_query(int lattice, const Geo& g, int nvec, const QuerySrc& src, const ScaleSink& snk, void* work,
+               const double2* tw, cudaStream_t s) {
+    fwd_impl(lattice, g, nvec, src, snk, work, tw, s);
+}
+
 int grad_blocks(int lattice, const Geo& g, bool split) {
     (void)lattice;
     if (split) return gen_blocks(1ll << g.m, GEN_EPT);

@@ -33,6 +33,8 @@ void fwd_gen(int lattice, const Geo& g, int nvec, const GenSrc& src, const SpecS
              const double2* tw, cudaStream_t s);
 void fwd_array(int lattice, const Geo& g, int nvec, const ArraySrc& src, const ScaleSink& snk, void* work,
                const double2* tw, cudaStream_t s);
+void fwd_query(int lattice, const Geo& g, int nvec, const QuerySrc& src, const ScaleSink& snk, void* work,
+               const double2* tw, cudaStream_t s);
 
 // inverse transforms of slot arrays (vector v at in + in_off[v]) into a sink
 void inv_grad(int lattice, const Geo& g, int nvec, const void* in, const long long* in_off, long long cstride,

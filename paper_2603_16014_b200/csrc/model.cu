@@ -18,6 +18,7 @@
 
 #include "../../include/fastmtgp_b200.h"
 #include "kernels.cuh"
+#include "fold.cuh"
 #include "posterior.cuh"
 #include "unequal.cuh"
 
@@ -262,6 +263,7 @@ struct fmtgp_model {
     };
     std::vector<GraphEntry> graphs;
     bool use_graphs = true;
+    long long spec_version = 0;  // bumped whenever d_lam is rewritten
 };
 
 namespace {
@@ -378,6 +380,7 @@ GenSrc gensrc_of(fmtgp_model* M, const Group& g, int si_alpha, const double* b) 
 
 // build_spectrum for nc candidates (fast_gram.cpp:42-89)
 void build_spectra(fmtgp_model* M, int nc, int si_alpha, const double* b) {
+    ++M->spec_version;
     for (auto& g : M->groups) {
         const int np = int(g.pairs.size());
         GenSrc src = gensrc_of(M, g, si_alpha, b);
@@ -561,6 +564,7 @@ void eval_equal(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, const doub
         CK(cudaGraphInstantiate(&ge->exec, graph, 0));
         cudaGraphDestroy(graph);
     }
+    ++M->spec_version;
     CK(cudaGraphLaunch(ge->exec, M->st));
     CK(cudaStreamSynchronize(M->st));
     if (prof) M->prof.add_graph(ge->recs);
@@ -829,7 +833,7 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
         CK(cudaMallocHost(reinterpret_cast<void**>(&M->h_out), sizeof(double) * NOUT * max_cand));
         CK(cudaMallocHost(reinterpret_cast<void**>(&M->h_bad), sizeof(int) * 2 * max_cand));
         CK(cudaMemsetAsync(M->d_yhat, 0, M->task_slots * es, M->st));
-        if (!M->equal) M->uneq = unequal::create(M);
+        M->uneq = unequal::create(M);
         CK(cudaStreamSynchronize(M->st));
     } catch (...) {
         fmtgp_model_destroy(M);

@@ -125,6 +125,53 @@ struct BufSrc {
     __device__ __forceinline__ double operator()(int v, uint64_t idx) const { return buf[v * n + idx]; }
 };
 
+// Kernel column of a query point against task l's design (posterior variance): value at
+// transform-input index idx of vector v = (query q, task l) is R_{t,l} Q(x_q, x_{l, i(idx)})
+// with the reference's floating SI difference for the free query coordinate
+// (kernel_against_data, gp_core.cpp:386-397).
+struct QuerySrc {
+    int family, d, si_alpha, m, ntg, pad_;
+    double b[4];
+    double gamma;
+    const double* X;          // [count][d]
+    const double* eta;        // [d]
+    const double* Rrow;       // [T] R_{task, l}
+    const uint64_t* g;        // lattice [d]
+    const uint64_t* cols;     // digital [d][m_cols]
+    int m_cols;
+    const uint64_t* shifts;   // [T][d]
+    const int* vec_task;      // [ntg] task of each vector of the group
+    __device__ double operator()(int v, uint64_t idx) const {
+        const int q = v / ntg, l = vec_task[v - q * ntg];
+        double prod = gamma;
+        for (int j = 0; j < d; ++j) {
+            const uint64_t sh = shifts[l * d + j];
+            const double xq = X[(long long)q * d + j];
+            double base;
+            if (family == 0) {
+                const uint64_t frac = ((idx * g[j]) & ((uint64_t(1) << m) - 1)) << (DIGITAL_BITS - m);
+                const double xp = double((frac + sh) & MASK53) * 0x1p-53;
+                const double diff = xq - xp;
+                const double u1 = diff - floor(diff), u2 = -diff - floor(-diff);
+                double u = fmin(u1, u2);
+                if (u >= 1.0) u = 0.0;
+                constexpr double pi2 = 9.869604401089358618834491;
+                base = si_alpha == 1 ? 2.0 * pi2 * (u * (u - 1.0) + 1.0 / 6.0)
+                                     : -(2.0 / 3.0) * pi2 * pi2 * (((u - 2.0) * u + 1.0) * u * u - 1.0 / 30.0);
+            } else {
+                uint64_t z = sh;
+                const uint64_t* c = cols + size_t(j) * m_cols;
+                uint64_t i = idx;
+                for (int p = 0; i; ++p, i >>= 1)
+                    if (i & 1) z ^= c[p];
+                base = dsi_walsh(uint64_t(xq * 0x1p53) ^ z, b);
+            }
+            prod *= 1.0 + eta[j] * base;
+        }
+        return Rrow[l] * prod;
+    }
+};
+
 // --------------------------------------------------------------------- forward sinks
 // lam = coef * A + xi, coef = R_ab * sqrt(n_b / n_a) (fast_gram.cpp:82-85).
 // Lattice slot 0 packs (A(0), A(n/2)): both real, both get + xi.
