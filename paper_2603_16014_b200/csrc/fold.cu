@@ -84,17 +84,18 @@ void nat_to_slots(int lattice, int nvec, int nblk, const VecMap* maps, const voi
 // Pivots of stage s: d_s = Re lam_ss (fast_gram.cpp:167-178 check_positive semantics).
 template <bool CX>
 __global__ void __launch_bounds__(256) k_pivot(FoldDims D, int s, const void* lam_v, double* partial, int nblk,
-                                               int* bad) {
+                                               int* bad, unsigned long long* imre) {
     using S = Sc<CX>;
     using V = typename S::T;
     const V* lss = static_cast<const V*>(lam_v) + D.poff[D.pid[s][s]];
     const long long n = D.n[s], H = D.H[s];
-    double acc = 0.0;
-    int first = 0x7f7f7f7f, nonreal = 0;
+    double acc = 0.0, imx = 0.0, rex = 0.0;
+    int first = 0x7f7f7f7f;
     for (long long i = blockIdx.x * 256ll + threadIdx.x; i < H; i += (long long)gridDim.x * 256) {
         const V v = lss[i];
         const double d = S::re(v);
-        if (fabs(S::im(v)) > 1e-8 * fmax(1.0, fabs(d))) nonreal = 1;
+        imx = fmax(imx, fabs(S::im(v)));
+        rex = fmax(rex, d);
         if (!(d > 0.0)) {
             if (i < first) first = int(i);
             continue;
@@ -105,7 +106,16 @@ __global__ void __launch_bounds__(256) k_pivot(FoldDims D, int s, const void* la
     acc = block_sum<256>(acc, red);
     if (threadIdx.x == 0) partial[s * nblk + blockIdx.x] = acc;
     if (first != 0x7f7f7f7f) atomicMin(bad, first);
-    if (nonreal) atomicOr(bad + 1, 1);
+    // stage maxima for the non-real test |Im S| > 1e-8 max(1, max Re S) (fast_gram.cpp:167-172)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        imx = fmax(imx, __shfl_xor_sync(0xffffffffu, imx, o));
+        rex = fmax(rex, __shfl_xor_sync(0xffffffffu, rex, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(imre + 2 * s, (unsigned long long)__double_as_longlong(imx));
+        atomicMax(imre + 2 * s + 1, (unsigned long long)__double_as_longlong(rex));
+    }
 }
 
 struct StagePairs {
@@ -137,12 +147,13 @@ __global__ void __launch_bounds__(256) k_fold_update(FoldDims D, int s, StagePai
     }
 }
 
-void fold_factor(const FoldDims& D, void* lam, double* partial, int nblk, int* bad, cudaStream_t s) {
+void fold_factor(const FoldDims& D, void* lam, double* partial, int nblk, int* bad, unsigned long long* imre,
+                 cudaStream_t s) {
     for (int st = 0; st < D.T; ++st) {
         {
             ProfScope ps("fold_pivot", s);
-            if (D.lattice) k_pivot<true><<<nblk, 256, 0, s>>>(D, st, lam, partial, nblk, bad);
-            else k_pivot<false><<<nblk, 256, 0, s>>>(D, st, lam, partial, nblk, bad);
+            if (D.lattice) k_pivot<true><<<nblk, 256, 0, s>>>(D, st, lam, partial, nblk, bad, imre);
+            else k_pivot<false><<<nblk, 256, 0, s>>>(D, st, lam, partial, nblk, bad, imre);
         }
         if (st + 1 == D.T) break;
         StagePairs sp{};

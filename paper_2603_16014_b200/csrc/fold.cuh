@@ -42,8 +42,9 @@ void nat_to_slots(int lattice, int nvec, int nblk, const VecMap* maps, const voi
                   void* slots, long long sstride, cudaStream_t s);
 
 // factor in place; per-stage pivot partials: partial[s][blk] (logdet), bad[0] first failing
-// natural index (0x7f7f7f7f none), bad[1] non-real flag
-void fold_factor(const FoldDims& D, void* lam, double* partial, int nblk, int* bad, cudaStream_t s);
+// natural index (0x7f7f7f7f none), imre[s] = (max |Im Lam_ss|, max pivot) as double bits
+void fold_factor(const FoldDims& D, void* lam, double* partial, int nblk, int* bad, unsigned long long* imre,
+                 cudaStream_t s);
 // nrhs right-hand sides [nrhs][tot_task] in place: forward substitution (+ quad partials
 // qpart[r][s][blk]) and optionally back substitution (-> Lam^-1 rhs)
 void fold_solve(const FoldDims& D, const void* lam, void* rhs, int nrhs, double* qpart, int nblk, bool back,

@@ -758,7 +758,7 @@ void inv_coef(int lattice, const Geo& g, int nvec, const void* in, const long lo
 template <int T, bool CX>
 __device__ __forceinline__ int ldl_solve(const typename Sc<CX>::T* A, const typename Sc<CX>::T* r, bool want_inv,
                                          double& logdet, double& quad, typename Sc<CX>::T* chat,
-                                         typename Sc<CX>::T* Ainv) {
+                                         typename Sc<CX>::T* Ainv, double* imx, double* rex) {
     using S = Sc<CX>;
     using V = typename S::T;
     V L[T][T];
@@ -770,13 +770,15 @@ __device__ __forceinline__ int ldl_solve(const typename Sc<CX>::T* A, const type
 #pragma unroll
     for (int s = 0; s < T; ++s) {
         double dd = S::re(A[pidx(s, s)]);
-        if (fabs(S::im(A[pidx(s, s)])) > 1e-8 * fmax(1.0, fabs(dd))) status = status ? status : 2;
+        // non-real check is global per stage (|Im S| vs 1e-8 max(1, max Re S)), fast_gram.cpp:167-172
+        imx[s] = fmax(imx[s], fabs(S::im(A[pidx(s, s)])));
 #pragma unroll
         for (int k = 0; k < s; ++k) dd -= S::abs2(L[s][k]) / dinv[k];
         if (!(dd > 0.0)) {
             status = 1;
             dd = 1.0;
         }
+        rex[s] = fmax(rex[s], dd);
         dinv[s] = 1.0 / dd;
         logdet += log(dd);
 #pragma unroll
@@ -847,7 +849,10 @@ __global__ void __launch_bounds__(256) k_solve_equal(SolveArgs a) {
     const V* lam = static_cast<const V*>(a.lam) + c * a.cstride;
     const V* yh = static_cast<const V*>(a.yhat);
     double ld_acc = 0.0, q_acc = 0.0;
-    int first_bad = INT_MAX, nonreal = 0;
+    int first_bad = INT_MAX;
+    double imx[T], rex[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) imx[t] = rex[t] = 0.0;
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < a.nslots;
          p += (long long)gridDim.x * blockDim.x) {
         V A[P], r[T], ch[T], Ai[P];
@@ -865,10 +870,10 @@ __global__ void __launch_bounds__(256) k_solve_equal(SolveArgs a) {
 #pragma unroll
                 for (int t = 0; t < T; ++t) r0[t] = 0.0, rN[t] = r[t].y;
                 const bool want = a.M || a.lam_inv;
-                int st0 = ldl_solve<T, false>(A0, r0, want, l0, q0, c0, I0);
+                int st0 = ldl_solve<T, false>(A0, r0, want, l0, q0, c0, I0, imx, rex);
                 int stN = 0;
                 if (a.has_nyq) {
-                    stN = ldl_solve<T, false>(AN, rN, want, lN, qN, cN, IN);
+                    stN = ldl_solve<T, false>(AN, rN, want, lN, qN, cN, IN, imx, rex);
                 } else {  // n == 1: no Nyquist frequency
                     lN = qN = 0.0;
 #pragma unroll
@@ -907,9 +912,8 @@ __global__ void __launch_bounds__(256) k_solve_equal(SolveArgs a) {
             }
         }
         double ld, qd;
-        const int st = ldl_solve<T, CX>(A, r, a.M || a.lam_inv, ld, qd, ch, Ai);
+        const int st = ldl_solve<T, CX>(A, r, a.M || a.lam_inv, ld, qd, ch, Ai, imx, rex);
         if (st == 1 && p < first_bad) first_bad = int(p);
-        if (st == 2) nonreal = 1;
         const double w = CX ? 2.0 : 1.0;  // lattice slot k >= 1 stands for k and n - k
         ld_acc += w * ld;
         q_acc += w * qd;
@@ -940,7 +944,20 @@ __global__ void __launch_bounds__(256) k_solve_equal(SolveArgs a) {
         a.partial[((size_t)c * a.nblk + blockIdx.x) * 2 + 1] = qs;
     }
     if (first_bad != INT_MAX) atomicMin(a.bad + c, first_bad);
-    if (nonreal) atomicOr(a.bad + gridDim.y + c, 1);
+    // per-stage maxima (non-negative doubles order like their bit patterns)
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+        double vi = imx[t], vr = rex[t];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            vi = fmax(vi, __shfl_xor_sync(0xffffffffu, vi, o));
+            vr = fmax(vr, __shfl_xor_sync(0xffffffffu, vr, o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicMax(a.imre + ((size_t)c * MAXT + t) * 2 + 0, (unsigned long long)__double_as_longlong(vi));
+            atomicMax(a.imre + ((size_t)c * MAXT + t) * 2 + 1, (unsigned long long)__double_as_longlong(vr));
+        }
+    }
 }
 
 template <int T>

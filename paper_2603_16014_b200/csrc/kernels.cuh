@@ -55,7 +55,8 @@ struct SolveArgs {
     void* lam_inv;          // [ncand][P][nslots]  Lam^-1 upper (nullptr: skip)
     void* chat;             // [ncand][T][nslots]  (nullptr: skip)
     double* partial;        // [ncand][nblk][2] (logdet, quad)
-    int* bad;               // [ncand] first failing slot (INT_MAX if none), nonreal flag in bad[ncand+c]
+    int* bad;               // [ncand] first failing slot (0x7f7f7f7f if none)
+    unsigned long long* imre;  // [ncand][MAXT][2] per-stage max |Im Lam_ss|, max pivot (double bits)
     int nblk;
 };
 void solve_equal(const SolveArgs& a, int ncand, cudaStream_t s);

@@ -228,6 +228,8 @@ struct fmtgp_model {
     double* d_psolve = nullptr;
     double* d_pgrad = nullptr;
     int* d_bad = nullptr;
+    unsigned long long* d_imre = nullptr;  // [max_cand][MAXT][2]
+    double* h_imre = nullptr;
     double* d_out = nullptr;
     int nblk_solve = 0, nblk_grad = 0;
     // scratch vectors for the seam calls
@@ -468,6 +470,7 @@ void eval_equal_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, boo
     build_spectra(M, nc, si_alpha, bw);
     CK(cudaMemsetAsync(M->d_bad, 0x7f, sizeof(int) * nc, M->st));
     CK(cudaMemsetAsync(M->d_bad + nc, 0, sizeof(int) * nc, M->st));
+    CK(cudaMemsetAsync(M->d_imre, 0, sizeof(unsigned long long) * 2 * MAXT * nc, M->st));
     SolveArgs sa{};
     sa.T = M->T;
     sa.P = M->P;
@@ -482,6 +485,7 @@ void eval_equal_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, boo
     sa.chat = keep_chat ? M->d_chat : nullptr;
     sa.partial = M->d_psolve;
     sa.bad = M->d_bad;
+    sa.imre = M->d_imre;
     sa.nblk = M->nblk_solve;
     solve_equal(sa, nc, M->st);
     CK(cudaGetLastError());
@@ -514,6 +518,16 @@ void eval_equal_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, boo
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(M->h_out, M->d_out, sizeof(double) * NOUT * nc, cudaMemcpyDeviceToHost, M->st));
     CK(cudaMemcpyAsync(M->h_bad, M->d_bad, sizeof(int) * 2 * nc, cudaMemcpyDeviceToHost, M->st));
+    CK(cudaMemcpyAsync(M->h_imre, M->d_imre, sizeof(double) * 2 * MAXT * nc, cudaMemcpyDeviceToHost, M->st));
+}
+
+// non-real Schur complement test of candidate c (fast_gram.cpp:167-172), stage-global like the reference
+bool nonreal_of(const fmtgp_model* M, int c) {
+    for (int t = 0; t < M->T; ++t) {
+        const double im = M->h_imre[(size_t(c) * MAXT + t) * 2], re = M->h_imre[(size_t(c) * MAXT + t) * 2 + 1];
+        if (im > 1e-8 * std::max(1.0, re)) return true;
+    }
+    return false;
 }
 
 // One batched evaluation attempt (equal n).  Results land in M->h_out / M->h_bad.  The first
@@ -615,7 +629,7 @@ void nll_batch_impl(fmtgp_model* M, int nc, const fmtgp_hyper* hin, bool grad, f
             for (int i = 0; i < cnt; ++i) {
                 const int c = todo[base + i];
                 out[c] = tmp[i];
-                if (M->h_bad[cnt + i]) status[c] = FMTGP_ERR_NONREAL;
+                if (nonreal_of(M, i)) status[c] = FMTGP_ERR_NONREAL;
                 else if (M->h_bad[i] != BAD_NONE) status[c] = FMTGP_ERR_SCHUR;
                 else status[c] = FMTGP_OK;
             }
@@ -825,6 +839,8 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
         }
         M->d_psolve = dalloc<double>(size_t(max_cand) * std::max(M->nblk_solve, 1) * 3);
         M->d_bad = dalloc<int>(2 * size_t(max_cand));
+        M->d_imre = dalloc<unsigned long long>(2 * MAXT * size_t(max_cand));
+        CK(cudaMallocHost(reinterpret_cast<void**>(&M->h_imre), sizeof(double) * 2 * MAXT * max_cand));
         M->d_out = dalloc<double>(size_t(max_cand) * NOUT);
         M->d_vecA = dalloc<double>(M->N);
         M->d_vecB = dalloc<double>(M->N);
@@ -913,6 +929,8 @@ int fmtgp_model_destroy(fmtgp_model_t M) {
     F(M->d_psolve);
     F(M->d_pgrad);
     F(M->d_bad);
+    F(M->d_imre);
+    if (M->h_imre) cudaFreeHost(M->h_imre);
     F(M->d_out);
     F(M->d_vecA);
     F(M->d_vecB);
@@ -1038,6 +1056,8 @@ int fmtgp_invert_and_logdet(fmtgp_model_t M, double* logdet) {
         sa.lam_inv = M->d_laminv;
         sa.partial = M->d_psolve;
         sa.bad = M->d_bad;
+        sa.imre = M->d_imre;
+        CK(cudaMemsetAsync(M->d_imre, 0, sizeof(unsigned long long) * 2 * MAXT, M->st));
         sa.nblk = M->nblk_solve;
         solve_equal(sa, 1, M->st);
         FinalArgs fa{};
@@ -1052,8 +1072,9 @@ int fmtgp_invert_and_logdet(fmtgp_model_t M, double* logdet) {
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(M->h_out, M->d_out, sizeof(double) * NOUT, cudaMemcpyDeviceToHost, M->st));
         CK(cudaMemcpyAsync(M->h_bad, M->d_bad, sizeof(int) * 2, cudaMemcpyDeviceToHost, M->st));
+        CK(cudaMemcpyAsync(M->h_imre, M->d_imre, sizeof(double) * 2 * MAXT, cudaMemcpyDeviceToHost, M->st));
         CK(cudaStreamSynchronize(M->st));
-        if (M->h_bad[1]) throw Fail{FMTGP_ERR_NONREAL, "invert_and_logdet: non-real Schur complement"};
+        if (nonreal_of(M, 0)) throw Fail{FMTGP_ERR_NONREAL, "invert_and_logdet: non-real Schur complement"};
         if (M->h_bad[0] != BAD_NONE)
             throw Fail{FMTGP_ERR_SCHUR, "non-positive Schur entry at slot " + std::to_string(M->h_bad[0])};
         M->last_logdet = M->h_out[OUT_LOGDET];
