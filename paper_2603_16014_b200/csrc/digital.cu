@@ -1,0 +1,324 @@
+// Equal-n digital-net fit in three fused kernels — see digital.cuh.
+#include "digital.cuh"
+
+namespace fmtgp {
+
+bool DigGeo::make(int m, int P, DigGeo& g) {
+    if (m < 1 || P < 1) return false;
+    // row length: all P rows of one frequency block in <= 64 KB of smem
+    int l2max = 0;
+    while (l2max < 13 && (long long)P * (2ll << l2max) * 8 <= 65536) ++l2max;
+    int l2 = std::min(l2max, (m + 1) / 2);
+    l2 = std::max(l2, m - 11);  // column length <= 2^11
+    if (l2 > l2max || l2 > m || l2 < 0) return false;
+    g.m = m;
+    g.l2 = l2;
+    g.l1 = m - l2;
+    g.lc = std::min(11 - g.l1, l2);
+    if (g.lc < 0) return false;
+    const int tile = 1 << (g.l1 + g.lc);
+    g.nt_col = std::max(32, std::min(512, tile / EPT));
+    int need = (P << l2) / EPT;
+    int nt = 32;
+    while (nt < need && nt < 512) nt <<= 1;
+    if (nt * EPT < (P << l2)) return false;
+    g.nt_mid = nt;
+    g.nblk_col = (1 << l2) >> g.lc;
+    return true;
+}
+
+// ------------------------------------------------------------------ design-time kappa table
+template <int D>
+__global__ void __launch_bounds__(GEN_NT_DIG) k_kappa_table(GenSrc g, const uint64_t* ofs, long long n, double* kap) {
+    __shared__ GenSmem<D> t;
+    gen_smem_init<D>(t, g, 0, /*load_eta=*/false);
+    const int o = blockIdx.y;
+    uint64_t off[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) off[j] = ofs[size_t(o) * MAXD + j];
+    __syncthreads();
+    for (long long i = blockIdx.x * (long long)GEN_NT_DIG + threadIdx.x; i < n; i += (long long)gridDim.x * GEN_NT_DIG) {
+        double kappa[D];
+        kappa_d<D>(g, t, off, i, kappa);
+#pragma unroll
+        for (int j = 0; j < D; ++j) kap[(size_t(o) * D + j) * n + i] = kappa[j];
+    }
+}
+
+void dig_kappa_table(const Spatial& sp, const PointGen& pg, const uint64_t* d_ofs, int nofs, long long n, double* kap,
+                     cudaStream_t s) {
+    GenSrc g{};
+    g.sp = sp;
+    g.pg = pg;
+    const long long b = std::min<long long>((n + GEN_NT_DIG - 1) / GEN_NT_DIG, 2048);
+    ProfScope ps("kappa_table", s);
+    FM_D_DISPATCH(sp.d, k_kappa_table<D><<<dim3(unsigned(b), nofs), GEN_NT_DIG, 0, s>>>(g, d_ofs, n, kap))
+}
+
+// ------------------------------------------------------------------ K1: generator x column FWHT
+template <int NT, int D>
+__global__ void __launch_bounds__(NT) k_dig_col_fwd(DigArgs a, int l1, int l2, int lc) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ GenSmem<D> tab;
+    const int v = blockIdx.y, c = v / a.P, p = v - c * a.P;
+    const int C = 1 << lc, N1 = 1 << l1, ld = N1 + 1;
+    const long long c0 = (long long)blockIdx.x << lc, n = a.n;
+    double eta[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) eta[j] = __ldg(a.eta + size_t(c) * D + j);
+    const double gam = __ldg(a.gamma + c);
+    GenSrc g{};
+    uint64_t off[D];
+    if (!a.kap) {
+        g.sp = a.sp;
+        g.pg = a.pg;
+        g.eta = a.eta;
+        gen_smem_init<D>(tab, g, c);
+#pragma unroll
+        for (int j = 0; j < D; ++j) off[j] = __ldg(a.offs + size_t(p) * MAXD + j);
+        __syncthreads();
+    }
+    const double* kp = a.kap ? a.kap + size_t(__ldg(a.pair_ofs + p)) * D * n : nullptr;
+    for (int e = threadIdx.x; e < (C << l1); e += NT) {
+        const int j1 = e >> lc, cc = e & (C - 1);
+        const long long i = ((long long)j1 << l2) + c0 + cc;
+        double kappa[D];
+        if (kp) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) kappa[j] = __ldg(kp + size_t(j) * n + i);
+        } else {
+            kappa_d<D>(g, tab, off, uint64_t(i), kappa);
+        }
+        sm[cc * ld + j1] = product_kernel_d<D, false>(kappa, eta, gam, nullptr);
+    }
+    __syncthreads();
+    smem_wht<NT>(sm, l1, C, ld);
+    double* out = a.Y + size_t(v) * n;
+    for (int e = threadIdx.x; e < (C << l1); e += NT) {
+        const int k1 = e >> lc, cc = e & (C - 1);
+        out[((long long)k1 << l2) + c0 + cc] = sm[cc * ld + k1];
+    }
+}
+
+// ------------------------------------------------------------------ K2: row FWHT + solve + inverse row FWHT
+template <int NT, int T>
+__global__ void __launch_bounds__(NT) k_dig_mid(DigArgs a, int l2) {
+    constexpr int P = T * (T + 1) / 2;
+    extern __shared__ __align__(16) double sm[];  // [P][N2]
+    const int row = blockIdx.x, c = blockIdx.y, N2 = 1 << l2;
+    const long long n = a.n, base = (long long)row << l2;
+    double* Yc = a.Y + size_t(c) * P * n;
+    for (int e = threadIdx.x; e < (P << l2); e += NT) {
+        const int p = e >> l2, k2 = e & (N2 - 1);
+        sm[e] = Yc[size_t(p) * n + base + k2];
+    }
+    __syncthreads();
+    smem_wht<NT>(sm, l2, P, N2);
+    double coef[P], xi[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+        coef[q] = __ldg(a.coef + size_t(c) * P + q);
+        xi[q] = __ldg(a.xi + size_t(c) * P + q);
+    }
+    double ld_acc = 0.0, q_acc = 0.0, imx[T], rex[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) imx[t] = rex[t] = 0.0;
+    int first_bad = 0x7f7f7f7f;
+    for (int k2 = threadIdx.x; k2 < N2; k2 += NT) {
+        const long long k = base + k2;
+        double A[P], r[T], ch[T], Ai[P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            A[q] = fma(coef[q], sm[q * N2 + k2], xi[q]);  // lam = R_ab * H q + xi (fast_gram.cpp:82-85)
+            if (a.lam_out) a.lam_out[(size_t(c) * P + q) * n + k] = A[q];
+        }
+#pragma unroll
+        for (int t = 0; t < T; ++t) r[t] = k == 0 ? 0.0 : __ldg(a.yhat + size_t(t) * n + k);
+        double ld, qd;
+        const int st = ldl_solve<T, false>(A, r, a.want_grad != 0, ld, qd, ch, Ai, imx, rex);
+        if (st == 1 && int(k) < first_bad) first_bad = int(k);
+        ld_acc += ld;
+        q_acc += qd;
+        if (a.want_grad) {
+            int q = 0;
+#pragma unroll
+            for (int x = 0; x < T; ++x)
+#pragma unroll
+                for (int y = x; y < T; ++y, ++q) sm[q * N2 + k2] = Ai[q] - ch[x] * ch[y];  // M
+        }
+        if (a.chat_out && c == 0) {
+#pragma unroll
+            for (int t = 0; t < T; ++t) a.chat_out[size_t(t) * n + k] = ch[t];
+        }
+    }
+    __shared__ double red[32];
+    ld_acc = block_sum<NT>(ld_acc, red);
+    q_acc = block_sum<NT>(q_acc, red);
+    const int nrows = gridDim.x;
+    if (threadIdx.x == 0) {
+        a.part_mid[(size_t(c) * nrows + row) * 2 + 0] = ld_acc;
+        a.part_mid[(size_t(c) * nrows + row) * 2 + 1] = q_acc;
+    }
+    if (first_bad != 0x7f7f7f7f) atomicMin(a.bad + c, first_bad);
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+        double vi = imx[t], vr = rex[t];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            vi = fmax(vi, __shfl_xor_sync(0xffffffffu, vi, o));
+            vr = fmax(vr, __shfl_xor_sync(0xffffffffu, vr, o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicMax(a.imre + (size_t(c) * MAXT + t) * 2 + 0, (unsigned long long)__double_as_longlong(vi));
+            atomicMax(a.imre + (size_t(c) * MAXT + t) * 2 + 1, (unsigned long long)__double_as_longlong(vr));
+        }
+    }
+    if (!a.want_grad) return;
+    __syncthreads();
+    smem_wht<NT>(sm, l2, P, N2);  // inverse FWHT over the row bits (self-inverse up to scale)
+    for (int e = threadIdx.x; e < (P << l2); e += NT) {
+        const int p = e >> l2, k2 = e & (N2 - 1);
+        Yc[size_t(p) * n + base + k2] = sm[e];
+    }
+}
+
+// ------------------------------------------------------------------ K3: column FWHT -> W -> gradient dot
+template <int NT, int D>
+__global__ void __launch_bounds__(NT) k_dig_col_inv(DigArgs a, int l1, int l2, int lc, int nrows) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ GenSmem<D> tab;
+    __shared__ double red[32];
+    __shared__ int s_last;
+    const int v = blockIdx.y, c = v / a.P, p = v - c * a.P;
+    const int C = 1 << lc, N1 = 1 << l1, ld = N1 + 1;
+    const long long c0 = (long long)blockIdx.x << lc, n = a.n;
+    const double* x = a.Y + size_t(v) * n;
+    for (int e = threadIdx.x; e < (C << l1); e += NT) {
+        const int k1 = e >> lc, cc = e & (C - 1);
+        sm[cc * ld + k1] = x[((long long)k1 << l2) + c0 + cc];
+    }
+    double eta[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) eta[j] = __ldg(a.eta + size_t(c) * D + j);
+    const double gam = __ldg(a.gamma + c);
+    GenSrc g{};
+    uint64_t off[D];
+    if (!a.kap) {
+        g.sp = a.sp;
+        g.pg = a.pg;
+        g.eta = a.eta;
+        gen_smem_init<D>(tab, g, c);
+#pragma unroll
+        for (int j = 0; j < D; ++j) off[j] = __ldg(a.offs + size_t(p) * MAXD + j);
+    }
+    __syncthreads();
+    smem_wht<NT>(sm, l1, C, ld);
+    const double* kp = a.kap ? a.kap + size_t(__ldg(a.pair_ofs + p)) * D * n : nullptr;
+    double acc[D + 1];
+#pragma unroll
+    for (int j = 0; j <= D; ++j) acc[j] = 0.0;
+    for (int e = threadIdx.x; e < (C << l1); e += NT) {
+        const int j1 = e >> lc, cc = e & (C - 1);
+        const long long i = ((long long)j1 << l2) + c0 + cc;
+        const double W = sm[cc * ld + j1];  // W = H M (unnormalised), natural index i
+        double kappa[D], dq[D];
+        if (kp) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) kappa[j] = __ldg(kp + size_t(j) * n + i);
+        } else {
+            kappa_d<D>(g, tab, off, uint64_t(i), kappa);
+        }
+        const double q = product_kernel_d<D, true>(kappa, eta, gam, dq);
+#pragma unroll
+        for (int j = 0; j < D; ++j) acc[j] = fma(W, dq[j], acc[j]);
+        acc[D] = fma(W, q, acc[D]);
+    }
+    const int nblk = gridDim.x;
+    double* out = a.part_dot + ((size_t(c) * a.P + p) * nblk + blockIdx.x) * (MAXD + 1);
+#pragma unroll
+    for (int j = 0; j <= D; ++j) {
+        const double s = block_sum<NT>(acc[j], red);
+        if (threadIdx.x == 0) out[j == D ? MAXD : j] = s;
+    }
+    // last CTA of this candidate reduces everything (threadFenceReduction pattern)
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned total = unsigned(a.P) * nblk;
+        const unsigned ticket = atomicAdd(a.counter + c, 1u);
+        s_last = ticket == total - 1;
+        if (s_last) a.counter[c] = 0;  // self-reset for the next replay
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    FinalArgs fa{};
+    fa.T = a.T;
+    fa.P = a.P;
+    fa.d = D;
+    fa.ncand = a.nc;
+    fa.nblk_solve = nrows;
+    fa.nblk_grad = nblk;
+    fa.solve_partial = a.part_mid;
+    fa.grad_partial = a.part_dot;
+    fa.Rpair = a.Rpair;
+    fa.gamma = a.gamma;
+    fa.pair_a = a.pair_a;
+    fa.pair_b = a.pair_b;
+    fa.out = a.out;
+    finalize_candidate<NT>(fa, c);
+}
+
+// ------------------------------------------------------------------ launcher
+template <class K>
+static void set_smem_dig(K kern, size_t bytes) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+}
+
+template <int T>
+static void mid_launch(const DigGeo& g, const DigArgs& a, size_t sm, cudaStream_t s) {
+    const dim3 grid(1u << g.l1, a.nc);
+    FM_NT_DISPATCH(g.nt_mid, {
+        auto k = k_dig_mid<NT, T>;
+        set_smem_dig(k, sm);
+        ProfScope ps("dig_mid", s);
+        k<<<grid, NT, sm, s>>>(a, g.l2);
+    })
+}
+
+void dig_fit(const DigGeo& g, const DigArgs& a, cudaStream_t s) {
+    const int C = 1 << g.lc;
+    const size_t sm_col = size_t(C) * ((1 << g.l1) + 1) * sizeof(double);
+    const dim3 gcol(g.nblk_col, a.P * a.nc);
+    FM_D_DISPATCH(a.d, {
+        FM_NT_DISPATCH(g.nt_col, {
+            auto k1 = k_dig_col_fwd<NT, D>;
+            set_smem_dig(k1, sm_col);
+            ProfScope ps("dig_col_fwd", s);
+            k1<<<gcol, NT, sm_col, s>>>(a, g.l1, g.l2, g.lc);
+        })
+    })
+    const size_t sm_mid = size_t(a.P) << g.l2 << 3;
+    switch (a.T) {
+        case 1: mid_launch<1>(g, a, sm_mid, s); break;
+        case 2: mid_launch<2>(g, a, sm_mid, s); break;
+        case 3: mid_launch<3>(g, a, sm_mid, s); break;
+        case 4: mid_launch<4>(g, a, sm_mid, s); break;
+        case 5: mid_launch<5>(g, a, sm_mid, s); break;
+        case 6: mid_launch<6>(g, a, sm_mid, s); break;
+        case 7: mid_launch<7>(g, a, sm_mid, s); break;
+        default: mid_launch<8>(g, a, sm_mid, s); break;
+    }
+    if (!a.want_grad) return;
+    const int nrows = 1 << g.l1;
+    FM_D_DISPATCH(a.d, {
+        FM_NT_DISPATCH(g.nt_col, {
+            auto k3 = k_dig_col_inv<NT, D>;
+            set_smem_dig(k3, sm_col);
+            ProfScope ps("dig_col_inv", s);
+            k3<<<gcol, NT, sm_col, s>>>(a, g.l1, g.l2, g.lc, nrows);
+        })
+    })
+}
+
+}  // namespace fmtgp

@@ -1,0 +1,60 @@
+// Equal-n digital-net (DSI / FWHT) fit in three fused kernels — the configuration-2/5 hot path.
+//
+//   K1 k_dig_col_fwd : generator q_ab(i) (design-time kappa table or on the fly) x column FWHT
+//   K2 k_dig_mid     : row FWHT of every pair + spectrum epilogue (R, xi) + per-frequency T x T
+//                      LDL^H solve (logdet, quad, M = Lam^-1 - chat chat^H) + inverse row FWHT of M
+//   K3 k_dig_col_inv : inverse column FWHT -> W = H M -> gradient dot with dq/deta, q -> partials,
+//                      last CTA reduces everything into the result record
+//
+// n = N1 * N2 (natural index i = j1 * N2 + j2); FWHT over the two bit groups commutes, and the
+// spectrum index after both passes is natural, so K2 owns the frequencies {k1 * N2 + k2}: all
+// pairs of one frequency meet in one CTA and the solve needs no extra HBM round trip — the
+// fused four-step of SURVEY.md §8d (8n(6P+T) bytes instead of 8n(8P+T)).
+#pragma once
+
+#include "kernels.cuh"
+
+namespace fmtgp {
+
+struct DigGeo {
+    int m, l1, l2;   // n = 2^m = 2^l1 (columns) * 2^l2 (rows)
+    int lc;          // log2 columns per K1/K3 CTA (tile = 2^(l1 + lc) <= 2^11)
+    int nt_col, nt_mid;
+    int nblk_col;    // K1/K3 CTAs per vector
+    static bool make(int m, int P, DigGeo& g);
+};
+
+struct DigArgs {
+    int T, P, d, nc;
+    long long n;
+    Spatial sp;
+    PointGen pg;
+    const uint64_t* offs;     // [P][MAXD]
+    const double* kap;        // design-time table [nofs][d][n] (nullptr: evaluate on the fly)
+    const int* pair_ofs;      // [P] pair -> distinct offset index
+    const double* eta;        // [nc][d]
+    const double* gamma;      // [nc]
+    const double* coef;       // [nc][P]  R_ab
+    const double* xi;         // [nc][P]
+    const double* Rpair;      // [nc][P]
+    const int* pair_a;
+    const int* pair_b;
+    const double* yhat;       // [T][n]
+    double* Y;                // [nc][P][n] intermediate (column pass out, row pass in/out)
+    double* lam_out;          // [nc][P][n] spectrum (nullptr: skip)
+    double* chat_out;         // [T][n] chat of candidate 0 (nullptr: skip)
+    double* part_mid;         // [nc][nrows][2]
+    double* part_dot;         // [nc][P][nblk_col][MAXD+1]
+    int* bad;                 // [nc] first failing slot, 0x7f7f7f7f none
+    unsigned long long* imre; // [nc][MAXT][2]
+    unsigned int* counter;    // [nc] last-CTA tickets (self-resetting)
+    double* out;              // [nc][NOUT]
+    int want_grad;
+};
+
+// design-time kappa table: kap[o][j][i] = dsi_walsh(z_i ^ off_o[j], b)
+void dig_kappa_table(const Spatial& sp, const PointGen& pg, const uint64_t* d_ofs /*[nofs][MAXD]*/, int nofs,
+                     long long n, double* kap, cudaStream_t s);
+void dig_fit(const DigGeo& g, const DigArgs& a, cudaStream_t s);
+
+}  // namespace fmtgp

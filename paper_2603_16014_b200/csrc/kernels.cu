@@ -161,61 +161,6 @@ __global__ void __launch_bounds__(NT) k_fwd_row_dig(const double* __restrict__ Y
 // sets the parallelism.  Compile-time dimension D keeps kappa / dq / accumulators in
 // registers.  Digital z_i comes from two 32-entry XOR tables per dimension in smem, X3 of
 // the order-4 Walsh kernel from an 8-bit table.
-template <int D>
-struct GenSmem {
-    uint64_t lo[D][32], mid[D][32];
-    double T8[256];
-    double eta[D];
-};
-
-template <int D>
-__device__ __forceinline__ void gen_smem_init(GenSmem<D>& t, const GenSrc& g, int c) {
-    if (g.sp.family == 1) {
-        for (int e = threadIdx.x; e < D * 64; e += blockDim.x) {
-            const int j = e >> 6, r = e & 63;
-            const int shift = r < 32 ? 0 : 5;
-            const int val = r & 31;
-            uint64_t z = 0;
-            const uint64_t* col = g.pg.cols + size_t(j) * g.pg.m_cols;
-            for (int p = 0; p < 5; ++p)
-                if (((val >> p) & 1) && p + shift < g.pg.m_cols) z ^= __ldg(col + p + shift);
-            if (r < 32) t.lo[j][val] = z;
-            else t.mid[j][val] = z;
-        }
-        for (int b = threadIdx.x; b < 256; b += blockDim.x) {
-            double acc = 0.0;
-            for (int i = 7; i >= 0; --i)  // smallest terms first
-                if ((b >> (7 - i)) & 1) acc += pow2i(-3 * i);
-            t.T8[b] = acc;
-        }
-    }
-    for (int j = threadIdx.x; j < D; j += blockDim.x) t.eta[j] = g.eta[size_t(c) * D + j];
-}
-
-template <int D>
-__device__ __forceinline__ void kappa_d(const GenSrc& g, const GenSmem<D>& t, const uint64_t* off, uint64_t idx,
-                                        double* kappa) {
-    if (g.sp.family == 0) {
-#pragma unroll
-        for (int j = 0; j < D; ++j) kappa[j] = si_base(g.pg.lattice_word(idx, j, off[j]), g.sp.si_alpha);
-        return;
-    }
-    const uint64_t hi = idx >> 10;
-    const bool only4 = g.sp.b[0] == 0.0 && g.sp.b[1] == 0.0 && g.sp.b[2] == 0.0;
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-        uint64_t z = t.lo[j][idx & 31] ^ t.mid[j][(idx >> 5) & 31];
-        if (hi) {
-            const uint64_t* col = g.pg.cols + size_t(j) * g.pg.m_cols + 10;
-            uint64_t h = hi;
-            for (int q = 0; h; ++q, h >>= 1)
-                if (h & 1) z ^= __ldg(col + q);
-        }
-        const uint64_t w = z ^ off[j];
-        kappa[j] = only4 ? g.sp.b[3] * dsi_order4_t8(w, t.T8) : dsi_walsh(w, g.sp.b);
-    }
-}
-
 constexpr int GEN_NT = 256;
 constexpr int GEN_EPT = 4;  // elements per thread per block (dot kernel partial count)
 
@@ -273,21 +218,6 @@ __global__ void __launch_bounds__(GEN_NT) k_gen_dot(GradSink gs, const double* _
         if (threadIdx.x == 0) out[j == D ? MAXD : j] = s;
     }
 }
-
-#define FM_D_DISPATCH(d, ...)                                                                          \
-    switch (d) {                                                                                       \
-        FM_D_CASE(1, __VA_ARGS__) FM_D_CASE(2, __VA_ARGS__) FM_D_CASE(3, __VA_ARGS__)                  \
-        FM_D_CASE(4, __VA_ARGS__) FM_D_CASE(5, __VA_ARGS__) FM_D_CASE(6, __VA_ARGS__)                  \
-        FM_D_CASE(7, __VA_ARGS__) FM_D_CASE(8, __VA_ARGS__) FM_D_CASE(9, __VA_ARGS__)                  \
-        FM_D_CASE(10, __VA_ARGS__) FM_D_CASE(11, __VA_ARGS__) FM_D_CASE(12, __VA_ARGS__)               \
-        FM_D_CASE(13, __VA_ARGS__) FM_D_CASE(14, __VA_ARGS__) FM_D_CASE(15, __VA_ARGS__)               \
-        FM_D_CASE(16, __VA_ARGS__) default : break;                                                    \
-    }
-#define FM_D_CASE(V, ...)    \
-    case V: {                \
-        constexpr int D = V; \
-        __VA_ARGS__;         \
-    } break;
 
 // ============================================================================ inverse sinks (device side)
 struct GradAcc {
@@ -561,21 +491,6 @@ static int nt_for(int tl) {
     return nt < 32 ? 32 : (nt > 512 ? 512 : nt);
 }
 
-#define FM_NT_CASE(V, ...)     \
-    case V: {                  \
-        constexpr int NT = V;  \
-        __VA_ARGS__;           \
-    } break;
-#define FM_NT_DISPATCH(nt, ...)                                                                      \
-    switch (nt) {                                                                                    \
-        FM_NT_CASE(32, __VA_ARGS__) FM_NT_CASE(64, __VA_ARGS__) FM_NT_CASE(128, __VA_ARGS__)         \
-        FM_NT_CASE(256, __VA_ARGS__) default : {                                                      \
-            constexpr int NT = 512;                                                                  \
-            __VA_ARGS__;                                                                             \
-        }                                                                                            \
-        break;                                                                                       \
-    }
-
 template <class Src, class Snk>
 static void fwd_impl(int lattice, const Geo& g, int nvec, const Src& src, const Snk& snk, void* work,
                      const double2* tw, cudaStream_t s) {
@@ -752,94 +667,6 @@ void inv_coef(int lattice, const Geo& g, int nvec, const void* in, const long lo
 }
 
 // ============================================================================ per-frequency T x T solve
-// Hermitian LDL^H of A (upper pairs, row by row), T <= 8.  Pivots are the diagonal Schur
-// complements of Algorithm 1 (fast_gram.cpp:167-178): logdet = sum log d_s.
-// Returns 0 ok, 1 non-positive pivot (SchurBreakdown), 2 non-real diagonal (FastMtgpError).
-template <int T, bool CX>
-__device__ __forceinline__ int ldl_solve(const typename Sc<CX>::T* A, const typename Sc<CX>::T* r, bool want_inv,
-                                         double& logdet, double& quad, typename Sc<CX>::T* chat,
-                                         typename Sc<CX>::T* Ainv, double* imx, double* rex) {
-    using S = Sc<CX>;
-    using V = typename S::T;
-    V L[T][T];
-    double dinv[T];
-    int status = 0;
-    // pair index of (a,b), a <= b, row by row (fast_gram.cpp:35-40)
-    auto pidx = [](int a, int b) { return a * T - a * (a - 1) / 2 + (b - a); };
-    logdet = 0.0;
-#pragma unroll
-    for (int s = 0; s < T; ++s) {
-        double dd = S::re(A[pidx(s, s)]);
-        // non-real check is global per stage (|Im S| vs 1e-8 max(1, max Re S)), fast_gram.cpp:167-172
-        imx[s] = fmax(imx[s], fabs(S::im(A[pidx(s, s)])));
-#pragma unroll
-        for (int k = 0; k < s; ++k) dd -= S::abs2(L[s][k]) / dinv[k];
-        if (!(dd > 0.0)) {
-            status = 1;
-            dd = 1.0;
-        }
-        rex[s] = fmax(rex[s], dd);
-        dinv[s] = 1.0 / dd;
-        logdet += log(dd);
-#pragma unroll
-        for (int i = s + 1; i < T; ++i) {
-            V acc = S::conj(A[pidx(s, i)]);
-#pragma unroll
-            for (int k = 0; k < s; ++k) acc = S::sub(acc, S::scale(S::mulc(L[i][k], L[s][k]), 1.0 / dinv[k]));
-            L[i][s] = S::scale(acc, dinv[s]);
-        }
-    }
-    // z = L^-1 r, quad = sum |z|^2 / d
-    V z[T];
-    quad = 0.0;
-#pragma unroll
-    for (int i = 0; i < T; ++i) {
-        V acc = r[i];
-#pragma unroll
-        for (int k = 0; k < i; ++k) acc = S::sub(acc, S::mul(L[i][k], z[k]));
-        z[i] = acc;
-        quad += S::abs2(acc) * dinv[i];
-    }
-    // chat = L^-H D^-1 z
-#pragma unroll
-    for (int i = T - 1; i >= 0; --i) {
-        V acc = S::scale(z[i], dinv[i]);
-#pragma unroll
-        for (int k = i + 1; k < T; ++k) acc = S::sub(acc, S::mul(S::conj(L[k][i]), chat[k]));
-        chat[i] = acc;
-    }
-    if (want_inv) {
-        // X = L^-1 (unit lower); Ainv_ab = sum_{s >= max(a,b)} conj(X_sa) X_sb / d_s
-        V X[T][T];
-#pragma unroll
-        for (int j = 0; j < T; ++j)
-#pragma unroll
-            for (int i = j + 1; i < T; ++i) {
-                V acc = S::sub(S::zero(), L[i][j]);
-#pragma unroll
-                for (int k = j + 1; k < i; ++k) acc = S::sub(acc, S::mul(L[i][k], X[k][j]));
-                X[i][j] = acc;
-            }
-#pragma unroll
-        for (int a = 0; a < T; ++a)
-#pragma unroll
-            for (int b = a; b < T; ++b) {
-                V acc = S::zero();
-#pragma unroll
-                for (int s = b; s < T; ++s) {
-                    // conj(X_sa) X_sb with X_ss = 1
-                    V term;
-                    if (s == a) term = S::one();  // then b == a == s
-                    else if (s == b) term = S::conj(X[s][a]);
-                    else term = S::mulc(X[s][b], X[s][a]);
-                    acc = S::add(acc, S::scale(term, dinv[s]));
-                }
-                Ainv[pidx(a, b)] = acc;
-            }
-    }
-    return status;
-}
-
 template <int T, bool CX>
 __global__ void __launch_bounds__(256) k_solve_equal(SolveArgs a) {
     using S = Sc<CX>;
@@ -984,60 +811,7 @@ void solve_equal(const SolveArgs& a, int ncand, cudaStream_t s) {
 // ============================================================================ finalize
 // Deterministic fixed-order reductions of the per-block partials into the per-candidate
 // result record (NLL = r^T c + logdet, gp_core.cpp:207-211; gradient chain to R, eta, gamma).
-__global__ void __launch_bounds__(256) k_finalize(FinalArgs a) {
-    const int c = blockIdx.x;
-    double* out = a.out + (size_t)c * NOUT;
-    __shared__ double red[32];
-    __shared__ double S[MAXP][MAXD + 1];
-    const int d = a.d, P = a.P;
-    double ld = 0.0, q = 0.0;
-    for (int b = threadIdx.x; b < a.nblk_solve; b += 256) {
-        ld += a.solve_partial[((size_t)c * a.nblk_solve + b) * 2 + 0];
-        q += a.solve_partial[((size_t)c * a.nblk_solve + b) * 2 + 1];
-    }
-    ld = block_sum<256>(ld, red);
-    q = block_sum<256>(q, red);
-    if (threadIdx.x == 0) {
-        out[OUT_LOGDET] = ld;
-        out[OUT_QUAD] = q;
-        out[OUT_NLL] = q + ld;  // rT c + logdet (gp_core.cpp:207-211)
-    }
-    if (!a.grad_partial) return;
-    // one warp per (pair, component): fixed-order strided sums + warp tree (deterministic)
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int t = warp; t < P * (MAXD + 1); t += 256 / 32) {
-        const int p = t / (MAXD + 1), i = t % (MAXD + 1);
-        double acc = 0.0;
-        if (i < d || i == MAXD)
-            for (int b = lane; b < a.nblk_grad; b += 32)
-                acc += a.grad_partial[(((size_t)c * P + p) * a.nblk_grad + b) * (MAXD + 1) + i];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) S[p][i] = acc;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double dgam = 0.0;
-        double deta[MAXD];
-        for (int j = 0; j < MAXD; ++j) deta[j] = 0.0;
-        for (int x = 0; x < MAXT * MAXT; ++x) out[OUT_DR + x] = 0.0;
-        for (int p = 0; p < P; ++p) {
-            const int pa = a.pair_a[p], pb = a.pair_b[p];
-            const double w = pa == pb ? 1.0 : 2.0;
-            const double Rp = a.Rpair[(size_t)c * P + p];
-            const double dRp = w * S[p][MAXD];  // dNLL / dR_ab, symmetric pair counted once
-            for (int j = 0; j < d; ++j) deta[j] += w * Rp * S[p][j];
-            dgam += w * Rp * S[p][MAXD];
-            if (pa == pb) out[OUT_DR + pa * MAXT + pb] = dRp;
-            else {
-                out[OUT_DR + pa * MAXT + pb] = 0.5 * dRp;
-                out[OUT_DR + pb * MAXT + pa] = 0.5 * dRp;
-            }
-        }
-        out[OUT_DGAMMA] = dgam / a.gamma[c];
-        for (int j = 0; j < MAXD; ++j) out[OUT_DETA + j] = deta[j];
-    }
-}
+__global__ void __launch_bounds__(256) k_finalize(FinalArgs a) { finalize_candidate<256>(a, blockIdx.x); }
 
 void finalize(const FinalArgs& a, cudaStream_t s) {
     ProfScope ps("finalize", s);

@@ -5,6 +5,39 @@
 
 namespace fmtgp {
 
+// compile-time dispatch helpers (threads per CTA, spatial dimension)
+#define FM_NT_CASE(V, ...)     \
+    case V: {                  \
+        constexpr int NT = V;  \
+        __VA_ARGS__;           \
+    } break;
+#define FM_NT_DISPATCH(nt, ...)                                                                      \
+    switch (nt) {                                                                                    \
+        FM_NT_CASE(32, __VA_ARGS__) FM_NT_CASE(64, __VA_ARGS__) FM_NT_CASE(128, __VA_ARGS__)         \
+        FM_NT_CASE(256, __VA_ARGS__) default : {                                                      \
+            constexpr int NT = 512;                                                                  \
+            __VA_ARGS__;                                                                             \
+        }                                                                                            \
+        break;                                                                                       \
+    }
+
+#define FM_D_DISPATCH(d, ...)                                                                          \
+    switch (d) {                                                                                       \
+        FM_D_CASE(1, __VA_ARGS__) FM_D_CASE(2, __VA_ARGS__) FM_D_CASE(3, __VA_ARGS__)                  \
+        FM_D_CASE(4, __VA_ARGS__) FM_D_CASE(5, __VA_ARGS__) FM_D_CASE(6, __VA_ARGS__)                  \
+        FM_D_CASE(7, __VA_ARGS__) FM_D_CASE(8, __VA_ARGS__) FM_D_CASE(9, __VA_ARGS__)                  \
+        FM_D_CASE(10, __VA_ARGS__) FM_D_CASE(11, __VA_ARGS__) FM_D_CASE(12, __VA_ARGS__)               \
+        FM_D_CASE(13, __VA_ARGS__) FM_D_CASE(14, __VA_ARGS__) FM_D_CASE(15, __VA_ARGS__)               \
+        FM_D_CASE(16, __VA_ARGS__) default : break;                                                    \
+    }
+#define FM_D_CASE(V, ...)    \
+    case V: {                \
+        constexpr int D = V; \
+        __VA_ARGS__;         \
+    } break;
+
+constexpr int GEN_NT_DIG = 256;
+
 // ---------------------------------------------------------------- optional per-launch timing
 // When a model enables profiling, every kernel launch is bracketed by CUDA events on its
 // stream (bench.py's live roofline denominators).  Off by default: zero overhead.
@@ -72,11 +105,69 @@ struct FinalArgs {
     const int* pair_b;            // [P]
     double* out;                  // [ncand][NOUT]
 };
+// partials may come from other CTAs of the same kernel (last-CTA finalize): L2 loads (__ldcg)
 // per-candidate output record
 constexpr int OUT_LOGDET = 0, OUT_QUAD = 1, OUT_NLL = 2, OUT_DGAMMA = 3, OUT_DETA = 4;
 constexpr int OUT_DR = OUT_DETA + MAXD;             // [MAXT*MAXT] symmetric dNLL/dR (G with G_ab = G_ba = 1/2 dR_pair)
 constexpr int NOUT = OUT_DR + MAXT * MAXT;
 void finalize(const FinalArgs& a, cudaStream_t s);
+
+template <int NT>
+__device__ void finalize_candidate(const FinalArgs& a, int c) {
+    double* out = a.out + (size_t)c * NOUT;
+    __shared__ double red[32];
+    __shared__ double S[MAXP][MAXD + 1];
+    const int d = a.d, P = a.P;
+    double ld = 0.0, q = 0.0;
+    for (int b = threadIdx.x; b < a.nblk_solve; b += NT) {
+        ld += __ldcg(a.solve_partial + ((size_t)c * a.nblk_solve + b) * 2 + 0);
+        q += __ldcg(a.solve_partial + ((size_t)c * a.nblk_solve + b) * 2 + 1);
+    }
+    ld = block_sum<NT>(ld, red);
+    q = block_sum<NT>(q, red);
+    if (threadIdx.x == 0) {
+        out[OUT_LOGDET] = ld;
+        out[OUT_QUAD] = q;
+        out[OUT_NLL] = q + ld;  // rT c + logdet (gp_core.cpp:207-211)
+    }
+    if (!a.grad_partial) return;
+    // one warp per (pair, component): fixed-order strided sums + warp tree (deterministic)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int t = warp; t < P * (MAXD + 1); t += NT / 32) {
+        const int p = t / (MAXD + 1), i = t % (MAXD + 1);
+        double acc = 0.0;
+        if (i < d || i == MAXD)
+            for (int b = lane; b < a.nblk_grad; b += 32)
+                acc += __ldcg(a.grad_partial + (((size_t)c * P + p) * a.nblk_grad + b) * (MAXD + 1) + i);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) S[p][i] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double dgam = 0.0;
+        double deta[MAXD];
+        for (int j = 0; j < MAXD; ++j) deta[j] = 0.0;
+        for (int x = 0; x < MAXT * MAXT; ++x) out[OUT_DR + x] = 0.0;
+        for (int p = 0; p < P; ++p) {
+            const int pa = a.pair_a[p], pb = a.pair_b[p];
+            const double w = pa == pb ? 1.0 : 2.0;
+            const double Rp = a.Rpair[(size_t)c * P + p];
+            const double dRp = w * S[p][MAXD];  // dNLL / dR_ab, symmetric pair counted once
+            for (int j = 0; j < d; ++j) deta[j] += w * Rp * S[p][j];
+            dgam += w * Rp * S[p][MAXD];
+            if (pa == pb) out[OUT_DR + pa * MAXT + pb] = dRp;
+            else {
+                out[OUT_DR + pa * MAXT + pb] = 0.5 * dRp;
+                out[OUT_DR + pb * MAXT + pa] = 0.5 * dRp;
+            }
+        }
+        out[OUT_DGAMMA] = dgam / a.gamma[c];
+        for (int j = 0; j < MAXD; ++j) out[OUT_DETA + j] = deta[j];
+    }
+}
+
+
 
 // ---------------------------------------------------------------- per-slot matvec (solve / gram apply)
 // out_a = sum_b Op_ab(k) in_b(k) with Op Hermitian given by upper pairs (equal n)

@@ -10,6 +10,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
@@ -18,6 +19,7 @@
 
 #include "../../include/fastmtgp_b200.h"
 #include "kernels.cuh"
+#include "digital.cuh"
 #include "fold.cuh"
 #include "posterior.cuh"
 #include "unequal.cuh"
@@ -266,6 +268,19 @@ struct fmtgp_model {
     std::vector<GraphEntry> graphs;
     bool use_graphs = true;
     long long spec_version = 0;  // bumped whenever d_lam is rewritten
+    // fused three-kernel digital path (digital.cuh)
+    bool dig = false;
+    DigGeo dgeo{};
+    double* d_part_mid = nullptr;
+    double* d_part_dot = nullptr;
+    unsigned int* d_counter = nullptr;
+    int* d_pair_ofs = nullptr;
+    uint64_t* d_ofs = nullptr;  // distinct pair offsets [nofs][MAXD]
+    int nofs = 0;
+    double* d_kap = nullptr;    // design-time kappa table [nofs][d][n]
+    double kap_b[4]{};
+    bool kap_valid = false;
+    bool kap_enabled = true;
 };
 
 namespace {
@@ -464,8 +479,84 @@ void finish_results(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, bool g
     }
 }
 
+// Fused digital fit (digital.cuh): three kernels, spectra never leave L2 between them.
+void eval_digital_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, bool grad, bool keep_chat) {
+    copy_hyper(M);
+    CK(cudaMemsetAsync(M->d_bad, 0x7f, sizeof(int) * nc, M->st));
+    CK(cudaMemsetAsync(M->d_imre, 0, sizeof(unsigned long long) * 2 * MAXT * nc, M->st));
+    const Group& g = M->groups[0];
+    DigArgs a{};
+    a.T = M->T;
+    a.P = M->P;
+    a.d = M->d;
+    a.nc = nc;
+    a.n = M->n[0];
+    a.sp = spatial_of(M, si_alpha, bw);
+    a.pg = pointgen_of(M, M->m[0]);
+    a.offs = M->d_offs;
+    a.kap = M->kap_valid ? M->d_kap : nullptr;
+    a.pair_ofs = M->d_pair_ofs;
+    a.eta = M->d_eta;
+    a.gamma = M->d_gamma;
+    a.coef = g.d_coef;
+    a.xi = g.d_xi;
+    a.Rpair = M->d_Rpair;
+    a.pair_a = M->d_pa;
+    a.pair_b = M->d_pb;
+    a.yhat = static_cast<const double*>(M->d_yhat);
+    a.Y = static_cast<double*>(M->d_work);
+    a.lam_out = keep_chat ? static_cast<double*>(M->d_lam) : nullptr;
+    a.chat_out = keep_chat ? static_cast<double*>(M->d_chat) : nullptr;
+    a.part_mid = M->d_part_mid;
+    a.part_dot = M->d_part_dot;
+    a.bad = M->d_bad;
+    a.imre = M->d_imre;
+    a.counter = M->d_counter;
+    a.out = M->d_out;
+    a.want_grad = grad;
+    dig_fit(M->dgeo, a, M->st);
+    CK(cudaGetLastError());
+    if (!grad) {
+        FinalArgs fa{};
+        fa.T = M->T;
+        fa.P = M->P;
+        fa.d = M->d;
+        fa.ncand = nc;
+        fa.nblk_solve = 1 << M->dgeo.l1;
+        fa.solve_partial = M->d_part_mid;
+        fa.Rpair = M->d_Rpair;
+        fa.gamma = M->d_gamma;
+        fa.pair_a = M->d_pa;
+        fa.pair_b = M->d_pb;
+        fa.out = M->d_out;
+        finalize(fa, M->st);
+    }
+    CK(cudaMemcpyAsync(M->h_out, M->d_out, sizeof(double) * NOUT * nc, cudaMemcpyDeviceToHost, M->st));
+    CK(cudaMemcpyAsync(M->h_bad, M->d_bad, sizeof(int) * 2 * nc, cudaMemcpyDeviceToHost, M->st));
+    CK(cudaMemcpyAsync(M->h_imre, M->d_imre, sizeof(double) * 2 * MAXT * nc, cudaMemcpyDeviceToHost, M->st));
+}
+
+// The design-time kappa table depends on the design and the Walsh order weights only
+// (not on gamma, eta, R, xi): rebuilt when b changes, outside any captured graph.
+void ensure_kappa_table(fmtgp_model* M, int si_alpha, const double* bw) {
+    if (!M->dig || !M->d_kap || !M->kap_enabled) {
+        M->kap_valid = false;
+        return;
+    }
+    if (M->kap_valid && std::memcmp(M->kap_b, bw, sizeof(M->kap_b)) == 0) return;
+    dig_kappa_table(spatial_of(M, si_alpha, bw), pointgen_of(M, M->m[0]), M->d_ofs, M->nofs, M->n[0], M->d_kap,
+                    M->st);
+    CK(cudaGetLastError());
+    std::memcpy(M->kap_b, bw, sizeof(M->kap_b));
+    M->kap_valid = true;
+}
+
 // Stream-ordered body of one equal-n evaluation (captured into a CUDA graph).
 void eval_equal_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, bool grad, bool keep_chat) {
+    if (M->dig) {
+        eval_digital_body(M, nc, si_alpha, bw, grad, keep_chat);
+        return;
+    }
     copy_hyper(M);
     build_spectra(M, nc, si_alpha, bw);
     CK(cudaMemsetAsync(M->d_bad, 0x7f, sizeof(int) * nc, M->st));
@@ -537,6 +628,7 @@ void eval_equal(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, const doub
                 bool keep_chat) {
     const fmtgp_hyper* h0 = hs[0];
     fill_hyper(M, nc, hs, xi_scale);
+    ensure_kappa_table(M, h0->si_alpha, h0->b);
     const int prof = M->profiling ? 1 : 0;
     fmtgp_model::GraphEntry* ge = nullptr;
     for (auto& e : M->graphs)
@@ -675,6 +767,7 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
         M->d = dz->d;
         M->T = dz->L;
         M->max_cand = max_cand;
+        if (const char* e = std::getenv("FMTGP_KAPPA_TABLE")) M->kap_enabled = e[0] != '0';
         M->off[0] = 0;
         for (int l = 0; l < M->T; ++l) {
             M->m[l] = dz->m[l];
@@ -828,6 +921,35 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
         M->d_lam = dalloc<char>(size_t(max_cand) * M->total_slots * es);
         M->d_laminv = dalloc<char>(size_t(M->total_slots) * es);
         M->d_chat = dalloc<char>(size_t(M->task_slots) * es);
+        if (M->equal && !M->lattice && DigGeo::make(M->m[0], M->P, M->dgeo)) {
+            M->dig = true;
+            const DigGeo& g = M->dgeo;
+            M->d_part_mid = dalloc<double>(size_t(max_cand) * (size_t(1) << g.l1) * 2);
+            M->d_part_dot = dalloc<double>(size_t(max_cand) * M->P * g.nblk_col * (MAXD + 1));
+            M->d_counter = dalloc<unsigned int>(max_cand);
+            CK(cudaMemset(M->d_counter, 0, sizeof(unsigned int) * max_cand));
+            // distinct pair offsets (diagonal pairs share offset 0)
+            std::vector<int> pofs(M->P);
+            std::vector<uint64_t> uniq;
+            for (int p = 0; p < M->P; ++p) {
+                int found = -1;
+                for (int o = 0; o < M->nofs; ++o)
+                    if (std::equal(offs.begin() + size_t(p) * MAXD, offs.begin() + size_t(p + 1) * MAXD,
+                                   uniq.begin() + size_t(o) * MAXD))
+                        found = o;
+                if (found < 0) {
+                    uniq.insert(uniq.end(), offs.begin() + size_t(p) * MAXD, offs.begin() + size_t(p + 1) * MAXD);
+                    found = M->nofs++;
+                }
+                pofs[p] = found;
+            }
+            M->d_pair_ofs = dalloc<int>(M->P);
+            M->d_ofs = dalloc<uint64_t>(uniq.size());
+            CK(cudaMemcpy(M->d_pair_ofs, pofs.data(), M->P * sizeof(int), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(M->d_ofs, uniq.data(), uniq.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
+            const size_t kbytes = size_t(M->nofs) * M->d * (size_t(1) << M->m[0]) * sizeof(double);
+            if (kbytes <= (size_t(1) << 30)) M->d_kap = dalloc<double>(kbytes / sizeof(double));
+        }
         if (M->equal) {
             M->d_M = dalloc<char>(size_t(max_cand) * M->total_slots * es);
             const long long ns = M->pslots[0];
@@ -924,6 +1046,12 @@ int fmtgp_model_destroy(fmtgp_model_t M) {
     F(M->d_M);
     F(M->d_work);
     F(M->d_gen);
+    F(M->d_part_mid);
+    F(M->d_part_dot);
+    F(M->d_counter);
+    F(M->d_pair_ofs);
+    F(M->d_ofs);
+    F(M->d_kap);
     F(M->d_laminv);
     F(M->d_chat);
     F(M->d_psolve);

@@ -244,4 +244,150 @@ __device__ __forceinline__ double2 c2r_pre(double2 Ak, double2 Ap, double2 wk) {
     return make_double2(E.x - O.y, E.y + O.x);  // E + i O
 }
 
+// --------------------------------------------------------------------- per-frequency solve
+// Hermitian LDL^H of A (upper pairs, row by row), T <= 8.  Pivots are the diagonal Schur
+// complements of Algorithm 1 (fast_gram.cpp:167-178): logdet = sum log d_s.
+// Returns 0 ok, 1 non-positive pivot (SchurBreakdown), 2 non-real diagonal (FastMtgpError).
+template <int T, bool CX>
+__device__ __forceinline__ int ldl_solve(const typename Sc<CX>::T* A, const typename Sc<CX>::T* r, bool want_inv,
+                                         double& logdet, double& quad, typename Sc<CX>::T* chat,
+                                         typename Sc<CX>::T* Ainv, double* imx, double* rex) {
+    using S = Sc<CX>;
+    using V = typename S::T;
+    V L[T][T];
+    double dinv[T];
+    int status = 0;
+    // pair index of (a,b), a <= b, row by row (fast_gram.cpp:35-40)
+    auto pidx = [](int a, int b) { return a * T - a * (a - 1) / 2 + (b - a); };
+    logdet = 0.0;
+#pragma unroll
+    for (int s = 0; s < T; ++s) {
+        double dd = S::re(A[pidx(s, s)]);
+        // non-real check is global per stage (|Im S| vs 1e-8 max(1, max Re S)), fast_gram.cpp:167-172
+        imx[s] = fmax(imx[s], fabs(S::im(A[pidx(s, s)])));
+#pragma unroll
+        for (int k = 0; k < s; ++k) dd -= S::abs2(L[s][k]) / dinv[k];
+        if (!(dd > 0.0)) {
+            status = 1;
+            dd = 1.0;
+        }
+        rex[s] = fmax(rex[s], dd);
+        dinv[s] = 1.0 / dd;
+        logdet += log(dd);
+#pragma unroll
+        for (int i = s + 1; i < T; ++i) {
+            V acc = S::conj(A[pidx(s, i)]);
+#pragma unroll
+            for (int k = 0; k < s; ++k) acc = S::sub(acc, S::scale(S::mulc(L[i][k], L[s][k]), 1.0 / dinv[k]));
+            L[i][s] = S::scale(acc, dinv[s]);
+        }
+    }
+    // z = L^-1 r, quad = sum |z|^2 / d
+    V z[T];
+    quad = 0.0;
+#pragma unroll
+    for (int i = 0; i < T; ++i) {
+        V acc = r[i];
+#pragma unroll
+        for (int k = 0; k < i; ++k) acc = S::sub(acc, S::mul(L[i][k], z[k]));
+        z[i] = acc;
+        quad += S::abs2(acc) * dinv[i];
+    }
+    // chat = L^-H D^-1 z
+#pragma unroll
+    for (int i = T - 1; i >= 0; --i) {
+        V acc = S::scale(z[i], dinv[i]);
+#pragma unroll
+        for (int k = i + 1; k < T; ++k) acc = S::sub(acc, S::mul(S::conj(L[k][i]), chat[k]));
+        chat[i] = acc;
+    }
+    if (want_inv) {
+        // X = L^-1 (unit lower); Ainv_ab = sum_{s >= max(a,b)} conj(X_sa) X_sb / d_s
+        V X[T][T];
+#pragma unroll
+        for (int j = 0; j < T; ++j)
+#pragma unroll
+            for (int i = j + 1; i < T; ++i) {
+                V acc = S::sub(S::zero(), L[i][j]);
+#pragma unroll
+                for (int k = j + 1; k < i; ++k) acc = S::sub(acc, S::mul(L[i][k], X[k][j]));
+                X[i][j] = acc;
+            }
+#pragma unroll
+        for (int a = 0; a < T; ++a)
+#pragma unroll
+            for (int b = a; b < T; ++b) {
+                V acc = S::zero();
+#pragma unroll
+                for (int s = b; s < T; ++s) {
+                    // conj(X_sa) X_sb with X_ss = 1
+                    V term;
+                    if (s == a) term = S::one();  // then b == a == s
+                    else if (s == b) term = S::conj(X[s][a]);
+                    else term = S::mulc(X[s][b], X[s][a]);
+                    acc = S::add(acc, S::scale(term, dinv[s]));
+                }
+                Ainv[pidx(a, b)] = acc;
+            }
+    }
+    return status;
+}
+
+// --------------------------------------------------------------------- split-mode generator helpers
+template <int D>
+struct GenSmem {
+    uint64_t lo[D][32], mid[D][32];
+    double T8[256];
+    double eta[D];
+};
+
+template <int D>
+__device__ __forceinline__ void gen_smem_init(GenSmem<D>& t, const GenSrc& g, int c, bool load_eta = true) {
+    if (g.sp.family == 1) {
+        for (int e = threadIdx.x; e < D * 64; e += blockDim.x) {
+            const int j = e >> 6, r = e & 63;
+            const int shift = r < 32 ? 0 : 5;
+            const int val = r & 31;
+            uint64_t z = 0;
+            const uint64_t* col = g.pg.cols + size_t(j) * g.pg.m_cols;
+            for (int p = 0; p < 5; ++p)
+                if (((val >> p) & 1) && p + shift < g.pg.m_cols) z ^= __ldg(col + p + shift);
+            if (r < 32) t.lo[j][val] = z;
+            else t.mid[j][val] = z;
+        }
+        for (int b = threadIdx.x; b < 256; b += blockDim.x) {
+            double acc = 0.0;
+            for (int i = 7; i >= 0; --i)  // smallest terms first
+                if ((b >> (7 - i)) & 1) acc += pow2i(-3 * i);
+            t.T8[b] = acc;
+        }
+    }
+    if (load_eta)
+        for (int j = threadIdx.x; j < D; j += blockDim.x) t.eta[j] = g.eta[size_t(c) * D + j];
+}
+
+template <int D>
+__device__ __forceinline__ void kappa_d(const GenSrc& g, const GenSmem<D>& t, const uint64_t* off, uint64_t idx,
+                                        double* kappa) {
+    if (g.sp.family == 0) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) kappa[j] = si_base(g.pg.lattice_word(idx, j, off[j]), g.sp.si_alpha);
+        return;
+    }
+    const uint64_t hi = idx >> 10;
+    const bool only4 = g.sp.b[0] == 0.0 && g.sp.b[1] == 0.0 && g.sp.b[2] == 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        uint64_t z = t.lo[j][idx & 31] ^ t.mid[j][(idx >> 5) & 31];
+        if (hi) {
+            const uint64_t* col = g.pg.cols + size_t(j) * g.pg.m_cols + 10;
+            uint64_t h = hi;
+            for (int q = 0; h; ++q, h >>= 1)
+                if (h & 1) z ^= __ldg(col + q);
+        }
+        const uint64_t w = z ^ off[j];
+        kappa[j] = only4 ? g.sp.b[3] * dsi_order4_t8(w, t.T8) : dsi_walsh(w, g.sp.b);
+    }
+}
+
 }  // namespace fmtgp
