@@ -93,11 +93,21 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- roofline
 def algorithmic_bytes(kernel: str, inst, P: int, T: int) -> float:
     """Minimal HBM bytes one launch of `kernel` must move for this workload (8-byte words;
-    SURVEY.md §8d, per-kernel split of B_alg).  Real (digital) slots are 8 B, lattice
-    half-spectrum slots 16 B for n/2 of them: either way 8n bytes per vector."""
-    n = inst.design.n[0]
+    SURVEY.md §8d per-kernel split of B_alg = 8n(6P+T)).  Real (digital) slots are 8 B, lattice
+    half-spectrum slots 16 B for n/2 of them: either way 8n bytes per vector.  The fused
+    digital kernels also stream the design-time kappa table (d values per element for each
+    distinct pair offset) and K2 writes the fit's spectrum and chat."""
+    dz = inst.design
+    n = dz.n[0]
     vec = 8.0 * n
+    if dz.kind == 1:  # distinct pair offsets of the digital design: diagonal pairs share offset 0
+        nofs = 1 + P - T
+    else:
+        nofs = 0
     table = {
+        "dig_col_fwd": (P + nofs * dz.d) * vec,  # kappa table in, intermediate out
+        "dig_mid": (3 * P + 2 * T) * vec,  # intermediate + yhat in; M, spectrum, chat out
+        "dig_col_inv": (P + nofs * dz.d) * vec,  # intermediate + kappa table in
         "fwd_col_dig": P * vec, "fwd_col_lat": P * vec,  # generator on the fly -> write intermediate
         "fwd_row_dig": 2 * P * vec, "fwd_row_lat": 2 * P * vec,  # read intermediate, write spectra
         "fwd_small_dig": P * vec, "fwd_small_lat": P * vec,  # write spectra
@@ -159,6 +169,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-flush", action="store_true", help="diagnostics only: skip the L2 flush")
     args = ap.parse_args()
     warmup = max(args.warmup, 3)
 
@@ -220,8 +231,9 @@ def main():
     barrier()
     with ClockSampler(local_rank) as clk:
         for k in range(args.steps):
-            with torch.cuda.stream(stream):
-                flush.fill_(float(k))
+            if not args.no_flush:
+                with torch.cuda.stream(stream):
+                    flush.fill_(float(k))
             ev[k][0].record(stream)
             res = model.nll(hp, grad=True)
             ev[k][1].record(stream)

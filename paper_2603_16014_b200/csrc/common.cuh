@@ -45,6 +45,13 @@ __device__ __forceinline__ double2 twiddle(const double2* __restrict__ tab, uint
     return cmul(hi, lo);
 }
 
+// ---------------------------------------------------------------- async global -> shared copies (LDGSTS)
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 // ---------------------------------------------------------------- reductions
 template <int NT>
 __device__ __forceinline__ double block_sum(double v, double* scratch /* >= NT/32 */) {
@@ -61,6 +68,32 @@ __device__ __forceinline__ double block_sum(double v, double* scratch /* >= NT/3
         for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
     }
     return r;  // valid in thread 0
+}
+
+// K block sums with a single barrier pair: warp shuffles, one smem transpose, warp 0 folds.
+// scratch >= (NT/32) * K doubles; results valid in thread 0 (out[k]).
+template <int NT, int K>
+__device__ __forceinline__ void block_sum_vec(double (&v)[K], double* scratch) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+    }
+    __syncthreads();
+    if (l == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) scratch[w * K + k] = v[k];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            double s = 0.0;
+            for (int ww = 0; ww < NT / 32; ++ww) s += scratch[ww * K + k];
+            v[k] = s;
+        }
+    }
 }
 
 __device__ __forceinline__ uint32_t bitrev32(uint32_t x, int m) { return m == 0 ? 0u : (__brev(x) >> (32 - m)); }

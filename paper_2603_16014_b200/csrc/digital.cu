@@ -3,7 +3,7 @@
 
 namespace fmtgp {
 
-bool DigGeo::make(int m, int P, DigGeo& g) {
+bool DigGeo::make(int m, int P, DigGeo& g, long long total_vecs) {
     if (m < 1 || P < 1) return false;
     // row length: all P rows of one frequency block in <= 64 KB of smem
     int l2max = 0;
@@ -14,12 +14,15 @@ bool DigGeo::make(int m, int P, DigGeo& g) {
     g.m = m;
     g.l2 = l2;
     g.l1 = m - l2;
-    g.lc = std::min(11 - g.l1, l2);
+    // column tile: >= ~4 CTAs per SM over all vectors, 2^10..2^11 elements, <= 2^(l1 + l2)
+    int tl = 11;
+    if (total_vecs > 0 && ((total_vecs << m) >> tl) < 4 * 148) tl = 10;
+    tl = std::max(tl, g.l1);
+    g.lc = std::min(tl - g.l1, l2);
     if (g.lc < 0) return false;
-    const int tile = 1 << (g.l1 + g.lc);
-    g.nt_col = std::max(32, std::min(512, tile / EPT));
+    g.nt_col = std::max(32, (1 << (g.l1 + g.lc)) / 4);  // 4 elements per thread in the load phases
     int need = (P << l2) / EPT;
-    int nt = 32;
+    int nt = 256;
     while (nt < need && nt < 512) nt <<= 1;
     if (nt * EPT < (P << l2)) return false;
     g.nt_mid = nt;
@@ -57,11 +60,11 @@ void dig_kappa_table(const Spatial& sp, const PointGen& pg, const uint64_t* d_of
 
 // ------------------------------------------------------------------ K1: generator x column FWHT
 template <int NT, int D>
-__global__ void __launch_bounds__(NT) k_dig_col_fwd(DigArgs a, int l1, int l2, int lc) {
+__global__ void __launch_bounds__(NT, 3) k_dig_col_fwd(DigArgs a, int l1, int l2, int lc) {
     extern __shared__ __align__(16) double sm[];
     __shared__ GenSmem<D> tab;
     const int v = blockIdx.y, c = v / a.P, p = v - c * a.P;
-    const int C = 1 << lc, N1 = 1 << l1, ld = N1 + 1;
+    const int C = 1 << lc, N1 = 1 << l1, ld = padded_len(N1);
     const long long c0 = (long long)blockIdx.x << lc, n = a.n;
     double eta[D];
 #pragma unroll
@@ -79,24 +82,43 @@ __global__ void __launch_bounds__(NT) k_dig_col_fwd(DigArgs a, int l1, int l2, i
         __syncthreads();
     }
     const double* kp = a.kap ? a.kap + size_t(__ldg(a.pair_ofs + p)) * D * n : nullptr;
-    for (int e = threadIdx.x; e < (C << l1); e += NT) {
-        const int j1 = e >> lc, cc = e & (C - 1);
-        const long long i = ((long long)j1 << l2) + c0 + cc;
-        double kappa[D];
-        if (kp) {
-#pragma unroll
-            for (int j = 0; j < D; ++j) kappa[j] = __ldg(kp + size_t(j) * n + i);
-        } else {
-            kappa_d<D>(g, tab, off, uint64_t(i), kappa);
+    const int tile = C << l1;
+    if (kp) {
+        // design-time kappa tile -> smem with cp.async (no register staging)
+        double* kbuf = sm + C * ld;
+        for (int idx = threadIdx.x; idx < tile * D; idx += NT) {
+            const int j = idx / tile, e = idx - j * tile;
+            const long long i = ((long long)(e >> lc) << l2) + c0 + (e & (C - 1));
+            cp_async8(kbuf + idx, kp + size_t(j) * n + i);
         }
-        sm[cc * ld + j1] = product_kernel_d<D, false>(kappa, eta, gam, nullptr);
+        cp_async_wait_all();
+        __syncthreads();
+        for (int e = threadIdx.x; e < tile; e += NT) {
+            double kappa[D];
+#pragma unroll
+            for (int j = 0; j < D; ++j) kappa[j] = kbuf[j * tile + e];
+            sm[(e & (C - 1)) * ld + sidx<true>(e >> lc)] = product_kernel_d<D, false>(kappa, eta, gam, nullptr);
+        }
+    } else {
+        for (int e = threadIdx.x; e < tile; e += NT) {
+            const int j1 = e >> lc, cc = e & (C - 1);
+            const long long i = ((long long)j1 << l2) + c0 + cc;
+            double kappa[D];
+            kappa_d<D>(g, tab, off, uint64_t(i), kappa);
+            sm[cc * ld + sidx<true>(j1)] = product_kernel_d<D, false>(kappa, eta, gam, nullptr);
+        }
+    }
+    // zero the per-fit flags once per fit (K2 / K3 run after this kernel)
+    if (blockIdx.x == 0 && blockIdx.y == 0) {
+        for (int t = threadIdx.x; t < a.nc; t += NT) a.bad[t] = 0x7f7f7f7f;
+        for (int t = threadIdx.x; t < a.nc * MAXT * 2; t += NT) a.imre[t] = 0ull;
     }
     __syncthreads();
-    smem_wht<NT>(sm, l1, C, ld);
+    smem_wht<NT, true>(sm, l1, C, ld);
     double* out = a.Y + size_t(v) * n;
     for (int e = threadIdx.x; e < (C << l1); e += NT) {
         const int k1 = e >> lc, cc = e & (C - 1);
-        out[((long long)k1 << l2) + c0 + cc] = sm[cc * ld + k1];
+        out[((long long)k1 << l2) + c0 + cc] = sm[cc * ld + sidx<true>(k1)];
     }
 }
 
@@ -104,16 +126,16 @@ __global__ void __launch_bounds__(NT) k_dig_col_fwd(DigArgs a, int l1, int l2, i
 template <int NT, int T>
 __global__ void __launch_bounds__(NT) k_dig_mid(DigArgs a, int l2) {
     constexpr int P = T * (T + 1) / 2;
-    extern __shared__ __align__(16) double sm[];  // [P][N2]
-    const int row = blockIdx.x, c = blockIdx.y, N2 = 1 << l2;
+    extern __shared__ __align__(16) double sm[];  // [P][padded N2]
+    const int row = blockIdx.x, c = blockIdx.y, N2 = 1 << l2, lds = padded_len(N2);
     const long long n = a.n, base = (long long)row << l2;
     double* Yc = a.Y + size_t(c) * P * n;
     for (int e = threadIdx.x; e < (P << l2); e += NT) {
         const int p = e >> l2, k2 = e & (N2 - 1);
-        sm[e] = Yc[size_t(p) * n + base + k2];
+        sm[p * lds + sidx<true>(k2)] = Yc[size_t(p) * n + base + k2];
     }
     __syncthreads();
-    smem_wht<NT>(sm, l2, P, N2);
+    smem_wht<NT, true>(sm, l2, P, lds);
     double coef[P], xi[P];
 #pragma unroll
     for (int q = 0; q < P; ++q) {
@@ -129,7 +151,7 @@ __global__ void __launch_bounds__(NT) k_dig_mid(DigArgs a, int l2) {
         double A[P], r[T], ch[T], Ai[P];
 #pragma unroll
         for (int q = 0; q < P; ++q) {
-            A[q] = fma(coef[q], sm[q * N2 + k2], xi[q]);  // lam = R_ab * H q + xi (fast_gram.cpp:82-85)
+            A[q] = fma(coef[q], sm[q * lds + sidx<true>(k2)], xi[q]);  // lam = R_ab * H q + xi (fast_gram.cpp:82-85)
             if (a.lam_out) a.lam_out[(size_t(c) * P + q) * n + k] = A[q];
         }
 #pragma unroll
@@ -144,20 +166,20 @@ __global__ void __launch_bounds__(NT) k_dig_mid(DigArgs a, int l2) {
 #pragma unroll
             for (int x = 0; x < T; ++x)
 #pragma unroll
-                for (int y = x; y < T; ++y, ++q) sm[q * N2 + k2] = Ai[q] - ch[x] * ch[y];  // M
+                for (int y = x; y < T; ++y, ++q) sm[q * lds + sidx<true>(k2)] = Ai[q] - ch[x] * ch[y];  // M
         }
         if (a.chat_out && c == 0) {
 #pragma unroll
             for (int t = 0; t < T; ++t) a.chat_out[size_t(t) * n + k] = ch[t];
         }
     }
-    __shared__ double red[32];
-    ld_acc = block_sum<NT>(ld_acc, red);
-    q_acc = block_sum<NT>(q_acc, red);
+    __shared__ double redv[(NT / 32) * 2];
+    double lq[2] = {ld_acc, q_acc};
+    block_sum_vec<NT, 2>(lq, redv);
     const int nrows = gridDim.x;
     if (threadIdx.x == 0) {
-        a.part_mid[(size_t(c) * nrows + row) * 2 + 0] = ld_acc;
-        a.part_mid[(size_t(c) * nrows + row) * 2 + 1] = q_acc;
+        a.part_mid[(size_t(c) * nrows + row) * 2 + 0] = lq[0];
+        a.part_mid[(size_t(c) * nrows + row) * 2 + 1] = lq[1];
     }
     if (first_bad != 0x7f7f7f7f) atomicMin(a.bad + c, first_bad);
 #pragma unroll
@@ -175,27 +197,37 @@ __global__ void __launch_bounds__(NT) k_dig_mid(DigArgs a, int l2) {
     }
     if (!a.want_grad) return;
     __syncthreads();
-    smem_wht<NT>(sm, l2, P, N2);  // inverse FWHT over the row bits (self-inverse up to scale)
+    smem_wht<NT, true>(sm, l2, P, lds);  // inverse FWHT over the row bits (self-inverse up to scale)
     for (int e = threadIdx.x; e < (P << l2); e += NT) {
         const int p = e >> l2, k2 = e & (N2 - 1);
-        Yc[size_t(p) * n + base + k2] = sm[e];
+        Yc[size_t(p) * n + base + k2] = sm[p * lds + sidx<true>(k2)];
     }
 }
 
 // ------------------------------------------------------------------ K3: column FWHT -> W -> gradient dot
 template <int NT, int D>
-__global__ void __launch_bounds__(NT) k_dig_col_inv(DigArgs a, int l1, int l2, int lc, int nrows) {
+__global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2, int lc, int nrows) {
     extern __shared__ __align__(16) double sm[];
     __shared__ GenSmem<D> tab;
     __shared__ double red[32];
     __shared__ int s_last;
     const int v = blockIdx.y, c = v / a.P, p = v - c * a.P;
-    const int C = 1 << lc, N1 = 1 << l1, ld = N1 + 1;
+    const int C = 1 << lc, N1 = 1 << l1, ld = padded_len(N1);
     const long long c0 = (long long)blockIdx.x << lc, n = a.n;
     const double* x = a.Y + size_t(v) * n;
-    for (int e = threadIdx.x; e < (C << l1); e += NT) {
+    const int tile = C << l1;
+    double* kbuf = sm + C * ld;
+    if (a.kap) {  // kappa tile streams into smem while the column is loaded and transformed
+        const double* kp0 = a.kap + size_t(__ldg(a.pair_ofs + p)) * D * n;
+        for (int idx = threadIdx.x; idx < tile * D; idx += NT) {
+            const int j = idx / tile, e = idx - j * tile;
+            const long long i = ((long long)(e >> lc) << l2) + c0 + (e & (C - 1));
+            cp_async8(kbuf + idx, kp0 + size_t(j) * n + i);
+        }
+    }
+    for (int e = threadIdx.x; e < tile; e += NT) {
         const int k1 = e >> lc, cc = e & (C - 1);
-        sm[cc * ld + k1] = x[((long long)k1 << l2) + c0 + cc];
+        sm[cc * ld + sidx<true>(k1)] = x[((long long)k1 << l2) + c0 + cc];
     }
     double eta[D];
 #pragma unroll
@@ -211,42 +243,77 @@ __global__ void __launch_bounds__(NT) k_dig_col_inv(DigArgs a, int l1, int l2, i
 #pragma unroll
         for (int j = 0; j < D; ++j) off[j] = __ldg(a.offs + size_t(p) * MAXD + j);
     }
-    __syncthreads();
-    smem_wht<NT>(sm, l1, C, ld);
     const double* kp = a.kap ? a.kap + size_t(__ldg(a.pair_ofs + p)) * D * n : nullptr;
     double acc[D + 1];
 #pragma unroll
     for (int j = 0; j <= D; ++j) acc[j] = 0.0;
-    for (int e = threadIdx.x; e < (C << l1); e += NT) {
-        const int j1 = e >> lc, cc = e & (C - 1);
-        const long long i = ((long long)j1 << l2) + c0 + cc;
-        const double W = sm[cc * ld + j1];  // W = H M (unnormalised), natural index i
-        double kappa[D], dq[D];
-        if (kp) {
+    if (kp) {
+        cp_async_wait_all();
+        __syncthreads();
+        smem_wht<NT, true>(sm, l1, C, ld);
+        for (int e = threadIdx.x; e < tile; e += NT) {
+            const double W = sm[(e & (C - 1)) * ld + sidx<true>(e >> lc)];  // W = H M, natural index
+            double kappa[D], dq[D];
 #pragma unroll
-            for (int j = 0; j < D; ++j) kappa[j] = __ldg(kp + size_t(j) * n + i);
-        } else {
-            kappa_d<D>(g, tab, off, uint64_t(i), kappa);
+            for (int j = 0; j < D; ++j) kappa[j] = kbuf[j * tile + e];
+            const double q = product_kernel_d<D, true>(kappa, eta, gam, dq);
+#pragma unroll
+            for (int j = 0; j < D; ++j) acc[j] = fma(W, dq[j], acc[j]);
+            acc[D] = fma(W, q, acc[D]);
         }
-        const double q = product_kernel_d<D, true>(kappa, eta, gam, dq);
+    } else {
+        __syncthreads();
+        smem_wht<NT, true>(sm, l1, C, ld);
+        for (int e = threadIdx.x; e < tile; e += NT) {
+            const int j1 = e >> lc, cc = e & (C - 1);
+            const long long i = ((long long)j1 << l2) + c0 + cc;
+            const double W = sm[cc * ld + sidx<true>(j1)];
+            double kappa[D], dq[D];
+            kappa_d<D>(g, tab, off, uint64_t(i), kappa);
+            const double q = product_kernel_d<D, true>(kappa, eta, gam, dq);
 #pragma unroll
-        for (int j = 0; j < D; ++j) acc[j] = fma(W, dq[j], acc[j]);
-        acc[D] = fma(W, q, acc[D]);
+            for (int j = 0; j < D; ++j) acc[j] = fma(W, dq[j], acc[j]);
+            acc[D] = fma(W, q, acc[D]);
+        }
     }
     const int nblk = gridDim.x;
     double* out = a.part_dot + ((size_t(c) * a.P + p) * nblk + blockIdx.x) * (MAXD + 1);
+    __shared__ double redv[(NT / 32) * (D + 1)];
+    block_sum_vec<NT, D + 1>(acc, redv);
+    if (threadIdx.x == 0) {
 #pragma unroll
-    for (int j = 0; j <= D; ++j) {
-        const double s = block_sum<NT>(acc[j], red);
-        if (threadIdx.x == 0) out[j == D ? MAXD : j] = s;
+        for (int j = 0; j <= D; ++j) out[j == D ? MAXD : j] = acc[j];
     }
-    // last CTA of this candidate reduces everything (threadFenceReduction pattern)
+    // two-level last-CTA reduction (threadFenceReduction pattern, fixed order => deterministic):
+    // the last CTA of each vector folds its nblk partials, the last vector of a candidate
+    // finalises the candidate's record.
+    if (threadIdx.x == 0) __threadfence();  // thread 0 wrote this CTA's partial
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned ticket = atomicAdd(a.counter + a.nc + v, 1u);
+        s_last = ticket == unsigned(nblk) - 1;
+        if (s_last) a.counter[a.nc + v] = 0;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const double* pv = a.part_dot + (size_t(c) * a.P + p) * nblk * (MAXD + 1);
+        for (int j = warp; j <= D; j += NT / 32) {
+            const int comp = j == D ? MAXD : j;
+            double s = 0.0;
+            for (int b = lane; b < nblk; b += 32) s += __ldcg(pv + size_t(b) * (MAXD + 1) + comp);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == 0) a.vec_sum[size_t(v) * (MAXD + 1) + comp] = s;
+        }
+    }
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
-        const unsigned total = unsigned(a.P) * nblk;
         const unsigned ticket = atomicAdd(a.counter + c, 1u);
-        s_last = ticket == total - 1;
+        s_last = ticket == unsigned(a.P) - 1;
         if (s_last) a.counter[c] = 0;  // self-reset for the next replay
     }
     __syncthreads();
@@ -258,9 +325,9 @@ __global__ void __launch_bounds__(NT) k_dig_col_inv(DigArgs a, int l1, int l2, i
     fa.d = D;
     fa.ncand = a.nc;
     fa.nblk_solve = nrows;
-    fa.nblk_grad = nblk;
+    fa.nblk_grad = 1;
     fa.solve_partial = a.part_mid;
-    fa.grad_partial = a.part_dot;
+    fa.grad_partial = a.vec_sum;
     fa.Rpair = a.Rpair;
     fa.gamma = a.gamma;
     fa.pair_a = a.pair_a;
@@ -288,7 +355,8 @@ static void mid_launch(const DigGeo& g, const DigArgs& a, size_t sm, cudaStream_
 
 void dig_fit(const DigGeo& g, const DigArgs& a, cudaStream_t s) {
     const int C = 1 << g.lc;
-    const size_t sm_col = size_t(C) * ((1 << g.l1) + 1) * sizeof(double);
+    const size_t sm_col = (size_t(C) * padded_len(1 << g.l1) + (a.kap ? size_t(a.d) << (g.l1 + g.lc) : 0)) *
+                          sizeof(double);
     const dim3 gcol(g.nblk_col, a.P * a.nc);
     FM_D_DISPATCH(a.d, {
         FM_NT_DISPATCH(g.nt_col, {
@@ -298,7 +366,7 @@ void dig_fit(const DigGeo& g, const DigArgs& a, cudaStream_t s) {
             k1<<<gcol, NT, sm_col, s>>>(a, g.l1, g.l2, g.lc);
         })
     })
-    const size_t sm_mid = size_t(a.P) << g.l2 << 3;
+    const size_t sm_mid = size_t(a.P) * padded_len(1 << g.l2) * sizeof(double);
     switch (a.T) {
         case 1: mid_launch<1>(g, a, sm_mid, s); break;
         case 2: mid_launch<2>(g, a, sm_mid, s); break;

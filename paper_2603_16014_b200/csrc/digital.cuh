@@ -21,7 +21,7 @@ struct DigGeo {
     int lc;          // log2 columns per K1/K3 CTA (tile = 2^(l1 + lc) <= 2^11)
     int nt_col, nt_mid;
     int nblk_col;    // K1/K3 CTAs per vector
-    static bool make(int m, int P, DigGeo& g);
+    static bool make(int m, int P, DigGeo& g, long long total_vecs = 0);
 };
 
 struct DigArgs {
@@ -47,7 +47,8 @@ struct DigArgs {
     double* part_dot;         // [nc][P][nblk_col][MAXD+1]
     int* bad;                 // [nc] first failing slot, 0x7f7f7f7f none
     unsigned long long* imre; // [nc][MAXT][2]
-    unsigned int* counter;    // [nc] last-CTA tickets (self-resetting)
+    unsigned int* counter;    // [nc + nc*P] last-CTA tickets (self-resetting)
+    double* vec_sum;          // [nc][P][MAXD+1] per-vector gradient sums
     double* out;              // [nc][NOUT]
     int want_grad;
 };

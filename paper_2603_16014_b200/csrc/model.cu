@@ -214,6 +214,7 @@ struct fmtgp_model {
     uint64_t n_max = 0;
     int mgen = 0;
     double* d_fit = nullptr;       // last fit: eta [d] | R [T*T]
+    bool fit_dirty = true;
     double* d_c = nullptr;         // coefficients of the last fit [N]
     bool have_c = false;
     int *d_pa = nullptr, *d_pb = nullptr;
@@ -232,6 +233,9 @@ struct fmtgp_model {
     int* d_bad = nullptr;
     unsigned long long* d_imre = nullptr;  // [max_cand][MAXT][2]
     double* h_imre = nullptr;
+    double* d_res = nullptr;   // [out | bad | imre] block
+    double* h_res = nullptr;
+    size_t res_len = 0;
     double* d_out = nullptr;
     int nblk_solve = 0, nblk_grad = 0;
     // scratch vectors for the seam calls
@@ -274,6 +278,7 @@ struct fmtgp_model {
     double* d_part_mid = nullptr;
     double* d_part_dot = nullptr;
     unsigned int* d_counter = nullptr;
+    double* d_vec_sum = nullptr;
     int* d_pair_ofs = nullptr;
     uint64_t* d_ofs = nullptr;  // distinct pair offsets [nofs][MAXD]
     int nofs = 0;
@@ -481,9 +486,7 @@ void finish_results(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, bool g
 
 // Fused digital fit (digital.cuh): three kernels, spectra never leave L2 between them.
 void eval_digital_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, bool grad, bool keep_chat) {
-    copy_hyper(M);
-    CK(cudaMemsetAsync(M->d_bad, 0x7f, sizeof(int) * nc, M->st));
-    CK(cudaMemsetAsync(M->d_imre, 0, sizeof(unsigned long long) * 2 * MAXT * nc, M->st));
+    copy_hyper(M);  // failure flags are zeroed by the first kernel
     const Group& g = M->groups[0];
     DigArgs a{};
     a.T = M->T;
@@ -512,6 +515,7 @@ void eval_digital_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, b
     a.bad = M->d_bad;
     a.imre = M->d_imre;
     a.counter = M->d_counter;
+    a.vec_sum = M->d_vec_sum;
     a.out = M->d_out;
     a.want_grad = grad;
     dig_fit(M->dgeo, a, M->st);
@@ -531,9 +535,7 @@ void eval_digital_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, b
         fa.out = M->d_out;
         finalize(fa, M->st);
     }
-    CK(cudaMemcpyAsync(M->h_out, M->d_out, sizeof(double) * NOUT * nc, cudaMemcpyDeviceToHost, M->st));
-    CK(cudaMemcpyAsync(M->h_bad, M->d_bad, sizeof(int) * 2 * nc, cudaMemcpyDeviceToHost, M->st));
-    CK(cudaMemcpyAsync(M->h_imre, M->d_imre, sizeof(double) * 2 * MAXT * nc, cudaMemcpyDeviceToHost, M->st));
+    CK(cudaMemcpyAsync(M->h_res, M->d_res, sizeof(double) * M->res_len, cudaMemcpyDeviceToHost, M->st));
 }
 
 // The design-time kappa table depends on the design and the Walsh order weights only
@@ -607,9 +609,7 @@ void eval_equal_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, boo
     fa.out = M->d_out;
     finalize(fa, M->st);
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(M->h_out, M->d_out, sizeof(double) * NOUT * nc, cudaMemcpyDeviceToHost, M->st));
-    CK(cudaMemcpyAsync(M->h_bad, M->d_bad, sizeof(int) * 2 * nc, cudaMemcpyDeviceToHost, M->st));
-    CK(cudaMemcpyAsync(M->h_imre, M->d_imre, sizeof(double) * 2 * MAXT * nc, cudaMemcpyDeviceToHost, M->st));
+    CK(cudaMemcpyAsync(M->h_res, M->d_res, sizeof(double) * M->res_len, cudaMemcpyDeviceToHost, M->st));
 }
 
 // non-real Schur complement test of candidate c (fast_gram.cpp:167-172), stage-global like the reference
@@ -683,11 +683,17 @@ void remember_hyper(fmtgp_model* M, const fmtgp_hyper* h) {
     M->last_R = task_gram(M, h);
     M->last_alpha = h->si_alpha;
     for (int i = 0; i < 4; ++i) M->last_b[i] = h->b[i];
+    M->fit_dirty = true;  // device copy (posterior kernels only) refreshed lazily
+}
+
+void upload_fit(fmtgp_model* M) {
+    if (!M->fit_dirty) return;
     std::vector<double> buf(MAXD + MAXT * MAXT, 0.0);
     for (int j = 0; j < M->d; ++j) buf[j] = M->last_eta[j];
     for (size_t k = 0; k < M->last_R.size(); ++k) buf[MAXD + k] = M->last_R[k];
     CK(cudaMemcpyAsync(M->d_fit, buf.data(), buf.size() * sizeof(double), cudaMemcpyHostToDevice, M->st));
     CK(cudaStreamSynchronize(M->st));
+    M->fit_dirty = false;
 }
 
 // nll over a batch with the reference's escalation schedule per candidate
@@ -921,13 +927,14 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
         M->d_lam = dalloc<char>(size_t(max_cand) * M->total_slots * es);
         M->d_laminv = dalloc<char>(size_t(M->total_slots) * es);
         M->d_chat = dalloc<char>(size_t(M->task_slots) * es);
-        if (M->equal && !M->lattice && DigGeo::make(M->m[0], M->P, M->dgeo)) {
+        if (M->equal && !M->lattice && DigGeo::make(M->m[0], M->P, M->dgeo, (long long)M->P * max_cand)) {
             M->dig = true;
             const DigGeo& g = M->dgeo;
             M->d_part_mid = dalloc<double>(size_t(max_cand) * (size_t(1) << g.l1) * 2);
             M->d_part_dot = dalloc<double>(size_t(max_cand) * M->P * g.nblk_col * (MAXD + 1));
-            M->d_counter = dalloc<unsigned int>(max_cand);
-            CK(cudaMemset(M->d_counter, 0, sizeof(unsigned int) * max_cand));
+            M->d_counter = dalloc<unsigned int>(size_t(max_cand) * (1 + M->P));
+            CK(cudaMemset(M->d_counter, 0, sizeof(unsigned int) * max_cand * (1 + M->P)));
+            M->d_vec_sum = dalloc<double>(size_t(max_cand) * M->P * (MAXD + 1));
             // distinct pair offsets (diagonal pairs share offset 0)
             std::vector<int> pofs(M->P);
             std::vector<uint64_t> uniq;
@@ -960,16 +967,22 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
             M->nblk_solve = 1;
         }
         M->d_psolve = dalloc<double>(size_t(max_cand) * std::max(M->nblk_solve, 1) * 3);
-        M->d_bad = dalloc<int>(2 * size_t(max_cand));
-        M->d_imre = dalloc<unsigned long long>(2 * MAXT * size_t(max_cand));
-        CK(cudaMallocHost(reinterpret_cast<void**>(&M->h_imre), sizeof(double) * 2 * MAXT * max_cand));
-        M->d_out = dalloc<double>(size_t(max_cand) * NOUT);
+        // one result block [out | bad | imre] -> a single D2H copy per evaluation
+        M->res_len = size_t(max_cand) * (NOUT + 1 + 2 * MAXT);
+        M->d_res = dalloc<double>(M->res_len);
+        CK(cudaMallocHost(reinterpret_cast<void**>(&M->h_res), sizeof(double) * M->res_len));
+        M->d_out = M->d_res;
+        M->d_bad = reinterpret_cast<int*>(M->d_res + size_t(max_cand) * NOUT);
+        M->d_imre = reinterpret_cast<unsigned long long*>(M->d_res + size_t(max_cand) * (NOUT + 1));
+        M->h_out = M->h_res;
+        M->h_bad = reinterpret_cast<int*>(M->h_res + size_t(max_cand) * NOUT);
+        M->h_imre = M->h_res + size_t(max_cand) * (NOUT + 1);
+
         M->d_vecA = dalloc<double>(M->N);
         M->d_vecB = dalloc<double>(M->N);
         M->d_sA = dalloc<char>(M->task_slots * es);
         M->d_sB = dalloc<char>(M->task_slots * es);
-        CK(cudaMallocHost(reinterpret_cast<void**>(&M->h_out), sizeof(double) * NOUT * max_cand));
-        CK(cudaMallocHost(reinterpret_cast<void**>(&M->h_bad), sizeof(int) * 2 * max_cand));
+
         CK(cudaMemsetAsync(M->d_yhat, 0, M->task_slots * es, M->st));
         M->uneq = unequal::create(M);
         CK(cudaStreamSynchronize(M->st));
@@ -1049,6 +1062,7 @@ int fmtgp_model_destroy(fmtgp_model_t M) {
     F(M->d_part_mid);
     F(M->d_part_dot);
     F(M->d_counter);
+    F(M->d_vec_sum);
     F(M->d_pair_ofs);
     F(M->d_ofs);
     F(M->d_kap);
@@ -1056,18 +1070,15 @@ int fmtgp_model_destroy(fmtgp_model_t M) {
     F(M->d_chat);
     F(M->d_psolve);
     F(M->d_pgrad);
-    F(M->d_bad);
-    F(M->d_imre);
-    if (M->h_imre) cudaFreeHost(M->h_imre);
-    F(M->d_out);
+    F(M->d_res);
+    if (M->h_res) cudaFreeHost(M->h_res);
     F(M->d_vecA);
     F(M->d_vecB);
     F(M->d_sA);
     F(M->d_sB);
     if (M->uneq) unequal::destroy(M->uneq);
     if (M->h_stage) cudaFreeHost(M->h_stage);
-    if (M->h_out) cudaFreeHost(M->h_out);
-    if (M->h_bad) cudaFreeHost(M->h_bad);
+
     if (M->st) cudaStreamDestroy(M->st);
     delete M;
     return FMTGP_OK;
@@ -1341,6 +1352,7 @@ int fmtgp_posterior_mean(fmtgp_model_t M, int task, const double* X, int64_t cou
         if (count <= 0) return;
         CK(cudaSetDevice(M->dev));
         ensure_coefficients(M);
+        upload_fit(M);
         double* dX = dalloc<double>(size_t(count) * M->d);
         double* dO = dalloc<double>(size_t(count));
         try {

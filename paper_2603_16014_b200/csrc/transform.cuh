@@ -16,6 +16,14 @@ namespace fmtgp {
 
 constexpr int EPT = 16;
 
+// Bank-conflict-free smem addressing: one pad element after every 16 (a radix-16 group's
+// stride-1 stage would otherwise put 32 lanes 128 B apart, i.e. on one bank).
+template <bool PADDED>
+__device__ __forceinline__ int sidx(int i) {
+    return PADDED ? i + (i >> 4) : i;
+}
+__host__ __device__ constexpr int padded_len(int n) { return n + (n >> 4) + 1; }
+
 // In-register DFT of R points (natural order in, bit-reversed order out), dir = -1 / +1.
 template <int R>
 __device__ __forceinline__ void reg_dft(double2* v, int dir) {
@@ -102,7 +110,7 @@ __device__ __forceinline__ void reg_wht(double* v) {
 
 // One Stockham stage of radix R over nvec vectors of length 2^logN (vector q at
 // buf + q * vstride).  Ns = 2^ns_log is the size of the already-combined sub-DFTs.
-template <int NT, int R, int RL>
+template <int NT, int R, int RL, bool PADDED = false>
 __device__ __forceinline__ void fft_stage(double2* buf, int logN, int ns_log, int nvec, int vstride, int dir,
                                           const double2* __restrict__ tw) {
     constexpr int G = EPT / R;
@@ -118,7 +126,7 @@ __device__ __forceinline__ void fft_stage(double2* buf, int logN, int ns_log, in
             const double2* x = buf + vec * vstride;
             const int k = j & ((1 << ns_log) - 1);
 #pragma unroll
-            for (int r = 0; r < R; ++r) v[q][r] = x[j + (r << gpv_log)];
+            for (int r = 0; r < R; ++r) v[q][r] = x[sidx<PADDED>(j + (r << gpv_log))];
             if (ns_log > 0) {
 #pragma unroll
                 for (int r = 1; r < R; ++r) {
@@ -140,7 +148,7 @@ __device__ __forceinline__ void fft_stage(double2* buf, int logN, int ns_log, in
             const int k = j & ((1 << ns_log) - 1);
             const int o = ((j >> ns_log) << (ns_log + RL)) + k;
 #pragma unroll
-            for (int r = 0; r < R; ++r) x[o + (brev_c<R>(r) << ns_log)] = v[q][r];
+            for (int r = 0; r < R; ++r) x[sidx<PADDED>(o + (brev_c<R>(r) << ns_log))] = v[q][r];
         }
     }
     __syncthreads();
@@ -148,28 +156,28 @@ __device__ __forceinline__ void fft_stage(double2* buf, int logN, int ns_log, in
 
 // Full unnormalised DFT of nvec vectors of length 2^logN in smem (natural order).
 // Caller must __syncthreads() before (data in place); returns synchronised.
-template <int NT>
+template <int NT, bool PADDED = false>
 __device__ void smem_fft(double2* buf, int logN, int nvec, int vstride, int dir, const double2* __restrict__ tw) {
     int done = 0;
     while (done < logN) {
         const int left = logN - done;
         if (left >= 4) {
-            fft_stage<NT, 16, 4>(buf, logN, done, nvec, vstride, dir, tw);
+            fft_stage<NT, 16, 4, PADDED>(buf, logN, done, nvec, vstride, dir, tw);
             done += 4;
         } else if (left == 3) {
-            fft_stage<NT, 8, 3>(buf, logN, done, nvec, vstride, dir, tw);
+            fft_stage<NT, 8, 3, PADDED>(buf, logN, done, nvec, vstride, dir, tw);
             done += 3;
         } else if (left == 2) {
-            fft_stage<NT, 4, 2>(buf, logN, done, nvec, vstride, dir, tw);
+            fft_stage<NT, 4, 2, PADDED>(buf, logN, done, nvec, vstride, dir, tw);
             done += 2;
         } else {
-            fft_stage<NT, 2, 1>(buf, logN, done, nvec, vstride, dir, tw);
+            fft_stage<NT, 2, 1, PADDED>(buf, logN, done, nvec, vstride, dir, tw);
             done += 1;
         }
     }
 }
 
-template <int NT, int R, int RL>
+template <int NT, int R, int RL, bool PADDED = false>
 __device__ __forceinline__ void wht_stage(double* buf, int logN, int s, int nvec, int vstride) {
     constexpr int G = EPT / R;
     const int gpv_log = logN - RL;
@@ -185,32 +193,32 @@ __device__ __forceinline__ void wht_stage(double* buf, int logN, int s, int nvec
             const int base = (hi << (s + RL)) | lo;
             double v[R];
 #pragma unroll
-            for (int r = 0; r < R; ++r) v[r] = x[base + (r << s)];
+            for (int r = 0; r < R; ++r) v[r] = x[sidx<PADDED>(base + (r << s))];
             reg_wht<R>(v);
 #pragma unroll
-            for (int r = 0; r < R; ++r) x[base + (r << s)] = v[r];
+            for (int r = 0; r < R; ++r) x[sidx<PADDED>(base + (r << s))] = v[r];
         }
     }
     __syncthreads();
 }
 
 // Unnormalised Walsh-Hadamard transform of nvec vectors of length 2^logN in smem.
-template <int NT>
+template <int NT, bool PADDED = false>
 __device__ void smem_wht(double* buf, int logN, int nvec, int vstride) {
     int done = 0;
     while (done < logN) {
         const int left = logN - done;
         if (left >= 4) {
-            wht_stage<NT, 16, 4>(buf, logN, done, nvec, vstride);
+            wht_stage<NT, 16, 4, PADDED>(buf, logN, done, nvec, vstride);
             done += 4;
         } else if (left == 3) {
-            wht_stage<NT, 8, 3>(buf, logN, done, nvec, vstride);
+            wht_stage<NT, 8, 3, PADDED>(buf, logN, done, nvec, vstride);
             done += 3;
         } else if (left == 2) {
-            wht_stage<NT, 4, 2>(buf, logN, done, nvec, vstride);
+            wht_stage<NT, 4, 2, PADDED>(buf, logN, done, nvec, vstride);
             done += 2;
         } else {
-            wht_stage<NT, 2, 1>(buf, logN, done, nvec, vstride);
+            wht_stage<NT, 2, 1, PADDED>(buf, logN, done, nvec, vstride);
             done += 1;
         }
     }

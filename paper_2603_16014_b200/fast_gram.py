@@ -141,9 +141,20 @@ class Model:
         return v.value
 
     # -- gp_core hot path
+    def _hyper_struct(self, hp: Hyper):
+        """CHyper for hp, reused while hp and its arrays are the same objects (the struct points
+        at the arrays' buffers, so in-place edits are seen)."""
+        key = (id(hp), id(hp.eta), id(hp.B), id(hp.t), id(hp.xi), hp.gamma, hp.si_alpha, tuple(hp.b))
+        cached = getattr(self, "_hcache", None)
+        if cached is not None and cached[0] == key:
+            return cached[1]
+        ch, keep = _chyper(hp)
+        self._hcache = (key, ch, keep)
+        return ch
+
     def nll(self, hp: Hyper, grad: bool = True) -> Dict:
         """refresh + loss_value (NMLL) with escalation, plus the analytic gradient."""
-        ch, keep = _chyper(hp)
+        ch = self._hyper_struct(hp)
         r = CResult()
         check(self.lib.fmtgp_nll(self.h, C.byref(ch), int(grad), C.byref(r)))
         self.hyper = hp
