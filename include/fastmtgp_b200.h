@@ -68,6 +68,14 @@ typedef struct fmtgp_hyper {
     const double* xi;    /* [L] >= 0 nugget */
 } fmtgp_hyper;
 
+/* SpatialKernel (kernels.hpp:53-66) for the explicit-R seam entry point. */
+typedef struct fmtgp_spatial {
+    double gamma;
+    const double* eta;   /* [d] */
+    int si_alpha;
+    double b[4];
+} fmtgp_spatial;
+
 /* One NLL evaluation: loss_value (gp_core.cpp:197-227) plus the analytic gradient that
  * replaces the reference's central finite differences (gp_core.cpp:341-351). */
 typedef struct fmtgp_result {
@@ -104,6 +112,10 @@ FMTGP_API void* fmtgp_model_stream(fmtgp_model_t model);
 /* ---- fast_gram.hpp seam ------------------------------------------------------------ */
 /* build_spectrum (fast_gram.cpp:42-89): Lam_{l,lp} for the hyperparameters. */
 FMTGP_API int fmtgp_build_spectrum(fmtgp_model_t model, const fmtgp_hyper* h);
+/* build_spectrum with the reference's exact argument list (fast_gram.hpp:34-36):
+ * R_internal [L * L] row-major task Gram, spatial kernel, xi_internal [L]. */
+FMTGP_API int fmtgp_build_spectrum_R(fmtgp_model_t model, const double* R_internal, const fmtgp_spatial* spatial,
+                                     const double* xi_internal);
 /* copy pair (l <= lp) back in natural frequency order, length n_l (tests / small N) */
 FMTGP_API int fmtgp_spectrum_read(fmtgp_model_t model, int l, int lp, double* re, double* im);
 /* invert_and_logdet (fast_gram.cpp:151-263): factorises the current spectrum.

@@ -1125,6 +1125,56 @@ int fmtgp_build_spectrum(fmtgp_model_t M, const fmtgp_hyper* h) {
     });
 }
 
+// build_spectrum(design, R_internal, spatial, xi_internal) with an explicit task Gram matrix
+// (the exact fast_gram.hpp:34-36 signature): R is any symmetric L x L (row-major).
+int fmtgp_build_spectrum_R(fmtgp_model_t M, const double* R, const fmtgp_spatial* sp, const double* xi) {
+    return guarded([&] {
+        ProfGuard pg_(M);
+        if (!M || !R || !sp || !sp->eta || !xi) invalid("build_spectrum: null argument");
+        if (M->lattice && sp->si_alpha != 1 && sp->si_alpha != 2) invalid("si_bernoulli_1d: alpha must be 1 or 2");
+        CK(cudaSetDevice(M->dev));
+        // express R through the hyperparameter record: B = 0 (s = 0) is not general, so load the
+        // packed block directly: coefficients are R_ab * sqrt(n_b / n_a)
+        const int T = M->T;
+        std::vector<double> Bf(size_t(T) * T, 0.0), tv(T, 1.0);
+        fmtgp_hyper h{};
+        h.gamma = sp->gamma;
+        h.eta = sp->eta;
+        h.si_alpha = sp->si_alpha;
+        for (int i = 0; i < 4; ++i) h.b[i] = sp->b[i];
+        h.B = Bf.data();
+        h.s = T;
+        h.t = tv.data();
+        h.xi = xi;
+        const double one = 1.0;
+        const fmtgp_hyper* hs[1] = {&h};
+        fill_hyper(M, 1, hs, &one);
+        // overwrite Rpair and the per-group coefficients with the explicit R
+        double* Rp = M->h_hyp + size_t(M->max_cand) * (M->d + 1);
+        for (int p = 0; p < M->P; ++p) Rp[p] = R[M->pa[p] * T + M->pb[p]];
+        double* cur = Rp + size_t(M->max_cand) * M->P;
+        for (auto& g : M->groups) {
+            const int np = int(g.pairs.size());
+            for (int q = 0; q < np; ++q) {
+                const int p = g.pairs[q];
+                cur[q] = R[M->pa[p] * T + M->pb[p]] * std::sqrt(double(M->n[M->pb[p]]) / double(M->n[M->pa[p]]));
+            }
+            cur += 2 * size_t(M->max_cand) * np;
+        }
+        copy_hyper(M);
+        build_spectra(M, 1, sp->si_alpha, sp->b);
+        CK(cudaStreamSynchronize(M->st));
+        M->last_gamma = sp->gamma;
+        M->last_eta.assign(sp->eta, sp->eta + M->d);
+        M->last_R.assign(R, R + size_t(T) * T);
+        M->last_alpha = sp->si_alpha;
+        for (int i = 0; i < 4; ++i) M->last_b[i] = sp->b[i];
+        M->fit_dirty = true;
+        M->have_spec = true;
+        M->have_inv = false;
+    });
+}
+
 int fmtgp_spectrum_read(fmtgp_model_t M, int l, int lp, double* re, double* im) {
     return guarded([&] {
         if (!M || !re || !im) invalid("spectrum_read: null argument");
