@@ -256,6 +256,7 @@ __device__ void grad_flush(const GradSink& gs, int v, int blk, GradAcc& acc) {
 }
 
 struct SinkGrad {  // fused dot (large problems)
+    using Acc = GradAcc;
     GradSink gs;
     int lattice, m;
     __device__ __forceinline__ void lat(int v, uint64_t j, double2 z, GradAcc& acc) const {
@@ -273,7 +274,57 @@ struct SinkGrad {  // fused dot (large problems)
     }
 };
 
+template <int DC>
+struct GradAccD {
+    double a[DC + 1];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int i = 0; i <= DC; ++i) a[i] = 0.0;
+    }
+};
+
+// Fused gradient dot with DC-sized register arrays (large problems).
+template <int DC>
+struct SinkGradD {
+    GradSink gs;
+    int lattice, m;
+    using Acc = GradAccD<DC>;
+    __device__ __forceinline__ void add(int v, uint64_t idx, double W, Acc& acc) const {
+        int p, c;
+        gs.gen.coords(v, p, c);
+        double kappa[DC], dq[DC];
+        GenSrcD<DC>{gs.gen}.kappa_c(p, idx, kappa);
+        const int d = gs.gen.sp.d;
+        const double q = product_kernel_c<DC>(kappa, gs.gen.eta + size_t(c) * d, d, __ldg(gs.gen.gamma + c), dq, true);
+#pragma unroll
+        for (int j = 0; j < DC; ++j)
+            if (j < d) acc.a[j] = fma(W, dq[j], acc.a[j]);
+        acc.a[DC] = fma(W, q, acc.a[DC]);
+    }
+    __device__ __forceinline__ void lat(int v, uint64_t j, double2 z, Acc& acc) const {
+        if (m == 0) {
+            add(v, 0, z.x, acc);
+            return;
+        }
+        add(v, 2 * j, 2.0 * z.x, acc);
+        add(v, 2 * j + 1, 2.0 * z.y, acc);
+    }
+    __device__ __forceinline__ void dig(int v, uint64_t j, double w, Acc& acc) const { add(v, j, w, acc); }
+    template <int NT>
+    __device__ __forceinline__ void flush(int v, int blk, Acc& acc) const {
+        __shared__ double redv[(NT / 32) * (DC + 1)];
+        block_sum_vec<NT, DC + 1>(acc.a, redv);
+        if (threadIdx.x == 0) {
+            double* out = gs.partial + ((size_t)v * gs.nblk + blk) * (MAXD + 1);
+            const int d = gs.gen.sp.d;
+            for (int j = 0; j < d; ++j) out[j] = acc.a[j];
+            out[MAXD] = acc.a[DC];
+        }
+    }
+};
+
 struct SinkStoreW {  // W in transform-input order for k_gen_dot (small problems)
+    using Acc = GradAcc;
     double* W;
     long long n;
     int m;
@@ -292,6 +343,7 @@ struct SinkStoreW {  // W in transform-input order for k_gen_dot (small problems
 };
 
 struct SinkCoef {
+    using Acc = GradAcc;
     CoefSink cs;
     int lattice, m;
     __device__ __forceinline__ void lat(int v, uint64_t j, double2 z, GradAcc&) const {
@@ -320,7 +372,7 @@ __global__ void __launch_bounds__(NT) k_inv_small_lat(const double2* __restrict_
     const int v = blockIdx.x;
     const int c = v / nvpc;
     const double2* x = in + c * cstride + in_off[v - c * nvpc];
-    GradAcc acc;
+    typename Snk::Acc acc;
     acc.zero();
     if (m == 0) {
         if (threadIdx.x == 0) snk.lat(v, 0, x[0], acc);
@@ -356,7 +408,7 @@ __global__ void __launch_bounds__(NT) k_inv_small_dig(const double* __restrict__
     for (int e = threadIdx.x; e < n; e += NT) sm[e] = x[e];
     __syncthreads();
     smem_wht<NT>(sm, m, 1, n);
-    GradAcc acc;
+    typename Snk::Acc acc;
     acc.zero();
     for (int e = threadIdx.x; e < n; e += NT) snk.dig(v, e, sm[e], acc);
     snk.template flush<NT>(v, 0, acc);
@@ -438,7 +490,7 @@ __global__ void __launch_bounds__(NT) k_inv_col_lat(const double2* __restrict__ 
     }
     __syncthreads();
     smem_fft<NT>(sm, l1, C, N1, +1, tw);
-    GradAcc acc;
+    typename Snk::Acc acc;
     acc.zero();
     for (int e = threadIdx.x; e < (C << l1); e += NT) {
         const int j1 = e >> lc, c = e & (C - 1);
@@ -462,7 +514,7 @@ __global__ void __launch_bounds__(NT) k_inv_col_dig(const double* __restrict__ U
     }
     __syncthreads();
     smem_wht<NT>(sm, l1, C, N1);
-    GradAcc acc;
+    typename Snk::Acc acc;
     acc.zero();
     for (int e = threadIdx.x; e < (C << l1); e += NT) {
         const int j1 = e >> lc, c = e & (C - 1);
@@ -565,7 +617,10 @@ void fwd_gen(int lattice, const Geo& g, int nvec, const GenSrc& src, const SpecS
         fwd_impl(lattice, g, nvec, BufSrc{static_cast<const double*>(genbuf), n}, snk, work, tw, s);
         return;
     }
-    fwd_impl(lattice, g, nvec, src, snk, work, tw, s);
+    const int d = src.sp.d;
+    if (d <= 4) fwd_impl(lattice, g, nvec, GenSrcD<4>{src}, snk, work, tw, s);
+    else if (d <= 8) fwd_impl(lattice, g, nvec, GenSrcD<8>{src}, snk, work, tw, s);
+    else fwd_impl(lattice, g, nvec, GenSrcD<16>{src}, snk, work, tw, s);
 }
 
 void fwd_array(int lattice, const Geo& g, int nvec, const ArraySrc& src, const ScaleSink& snk, void* work,
@@ -656,8 +711,10 @@ void inv_grad(int lattice, const Geo& g, int nvec, const void* in, const long lo
                                        gs, static_cast<const double*>(genbuf), n))
         return;
     }
-    SinkGrad snk{gs, lattice, g.m};
-    inv_impl(lattice, g, nvec, in, in_off, cstride, nvpc, snk, work, tw, s);
+    const int d = gs.gen.sp.d;
+    if (d <= 4) inv_impl(lattice, g, nvec, in, in_off, cstride, nvpc, SinkGradD<4>{gs, lattice, g.m}, work, tw, s);
+    else if (d <= 8) inv_impl(lattice, g, nvec, in, in_off, cstride, nvpc, SinkGradD<8>{gs, lattice, g.m}, work, tw, s);
+    else inv_impl(lattice, g, nvec, in, in_off, cstride, nvpc, SinkGradD<16>{gs, lattice, g.m}, work, tw, s);
 }
 
 void inv_coef(int lattice, const Geo& g, int nvec, const void* in, const long long* in_off, const CoefSink& cs,

@@ -105,6 +105,62 @@ struct GenSrc {
     }
 };
 
+// GenSrc with register arrays sized by a compile-time dimension cap DC >= d (4, 8 or 16):
+// the generic MAXD = 16 arrays made the fused transform kernels spill.
+template <int DC>
+__device__ __forceinline__ double product_kernel_c(const double* kappa, const double* eta, int d, double gamma,
+                                                   double* dq, bool grad) {
+    double f[DC];
+    double prod = gamma;
+#pragma unroll
+    for (int j = 0; j < DC; ++j)
+        if (j < d) {
+            f[j] = 1.0 + __ldg(eta + j) * kappa[j];
+            prod *= f[j];
+        }
+    if (grad) {
+        double pre = gamma;
+#pragma unroll
+        for (int j = 0; j < DC; ++j)
+            if (j < d) {
+                dq[j] = pre * kappa[j];
+                pre *= f[j];
+            }
+        double suf = 1.0;
+#pragma unroll
+        for (int j = DC - 1; j >= 0; --j)
+            if (j < d) {
+                dq[j] *= suf;
+                suf *= f[j];
+            }
+    }
+    return prod;
+}
+
+template <int DC>
+struct GenSrcD {
+    GenSrc g;
+    __device__ __forceinline__ void kappa_c(int p, uint64_t idx, double* kappa) const {
+        const uint64_t* off = g.offs + size_t(p) * MAXD;
+        if (g.sp.family == 0) {
+#pragma unroll
+            for (int j = 0; j < DC; ++j)
+                if (j < g.sp.d) kappa[j] = si_base(g.pg.lattice_word(idx, j, __ldg(off + j)), g.sp.si_alpha);
+        } else {
+#pragma unroll
+            for (int j = 0; j < DC; ++j)
+                if (j < g.sp.d) kappa[j] = dsi_walsh(g.pg.digital_z(idx, j) ^ __ldg(off + j), g.sp.b);
+        }
+    }
+    __device__ __forceinline__ double operator()(int v, uint64_t idx) const {
+        int p, c;
+        g.coords(v, p, c);
+        double kappa[DC];
+        kappa_c(p, idx, kappa);
+        return product_kernel_c<DC>(kappa, g.eta + size_t(c) * g.sp.d, g.sp.d, __ldg(g.gamma + c), nullptr, false);
+    }
+};
+
 // Data vector gathered into transform order: lattice y(bitrev_m(j)) (V̄ = DFT o bitrev),
 // digital y(i).  src + vec_off[v] is the task's block.
 struct ArraySrc {

@@ -110,8 +110,10 @@ __device__ __forceinline__ void reg_wht(double* v) {
 
 // One Stockham stage of radix R over nvec vectors of length 2^logN (vector q at
 // buf + q * vstride).  Ns = 2^ns_log is the size of the already-combined sub-DFTs.
+// Tail stages (R < 16) hold G = 16/R groups per thread; kept out of line so their register
+// allocation does not stack on top of the radix-16 stages inlined in the same kernel.
 template <int NT, int R, int RL, bool PADDED = false>
-__device__ __forceinline__ void fft_stage(double2* buf, int logN, int ns_log, int nvec, int vstride, int dir,
+__device__ __forceinline__ void fft_stage_body(double2* buf, int logN, int ns_log, int nvec, int vstride, int dir,
                                           const double2* __restrict__ tw) {
     constexpr int G = EPT / R;
     const int gpv_log = logN - RL;
@@ -152,6 +154,19 @@ __device__ __forceinline__ void fft_stage(double2* buf, int logN, int ns_log, in
         }
     }
     __syncthreads();
+}
+
+template <int NT, int R, int RL, bool PADDED>
+__device__ __noinline__ void fft_stage_tail(double2* buf, int logN, int ns_log, int nvec, int vstride, int dir,
+                                            const double2* __restrict__ tw) {
+    fft_stage_body<NT, R, RL, PADDED>(buf, logN, ns_log, nvec, vstride, dir, tw);
+}
+
+template <int NT, int R, int RL, bool PADDED = false>
+__device__ __forceinline__ void fft_stage(double2* buf, int logN, int ns_log, int nvec, int vstride, int dir,
+                                          const double2* __restrict__ tw) {
+    if constexpr (R == 16) fft_stage_body<NT, R, RL, PADDED>(buf, logN, ns_log, nvec, vstride, dir, tw);
+    else fft_stage_tail<NT, R, RL, PADDED>(buf, logN, ns_log, nvec, vstride, dir, tw);
 }
 
 // Full unnormalised DFT of nvec vectors of length 2^logN in smem (natural order).
