@@ -50,6 +50,18 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+// One element of a global -> shared staging loop (double or double2), issued asynchronously so a
+// thread keeps all of its loads in flight; pair with cp_async_wait_all() before the barrier.
+template <class T>
+__device__ __forceinline__ void cp_async_el(T* smem, const T* gmem) {
+    static_assert(sizeof(T) == 8 || sizeof(T) == 16, "cp_async_el: 8 or 16 bytes");
+    if constexpr (sizeof(T) == 16) cp_async16(smem, gmem);
+    else cp_async8(smem, gmem);
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // ---------------------------------------------------------------- reductions

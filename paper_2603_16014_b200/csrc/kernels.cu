@@ -32,23 +32,24 @@ template <int NT, class Src, class Snk>
 __global__ void __launch_bounds__(NT) k_fwd_small_lat(Src src, Snk snk, int m, const double2* __restrict__ tw) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double2* sm = reinterpret_cast<double2*>(smraw);
+    constexpr auto S = sidx<true>;
     const int v = blockIdx.x;
     if (m == 0) {
         if (threadIdx.x == 0) snk.put(v, 0, make_double2(src(v, 0), 0.0));
         return;
     }
     const int lp = m - 1, Np = 1 << lp;
-    for (int e = threadIdx.x; e < Np; e += NT) sm[e] = make_double2(src(v, 2ull * e), src(v, 2ull * e + 1));
+    for (int e = threadIdx.x; e < Np; e += NT) sm[S(e)] = make_double2(src(v, 2ull * e), src(v, 2ull * e + 1));
     __syncthreads();
-    smem_fft<NT>(sm, lp, 1, Np, -1, tw);
+    smem_fft<NT, true>(sm, lp, 1, padded_len(Np), -1, tw);
     for (int k = threadIdx.x; k <= Np / 2; k += NT) {
         if (k == 0) {
-            const double2 Z0 = sm[0];
+            const double2 Z0 = sm[S(0)];
             snk.put(v, 0, make_double2(Z0.x + Z0.y, Z0.x - Z0.y));
             continue;
         }
         const int kp = Np - k;
-        const double2 Zk = sm[k], Zp = sm[kp];
+        const double2 Zk = sm[S(k)], Zp = sm[S(kp)];
         snk.put(v, k, r2c_post(Zk, Zp, twiddle(tw, k, m)));
         if (kp != k) snk.put(v, kp, r2c_post(Zp, Zk, twiddle(tw, kp, m)));
     }
@@ -58,11 +59,12 @@ template <int NT, class Src, class Snk>
 __global__ void __launch_bounds__(NT) k_fwd_small_dig(Src src, Snk snk, int m) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double* sm = reinterpret_cast<double*>(smraw);
+    constexpr auto S = sidx<true>;
     const int v = blockIdx.x, n = 1 << m;
-    for (int e = threadIdx.x; e < n; e += NT) sm[e] = src(v, e);
+    for (int e = threadIdx.x; e < n; e += NT) sm[S(e)] = src(v, e);
     __syncthreads();
-    smem_wht<NT>(sm, m, 1, n);
-    for (int e = threadIdx.x; e < n; e += NT) snk.put(v, e, sm[e]);
+    smem_wht<NT, true>(sm, m, 1, padded_len(n));
+    for (int e = threadIdx.x; e < n; e += NT) snk.put(v, e, sm[S(e)]);
 }
 
 // ============================================================================ forward, two pass
@@ -71,20 +73,21 @@ __global__ void __launch_bounds__(NT) k_fwd_col_lat(Src src, double2* __restrict
                                                     long long vstride, const double2* __restrict__ tw) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double2* sm = reinterpret_cast<double2*>(smraw);
-    const int v = blockIdx.y, C = 1 << lc, N1 = 1 << l1;
+    constexpr auto S = sidx<true>;
+    const int v = blockIdx.y, C = 1 << lc, N1 = 1 << l1, ld = padded_len(N1);
     const long long c0 = (long long)blockIdx.x << lc;
     for (int e = threadIdx.x; e < (C << l1); e += NT) {
         const int j1 = e >> lc, c = e & (C - 1);
         const uint64_t j = (uint64_t(j1) << l2) + c0 + c;
-        sm[c * N1 + j1] = make_double2(src(v, 2 * j), src(v, 2 * j + 1));
+        sm[c * ld + S(j1)] = make_double2(src(v, 2 * j), src(v, 2 * j + 1));
     }
     __syncthreads();
-    smem_fft<NT>(sm, l1, C, N1, -1, tw);
+    smem_fft<NT, true>(sm, l1, C, ld, -1, tw);
     double2* out = Y + v * vstride;
     for (int e = threadIdx.x; e < (C << l1); e += NT) {
         const int k1 = e >> lc, c = e & (C - 1);
         const uint64_t j2 = c0 + c;
-        out[((long long)k1 << l2) + j2] = cmul(sm[c * N1 + k1], twiddle(tw, j2 * uint64_t(k1), l1 + l2));
+        out[((long long)k1 << l2) + j2] = cmul(sm[c * ld + S(k1)], twiddle(tw, j2 * uint64_t(k1), l1 + l2));
     }
 }
 
@@ -93,18 +96,19 @@ __global__ void __launch_bounds__(NT) k_fwd_col_dig(Src src, double* __restrict_
                                                     long long vstride) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double* sm = reinterpret_cast<double*>(smraw);
-    const int v = blockIdx.y, C = 1 << lc, N1 = 1 << l1;
+    constexpr auto S = sidx<true>;
+    const int v = blockIdx.y, C = 1 << lc, N1 = 1 << l1, ld = padded_len(N1);
     const long long c0 = (long long)blockIdx.x << lc;
     for (int e = threadIdx.x; e < (C << l1); e += NT) {
         const int j1 = e >> lc, c = e & (C - 1);
-        sm[c * N1 + j1] = src(v, (uint64_t(j1) << l2) + c0 + c);
+        sm[c * ld + S(j1)] = src(v, (uint64_t(j1) << l2) + c0 + c);
     }
     __syncthreads();
-    smem_wht<NT>(sm, l1, C, N1);
+    smem_wht<NT, true>(sm, l1, C, ld);
     double* out = Y + v * vstride;
     for (int e = threadIdx.x; e < (C << l1); e += NT) {
         const int k1 = e >> lc, c = e & (C - 1);
-        out[((long long)k1 << l2) + c0 + c] = sm[c * N1 + k1];
+        out[((long long)k1 << l2) + c0 + c] = sm[c * ld + S(k1)];
     }
 }
 
@@ -119,27 +123,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT)
                   const double2* __restrict__ tw) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double2* sm = reinterpret_cast<double2*>(smraw);
+    constexpr auto S = sidx<true>;
     cg::cluster_group cl = cg::this_cluster();
     const int rank = int(cl.block_rank());
     const int q = blockIdx.x >> 1, v = blockIdx.y;
     const int N1 = 1 << l1, N2 = 1 << l2;
     const int row = row_of_cluster(q, rank, N1);
     const double2* in = Y + v * vstride + ((long long)row << l2);
-    for (int e = threadIdx.x; e < N2; e += NT) sm[e] = in[e];
+    for (int e = threadIdx.x; e < N2; e += NT) cp_async_el(&sm[S(e)], &in[e]);
+    cp_async_wait_all();
     __syncthreads();
-    smem_fft<NT>(sm, l2, 1, N2, -1, tw);
+    smem_fft<NT, true>(sm, l2, 1, padded_len(N2), -1, tw);
     cl.sync();
     const bool self = (row == 0) || (row == N1 / 2);
     const double2* psm = self ? sm : cl.map_shared_rank(sm, rank ^ 1);
     for (int k2 = threadIdx.x; k2 < N2; k2 += NT) {
         const long long k = row + ((long long)k2 << l1);
         if (k == 0) {
-            const double2 Z0 = sm[0];
+            const double2 Z0 = sm[S(0)];
             snk.put(v, 0, make_double2(Z0.x + Z0.y, Z0.x - Z0.y));
             continue;
         }
         const int kc = (row == 0) ? ((N2 - k2) & (N2 - 1)) : (N2 - 1 - k2);
-        snk.put(v, ((long long)row << l2) + k2, r2c_post(sm[k2], psm[kc], twiddle(tw, uint64_t(k), m)));
+        snk.put(v, ((long long)row << l2) + k2, r2c_post(sm[S(k2)], psm[S(kc)], twiddle(tw, uint64_t(k), m)));
     }
     cl.sync();
 }
@@ -148,12 +154,14 @@ template <int NT, class Snk>
 __global__ void __launch_bounds__(NT) k_fwd_row_dig(const double* __restrict__ Y, Snk snk, int l2, long long vstride) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double* sm = reinterpret_cast<double*>(smraw);
+    constexpr auto S = sidx<true>;
     const int row = blockIdx.x, v = blockIdx.y, N2 = 1 << l2;
     const double* in = Y + v * vstride + ((long long)row << l2);
-    for (int e = threadIdx.x; e < N2; e += NT) sm[e] = in[e];
+    for (int e = threadIdx.x; e < N2; e += NT) cp_async_el(&sm[S(e)], &in[e]);
+    cp_async_wait_all();
     __syncthreads();
-    smem_wht<NT>(sm, l2, 1, N2);
-    for (int e = threadIdx.x; e < N2; e += NT) snk.put(v, ((long long)row << l2) + e, sm[e]);
+    smem_wht<NT, true>(sm, l2, 1, padded_len(N2));
+    for (int e = threadIdx.x; e < N2; e += NT) snk.put(v, ((long long)row << l2) + e, sm[S(e)]);
 }
 
 // ============================================================================ generator / gradient-dot (split mode)
@@ -369,6 +377,7 @@ __global__ void __launch_bounds__(NT) k_inv_small_lat(const double2* __restrict_
                                                       const double2* __restrict__ tw) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double2* sm = reinterpret_cast<double2*>(smraw);
+    constexpr auto S = sidx<true>;
     const int v = blockIdx.x;
     const int c = v / nvpc;
     const double2* x = in + c * cstride + in_off[v - c * nvpc];
@@ -383,17 +392,17 @@ __global__ void __launch_bounds__(NT) k_inv_small_lat(const double2* __restrict_
     for (int k = threadIdx.x; k <= Np / 2; k += NT) {
         if (k == 0) {
             const double2 A = x[0];
-            sm[0] = make_double2(0.5 * (A.x + A.y), 0.5 * (A.x - A.y));
+            sm[S(0)] = make_double2(0.5 * (A.x + A.y), 0.5 * (A.x - A.y));
             continue;
         }
         const int kp = Np - k;
         const double2 Ak = x[k], Ap = x[kp];
-        sm[k] = c2r_pre(Ak, Ap, twiddle(tw, k, m));
-        if (kp != k) sm[kp] = c2r_pre(Ap, Ak, twiddle(tw, kp, m));
+        sm[S(k)] = c2r_pre(Ak, Ap, twiddle(tw, k, m));
+        if (kp != k) sm[S(kp)] = c2r_pre(Ap, Ak, twiddle(tw, kp, m));
     }
     __syncthreads();
-    smem_fft<NT>(sm, lp, 1, Np, +1, tw);
-    for (int j = threadIdx.x; j < Np; j += NT) snk.lat(v, j, sm[j], acc);
+    smem_fft<NT, true>(sm, lp, 1, padded_len(Np), +1, tw);
+    for (int j = threadIdx.x; j < Np; j += NT) snk.lat(v, j, sm[S(j)], acc);
     snk.template flush<NT>(v, 0, acc);
 }
 
@@ -402,15 +411,17 @@ __global__ void __launch_bounds__(NT) k_inv_small_dig(const double* __restrict__
                                                       long long cstride, int nvpc, Snk snk, int m) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double* sm = reinterpret_cast<double*>(smraw);
+    constexpr auto S = sidx<true>;
     const int v = blockIdx.x, n = 1 << m;
     const int c = v / nvpc;
     const double* x = in + c * cstride + in_off[v - c * nvpc];
-    for (int e = threadIdx.x; e < n; e += NT) sm[e] = x[e];
+    for (int e = threadIdx.x; e < n; e += NT) cp_async_el(&sm[S(e)], &x[e]);
+    cp_async_wait_all();
     __syncthreads();
-    smem_wht<NT>(sm, m, 1, n);
+    smem_wht<NT, true>(sm, m, 1, padded_len(n));
     typename Snk::Acc acc;
     acc.zero();
-    for (int e = threadIdx.x; e < n; e += NT) snk.dig(v, e, sm[e], acc);
+    for (int e = threadIdx.x; e < n; e += NT) snk.dig(v, e, sm[S(e)], acc);
     snk.template flush<NT>(v, 0, acc);
 }
 
@@ -421,6 +432,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT)
                   double2* __restrict__ U, long long vstride, int l1, int l2, int m, const double2* __restrict__ tw) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double2* sm = reinterpret_cast<double2*>(smraw);
+    constexpr auto S = sidx<true>;
     cg::cluster_group cl = cg::this_cluster();
     const int rank = int(cl.block_rank());
     const int q = blockIdx.x >> 1, v = blockIdx.y;
@@ -428,7 +440,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT)
     const int row = row_of_cluster(q, rank, N1);
     const int c = v / nvpc;
     const double2* x = in + c * cstride + in_off[v - c * nvpc] + ((long long)row << l2);
-    for (int e = threadIdx.x; e < N2; e += NT) sm[e] = x[e];
+    for (int e = threadIdx.x; e < N2; e += NT) cp_async_el(&sm[S(e)], &x[e]);
+    cp_async_wait_all();
     cl.sync();
     const bool self = (row == 0) || (row == N1 / 2);
     const double2* psm = self ? sm : cl.map_shared_rank(sm, rank ^ 1);
@@ -439,11 +452,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT)
         if (k2 < N2) {
             const long long k = row + ((long long)k2 << l1);
             if (k == 0) {
-                const double2 A = sm[0];
+                const double2 A = sm[S(0)];
                 zr[t] = make_double2(0.5 * (A.x + A.y), 0.5 * (A.x - A.y));
             } else {
                 const int kc = (row == 0) ? ((N2 - k2) & (N2 - 1)) : (N2 - 1 - k2);
-                zr[t] = c2r_pre(sm[k2], psm[kc], twiddle(tw, uint64_t(k), m));
+                zr[t] = c2r_pre(sm[S(k2)], psm[S(kc)], twiddle(tw, uint64_t(k), m));
             }
         }
     }
@@ -451,13 +464,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT)
 #pragma unroll
     for (int t = 0; t < EPT; ++t) {
         const int k2 = threadIdx.x + t * NT;
-        if (k2 < N2) sm[k2] = zr[t];
+        if (k2 < N2) sm[S(k2)] = zr[t];
     }
     __syncthreads();
-    smem_fft<NT>(sm, l2, 1, N2, +1, tw);
+    smem_fft<NT, true>(sm, l2, 1, padded_len(N2), +1, tw);
     double2* out = U + v * vstride + ((long long)row << l2);
     for (int j2 = threadIdx.x; j2 < N2; j2 += NT)
-        out[j2] = cmulc(sm[j2], twiddle(tw, uint64_t(j2) * uint64_t(row), l1 + l2));
+        out[j2] = cmulc(sm[S(j2)], twiddle(tw, uint64_t(j2) * uint64_t(row), l1 + l2));
 }
 
 template <int NT>
@@ -466,14 +479,16 @@ __global__ void __launch_bounds__(NT) k_inv_row_dig(const double* __restrict__ i
                                                     long long vstride, int l2) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double* sm = reinterpret_cast<double*>(smraw);
+    constexpr auto S = sidx<true>;
     const int row = blockIdx.x, v = blockIdx.y, N2 = 1 << l2;
     const int c = v / nvpc;
     const double* x = in + c * cstride + in_off[v - c * nvpc] + ((long long)row << l2);
-    for (int e = threadIdx.x; e < N2; e += NT) sm[e] = x[e];
+    for (int e = threadIdx.x; e < N2; e += NT) cp_async_el(&sm[S(e)], &x[e]);
+    cp_async_wait_all();
     __syncthreads();
-    smem_wht<NT>(sm, l2, 1, N2);
+    smem_wht<NT, true>(sm, l2, 1, padded_len(N2));
     double* out = U + v * vstride + ((long long)row << l2);
-    for (int e = threadIdx.x; e < N2; e += NT) out[e] = sm[e];
+    for (int e = threadIdx.x; e < N2; e += NT) out[e] = sm[S(e)];
 }
 
 template <int NT, class Snk>
@@ -481,21 +496,23 @@ __global__ void __launch_bounds__(NT) k_inv_col_lat(const double2* __restrict__ 
                                                     int l2, int lc, const double2* __restrict__ tw) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double2* sm = reinterpret_cast<double2*>(smraw);
-    const int v = blockIdx.y, C = 1 << lc, N1 = 1 << l1;
+    constexpr auto S = sidx<true>;
+    const int v = blockIdx.y, C = 1 << lc, N1 = 1 << l1, ld = padded_len(N1);
     const long long c0 = (long long)blockIdx.x << lc;
     const double2* x = U + v * vstride;
     for (int e = threadIdx.x; e < (C << l1); e += NT) {
         const int k1 = e >> lc, c = e & (C - 1);
-        sm[c * N1 + k1] = x[((long long)k1 << l2) + c0 + c];
+        cp_async_el(&sm[c * ld + S(k1)], &x[((long long)k1 << l2) + c0 + c]);
     }
+    cp_async_wait_all();
     __syncthreads();
-    smem_fft<NT>(sm, l1, C, N1, +1, tw);
+    smem_fft<NT, true>(sm, l1, C, ld, +1, tw);
     typename Snk::Acc acc;
     acc.zero();
     for (int e = threadIdx.x; e < (C << l1); e += NT) {
         const int j1 = e >> lc, c = e & (C - 1);
         const uint64_t j = (uint64_t(j1) << l2) + c0 + c;
-        snk.lat(v, j, sm[c * N1 + j1], acc);
+        snk.lat(v, j, sm[c * ld + S(j1)], acc);
     }
     snk.template flush<NT>(v, blockIdx.x, acc);
 }
@@ -505,20 +522,22 @@ __global__ void __launch_bounds__(NT) k_inv_col_dig(const double* __restrict__ U
                                                     int l2, int lc) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double* sm = reinterpret_cast<double*>(smraw);
-    const int v = blockIdx.y, C = 1 << lc, N1 = 1 << l1;
+    constexpr auto S = sidx<true>;
+    const int v = blockIdx.y, C = 1 << lc, N1 = 1 << l1, ld = padded_len(N1);
     const long long c0 = (long long)blockIdx.x << lc;
     const double* x = U + v * vstride;
     for (int e = threadIdx.x; e < (C << l1); e += NT) {
         const int k1 = e >> lc, c = e & (C - 1);
-        sm[c * N1 + k1] = x[((long long)k1 << l2) + c0 + c];
+        cp_async_el(&sm[c * ld + S(k1)], &x[((long long)k1 << l2) + c0 + c]);
     }
+    cp_async_wait_all();
     __syncthreads();
-    smem_wht<NT>(sm, l1, C, N1);
+    smem_wht<NT, true>(sm, l1, C, ld);
     typename Snk::Acc acc;
     acc.zero();
     for (int e = threadIdx.x; e < (C << l1); e += NT) {
         const int j1 = e >> lc, c = e & (C - 1);
-        snk.dig(v, (uint64_t(j1) << l2) + c0 + c, sm[c * N1 + j1], acc);
+        snk.dig(v, (uint64_t(j1) << l2) + c0 + c, sm[c * ld + S(j1)], acc);
     }
     snk.template flush<NT>(v, blockIdx.x, acc);
 }
@@ -548,7 +567,7 @@ static void fwd_impl(int lattice, const Geo& g, int nvec, const Src& src, const 
                      const double2* tw, cudaStream_t s) {
     const size_t es = lattice ? sizeof(double2) : sizeof(double);
     if (!g.two) {
-        const size_t sm = (size_t(1) << g.lt) * es;
+        const size_t sm = size_t(padded_len(1 << g.lt)) * es;
         const int nt = nt_for(g.lt);
         if (lattice) {
             FM_NT_DISPATCH(nt, {
@@ -567,7 +586,7 @@ static void fwd_impl(int lattice, const Geo& g, int nvec, const Src& src, const 
         }
         return;
     }
-    const size_t sm = (size_t(1) << g.cap) * es;
+    const size_t sm = size_t(std::max((1 << (g.cap - g.l1)) * padded_len(1 << g.l1), padded_len(1 << g.l2))) * es;
     const long long vstride = 1ll << g.lt;
     const int lc = g.cap - g.l1;
     const int ncol_blk = (1 << g.l2) >> lc;
@@ -646,7 +665,7 @@ static void inv_impl(int lattice, const Geo& g, int nvec, const void* in, const 
                      int nvpc, const Snk& snk, void* work, const double2* tw, cudaStream_t s) {
     const size_t es = lattice ? sizeof(double2) : sizeof(double);
     if (!g.two) {
-        const size_t sm = (size_t(1) << g.lt) * es;
+        const size_t sm = size_t(padded_len(1 << g.lt)) * es;
         const int nt = nt_for(g.lt);
         if (lattice) {
             FM_NT_DISPATCH(nt, {
@@ -665,7 +684,7 @@ static void inv_impl(int lattice, const Geo& g, int nvec, const void* in, const 
         }
         return;
     }
-    const size_t sm = (size_t(1) << g.cap) * es;
+    const size_t sm = size_t(std::max((1 << (g.cap - g.l1)) * padded_len(1 << g.l1), padded_len(1 << g.l2))) * es;
     const long long vstride = 1ll << g.lt;
     const int lc = g.cap - g.l1;
     const int ncol_blk = (1 << g.l2) >> lc;

@@ -130,11 +130,20 @@ __device__ __forceinline__ void fft_stage_body(double2* buf, int logN, int ns_lo
 #pragma unroll
             for (int r = 0; r < R; ++r) v[q][r] = x[sidx<PADDED>(j + (r << gpv_log))];
             if (ns_log > 0) {
+                // w^r for r < R: table reads at r = 1, 4, 8, 12 and at most three products by w in
+                // between (4 loads instead of R-1 — those loads were this loop's long-scoreboard
+                // stalls; error a few ulp; 12 live registers, no spill at NT = 512).
+                double2 w1 = make_double2(1.0, 0.0), cur = w1;
 #pragma unroll
                 for (int r = 1; r < R; ++r) {
-                    double2 w = twiddle(tw, uint64_t(r) * uint64_t(k), ns_log + RL);
-                    if (dir > 0) w.y = -w.y;
-                    v[q][r] = cmul(v[q][r], w);
+                    if (r == 1 || (r & 3) == 0) {
+                        cur = twiddle(tw, uint64_t(r) * uint64_t(k), ns_log + RL);
+                        if (dir > 0) cur.y = -cur.y;
+                        if (r == 1) w1 = cur;
+                    } else {
+                        cur = cmul(cur, w1);
+                    }
+                    v[q][r] = cmul(v[q][r], cur);
                 }
             }
             reg_dft<R>(v[q], dir);
