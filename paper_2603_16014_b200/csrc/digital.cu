@@ -5,7 +5,7 @@ namespace fmtgp {
 
 bool DigGeo::make(int m, int P, DigGeo& g, long long total_vecs) {
     if (m < 1 || P < 1) return false;
-    // row length: all P rows of one frequency block in <= 64 KB of smem
+    // row length: all P (= class count V) rows of one frequency block in <= 64 KB of smem
     int l2max = 0;
     while (l2max < 13 && (long long)P * (2ll << l2max) * 8 <= 65536) ++l2max;
     int l2 = std::min(l2max, (m + 1) / 2);
@@ -63,7 +63,7 @@ template <int NT, int D>
 __global__ void __launch_bounds__(NT, 3) k_dig_col_fwd(DigArgs a, int l1, int l2, int lc) {
     extern __shared__ __align__(16) double sm[];
     __shared__ GenSmem<D> tab;
-    const int v = blockIdx.y, c = v / a.P, p = v - c * a.P;
+    const int v = blockIdx.y, c = v / a.V, o = v - c * a.V;
     const int C = 1 << lc, N1 = 1 << l1, ld = padded_len(N1);
     const long long c0 = (long long)blockIdx.x << lc, n = a.n;
     double eta[D];
@@ -78,10 +78,10 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_fwd(DigArgs a, int l1, int l2
         g.eta = a.eta;
         gen_smem_init<D>(tab, g, c);
 #pragma unroll
-        for (int j = 0; j < D; ++j) off[j] = __ldg(a.offs + size_t(p) * MAXD + j);
+        for (int j = 0; j < D; ++j) off[j] = __ldg(a.cofs + size_t(o) * MAXD + j);
         __syncthreads();
     }
-    const double* kp = a.kap ? a.kap + size_t(__ldg(a.pair_ofs + p)) * D * n : nullptr;
+    const double* kp = a.kap ? a.kap + size_t(o) * D * n : nullptr;
     const int tile = C << l1;
     if (kp) {
         // design-time kappa tile -> smem with cp.async (no register staging)
@@ -126,32 +126,39 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_fwd(DigArgs a, int l1, int l2
 template <int NT, int T>
 __global__ void __launch_bounds__(NT) k_dig_mid(DigArgs a, int l2) {
     constexpr int P = T * (T + 1) / 2;
-    extern __shared__ __align__(16) double sm[];  // [P][padded N2]
-    const int row = blockIdx.x, c = blockIdx.y, N2 = 1 << l2, lds = padded_len(N2);
+    extern __shared__ __align__(16) double sm[];  // [V][padded N2]
+    __shared__ double s_coef[P], s_xi[P], s_wR[P];
+    __shared__ int s_cls[P];
+    const int row = blockIdx.x, c = blockIdx.y, N2 = 1 << l2, lds = padded_len(N2), V = a.V;
     const long long n = a.n, base = (long long)row << l2;
-    double* Yc = a.Y + size_t(c) * P * n;
-    for (int e = threadIdx.x; e < (P << l2); e += NT) {
-        const int p = e >> l2, k2 = e & (N2 - 1);
-        sm[p * lds + sidx<true>(k2)] = Yc[size_t(p) * n + base + k2];
+    double* Yc = a.Y + size_t(c) * V * n;
+    for (int e = threadIdx.x; e < (V << l2); e += NT) {
+        const int o = e >> l2, k2 = e & (N2 - 1);
+        cp_async8(&sm[o * lds + sidx<true>(k2)], &Yc[size_t(o) * n + base + k2]);
     }
+    if (threadIdx.x < P) {
+        const int q = threadIdx.x;
+        s_coef[q] = __ldg(a.coef + size_t(c) * P + q);
+        s_xi[q] = __ldg(a.xi + size_t(c) * P + q);
+        s_wR[q] = (a.pair_a[q] == a.pair_b[q] ? 1.0 : 2.0) * __ldg(a.Rpair + size_t(c) * P + q);
+        s_cls[q] = a.pair_ofs[q];
+    }
+    cp_async_wait_all();
     __syncthreads();
-    smem_wht<NT, true>(sm, l2, P, lds);
-    double coef[P], xi[P];
+    smem_wht<NT, true>(sm, l2, V, lds);
+    double acc[2 + P], imx[T], rex[T];  // logdet, quad, sum_k M_p qhat_o (dR partials)
 #pragma unroll
-    for (int q = 0; q < P; ++q) {
-        coef[q] = __ldg(a.coef + size_t(c) * P + q);
-        xi[q] = __ldg(a.xi + size_t(c) * P + q);
-    }
-    double ld_acc = 0.0, q_acc = 0.0, imx[T], rex[T];
+    for (int q = 0; q < 2 + P; ++q) acc[q] = 0.0;
 #pragma unroll
     for (int t = 0; t < T; ++t) imx[t] = rex[t] = 0.0;
     int first_bad = 0x7f7f7f7f;
     for (int k2 = threadIdx.x; k2 < N2; k2 += NT) {
         const long long k = base + k2;
+        const int si = sidx<true>(k2);
         double A[P], r[T], ch[T], Ai[P];
 #pragma unroll
         for (int q = 0; q < P; ++q) {
-            A[q] = fma(coef[q], sm[q * lds + sidx<true>(k2)], xi[q]);  // lam = R_ab * H q + xi (fast_gram.cpp:82-85)
+            A[q] = fma(s_coef[q], sm[s_cls[q] * lds + si], s_xi[q]);  // lam = R_ab * H q + xi (fast_gram.cpp:82-85)
             if (a.lam_out) a.lam_out[(size_t(c) * P + q) * n + k] = A[q];
         }
 #pragma unroll
@@ -159,48 +166,42 @@ __global__ void __launch_bounds__(NT) k_dig_mid(DigArgs a, int l2) {
         double ld, qd;
         const int st = ldl_solve<T, false>(A, r, a.want_grad != 0, ld, qd, ch, Ai, imx, rex);
         if (st == 1 && int(k) < first_bad) first_bad = int(k);
-        ld_acc += ld;
-        q_acc += qd;
+        acc[0] += ld;
+        acc[1] += qd;
         if (a.want_grad) {
+            double Mq[P];
             int q = 0;
 #pragma unroll
             for (int x = 0; x < T; ++x)
 #pragma unroll
-                for (int y = x; y < T; ++y, ++q) sm[q * lds + sidx<true>(k2)] = Ai[q] - ch[x] * ch[y];  // M
+                for (int y = x; y < T; ++y, ++q) Mq[q] = Ai[q] - ch[x] * ch[y];  // M = dNLL/dLam
+#pragma unroll
+            for (int q2 = 0; q2 < P; ++q2) acc[2 + q2] = fma(Mq[q2], sm[s_cls[q2] * lds + si], acc[2 + q2]);
+            for (int o = 0; o < V; ++o) sm[o * lds + si] = 0.0;  // this thread owns column k2 of every class
+#pragma unroll
+            for (int q2 = 0; q2 < P; ++q2) sm[s_cls[q2] * lds + si] += s_wR[q2] * Mq[q2];  // Z_o
         }
         if (a.chat_out && c == 0) {
 #pragma unroll
             for (int t = 0; t < T; ++t) a.chat_out[size_t(t) * n + k] = ch[t];
         }
     }
-    __shared__ double redv[(NT / 32) * 2];
-    double lq[2] = {ld_acc, q_acc};
-    block_sum_vec<NT, 2>(lq, redv);
+    __shared__ double redv[(NT / 32) * (2 + P)];
+    block_sum_vec<NT, 2 + P>(acc, redv);
     const int nrows = gridDim.x;
     if (threadIdx.x == 0) {
-        a.part_mid[(size_t(c) * nrows + row) * 2 + 0] = lq[0];
-        a.part_mid[(size_t(c) * nrows + row) * 2 + 1] = lq[1];
+        double* pm = a.part_mid + (size_t(c) * nrows + row) * (2 + P);
+#pragma unroll
+        for (int q = 0; q < 2 + P; ++q) pm[q] = acc[q];
     }
     if (first_bad != 0x7f7f7f7f) atomicMin(a.bad + c, first_bad);
-#pragma unroll
-    for (int t = 0; t < T; ++t) {
-        double vi = imx[t], vr = rex[t];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            vi = fmax(vi, __shfl_xor_sync(0xffffffffu, vi, o));
-            vr = fmax(vr, __shfl_xor_sync(0xffffffffu, vr, o));
-        }
-        if ((threadIdx.x & 31) == 0) {
-            atomicMax(a.imre + (size_t(c) * MAXT + t) * 2 + 0, (unsigned long long)__double_as_longlong(vi));
-            atomicMax(a.imre + (size_t(c) * MAXT + t) * 2 + 1, (unsigned long long)__double_as_longlong(vr));
-        }
-    }
+    // real spectra: the stage-global non-real test cannot fire, imre stays zeroed by K1
     if (!a.want_grad) return;
     __syncthreads();
-    smem_wht<NT, true>(sm, l2, P, lds);  // inverse FWHT over the row bits (self-inverse up to scale)
-    for (int e = threadIdx.x; e < (P << l2); e += NT) {
-        const int p = e >> l2, k2 = e & (N2 - 1);
-        Yc[size_t(p) * n + base + k2] = sm[p * lds + sidx<true>(k2)];
+    smem_wht<NT, true>(sm, l2, V, lds);  // inverse FWHT over the row bits (self-inverse up to scale)
+    for (int e = threadIdx.x; e < (V << l2); e += NT) {
+        const int o = e >> l2, k2 = e & (N2 - 1);
+        Yc[size_t(o) * n + base + k2] = sm[o * lds + sidx<true>(k2)];
     }
 }
 
@@ -211,14 +212,14 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
     __shared__ GenSmem<D> tab;
     __shared__ double red[32];
     __shared__ int s_last;
-    const int v = blockIdx.y, c = v / a.P, p = v - c * a.P;
+    const int v = blockIdx.y, c = v / a.V, o = v - c * a.V;
     const int C = 1 << lc, N1 = 1 << l1, ld = padded_len(N1);
     const long long c0 = (long long)blockIdx.x << lc, n = a.n;
     const double* x = a.Y + size_t(v) * n;
     const int tile = C << l1;
     double* kbuf = sm + C * ld;
     if (a.kap) {  // kappa tile streams into smem while the column is loaded and transformed
-        const double* kp0 = a.kap + size_t(__ldg(a.pair_ofs + p)) * D * n;
+        const double* kp0 = a.kap + size_t(o) * D * n;
         for (int idx = threadIdx.x; idx < tile * D; idx += NT) {
             const int j = idx / tile, e = idx - j * tile;
             const long long i = ((long long)(e >> lc) << l2) + c0 + (e & (C - 1));
@@ -241,9 +242,9 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
         g.eta = a.eta;
         gen_smem_init<D>(tab, g, c);
 #pragma unroll
-        for (int j = 0; j < D; ++j) off[j] = __ldg(a.offs + size_t(p) * MAXD + j);
+        for (int j = 0; j < D; ++j) off[j] = __ldg(a.cofs + size_t(o) * MAXD + j);
     }
-    const double* kp = a.kap ? a.kap + size_t(__ldg(a.pair_ofs + p)) * D * n : nullptr;
+    const double* kp = a.kap ? a.kap + size_t(o) * D * n : nullptr;
     double acc[D + 1];
 #pragma unroll
     for (int j = 0; j <= D; ++j) acc[j] = 0.0;
@@ -277,63 +278,53 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
         }
     }
     const int nblk = gridDim.x;
-    double* out = a.part_dot + ((size_t(c) * a.P + p) * nblk + blockIdx.x) * (MAXD + 1);
+    double* out = a.part_dot + (size_t(v) * nblk + blockIdx.x) * (MAXD + 1);
     __shared__ double redv[(NT / 32) * (D + 1)];
     block_sum_vec<NT, D + 1>(acc, redv);
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int j = 0; j <= D; ++j) out[j == D ? MAXD : j] = acc[j];
     }
-    // two-level last-CTA reduction (threadFenceReduction pattern, fixed order => deterministic):
-    // the last CTA of each vector folds its nblk partials, the last vector of a candidate
-    // finalises the candidate's record.
+    // last-CTA reduction (threadFenceReduction pattern, one ticket per candidate over all of its
+    // V * nblk CTAs; fixed summation order => deterministic)
     if (threadIdx.x == 0) __threadfence();  // thread 0 wrote this CTA's partial
     __syncthreads();
     if (threadIdx.x == 0) {
-        const unsigned ticket = atomicAdd(a.counter + a.nc + v, 1u);
-        s_last = ticket == unsigned(nblk) - 1;
-        if (s_last) a.counter[a.nc + v] = 0;
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    {
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        const double* pv = a.part_dot + (size_t(c) * a.P + p) * nblk * (MAXD + 1);
-        for (int j = warp; j <= D; j += NT / 32) {
-            const int comp = j == D ? MAXD : j;
-            double s = 0.0;
-            for (int b = lane; b < nblk; b += 32) s += __ldcg(pv + size_t(b) * (MAXD + 1) + comp);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            if (lane == 0) a.vec_sum[size_t(v) * (MAXD + 1) + comp] = s;
-        }
-    }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
         const unsigned ticket = atomicAdd(a.counter + c, 1u);
-        s_last = ticket == unsigned(a.P) - 1;
+        s_last = ticket == unsigned(a.V * nblk) - 1;
         if (s_last) a.counter[c] = 0;  // self-reset for the next replay
     }
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    FinalArgs fa{};
+    __shared__ double s_vec[MAXP * (MAXD + 1)];
+    {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const double* pc = a.part_dot + size_t(c) * a.V * nblk * (MAXD + 1);
+        for (int t = warp; t < a.V * (D + 1); t += NT / 32) {
+            const int oo = t / (D + 1), j = t - oo * (D + 1), comp = j == D ? MAXD : j;
+            double s = 0.0;
+            for (int b = lane; b < nblk; b += 32) s += __ldcg(pc + (size_t(oo) * nblk + b) * (MAXD + 1) + comp);
+#pragma unroll
+            for (int o2 = 16; o2 > 0; o2 >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o2);
+            if (lane == 0) s_vec[oo * (MAXD + 1) + comp] = s;
+        }
+    }
+    __syncthreads();
+    ClassFinal fa{};
     fa.T = a.T;
     fa.P = a.P;
+    fa.V = a.V;
     fa.d = D;
-    fa.ncand = a.nc;
-    fa.nblk_solve = nrows;
-    fa.nblk_grad = 1;
-    fa.solve_partial = a.part_mid;
-    fa.grad_partial = a.vec_sum;
+    fa.nrows = nrows;
+    fa.part_mid = a.part_mid;
+    fa.vec_sum = s_vec;
     fa.Rpair = a.Rpair;
     fa.gamma = a.gamma;
     fa.pair_a = a.pair_a;
     fa.pair_b = a.pair_b;
     fa.out = a.out;
-    finalize_candidate<NT>(fa, c);
+    finalize_classes<NT>(fa, c);
 }
 
 // ------------------------------------------------------------------ launcher
@@ -357,7 +348,7 @@ void dig_fit(const DigGeo& g, const DigArgs& a, cudaStream_t s) {
     const int C = 1 << g.lc;
     const size_t sm_col = (size_t(C) * padded_len(1 << g.l1) + (a.kap ? size_t(a.d) << (g.l1 + g.lc) : 0)) *
                           sizeof(double);
-    const dim3 gcol(g.nblk_col, a.P * a.nc);
+    const dim3 gcol(g.nblk_col, a.V * a.nc);
     FM_D_DISPATCH(a.d, {
         FM_NT_DISPATCH(g.nt_col, {
             auto k1 = k_dig_col_fwd<NT, D>;
@@ -366,7 +357,7 @@ void dig_fit(const DigGeo& g, const DigArgs& a, cudaStream_t s) {
             k1<<<gcol, NT, sm_col, s>>>(a, g.l1, g.l2, g.lc);
         })
     })
-    const size_t sm_mid = size_t(a.P) * padded_len(1 << g.l2) * sizeof(double);
+    const size_t sm_mid = size_t(a.V) * padded_len(1 << g.l2) * sizeof(double);
     switch (a.T) {
         case 1: mid_launch<1>(g, a, sm_mid, s); break;
         case 2: mid_launch<2>(g, a, sm_mid, s); break;

@@ -1,10 +1,13 @@
 // Equal-n digital-net (DSI / FWHT) fit in three fused kernels — the configuration-2/5 hot path.
 //
-//   K1 k_dig_col_fwd : generator q_ab(i) (design-time kappa table or on the fly) x column FWHT
-//   K2 k_dig_mid     : row FWHT of every pair + spectrum epilogue (R, xi) + per-frequency T x T
-//                      LDL^H solve (logdet, quad, M = Lam^-1 - chat chat^H) + inverse row FWHT of M
-//   K3 k_dig_col_inv : inverse column FWHT -> W = H M -> gradient dot with dq/deta, q -> partials,
-//                      last CTA reduces everything into the result record
+//   K1 k_dig_col_fwd : generator q_o(i) (design-time kappa table or on the fly) x column FWHT,
+//                      one vector per pair-offset CLASS o (pairs with equal Delta_a ^ Delta_b share
+//                      q — all diagonal pairs do), not per pair
+//   K2 k_dig_mid     : row FWHT of every class + spectrum epilogue per pair (R, xi) + per-frequency
+//                      T x T LDL^H solve (logdet, quad, M = Lam^-1 - chat chat^H) + dR partials
+//                      sum_k M_p qhat_o (Parseval) + Z_o = sum_{p in o} w_p R_p M_p + inverse row FWHT
+//   K3 k_dig_col_inv : inverse column FWHT -> H Z_o -> dot with dq_o/deta -> partials,
+//                      last CTA reduces everything into the result record (ClassFinal)
 //
 // n = N1 * N2 (natural index i = j1 * N2 + j2); FWHT over the two bit groups commutes, and the
 // spectrum index after both passes is natural, so K2 owns the frequencies {k1 * N2 + k2}: all
@@ -21,17 +24,18 @@ struct DigGeo {
     int lc;          // log2 columns per K1/K3 CTA (tile = 2^(l1 + lc) <= 2^11)
     int nt_col, nt_mid;
     int nblk_col;    // K1/K3 CTAs per vector
-    static bool make(int m, int P, DigGeo& g, long long total_vecs = 0);
+    static bool make(int m, int V, DigGeo& g, long long total_vecs = 0);  // V rows per K2 CTA
 };
 
 struct DigArgs {
     int T, P, d, nc;
+    int V;                    // distinct pair-offset classes (transforms run per class)
     long long n;
     Spatial sp;
     PointGen pg;
-    const uint64_t* offs;     // [P][MAXD]
-    const double* kap;        // design-time table [nofs][d][n] (nullptr: evaluate on the fly)
-    const int* pair_ofs;      // [P] pair -> distinct offset index
+    const uint64_t* cofs;     // [V][MAXD] class offsets
+    const double* kap;        // design-time table [V][d][n] (nullptr: evaluate on the fly)
+    const int* pair_ofs;      // [P] pair -> class
     const double* eta;        // [nc][d]
     const double* gamma;      // [nc]
     const double* coef;       // [nc][P]  R_ab
@@ -40,15 +44,15 @@ struct DigArgs {
     const int* pair_a;
     const int* pair_b;
     const double* yhat;       // [T][n]
-    double* Y;                // [nc][P][n] intermediate (column pass out, row pass in/out)
+    double* Y;                // [nc][V][n] intermediate (column pass out, row pass in/out)
     double* lam_out;          // [nc][P][n] spectrum (nullptr: skip)
     double* chat_out;         // [T][n] chat of candidate 0 (nullptr: skip)
-    double* part_mid;         // [nc][nrows][2]
-    double* part_dot;         // [nc][P][nblk_col][MAXD+1]
+    double* part_mid;         // [nc][nrows][2 + P]  logdet, quad, sum_k M_p qhat_o (ClassFinal)
+    double* part_dot;         // [nc][V][nblk_col][MAXD+1]
     int* bad;                 // [nc] first failing slot, 0x7f7f7f7f none
     unsigned long long* imre; // [nc][MAXT][2]
-    unsigned int* counter;    // [nc + nc*P] last-CTA tickets (self-resetting)
-    double* vec_sum;          // [nc][P][MAXD+1] per-vector gradient sums
+    unsigned int* counter;    // [nc + nc*V] last-CTA tickets (self-resetting)
+    double* vec_sum;          // [nc][V][MAXD+1] per-class gradient sums
     double* out;              // [nc][NOUT]
     int want_grad;
 };

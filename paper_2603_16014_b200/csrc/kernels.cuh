@@ -104,6 +104,7 @@ struct FinalArgs {
     const int* pair_a;            // [P]
     const int* pair_b;            // [P]
     double* out;                  // [ncand][NOUT]
+    int solve_stride = 2;         // doubles per solve partial record (logdet, quad, ...)
 };
 // partials may come from other CTAs of the same kernel (last-CTA finalize): L2 loads (__ldcg)
 // per-candidate output record
@@ -120,8 +121,8 @@ __device__ void finalize_candidate(const FinalArgs& a, int c) {
     const int d = a.d, P = a.P;
     double ld = 0.0, q = 0.0;
     for (int b = threadIdx.x; b < a.nblk_solve; b += NT) {
-        ld += __ldcg(a.solve_partial + ((size_t)c * a.nblk_solve + b) * 2 + 0);
-        q += __ldcg(a.solve_partial + ((size_t)c * a.nblk_solve + b) * 2 + 1);
+        ld += __ldcg(a.solve_partial + ((size_t)c * a.nblk_solve + b) * a.solve_stride + 0);
+        q += __ldcg(a.solve_partial + ((size_t)c * a.nblk_solve + b) * a.solve_stride + 1);
     }
     ld = block_sum<NT>(ld, red);
     q = block_sum<NT>(q, red);
@@ -168,6 +169,78 @@ __device__ void finalize_candidate(const FinalArgs& a, int c) {
 }
 
 
+// Gradient bookkeeping when the transforms run per OFFSET CLASS instead of per pair (pairs whose
+// generators share the shift difference Delta_a - Delta_b share q, e.g. every diagonal pair):
+//   dNLL/dR_p = w_p <W_p, q_o> = w_p sum_k M_p(k) qhat_o(k)        (Parseval, per-frequency partials)
+//   dNLL/deta = sum_o <Z_o, dq_o/deta>,  Z_o = H^-1 (sum_{p in o} w_p R_p M_p)   (one inverse per class)
+//   dNLL/dgamma = sum_p R_p dNLL/dR_p / gamma                          (q is linear in gamma)
+struct ClassFinal {
+    int T, P, V, d, nrows;
+    const double* part_mid;  // [ncand][nrows][2 + P]  logdet, quad, sum_k M_p qhat
+    const double* vec_sum;   // [V][MAXD + 1] of candidate c (global or shared)  <Z_o, dq_o/deta_j>
+    const double* Rpair;     // [ncand][P]
+    const double* gamma;     // [ncand]
+    const int* pair_a;
+    const int* pair_b;
+    double* out;             // [ncand][NOUT]
+};
+
+template <int NT>
+__device__ void finalize_classes(const ClassFinal& a, int c) {
+    double* out = a.out + (size_t)c * NOUT;
+    __shared__ double red[32];
+    __shared__ double sdr[MAXP], sR[MAXP], sdeta[MAXD];
+    __shared__ int spa[MAXP], spb[MAXP];
+    const int S = 2 + a.P;
+    const double* pm = a.part_mid + (size_t)c * a.nrows * S;
+    double ld = 0.0, q = 0.0;
+    for (int b = threadIdx.x; b < a.nrows; b += NT) {
+        ld += __ldcg(pm + (size_t)b * S + 0);
+        q += __ldcg(pm + (size_t)b * S + 1);
+    }
+    ld = block_sum<NT>(ld, red);
+    q = block_sum<NT>(q, red);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int p = warp; p < a.P; p += NT / 32) {  // fixed-order strided sums + warp tree (deterministic)
+        double s = 0.0;
+        for (int b = lane; b < a.nrows; b += 32) s += __ldcg(pm + (size_t)b * S + 2 + p);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) sdr[p] = s;
+    }
+    // everything thread 0 needs is staged in parallel (no serial L2 round trips in the tail)
+    for (int p = threadIdx.x; p < a.P; p += NT) {
+        spa[p] = a.pair_a[p];
+        spb[p] = a.pair_b[p];
+        sR[p] = a.Rpair[(size_t)c * a.P + p];
+    }
+    for (int j = threadIdx.x; j < MAXD; j += NT) {
+        double s = 0.0;
+        if (j < a.d)
+            for (int o = 0; o < a.V; ++o) s += a.vec_sum[(size_t)o * (MAXD + 1) + j];
+        sdeta[j] = s;
+    }
+    for (int x = threadIdx.x; x < MAXT * MAXT; x += NT) out[OUT_DR + x] = 0.0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        out[OUT_LOGDET] = ld;
+        out[OUT_QUAD] = q;
+        out[OUT_NLL] = q + ld;  // rT c + logdet (gp_core.cpp:207-211)
+        double dgam = 0.0;
+        for (int p = 0; p < a.P; ++p) {
+            const int pa = spa[p], pb = spb[p];
+            const double dRp = (pa == pb ? 1.0 : 2.0) * sdr[p];
+            dgam += sR[p] * dRp;
+            if (pa == pb) out[OUT_DR + pa * MAXT + pb] = dRp;
+            else {
+                out[OUT_DR + pa * MAXT + pb] = 0.5 * dRp;
+                out[OUT_DR + pb * MAXT + pa] = 0.5 * dRp;
+            }
+        }
+        out[OUT_DGAMMA] = dgam / a.gamma[c];
+        for (int j = 0; j < MAXD; ++j) out[OUT_DETA + j] = sdeta[j];
+    }
+}
 
 // ---------------------------------------------------------------- per-slot matvec (solve / gram apply)
 // out_a = sum_b Op_ab(k) in_b(k) with Op Hermitian given by upper pairs (equal n)

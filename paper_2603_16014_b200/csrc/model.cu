@@ -248,6 +248,25 @@ struct fmtgp_model {
     int* h_bad = nullptr;
     // state of the last spectrum / fit (candidate 0)
     bool have_spec = false, have_inv = false, have_fit = false;
+    // fmtgp_nll does not write the fit's spectrum / chat (hot loop); they are re-derived from the
+    // remembered hyperparameters (incl. the escalated noise scale) when an API call needs them
+    bool fit_lazy = false;
+    double fit_xi_scale = 1.0;
+    struct StoredHyper {
+        fmtgp_hyper h{};
+        std::vector<double> eta, B, t, xi;
+        void store(const fmtgp_hyper* src, int d, int L) {
+            h = *src;
+            eta.assign(src->eta, src->eta + d);
+            B.assign(src->B, src->B + size_t(L) * src->s);
+            t.assign(src->t, src->t + L);
+            xi.assign(src->xi, src->xi + L);
+            h.eta = eta.data();
+            h.B = B.data();
+            h.t = t.data();
+            h.xi = xi.data();
+        }
+    } fit_h;
     double last_gamma = 1.0;
     std::vector<double> last_eta, last_R;  // R internal [T*T]
     int last_alpha = 1;
@@ -496,7 +515,8 @@ void eval_digital_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, b
     a.n = M->n[0];
     a.sp = spatial_of(M, si_alpha, bw);
     a.pg = pointgen_of(M, M->m[0]);
-    a.offs = M->d_offs;
+    a.V = M->nofs;
+    a.cofs = M->d_ofs;
     a.kap = M->kap_valid ? M->d_kap : nullptr;
     a.pair_ofs = M->d_pair_ofs;
     a.eta = M->d_eta;
@@ -528,6 +548,7 @@ void eval_digital_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, b
         fa.ncand = nc;
         fa.nblk_solve = 1 << M->dgeo.l1;
         fa.solve_partial = M->d_part_mid;
+        fa.solve_stride = 2 + M->P;
         fa.Rpair = M->d_Rpair;
         fa.gamma = M->d_gamma;
         fa.pair_a = M->d_pa;
@@ -927,33 +948,33 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
         M->d_lam = dalloc<char>(size_t(max_cand) * M->total_slots * es);
         M->d_laminv = dalloc<char>(size_t(M->total_slots) * es);
         M->d_chat = dalloc<char>(size_t(M->task_slots) * es);
-        if (M->equal && !M->lattice && DigGeo::make(M->m[0], M->P, M->dgeo, (long long)M->P * max_cand)) {
+        // distinct pair offsets (diagonal pairs share offset 0): the transforms run per class
+        std::vector<int> pofs(M->P);
+        std::vector<uint64_t> uniq;
+        for (int p = 0; p < M->P; ++p) {
+            int found = -1;
+            for (int o = 0; o < M->nofs; ++o)
+                if (std::equal(offs.begin() + size_t(p) * MAXD, offs.begin() + size_t(p + 1) * MAXD,
+                               uniq.begin() + size_t(o) * MAXD))
+                    found = o;
+            if (found < 0) {
+                uniq.insert(uniq.end(), offs.begin() + size_t(p) * MAXD, offs.begin() + size_t(p + 1) * MAXD);
+                found = M->nofs++;
+            }
+            pofs[p] = found;
+        }
+        M->d_pair_ofs = dalloc<int>(M->P);
+        M->d_ofs = dalloc<uint64_t>(uniq.size());
+        CK(cudaMemcpy(M->d_pair_ofs, pofs.data(), M->P * sizeof(int), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(M->d_ofs, uniq.data(), uniq.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
+        if (M->equal && !M->lattice && DigGeo::make(M->m[0], M->nofs, M->dgeo, (long long)M->nofs * max_cand)) {
             M->dig = true;
             const DigGeo& g = M->dgeo;
-            M->d_part_mid = dalloc<double>(size_t(max_cand) * (size_t(1) << g.l1) * 2);
-            M->d_part_dot = dalloc<double>(size_t(max_cand) * M->P * g.nblk_col * (MAXD + 1));
-            M->d_counter = dalloc<unsigned int>(size_t(max_cand) * (1 + M->P));
-            CK(cudaMemset(M->d_counter, 0, sizeof(unsigned int) * max_cand * (1 + M->P)));
-            M->d_vec_sum = dalloc<double>(size_t(max_cand) * M->P * (MAXD + 1));
-            // distinct pair offsets (diagonal pairs share offset 0)
-            std::vector<int> pofs(M->P);
-            std::vector<uint64_t> uniq;
-            for (int p = 0; p < M->P; ++p) {
-                int found = -1;
-                for (int o = 0; o < M->nofs; ++o)
-                    if (std::equal(offs.begin() + size_t(p) * MAXD, offs.begin() + size_t(p + 1) * MAXD,
-                                   uniq.begin() + size_t(o) * MAXD))
-                        found = o;
-                if (found < 0) {
-                    uniq.insert(uniq.end(), offs.begin() + size_t(p) * MAXD, offs.begin() + size_t(p + 1) * MAXD);
-                    found = M->nofs++;
-                }
-                pofs[p] = found;
-            }
-            M->d_pair_ofs = dalloc<int>(M->P);
-            M->d_ofs = dalloc<uint64_t>(uniq.size());
-            CK(cudaMemcpy(M->d_pair_ofs, pofs.data(), M->P * sizeof(int), cudaMemcpyHostToDevice));
-            CK(cudaMemcpy(M->d_ofs, uniq.data(), uniq.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
+            M->d_part_mid = dalloc<double>(size_t(max_cand) * (size_t(1) << g.l1) * (2 + M->P));
+            M->d_part_dot = dalloc<double>(size_t(max_cand) * M->nofs * g.nblk_col * (MAXD + 1));
+            M->d_counter = dalloc<unsigned int>(size_t(max_cand) * (1 + M->nofs));
+            CK(cudaMemset(M->d_counter, 0, sizeof(unsigned int) * max_cand * (1 + M->nofs)));
+            M->d_vec_sum = dalloc<double>(size_t(max_cand) * M->nofs * (MAXD + 1));
             const size_t kbytes = size_t(M->nofs) * M->d * (size_t(1) << M->m[0]) * sizeof(double);
             if (kbytes <= (size_t(1) << 30)) M->d_kap = dalloc<double>(kbytes / sizeof(double));
         }
@@ -995,7 +1016,15 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
 
 }  // namespace
 
+void ensure_fit_state(fmtgp_model* M) {
+    if (!M->fit_lazy) return;
+    const fmtgp_hyper* hs[1] = {&M->fit_h.h};
+    eval_equal(M, 1, hs, &M->fit_xi_scale, /*grad=*/false, /*keep_chat=*/true);
+    M->fit_lazy = false;
+}
+
 void ensure_coefficients(fmtgp_model* M) {
+    ensure_fit_state(M);
     if (M->have_c) return;
     if (M->equal) inverse_vector(M, M->d_chat, M->d_c);
     else unequal::coefficients(M->uneq, M, M->d_c);
@@ -1094,6 +1123,7 @@ int fmtgp_model_set_y(fmtgp_model_t M, const double* y) {
         CK(cudaMemcpyAsync(M->d_y, y, sizeof(double) * M->N, cudaMemcpyHostToDevice, M->st));
         compute_yhat_tau(M);
         M->have_fit = false;
+        M->fit_lazy = false;
     });
 }
 
@@ -1105,6 +1135,7 @@ int fmtgp_model_set_y_device(fmtgp_model_t M, const double* y) {
         CK(cudaMemcpyAsync(M->d_y, y, sizeof(double) * M->N, cudaMemcpyDeviceToDevice, M->st));
         compute_yhat_tau(M);
         M->have_fit = false;
+        M->fit_lazy = false;
     });
 }
 
@@ -1114,6 +1145,7 @@ int fmtgp_build_spectrum(fmtgp_model_t M, const fmtgp_hyper* h) {
         if (!M) invalid("build_spectrum: null model");
         CK(cudaSetDevice(M->dev));
         validate_hyper(M, h);
+        ensure_fit_state(M);  // a pending fit keeps its chat / coefficients
         const double one = 1.0;
         const fmtgp_hyper* hs[1] = {h};
         upload_hyper(M, 1, hs, &one);
@@ -1133,6 +1165,7 @@ int fmtgp_build_spectrum_R(fmtgp_model_t M, const double* R, const fmtgp_spatial
         if (!M || !R || !sp || !sp->eta || !xi) invalid("build_spectrum: null argument");
         if (M->lattice && sp->si_alpha != 1 && sp->si_alpha != 2) invalid("si_bernoulli_1d: alpha must be 1 or 2");
         CK(cudaSetDevice(M->dev));
+        ensure_fit_state(M);
         // express R through the hyperparameter record: B = 0 (s = 0) is not general, so load the
         // packed block directly: coefficients are R_ab * sqrt(n_b / n_a)
         const int T = M->T;
@@ -1179,6 +1212,7 @@ int fmtgp_spectrum_read(fmtgp_model_t M, int l, int lp, double* re, double* im) 
     return guarded([&] {
         if (!M || !re || !im) invalid("spectrum_read: null argument");
         if (!M->have_spec) invalid("spectrum_read: no spectrum built");
+        ensure_fit_state(M);
         if (l < 0 || lp < l || lp >= M->T) invalid("pair_index: need 0 <= l <= lp < L");
         const int p = pair_index(M->T, l, lp);
         const long long ns = M->pslots[p], n = M->n[l];
@@ -1224,6 +1258,7 @@ int fmtgp_invert_and_logdet(fmtgp_model_t M, double* logdet) {
         ProfGuard pg_(M);
         if (!M || !logdet) invalid("invert_and_logdet: null argument");
         if (!M->have_spec) invalid("invert_and_logdet: no spectrum built");
+        ensure_fit_state(M);
         CK(cudaSetDevice(M->dev));
         if (!M->equal) {
             unequal::invert(M->uneq, M, logdet);
@@ -1293,6 +1328,7 @@ int fmtgp_gram_matvec(fmtgp_model_t M, const double* b, double* out) {
         ProfGuard pg_(M);
         if (!M || !b || !out) invalid("gram_matvec: null argument");
         if (!M->have_spec) invalid("gram_matvec: no spectrum built");
+        ensure_fit_state(M);
         CK(cudaSetDevice(M->dev));
         CK(cudaMemcpyAsync(M->d_vecA, b, sizeof(double) * M->N, cudaMemcpyHostToDevice, M->st));
         forward_vector(M, M->d_vecA, M->d_sA);
@@ -1356,12 +1392,18 @@ int fmtgp_nll(fmtgp_model_t M, const fmtgp_hyper* h, int want_grad, fmtgp_result
         ProfGuard pg_(M);
         if (!M || !h || !out) invalid("nll: null argument");
         CK(cudaSetDevice(M->dev));
-        nll_batch_impl(M, 1, h, want_grad != 0, out, true);
+        M->fit_lazy = false;
+        nll_batch_impl(M, 1, h, want_grad != 0, out, /*keep_chat=*/!M->equal);
         if (out->status != FMTGP_OK) {
             if (out->status == FMTGP_ERR_SCHUR) throw Fail{FMTGP_ERR_SCHUR, "noise escalation schedule exhausted"};
             throw Fail{out->status, "invert_and_logdet: non-real Schur complement"};
         }
         remember_hyper(M, h);
+        if (M->equal) {
+            M->fit_h.store(h, M->d, M->T);
+            M->fit_xi_scale = out->xi_scale;
+            M->fit_lazy = true;
+        }
         M->have_fit = true;
         M->have_c = false;
         M->have_spec = true;
@@ -1374,6 +1416,7 @@ int fmtgp_nll_batch(fmtgp_model_t M, int ncand, const fmtgp_hyper* h, int want_g
         ProfGuard pg_(M);
         if (!M || !h || !out || ncand < 1) invalid("nll_batch: bad argument");
         CK(cudaSetDevice(M->dev));
+        M->fit_lazy = false;
         nll_batch_impl(M, ncand, h, want_grad != 0, out, false);
         M->have_fit = false;
         M->have_spec = false;
@@ -1451,6 +1494,7 @@ int fmtgp_posterior_var(fmtgp_model_t M, int task, const double* X, int64_t coun
         ProfGuard pg_(M);
         if (!M || (!X && count > 0) || (!out && count > 0)) invalid("posterior_var: null argument");
         if (!M->have_fit) invalid("posterior_var: model not refreshed");
+        ensure_fit_state(M);
         if (task < 0 || task >= M->T) invalid("posterior_var: task out of range");
         CK(cudaSetDevice(M->dev));
         if (!M->uneq) throw Fail{FMTGP_ERR_UNSUPPORTED, "posterior_var: needs the fold plan"};
@@ -1464,6 +1508,7 @@ int fmtgp_cubature(fmtgp_model_t M, double* mu, double* Sigma) {
         ProfGuard pg_(M);
         if (!M || !mu || !Sigma) invalid("cubature: null argument");
         if (!M->have_fit) invalid("cubature: model not refreshed");
+        ensure_fit_state(M);
         CK(cudaSetDevice(M->dev));
         const int T = M->T;
         std::vector<double> Pi(size_t(T) * T), etc(T, 0.0);

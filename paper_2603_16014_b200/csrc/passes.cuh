@@ -311,33 +311,41 @@ __device__ __forceinline__ int ldl_solve(const typename Sc<CX>::T* A, const type
     using S = Sc<CX>;
     using V = typename S::T;
     V L[T][T];
-    double dinv[T];
+    double dinv[T], piv[T];
     int status = 0;
     // pair index of (a,b), a <= b, row by row (fast_gram.cpp:35-40)
     auto pidx = [](int a, int b) { return a * T - a * (a - 1) / 2 + (b - a); };
-    logdet = 0.0;
+    // log det = log(prod of pivots): one log per frequency; the running product is kept
+    // normalised (frexp) so no pivot range can overflow it
+    double pm = 1.0;
+    int pe = 0;
 #pragma unroll
     for (int s = 0; s < T; ++s) {
         double dd = S::re(A[pidx(s, s)]);
-        // non-real check is global per stage (|Im S| vs 1e-8 max(1, max Re S)), fast_gram.cpp:167-172
-        imx[s] = fmax(imx[s], fabs(S::im(A[pidx(s, s)])));
+        // non-real check is global per stage (|Im S| vs 1e-8 max(1, max Re S)), fast_gram.cpp:167-172;
+        // real (digital) spectra have no imaginary part to test
+        if constexpr (CX) imx[s] = fmax(imx[s], fabs(S::im(A[pidx(s, s)])));
 #pragma unroll
-        for (int k = 0; k < s; ++k) dd -= S::abs2(L[s][k]) / dinv[k];
+        for (int k = 0; k < s; ++k) dd -= S::abs2(L[s][k]) * piv[k];
         if (!(dd > 0.0)) {
             status = 1;
             dd = 1.0;
         }
-        rex[s] = fmax(rex[s], dd);
+        if constexpr (CX) rex[s] = fmax(rex[s], dd);
+        piv[s] = dd;
         dinv[s] = 1.0 / dd;
-        logdet += log(dd);
+        int e;
+        pm = frexp(pm * dd, &e);
+        pe += e;
 #pragma unroll
         for (int i = s + 1; i < T; ++i) {
             V acc = S::conj(A[pidx(s, i)]);
 #pragma unroll
-            for (int k = 0; k < s; ++k) acc = S::sub(acc, S::scale(S::mulc(L[i][k], L[s][k]), 1.0 / dinv[k]));
+            for (int k = 0; k < s; ++k) acc = S::sub(acc, S::scale(S::mulc(L[i][k], L[s][k]), piv[k]));
             L[i][s] = S::scale(acc, dinv[s]);
         }
     }
+    logdet = log(pm) + double(pe) * 0.69314718055994530942;
     // z = L^-1 r, quad = sum |z|^2 / d
     V z[T];
     quad = 0.0;
