@@ -1,6 +1,8 @@
 // Shared device helpers for the fastmtgp-b200 kernels (sm_100a, fp64).
 #pragma once
 
+#include <utility>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -63,6 +65,33 @@ __device__ __forceinline__ void cp_async_el(T* smem, const T* gmem) {
     else cp_async8(smem, gmem);
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// A kernel launched with launch_pdl() may start while its predecessor in the stream is still
+// running; it runs its independent prologue (prefetches) and then pdl_wait()s, which returns once
+// the predecessor grid has completed and its writes are visible.  pdl_trigger() lets the
+// dependent grid be scheduled early (safe anywhere: the dependent still pdl_wait()s).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
+// a failing launch also sets the runtime's last error, which the caller's cudaGetLastError() check reads
+#define CK_LAUNCH(x) ((void)(x))
+
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ---------------------------------------------------------------- reductions
 template <int NT>

@@ -58,6 +58,28 @@ void dig_kappa_table(const Spatial& sp, const PointGen& pg, const uint64_t* d_of
     FM_D_DISPATCH(sp.d, k_kappa_table<D><<<dim3(unsigned(b), nofs), GEN_NT_DIG, 0, s>>>(g, d_ofs, n, kap))
 }
 
+// Design-time kappa tile (D rows of the CTA's C columns x N1) -> smem, asynchronously: 16-byte
+// copies when a tile row holds >= 2 adjacent columns (kbuf must then be 16-byte aligned).
+template <int NT, int D>
+__device__ __forceinline__ void load_kappa_tile(double* kbuf, const double* kp, long long n, int l1, int l2, int lc,
+                                                long long c0) {
+    const int lt = l1 + lc;
+    if (lc >= 1) {
+        const int hl = lt - 1;
+        for (int idx = threadIdx.x; idx < (D << hl); idx += NT) {
+            const int j = idx >> hl, e = (idx & ((1 << hl) - 1)) << 1;
+            const long long i = ((long long)(e >> lc) << l2) + c0 + (e & ((1 << lc) - 1));
+            cp_async16(kbuf + (j << lt) + e, kp + size_t(j) * n + i);
+        }
+    } else {
+        for (int idx = threadIdx.x; idx < (D << lt); idx += NT) {
+            const int j = idx >> lt, e = idx & ((1 << lt) - 1);
+            cp_async8(kbuf + (j << lt) + e, kp + size_t(j) * n + ((long long)e << l2) + c0);
+        }
+    }
+}
+__host__ __device__ constexpr int kbuf_offset(int C, int ld) { return (C * ld + 1) & ~1; }
+
 // ------------------------------------------------------------------ K1: generator x column FWHT
 template <int NT, int D>
 __global__ void __launch_bounds__(NT, 3) k_dig_col_fwd(DigArgs a, int l1, int l2, int lc) {
@@ -85,12 +107,8 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_fwd(DigArgs a, int l1, int l2
     const int tile = C << l1;
     if (kp) {
         // design-time kappa tile -> smem with cp.async (no register staging)
-        double* kbuf = sm + C * ld;
-        for (int idx = threadIdx.x; idx < tile * D; idx += NT) {
-            const int j = idx / tile, e = idx - j * tile;
-            const long long i = ((long long)(e >> lc) << l2) + c0 + (e & (C - 1));
-            cp_async8(kbuf + idx, kp + size_t(j) * n + i);
-        }
+        double* kbuf = sm + kbuf_offset(C, ld);
+        load_kappa_tile<NT, D>(kbuf, kp, n, l1, l2, lc, c0);
         cp_async_wait_all();
         __syncthreads();
         for (int e = threadIdx.x; e < tile; e += NT) {
@@ -108,6 +126,7 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_fwd(DigArgs a, int l1, int l2
             sm[cc * ld + sidx<true>(j1)] = product_kernel_d<D, false>(kappa, eta, gam, nullptr);
         }
     }
+    pdl_trigger();
     // zero the per-fit flags once per fit (K2 / K3 run after this kernel)
     if (blockIdx.x == 0 && blockIdx.y == 0) {
         for (int t = threadIdx.x; t < a.nc; t += NT) a.bad[t] = 0x7f7f7f7f;
@@ -132,16 +151,28 @@ __global__ void __launch_bounds__(NT) k_dig_mid(DigArgs a, int l2) {
     const int row = blockIdx.x, c = blockIdx.y, N2 = 1 << l2, lds = padded_len(N2), V = a.V;
     const long long n = a.n, base = (long long)row << l2;
     double* Yc = a.Y + size_t(c) * V * n;
-    for (int e = threadIdx.x; e < (V << l2); e += NT) {
-        const int o = e >> l2, k2 = e & (N2 - 1);
-        cp_async8(&sm[o * lds + sidx<true>(k2)], &Yc[size_t(o) * n + base + k2]);
-    }
+    // prologue independent of K1 (overlaps its tail under programmatic dependent launch)
     if (threadIdx.x < P) {
         const int q = threadIdx.x;
         s_coef[q] = __ldg(a.coef + size_t(c) * P + q);
         s_xi[q] = __ldg(a.xi + size_t(c) * P + q);
         s_wR[q] = (a.pair_a[q] == a.pair_b[q] ? 1.0 : 2.0) * __ldg(a.Rpair + size_t(c) * P + q);
         s_cls[q] = a.pair_ofs[q];
+    }
+    constexpr int KPT = T <= 4 ? 2 : 1;  // frequencies per thread held in the yhat prefetch
+    double rpre[KPT][T];
+#pragma unroll
+    for (int u = 0; u < KPT; ++u) {
+        const int k2 = threadIdx.x + u * NT;
+#pragma unroll
+        for (int t = 0; t < T; ++t)
+            rpre[u][t] = (k2 < N2 && base + k2 != 0) ? __ldg(a.yhat + size_t(t) * n + base + k2) : 0.0;
+    }
+    pdl_wait();
+    pdl_trigger();
+    for (int e = threadIdx.x; e < (V << l2); e += NT) {
+        const int o = e >> l2, k2 = e & (N2 - 1);
+        cp_async8(&sm[o * lds + sidx<true>(k2)], &Yc[size_t(o) * n + base + k2]);
     }
     cp_async_wait_all();
     __syncthreads();
@@ -152,7 +183,8 @@ __global__ void __launch_bounds__(NT) k_dig_mid(DigArgs a, int l2) {
 #pragma unroll
     for (int t = 0; t < T; ++t) imx[t] = rex[t] = 0.0;
     int first_bad = 0x7f7f7f7f;
-    for (int k2 = threadIdx.x; k2 < N2; k2 += NT) {
+#pragma unroll 1
+    for (int u = 0, k2 = threadIdx.x; k2 < N2; ++u, k2 += NT) {
         const long long k = base + k2;
         const int si = sidx<true>(k2);
         double A[P], r[T], ch[T], Ai[P];
@@ -162,7 +194,13 @@ __global__ void __launch_bounds__(NT) k_dig_mid(DigArgs a, int l2) {
             if (a.lam_out) a.lam_out[(size_t(c) * P + q) * n + k] = A[q];
         }
 #pragma unroll
-        for (int t = 0; t < T; ++t) r[t] = k == 0 ? 0.0 : __ldg(a.yhat + size_t(t) * n + k);
+        for (int t = 0; t < T; ++t) {
+            double rv = 0.0;
+#pragma unroll
+            for (int w = 0; w < KPT; ++w)
+                if (u == w) rv = rpre[w][t];
+            r[t] = u < KPT ? rv : (k == 0 ? 0.0 : __ldg(a.yhat + size_t(t) * n + k));
+        }
         double ld, qd;
         const int st = ldl_solve<T, false>(A, r, a.want_grad != 0, ld, qd, ch, Ai, imx, rex);
         if (st == 1 && int(k) < first_bad) first_bad = int(k);
@@ -217,18 +255,14 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
     const long long c0 = (long long)blockIdx.x << lc, n = a.n;
     const double* x = a.Y + size_t(v) * n;
     const int tile = C << l1;
-    double* kbuf = sm + C * ld;
-    if (a.kap) {  // kappa tile streams into smem while the column is loaded and transformed
-        const double* kp0 = a.kap + size_t(o) * D * n;
-        for (int idx = threadIdx.x; idx < tile * D; idx += NT) {
-            const int j = idx / tile, e = idx - j * tile;
-            const long long i = ((long long)(e >> lc) << l2) + c0 + (e & (C - 1));
-            cp_async8(kbuf + idx, kp0 + size_t(j) * n + i);
-        }
-    }
+    double* kbuf = sm + kbuf_offset(C, ld);
+    // the kappa tile does not depend on K2: it streams in while K2 finishes (PDL) and while the
+    // column is loaded and transformed
+    if (a.kap) load_kappa_tile<NT, D>(kbuf, a.kap + size_t(o) * D * n, n, l1, l2, lc, c0);
+    pdl_wait();
     for (int e = threadIdx.x; e < tile; e += NT) {
         const int k1 = e >> lc, cc = e & (C - 1);
-        sm[cc * ld + sidx<true>(k1)] = x[((long long)k1 << l2) + c0 + cc];
+        cp_async8(&sm[cc * ld + sidx<true>(k1)], &x[((long long)k1 << l2) + c0 + cc]);
     }
     double eta[D];
 #pragma unroll
@@ -263,6 +297,7 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
             acc[D] = fma(W, q, acc[D]);
         }
     } else {
+        cp_async_wait_all();
         __syncthreads();
         smem_wht<NT, true>(sm, l1, C, ld);
         for (int e = threadIdx.x; e < tile; e += NT) {
@@ -285,46 +320,33 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
 #pragma unroll
         for (int j = 0; j <= D; ++j) out[j == D ? MAXD : j] = acc[j];
     }
-    // last-CTA reduction (threadFenceReduction pattern, one ticket per candidate over all of its
-    // V * nblk CTAs; fixed summation order => deterministic)
-    if (threadIdx.x == 0) __threadfence();  // thread 0 wrote this CTA's partial
+    // last-CTA reduction: one acq_rel ticket per candidate over its V * nblk CTAs (the release
+    // publishes this CTA's partial, the last arrival's acquire sees all of them); fixed
+    // summation order => deterministic
     __syncthreads();
     if (threadIdx.x == 0) {
-        const unsigned ticket = atomicAdd(a.counter + c, 1u);
+        const unsigned ticket = atom_add_acq_rel_gpu(a.counter + c, 1u);
         s_last = ticket == unsigned(a.V * nblk) - 1;
         if (s_last) a.counter[c] = 0;  // self-reset for the next replay
     }
     __syncthreads();
     if (!s_last) return;
-    __threadfence();
-    __shared__ double s_vec[MAXP * (MAXD + 1)];
-    {
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        const double* pc = a.part_dot + size_t(c) * a.V * nblk * (MAXD + 1);
-        for (int t = warp; t < a.V * (D + 1); t += NT / 32) {
-            const int oo = t / (D + 1), j = t - oo * (D + 1), comp = j == D ? MAXD : j;
-            double s = 0.0;
-            for (int b = lane; b < nblk; b += 32) s += __ldcg(pc + (size_t(oo) * nblk + b) * (MAXD + 1) + comp);
-#pragma unroll
-            for (int o2 = 16; o2 > 0; o2 >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o2);
-            if (lane == 0) s_vec[oo * (MAXD + 1) + comp] = s;
-        }
-    }
-    __syncthreads();
-    ClassFinal fa{};
-    fa.T = a.T;
-    fa.P = a.P;
-    fa.V = a.V;
-    fa.d = D;
-    fa.nrows = nrows;
-    fa.part_mid = a.part_mid;
-    fa.vec_sum = s_vec;
-    fa.Rpair = a.Rpair;
-    fa.gamma = a.gamma;
-    fa.pair_a = a.pair_a;
-    fa.pair_b = a.pair_b;
-    fa.out = a.out;
-    finalize_classes<NT>(fa, c);
+    ClassTail t{};
+    t.P = a.P;
+    t.V = a.V;
+    t.ncomp = D + 1;
+    t.d = D;
+    t.nrows = nrows;
+    t.nblk = nblk;
+    t.part_mid = a.part_mid + size_t(c) * nrows * (2 + a.P);
+    t.part_dot = a.part_dot + size_t(c) * a.V * nblk * (MAXD + 1);
+    t.pair_a = a.pair_a;
+    t.pair_b = a.pair_b;
+    t.Rpair = a.Rpair + size_t(c) * a.P;
+    t.gamma = __ldg(a.gamma + c);
+    t.out = a.out + size_t(c) * NOUT;
+    t.stage = sm;
+    class_tail<NT>(t);
 }
 
 // ------------------------------------------------------------------ launcher
@@ -340,14 +362,16 @@ static void mid_launch(const DigGeo& g, const DigArgs& a, size_t sm, cudaStream_
         auto k = k_dig_mid<NT, T>;
         set_smem_dig(k, sm);
         ProfScope ps("dig_mid", s);
-        k<<<grid, NT, sm, s>>>(a, g.l2);
+        CK_LAUNCH(launch_pdl(k, grid, dim3(NT), sm, s, true, a, g.l2));
     })
 }
 
 void dig_fit(const DigGeo& g, const DigArgs& a, cudaStream_t s) {
     const int C = 1 << g.lc;
-    const size_t sm_col = (size_t(C) * padded_len(1 << g.l1) + (a.kap ? size_t(a.d) << (g.l1 + g.lc) : 0)) *
-                          sizeof(double);
+    // K1/K3 dynamic smem: column tile (+ kappa tile); K3's last CTA reuses it to stage partials
+    const size_t tile_words = size_t(kbuf_offset(C, padded_len(1 << g.l1))) + (a.kap ? size_t(a.d) << (g.l1 + g.lc) : 0);
+    const size_t stage_words = ((size_t(1 << g.l1) * (2 + a.P) + 1) & ~size_t(1)) + size_t(a.V) * g.nblk_col * (a.d + 1);
+    const size_t sm_col = std::max(tile_words, stage_words) * sizeof(double);
     const dim3 gcol(g.nblk_col, a.V * a.nc);
     FM_D_DISPATCH(a.d, {
         FM_NT_DISPATCH(g.nt_col, {
@@ -375,7 +399,7 @@ void dig_fit(const DigGeo& g, const DigArgs& a, cudaStream_t s) {
             auto k3 = k_dig_col_inv<NT, D>;
             set_smem_dig(k3, sm_col);
             ProfScope ps("dig_col_inv", s);
-            k3<<<gcol, NT, sm_col, s>>>(a, g.l1, g.l2, g.lc, nrows);
+            CK_LAUNCH(launch_pdl(k3, gcol, dim3(NT), sm_col, s, true, a, g.l1, g.l2, g.lc, nrows));
         })
     })
 }

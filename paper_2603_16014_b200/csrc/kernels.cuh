@@ -195,15 +195,15 @@ __device__ void finalize_classes(const ClassFinal& a, int c) {
     const double* pm = a.part_mid + (size_t)c * a.nrows * S;
     double ld = 0.0, q = 0.0;
     for (int b = threadIdx.x; b < a.nrows; b += NT) {
-        ld += __ldcg(pm + (size_t)b * S + 0);
-        q += __ldcg(pm + (size_t)b * S + 1);
+        ld += pm[(size_t)b * S + 0];
+        q += pm[(size_t)b * S + 1];
     }
     ld = block_sum<NT>(ld, red);
     q = block_sum<NT>(q, red);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int p = warp; p < a.P; p += NT / 32) {  // fixed-order strided sums + warp tree (deterministic)
         double s = 0.0;
-        for (int b = lane; b < a.nrows; b += 32) s += __ldcg(pm + (size_t)b * S + 2 + p);
+        for (int b = lane; b < a.nrows; b += 32) s += pm[(size_t)b * S + 2 + p];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         if (lane == 0) sdr[p] = s;
@@ -239,6 +239,96 @@ __device__ void finalize_classes(const ClassFinal& a, int c) {
         }
         out[OUT_DGAMMA] = dgam / a.gamma[c];
         for (int j = 0; j < MAXD; ++j) out[OUT_DETA + j] = sdeta[j];
+    }
+}
+
+// Compact last-CTA tail of a class-layout fit (K3 of the fused digital path): every partial is
+// staged into shared memory with all copies in flight, every sum is one warp's fixed-order
+// strided loop + shuffle tree, and the serial assembly touches shared memory only.  Kept small
+// and out of line: after an L2 flush its instructions come from DRAM.
+struct ClassTail {
+    int P, V, ncomp, d, nrows, nblk;
+    const double* part_mid;  // [nrows][2 + P] of this candidate
+    const double* part_dot;  // [V * nblk][MAXD + 1] of this candidate (components j < d, and MAXD)
+    const int* pair_a;
+    const int* pair_b;
+    const double* Rpair;     // [P] of this candidate
+    double gamma;
+    double* out;             // [NOUT] of this candidate
+    double* stage;           // shared, >= ((nrows (2+P) + 1) & ~1) + V nblk ncomp doubles
+};
+
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
+template <int NT>
+__device__ __noinline__ void class_tail(const ClassTail& t) {
+    __shared__ double res[2 + MAXP + MAXP * (MAXD + 1)];
+    __shared__ double sR[MAXP];
+    __shared__ int spa[MAXP], spb[MAXP];
+    const int S = 2 + t.P, Q = S + t.V * t.ncomp;
+    double* st_mid = t.stage;
+    double* st_dot = t.stage + ((t.nrows * S + 1) & ~1);
+#pragma unroll 1
+    for (int i = threadIdx.x; i < t.nrows * S; i += NT) cp_async8(st_mid + i, t.part_mid + i);
+#pragma unroll 1
+    for (int i = threadIdx.x; i < t.V * t.nblk * t.ncomp; i += NT) {
+        const int r = i / t.ncomp, j = i - r * t.ncomp;
+        cp_async8(st_dot + i, t.part_dot + size_t(r) * (MAXD + 1) + (j == t.ncomp - 1 ? MAXD : j));
+    }
+    if (threadIdx.x < t.P) {
+        spa[threadIdx.x] = t.pair_a[threadIdx.x];
+        spb[threadIdx.x] = t.pair_b[threadIdx.x];
+        sR[threadIdx.x] = t.Rpair[threadIdx.x];
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll 1
+    for (int q = warp; q < Q; q += NT / 32) {
+        const double* base;
+        int stride, count;
+        if (q < S) {
+            base = st_mid + q, stride = S, count = t.nrows;
+        } else {
+            const int o = (q - S) / t.ncomp, j = (q - S) - o * t.ncomp;
+            base = st_dot + size_t(o) * t.nblk * t.ncomp + j, stride = t.ncomp, count = t.nblk;
+        }
+        double s = 0.0;
+#pragma unroll 1
+        for (int b = lane; b < count; b += 32) s += base[b * stride];
+#pragma unroll
+        for (int o2 = 16; o2 > 0; o2 >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o2);
+        if (lane == 0) res[q] = s;
+    }
+    __syncthreads();
+    double* out = t.out;
+#pragma unroll 1
+    for (int x = threadIdx.x; x < NOUT; x += NT) {
+        double v = 0.0;
+        if (x == OUT_LOGDET) v = res[0];
+        else if (x == OUT_QUAD) v = res[1];
+        else if (x == OUT_NLL) v = res[0] + res[1];  // rT c + logdet (gp_core.cpp:207-211)
+        else if (x >= OUT_DETA && x < OUT_DETA + MAXD) {
+            const int j = x - OUT_DETA;
+            if (j < t.d)
+#pragma unroll 1
+                for (int o = 0; o < t.V; ++o) v += res[S + o * t.ncomp + j];
+        } else if (x >= OUT_DR && x < OUT_DR + MAXT * MAXT) {
+            const int a = (x - OUT_DR) / MAXT, b = (x - OUT_DR) % MAXT;
+#pragma unroll 1
+            for (int p = 0; p < t.P; ++p)
+                if ((spa[p] == a && spb[p] == b) || (spa[p] == b && spb[p] == a))
+                    v = res[2 + p];  // diagonal dNLL/dR_aa; off-diagonal G_ab = G_ba = (2 res) / 2
+        } else if (x == OUT_DGAMMA) {
+#pragma unroll 1
+            for (int p = 0; p < t.P; ++p) v += sR[p] * (spa[p] == spb[p] ? 1.0 : 2.0) * res[2 + p];
+            v /= t.gamma;
+        }
+        out[x] = v;
     }
 }
 
