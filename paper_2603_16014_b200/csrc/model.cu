@@ -246,6 +246,12 @@ struct fmtgp_model {
     size_t stage_len = 0;
     double* h_out = nullptr;
     int* h_bad = nullptr;
+    // equal n: tau_l = yhat_l(0)/sqrt(n) travels with the next fit's result block (no sync in set_y)
+    double* d_tau_raw = nullptr;
+    double* h_tau_raw = nullptr;
+    bool tau_pending = false;
+    cudaEvent_t ev_h2d = nullptr;
+
     // state of the last spectrum / fit (candidate 0)
     bool have_spec = false, have_inv = false, have_fit = false;
     // fmtgp_nll does not write the fit's spectrum / chat (hot loop); they are re-derived from the
@@ -462,19 +468,35 @@ void compute_yhat_tau(fmtgp_model* M) {
     forward_vector(M, M->d_y, M->d_yhat);
     // tau: equal n -> tau_l = yhat_l(0) / sqrt(n) (the sample mean, gp_core.cpp:67-88 with
     // V̄ 1 = sqrt(n) e_0); unequal n -> class-0 normal equations at fit time.
-    std::vector<double> y0(M->T);
-    for (int t = 0; t < M->T; ++t) {
-        CK(cudaMemcpyAsync(&y0[t], static_cast<char*>(M->d_yhat) + M->toff_slots[t] * elem_size(M), sizeof(double),
-                           cudaMemcpyDeviceToHost, M->st));
+    if (M->equal) {
+        // yhat_l(0) (first double of each task block, uniform stride) -> tail of the result block,
+        // read back with the next fit's single D2H copy: no host round trip here
+        const size_t es = elem_size(M), pitch = size_t(M->T > 1 ? M->toff_slots[1] : 0) * es;
+        CK(cudaMemcpy2DAsync(M->d_tau_raw, sizeof(double), M->d_yhat, pitch ? pitch : sizeof(double), sizeof(double),
+                             M->T, cudaMemcpyDeviceToDevice, M->st));
+        M->tau_pending = true;
+    } else {
+        std::vector<double> y0(M->T);
+        for (int t = 0; t < M->T; ++t) {
+            CK(cudaMemcpyAsync(&y0[t], static_cast<char*>(M->d_yhat) + M->toff_slots[t] * elem_size(M),
+                               sizeof(double), cudaMemcpyDeviceToHost, M->st));
+        }
+        CK(cudaStreamSynchronize(M->st));
+        for (int t = 0; t < M->T; ++t) M->tau[t] = y0[t] / std::sqrt(double(M->n[t]));
     }
-    CK(cudaStreamSynchronize(M->st));
-    for (int t = 0; t < M->T; ++t) M->tau[t] = y0[t] / std::sqrt(double(M->n[t]));
     M->have_y = true;
+}
+
+void take_tau(fmtgp_model* M) {  // after a D2H of the result block
+    if (!M->tau_pending) return;
+    for (int t = 0; t < M->T; ++t) M->tau[t] = M->h_tau_raw[t] / std::sqrt(double(M->n[t]));
+    M->tau_pending = false;
 }
 
 void finish_results(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, bool grad, fmtgp_result* out,
                     const double* xi_scale, const int* esc) {
     const int T = M->T;
+    take_tau(M);
     for (int c = 0; c < nc; ++c) {
         const double* o = M->h_out + size_t(c) * NOUT;
         fmtgp_result& r = out[c];
@@ -989,9 +1011,12 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
         }
         M->d_psolve = dalloc<double>(size_t(max_cand) * std::max(M->nblk_solve, 1) * 3);
         // one result block [out | bad | imre] -> a single D2H copy per evaluation
-        M->res_len = size_t(max_cand) * (NOUT + 1 + 2 * MAXT);
+        M->res_len = size_t(max_cand) * (NOUT + 1 + 2 * MAXT) + MAXT;
         M->d_res = dalloc<double>(M->res_len);
         CK(cudaMallocHost(reinterpret_cast<void**>(&M->h_res), sizeof(double) * M->res_len));
+        M->d_tau_raw = M->d_res + size_t(max_cand) * (NOUT + 1 + 2 * MAXT);
+        M->h_tau_raw = M->h_res + size_t(max_cand) * (NOUT + 1 + 2 * MAXT);
+        CK(cudaEventCreateWithFlags(&M->ev_h2d, cudaEventDisableTiming));
         M->d_out = M->d_res;
         M->d_bad = reinterpret_cast<int*>(M->d_res + size_t(max_cand) * NOUT);
         M->d_imre = reinterpret_cast<unsigned long long*>(M->d_res + size_t(max_cand) * (NOUT + 1));
@@ -1101,6 +1126,7 @@ int fmtgp_model_destroy(fmtgp_model_t M) {
     F(M->d_pgrad);
     F(M->d_res);
     if (M->h_res) cudaFreeHost(M->h_res);
+    if (M->ev_h2d) cudaEventDestroy(M->ev_h2d);
     F(M->d_vecA);
     F(M->d_vecB);
     F(M->d_sA);
@@ -1120,8 +1146,12 @@ int fmtgp_model_set_y(fmtgp_model_t M, const double* y) {
         ProfGuard pg_(M);
         if (!M || !y) invalid("set_y: null argument");
         CK(cudaSetDevice(M->dev));
+        // (splitting this copy over several copy engines measured slower at these sizes)
         CK(cudaMemcpyAsync(M->d_y, y, sizeof(double) * M->N, cudaMemcpyHostToDevice, M->st));
+        CK(cudaEventRecord(M->ev_h2d, M->st));
         compute_yhat_tau(M);
+        // the caller may reuse y on return: wait for the copy only (the transform runs on)
+        CK(cudaEventSynchronize(M->ev_h2d));
         M->have_fit = false;
         M->fit_lazy = false;
     });

@@ -56,4 +56,36 @@ for name, fn in (("raw ctypes fmtgp_nll", lambda: lib.fmtgp_nll(h, C.byref(ch), 
     for _ in range(1000):
         fn()
     print(f"wall/step {name}: {(time.perf_counter() - t) * 1e3:.1f} us")
+
+# ---- end to end: pinned y -> set_y -> nll (as bench.py's e2e), split
+M = Model(inst.design)
+M.set_y(inst.y)
+stream = torch.cuda.ExternalStream(M.stream, device=torch.device("cuda", 0))
+y_pinned = torch.empty(inst.design.N, dtype=torch.float64).pin_memory().numpy()
+y_pinned[:] = inst.y
+for _ in range(5):
+    M.set_y(y_pinned)
+    M.nll(hp)
+for what in ("set_y", "set_y+nll"):
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(100)]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for k in range(100):
+        with torch.cuda.stream(stream):
+            flush.fill_(float(k))
+        ev[k][0].record(stream)
+        M.set_y(y_pinned)
+        if what != "set_y":
+            M.nll(hp)
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    print(f"e2e events/step {what}: {1e3 * sum(a.elapsed_time(b) for a, b in ev) / 100:.1f} us")
+t = time.perf_counter()
+for _ in range(200):
+    lib.fmtgp_model_set_y(M.h, y_pinned.ctypes.data_as(C.POINTER(C.c_double)))
+print(f"wall/step raw set_y pinned: {(time.perf_counter() - t) * 1e6 / 200:.1f} us")
+t = time.perf_counter()
+for _ in range(200):
+    lib.fmtgp_model_set_y(M.h, inst.y.ctypes.data_as(C.POINTER(C.c_double)))
+print(f"wall/step raw set_y pageable: {(time.perf_counter() - t) * 1e6 / 200:.1f} us")
 M.close()
