@@ -331,22 +331,39 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
     }
     __syncthreads();
     if (!s_last) return;
-    ClassTail t{};
+    // stage every partial into the (now free) dynamic smem with all copies in flight: the tail is
+    // one L2 round trip instead of a chain of dependent ones
+    const int S = 2 + a.P;
+    double* st_mid = sm;                                 // [nrows][2 + P]
+    double* st_dot = sm + ((nrows * S + 1) & ~1);        // [V][nblk][D]
+    {
+        const double* pm = a.part_mid + size_t(c) * nrows * S;
+#pragma unroll 1
+        for (int i = threadIdx.x; i < nrows * S; i += NT) cp_async8(st_mid + i, pm + i);
+        const double* pc = a.part_dot + size_t(c) * a.V * nblk * (MAXD + 1);
+#pragma unroll 1
+        for (int i = threadIdx.x; i < a.V * nblk * D; i += NT) {
+            const int r = i / D, j = i - r * D;
+            cp_async8(st_dot + i, pc + size_t(r) * (MAXD + 1) + j);
+        }
+        cp_async_wait_all();
+    }
+    __syncthreads();
+    ClassSums t{};
     t.P = a.P;
     t.V = a.V;
-    t.ncomp = D + 1;
     t.d = D;
     t.nrows = nrows;
     t.nblk = nblk;
-    t.part_mid = a.part_mid + size_t(c) * nrows * (2 + a.P);
-    t.part_dot = a.part_dot + size_t(c) * a.V * nblk * (MAXD + 1);
+    t.dstride = D;
+    t.mid = st_mid;
+    t.dot = st_dot;
     t.pair_a = a.pair_a;
     t.pair_b = a.pair_b;
     t.Rpair = a.Rpair + size_t(c) * a.P;
     t.gamma = __ldg(a.gamma + c);
     t.out = a.out + size_t(c) * NOUT;
-    t.stage = sm;
-    class_tail<NT>(t);
+    class_sums_out<NT>(t);
 }
 
 // ------------------------------------------------------------------ launcher
@@ -370,7 +387,7 @@ void dig_fit(const DigGeo& g, const DigArgs& a, cudaStream_t s) {
     const int C = 1 << g.lc;
     // K1/K3 dynamic smem: column tile (+ kappa tile); K3's last CTA reuses it to stage partials
     const size_t tile_words = size_t(kbuf_offset(C, padded_len(1 << g.l1))) + (a.kap ? size_t(a.d) << (g.l1 + g.lc) : 0);
-    const size_t stage_words = ((size_t(1 << g.l1) * (2 + a.P) + 1) & ~size_t(1)) + size_t(a.V) * g.nblk_col * (a.d + 1);
+    const size_t stage_words = ((size_t(1 << g.l1) * (2 + a.P) + 1) & ~size_t(1)) + size_t(a.V) * g.nblk_col * a.d;
     const size_t sm_col = std::max(tile_words, stage_words) * sizeof(double);
     const dim3 gcol(g.nblk_col, a.V * a.nc);
     FM_D_DISPATCH(a.d, {

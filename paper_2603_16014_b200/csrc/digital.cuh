@@ -7,7 +7,7 @@
 //                      T x T LDL^H solve (logdet, quad, M = Lam^-1 - chat chat^H) + dR partials
 //                      sum_k M_p qhat_o (Parseval) + Z_o = sum_{p in o} w_p R_p M_p + inverse row FWHT
 //   K3 k_dig_col_inv : inverse column FWHT -> H Z_o -> dot with dq_o/deta -> partials,
-//                      last CTA reduces everything into the result record (ClassFinal)
+//                      last CTA reduces everything into the result record (class_sums_out)
 //
 // n = N1 * N2 (natural index i = j1 * N2 + j2); FWHT over the two bit groups commutes, and the
 // spectrum index after both passes is natural, so K2 owns the frequencies {k1 * N2 + k2}: all
@@ -47,7 +47,7 @@ struct DigArgs {
     double* Y;                // [nc][V][n] intermediate (column pass out, row pass in/out)
     double* lam_out;          // [nc][P][n] spectrum (nullptr: skip)
     double* chat_out;         // [T][n] chat of candidate 0 (nullptr: skip)
-    double* part_mid;         // [nc][nrows][2 + P]  logdet, quad, sum_k M_p qhat_o (ClassFinal)
+    double* part_mid;         // [nc][nrows][2 + P]  logdet, quad, sum_k M_p qhat_o (class_sums_out)
     double* part_dot;         // [nc][V][nblk_col][MAXD+1]
     int* bad;                 // [nc] first failing slot, 0x7f7f7f7f none
     unsigned long long* imre; // [nc][MAXT][2]

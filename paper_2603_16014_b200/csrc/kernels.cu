@@ -863,10 +863,176 @@ __global__ void __launch_bounds__(256) k_solve_equal(SolveArgs a) {
     }
 }
 
+// Class-mode per-frequency solve (see SolveArgs): pairs sharing a shift offset share one raw
+// spectrum; dNLL/dR_p is accumulated here by Parseval, sum_j W_p(j) q_o(j) =
+// sum_k M_p(k) conj(qhat_o(k)) over all n frequencies (slot k >= 1 of the real FFT stands for k and
+// n - k: weight 2, Re; slot 0 packs frequency 0 and Nyquist), so only the V class adjoints go
+// through the inverse transform.
+template <int T, bool CX>
+__global__ void __launch_bounds__(256) k_solve_class(SolveArgs a) {
+    using S = Sc<CX>;
+    using Vt = typename S::T;
+    constexpr int P = T * (T + 1) / 2;
+    const int c = blockIdx.y;
+    const Vt* spec = static_cast<const Vt*>(a.lam) + c * a.cstride;
+    const Vt* yh = static_cast<const Vt*>(a.yhat);
+    Vt* Zo = a.M ? static_cast<Vt*>(a.M) + c * a.cstride : nullptr;
+    __shared__ double s_coef[P], s_xi[P], s_wR[P];
+    __shared__ int s_cls[P];
+    if (threadIdx.x < P) {
+        const int q = threadIdx.x;
+        s_coef[q] = a.coef[(size_t)c * P + q];
+        s_xi[q] = a.xi[(size_t)c * P + q];
+        s_wR[q] = (a.pair_a[q] == a.pair_b[q] ? 1.0 : 2.0) * a.Rpair[(size_t)c * P + q];
+        s_cls[q] = a.pair_cls[q];
+    }
+    __syncthreads();
+    double acc[2 + P];
+#pragma unroll
+    for (int q = 0; q < 2 + P; ++q) acc[q] = 0.0;
+    int first_bad = INT_MAX;
+    double imx[T], rex[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) imx[t] = rex[t] = 0.0;
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < a.nslots;
+         p += (long long)gridDim.x * blockDim.x) {
+        Vt H[P], A[P], r[T], ch[T], Ai[P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) H[q] = spec[s_cls[q] * a.nslots + p];  // shared classes hit L1
+#pragma unroll
+        for (int t = 0; t < T; ++t) r[t] = yh[t * a.nslots + p];
+        if constexpr (CX) {
+            if (p == 0) {
+                // packed slot 0: frequency 0 (.x) and Nyquist (.y), two real systems; tau zeroes
+                // the frequency-0 residual (gp_core.cpp:67-88)
+                double A0[P], AN[P], r0[T], rN[T], c0[T], cN[T], I0[P], IN[P], l0, lN, q0, qN;
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    A0[q] = fma(s_coef[q], H[q].x, s_xi[q]);
+                    AN[q] = fma(s_coef[q], H[q].y, s_xi[q]);
+                }
+#pragma unroll
+                for (int t = 0; t < T; ++t) r0[t] = 0.0, rN[t] = r[t].y;
+                const bool want = Zo != nullptr;
+                int st0 = ldl_solve<T, false>(A0, r0, want, l0, q0, c0, I0, imx, rex);
+                int stN = 0;
+                if (a.has_nyq) {
+                    stN = ldl_solve<T, false>(AN, rN, want, lN, qN, cN, IN, imx, rex);
+                } else {  // n == 1: no Nyquist frequency
+                    lN = qN = 0.0;
+#pragma unroll
+                    for (int t = 0; t < T; ++t) cN[t] = 0.0;
+#pragma unroll
+                    for (int q = 0; q < P; ++q) IN[q] = 0.0;
+                }
+                if (st0 == 1 || stN == 1) first_bad = 0;
+                acc[0] += l0 + lN;
+                acc[1] += q0 + qN;
+                if (Zo) {
+                    double2 M[P];
+                    int q = 0;
+#pragma unroll
+                    for (int x = 0; x < T; ++x)
+#pragma unroll
+                        for (int y = x; y < T; ++y, ++q) M[q] = make_double2(I0[q] - c0[x] * c0[y], IN[q] - cN[x] * cN[y]);
+#pragma unroll
+                    for (int q2 = 0; q2 < P; ++q2) acc[2 + q2] += M[q2].x * H[q2].x + M[q2].y * H[q2].y;
+#pragma unroll
+                    for (int o = 0; o < P; ++o) {
+                        if (o >= a.V) break;
+                        double2 z = make_double2(0.0, 0.0);
+#pragma unroll
+                        for (int q2 = 0; q2 < P; ++q2)
+                            if (s_cls[q2] == o) z = make_double2(fma(s_wR[q2], M[q2].x, z.x), fma(s_wR[q2], M[q2].y, z.y));
+                        Zo[o * a.nslots] = z;
+                    }
+                }
+                if (a.chat) {
+                    Vt* Co = static_cast<Vt*>(a.chat) + c * (long long)T * a.nslots;
+#pragma unroll
+                    for (int t = 0; t < T; ++t) Co[t * a.nslots] = make_double2(c0[t], cN[t]);
+                }
+                continue;
+            }
+        } else {
+            if (p == 0) {
+#pragma unroll
+                for (int t = 0; t < T; ++t) r[t] = 0.0;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            if constexpr (CX) A[q] = make_double2(fma(s_coef[q], H[q].x, s_xi[q]), s_coef[q] * H[q].y);
+            else A[q] = fma(s_coef[q], H[q], s_xi[q]);
+        }
+        double ld, qd;
+        const int st = ldl_solve<T, CX>(A, r, Zo != nullptr, ld, qd, ch, Ai, imx, rex);
+        if (st == 1 && p < first_bad) first_bad = int(p);
+        const double w = CX ? 2.0 : 1.0;  // lattice slot k >= 1 stands for k and n - k
+        acc[0] += w * ld;
+        acc[1] += w * qd;
+        if (Zo) {
+            Vt M[P];
+            int q = 0;
+#pragma unroll
+            for (int x = 0; x < T; ++x)
+#pragma unroll
+                for (int y = x; y < T; ++y, ++q) M[q] = S::sub(Ai[q], S::mulc(ch[x], ch[y]));
+#pragma unroll
+            for (int q2 = 0; q2 < P; ++q2) {
+                if constexpr (CX) acc[2 + q2] += w * (M[q2].x * H[q2].x + M[q2].y * H[q2].y);  // Re(M conj H)
+                else acc[2 + q2] += M[q2] * H[q2];
+            }
+#pragma unroll
+            for (int o = 0; o < P; ++o) {
+                if (o >= a.V) break;
+                Vt z = S::zero();
+#pragma unroll
+                for (int q2 = 0; q2 < P; ++q2)
+                    if (s_cls[q2] == o) z = S::add(z, S::scale(M[q2], s_wR[q2]));
+                Zo[o * a.nslots + p] = z;
+            }
+        }
+        if (a.chat) {
+            Vt* Co = static_cast<Vt*>(a.chat) + c * (long long)T * a.nslots;
+#pragma unroll
+            for (int t = 0; t < T; ++t) Co[t * a.nslots + p] = ch[t];
+        }
+    }
+    __shared__ double redv[8 * (2 + P)];
+    block_sum_vec<256, 2 + P>(acc, redv);
+    if (threadIdx.x == 0) {
+        double* pp = a.partial + ((size_t)c * a.nblk + blockIdx.x) * (2 + P);
+#pragma unroll
+        for (int q = 0; q < 2 + P; ++q) pp[q] = acc[q];
+    }
+    if (first_bad != INT_MAX) atomicMin(a.bad + c, first_bad);
+    if constexpr (CX) {
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+            double vi = imx[t], vr = rex[t];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                vi = fmax(vi, __shfl_xor_sync(0xffffffffu, vi, o));
+                vr = fmax(vr, __shfl_xor_sync(0xffffffffu, vr, o));
+            }
+            if ((threadIdx.x & 31) == 0) {
+                atomicMax(a.imre + ((size_t)c * MAXT + t) * 2 + 0, (unsigned long long)__double_as_longlong(vi));
+                atomicMax(a.imre + ((size_t)c * MAXT + t) * 2 + 1, (unsigned long long)__double_as_longlong(vr));
+            }
+        }
+    }
+}
+
 template <int T>
 static void solve_t(const SolveArgs& a, int ncand, cudaStream_t s) {
     dim3 grid(a.nblk, ncand);
     ProfScope ps("solve_equal", s);
+    if (a.classes) {
+        if (a.lattice) k_solve_class<T, true><<<grid, 256, 0, s>>>(a);
+        else k_solve_class<T, false><<<grid, 256, 0, s>>>(a);
+        return;
+    }
     if (a.lattice) k_solve_equal<T, true><<<grid, 256, 0, s>>>(a);
     else k_solve_equal<T, false><<<grid, 256, 0, s>>>(a);
 }
@@ -892,6 +1058,41 @@ __global__ void __launch_bounds__(256) k_finalize(FinalArgs a) { finalize_candid
 void finalize(const FinalArgs& a, cudaStream_t s) {
     ProfScope ps("finalize", s);
     k_finalize<<<a.ncand, 256, 0, s>>>(a);
+}
+
+__global__ void __launch_bounds__(256) k_finalize_classes(ClassFinalArgs a) {
+    const int c = blockIdx.x;
+    if (!a.grad_partial) {  // no gradient: logdet / quad only
+        FinalArgs f{};
+        f.P = a.P;
+        f.d = a.d;
+        f.nblk_solve = a.nblk_solve;
+        f.solve_partial = a.solve_partial;
+        f.solve_stride = 2 + a.P;
+        f.out = a.out;
+        finalize_candidate<256>(f, c);
+        return;
+    }
+    ClassSums t{};
+    t.P = a.P;
+    t.V = a.V;
+    t.d = a.d;
+    t.nrows = a.nblk_solve;
+    t.nblk = a.nblk_grad;
+    t.dstride = MAXD + 1;
+    t.mid = a.solve_partial + (size_t)c * a.nblk_solve * (2 + a.P);
+    t.dot = a.grad_partial + (size_t)c * a.V * a.nblk_grad * (MAXD + 1);
+    t.pair_a = a.pair_a;
+    t.pair_b = a.pair_b;
+    t.Rpair = a.Rpair + (size_t)c * a.P;
+    t.gamma = a.gamma[c];
+    t.out = a.out + (size_t)c * NOUT;
+    class_sums_out<256>(t);
+}
+
+void finalize_classes(const ClassFinalArgs& a, int ncand, cudaStream_t s) {
+    ProfScope ps("finalize", s);
+    k_finalize_classes<<<ncand, 256, 0, s>>>(a);
 }
 
 // ============================================================================ per-slot Hermitian apply

@@ -91,6 +91,16 @@ struct SolveArgs {
     int* bad;               // [ncand] first failing slot (0x7f7f7f7f if none)
     unsigned long long* imre;  // [ncand][MAXT][2] per-stage max |Im Lam_ss|, max pivot (double bits)
     int nblk;
+    // class mode (nll path): lam holds the raw spectra of the V offset classes [ncand][V][nslots];
+    // lambda_p = coef_p * lam[cls_p] + xi_p is formed in registers, M receives the class adjoints
+    // Z_o = sum_{p in o} w_p R_p M_p, partial records are [2 + P] (logdet, quad, sum_k M_p qhat)
+    int classes = 0, V = 0;
+    const int* pair_cls = nullptr;  // [P]
+    const double* coef = nullptr;   // [ncand][P]
+    const double* xi = nullptr;     // [ncand][P]
+    const double* Rpair = nullptr;  // [ncand][P]
+    const int* pair_a = nullptr;
+    const int* pair_b = nullptr;
 };
 void solve_equal(const SolveArgs& a, int ncand, cudaStream_t s);
 
@@ -174,138 +184,62 @@ __device__ void finalize_candidate(const FinalArgs& a, int c) {
 //   dNLL/dR_p = w_p <W_p, q_o> = w_p sum_k M_p(k) qhat_o(k)        (Parseval, per-frequency partials)
 //   dNLL/deta = sum_o <Z_o, dq_o/deta>,  Z_o = H^-1 (sum_{p in o} w_p R_p M_p)   (one inverse per class)
 //   dNLL/dgamma = sum_p R_p dNLL/dR_p / gamma                          (q is linear in gamma)
-struct ClassFinal {
-    int T, P, V, d, nrows;
-    const double* part_mid;  // [ncand][nrows][2 + P]  logdet, quad, sum_k M_p qhat
-    const double* vec_sum;   // [V][MAXD + 1] of candidate c (global or shared)  <Z_o, dq_o/deta_j>
-    const double* Rpair;     // [ncand][P]
-    const double* gamma;     // [ncand]
+// Class-layout result assembly (per candidate, one CTA).  Inputs: per-block solve partials
+// `mid` [nrows][2 + P] (logdet, quad, Parseval dR sums) and per-block class gradient partials
+// `dot` [V][nblk][dstride] (component j < d = <Z_o, dq_o/deta_j>).  Every sum is one warp's
+// fixed-order strided loop (four independent accumulators) + shuffle tree: deterministic.
+// Kept out of line and small: in the digital path it is the last CTA's tail, whose
+// instructions come from DRAM after an L2 flush.
+struct ClassSums {
+    int P, V, d, nrows, nblk, dstride;
+    const double* mid;
+    const double* dot;
     const int* pair_a;
     const int* pair_b;
-    double* out;             // [ncand][NOUT]
-};
-
-template <int NT>
-__device__ void finalize_classes(const ClassFinal& a, int c) {
-    double* out = a.out + (size_t)c * NOUT;
-    __shared__ double red[32];
-    __shared__ double sdr[MAXP], sR[MAXP], sdeta[MAXD];
-    __shared__ int spa[MAXP], spb[MAXP];
-    const int S = 2 + a.P;
-    const double* pm = a.part_mid + (size_t)c * a.nrows * S;
-    double ld = 0.0, q = 0.0;
-    for (int b = threadIdx.x; b < a.nrows; b += NT) {
-        ld += pm[(size_t)b * S + 0];
-        q += pm[(size_t)b * S + 1];
-    }
-    ld = block_sum<NT>(ld, red);
-    q = block_sum<NT>(q, red);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int p = warp; p < a.P; p += NT / 32) {  // fixed-order strided sums + warp tree (deterministic)
-        double s = 0.0;
-        for (int b = lane; b < a.nrows; b += 32) s += pm[(size_t)b * S + 2 + p];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) sdr[p] = s;
-    }
-    // everything thread 0 needs is staged in parallel (no serial L2 round trips in the tail)
-    for (int p = threadIdx.x; p < a.P; p += NT) {
-        spa[p] = a.pair_a[p];
-        spb[p] = a.pair_b[p];
-        sR[p] = a.Rpair[(size_t)c * a.P + p];
-    }
-    for (int j = threadIdx.x; j < MAXD; j += NT) {
-        double s = 0.0;
-        if (j < a.d)
-            for (int o = 0; o < a.V; ++o) s += a.vec_sum[(size_t)o * (MAXD + 1) + j];
-        sdeta[j] = s;
-    }
-    for (int x = threadIdx.x; x < MAXT * MAXT; x += NT) out[OUT_DR + x] = 0.0;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        out[OUT_LOGDET] = ld;
-        out[OUT_QUAD] = q;
-        out[OUT_NLL] = q + ld;  // rT c + logdet (gp_core.cpp:207-211)
-        double dgam = 0.0;
-        for (int p = 0; p < a.P; ++p) {
-            const int pa = spa[p], pb = spb[p];
-            const double dRp = (pa == pb ? 1.0 : 2.0) * sdr[p];
-            dgam += sR[p] * dRp;
-            if (pa == pb) out[OUT_DR + pa * MAXT + pb] = dRp;
-            else {
-                out[OUT_DR + pa * MAXT + pb] = 0.5 * dRp;
-                out[OUT_DR + pb * MAXT + pa] = 0.5 * dRp;
-            }
-        }
-        out[OUT_DGAMMA] = dgam / a.gamma[c];
-        for (int j = 0; j < MAXD; ++j) out[OUT_DETA + j] = sdeta[j];
-    }
-}
-
-// Compact last-CTA tail of a class-layout fit (K3 of the fused digital path): every partial is
-// staged into shared memory with all copies in flight, every sum is one warp's fixed-order
-// strided loop + shuffle tree, and the serial assembly touches shared memory only.  Kept small
-// and out of line: after an L2 flush its instructions come from DRAM.
-struct ClassTail {
-    int P, V, ncomp, d, nrows, nblk;
-    const double* part_mid;  // [nrows][2 + P] of this candidate
-    const double* part_dot;  // [V * nblk][MAXD + 1] of this candidate (components j < d, and MAXD)
-    const int* pair_a;
-    const int* pair_b;
-    const double* Rpair;     // [P] of this candidate
+    const double* Rpair;  // [P] of this candidate
     double gamma;
-    double* out;             // [NOUT] of this candidate
-    double* stage;           // shared, >= ((nrows (2+P) + 1) & ~1) + V nblk ncomp doubles
+    double* out;          // [NOUT] of this candidate
 };
 
-__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
-    unsigned old;
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
-    return old;
-}
-
 template <int NT>
-__device__ __noinline__ void class_tail(const ClassTail& t) {
-    __shared__ double res[2 + MAXP + MAXP * (MAXD + 1)];
+__device__ __noinline__ void class_sums_out(const ClassSums& t) {
+    __shared__ double res[2 + MAXP + MAXP * MAXD];
     __shared__ double sR[MAXP];
     __shared__ int spa[MAXP], spb[MAXP];
-    const int S = 2 + t.P, Q = S + t.V * t.ncomp;
-    double* st_mid = t.stage;
-    double* st_dot = t.stage + ((t.nrows * S + 1) & ~1);
-#pragma unroll 1
-    for (int i = threadIdx.x; i < t.nrows * S; i += NT) cp_async8(st_mid + i, t.part_mid + i);
-#pragma unroll 1
-    for (int i = threadIdx.x; i < t.V * t.nblk * t.ncomp; i += NT) {
-        const int r = i / t.ncomp, j = i - r * t.ncomp;
-        cp_async8(st_dot + i, t.part_dot + size_t(r) * (MAXD + 1) + (j == t.ncomp - 1 ? MAXD : j));
-    }
+    const int S = 2 + t.P, Q = S + t.V * t.d;
     if (threadIdx.x < t.P) {
         spa[threadIdx.x] = t.pair_a[threadIdx.x];
         spb[threadIdx.x] = t.pair_b[threadIdx.x];
         sR[threadIdx.x] = t.Rpair[threadIdx.x];
     }
-    cp_async_wait_all();
-    __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll 1
     for (int q = warp; q < Q; q += NT / 32) {
         const double* base;
         int stride, count;
         if (q < S) {
-            base = st_mid + q, stride = S, count = t.nrows;
+            base = t.mid + q, stride = S, count = t.nrows;
         } else {
-            const int o = (q - S) / t.ncomp, j = (q - S) - o * t.ncomp;
-            base = st_dot + size_t(o) * t.nblk * t.ncomp + j, stride = t.ncomp, count = t.nblk;
+            const int o = (q - S) / t.d, j = (q - S) - o * t.d;
+            base = t.dot + size_t(o) * t.nblk * t.dstride + j, stride = t.dstride, count = t.nblk;
         }
-        double s = 0.0;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int b = lane;
 #pragma unroll 1
-        for (int b = lane; b < count; b += 32) s += base[b * stride];
+        for (; b + 96 < count; b += 128) {
+            s0 += base[size_t(b) * stride];
+            s1 += base[size_t(b + 32) * stride];
+            s2 += base[size_t(b + 64) * stride];
+            s3 += base[size_t(b + 96) * stride];
+        }
+#pragma unroll 1
+        for (; b < count; b += 32) s0 += base[size_t(b) * stride];
+        double s = (s0 + s1) + (s2 + s3);
 #pragma unroll
         for (int o2 = 16; o2 > 0; o2 >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o2);
         if (lane == 0) res[q] = s;
     }
     __syncthreads();
-    double* out = t.out;
 #pragma unroll 1
     for (int x = threadIdx.x; x < NOUT; x += NT) {
         double v = 0.0;
@@ -316,7 +250,7 @@ __device__ __noinline__ void class_tail(const ClassTail& t) {
             const int j = x - OUT_DETA;
             if (j < t.d)
 #pragma unroll 1
-                for (int o = 0; o < t.V; ++o) v += res[S + o * t.ncomp + j];
+                for (int o = 0; o < t.V; ++o) v += res[S + o * t.d + j];
         } else if (x >= OUT_DR && x < OUT_DR + MAXT * MAXT) {
             const int a = (x - OUT_DR) / MAXT, b = (x - OUT_DR) % MAXT;
 #pragma unroll 1
@@ -328,9 +262,28 @@ __device__ __noinline__ void class_tail(const ClassTail& t) {
             for (int p = 0; p < t.P; ++p) v += sR[p] * (spa[p] == spb[p] ? 1.0 : 2.0) * res[2 + p];
             v /= t.gamma;
         }
-        out[x] = v;
+        t.out[x] = v;
     }
 }
+
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
+// Class-layout finalize as its own kernel (generic equal-n path): one CTA per candidate.
+struct ClassFinalArgs {
+    int P, V, d, nblk_solve, nblk_grad;
+    const double* solve_partial;  // [ncand][nblk_solve][2 + P]
+    const double* grad_partial;   // [ncand][V][nblk_grad][MAXD + 1] (nullptr: no gradient)
+    const double* Rpair;          // [ncand][P]
+    const double* gamma;          // [ncand]
+    const int* pair_a;
+    const int* pair_b;
+    double* out;                  // [ncand][NOUT]
+};
+void finalize_classes(const ClassFinalArgs& a, int ncand, cudaStream_t s);
 
 // ---------------------------------------------------------------- per-slot matvec (solve / gram apply)
 // out_a = sum_b Op_ab(k) in_b(k) with Op Hermitian given by upper pairs (equal n)

@@ -257,6 +257,7 @@ struct fmtgp_model {
     // fmtgp_nll does not write the fit's spectrum / chat (hot loop); they are re-derived from the
     // remembered hyperparameters (incl. the escalated noise scale) when an API call needs them
     bool fit_lazy = false;
+    bool class_mode = true;  // nll transforms per pair-offset class (FMTGP_CLASSES=0: per pair)
     double fit_xi_scale = 1.0;
     struct StoredHyper {
         fmtgp_hyper h{};
@@ -305,6 +306,10 @@ struct fmtgp_model {
     unsigned int* d_counter = nullptr;
     double* d_vec_sum = nullptr;
     int* d_pair_ofs = nullptr;
+    int* d_iota = nullptr;           // [P] 0..P-1 (class vector -> class offset row)
+    long long* d_cvoff = nullptr;    // [P] slot offset of class vector o (o * pslots)
+    double* d_ones = nullptr;        // [max_cand * P]
+    double* d_zeros = nullptr;       // [max_cand * P]
     uint64_t* d_ofs = nullptr;  // distinct pair offsets [nofs][MAXD]
     int nofs = 0;
     double* d_kap = nullptr;    // design-time kappa table [nofs][d][n]
@@ -440,6 +445,25 @@ void build_spectra(fmtgp_model* M, int nc, int si_alpha, const double* b) {
         snk.nvpc = np;
         fwd_gen(M->lattice, g.geo, np * nc, src, snk, M->d_work, M->split ? M->d_gen : nullptr, M->tw, M->st);
     }
+    CK(cudaGetLastError());
+}
+
+// raw spectra of the V pair-offset classes (equal n, nll path): lambda_p is formed in the solve
+void build_class_spectra(fmtgp_model* M, int nc, int si_alpha, const double* b) {
+    ++M->spec_version;
+    const Group& g = M->groups[0];
+    GenSrc src = gensrc_of(M, g, si_alpha, b);
+    src.offs = M->d_ofs;
+    src.vec_pair = M->d_iota;
+    src.nvpc = M->nofs;
+    SpecSink snk{};
+    snk.out = M->d_lam;
+    snk.voff = M->d_cvoff;
+    snk.cstride = M->total_slots;
+    snk.coef = M->d_ones;
+    snk.xi = M->d_zeros;
+    snk.nvpc = M->nofs;
+    fwd_gen(M->lattice, g.geo, M->nofs * nc, src, snk, M->d_work, M->split ? M->d_gen : nullptr, M->tw, M->st);
     CK(cudaGetLastError());
 }
 
@@ -603,7 +627,9 @@ void eval_equal_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, boo
         return;
     }
     copy_hyper(M);
-    build_spectra(M, nc, si_alpha, bw);
+    const bool classes = !keep_chat && M->class_mode;
+    if (classes) build_class_spectra(M, nc, si_alpha, bw);
+    else build_spectra(M, nc, si_alpha, bw);
     CK(cudaMemsetAsync(M->d_bad, 0x7f, sizeof(int) * nc, M->st));
     CK(cudaMemsetAsync(M->d_bad + nc, 0, sizeof(int) * nc, M->st));
     CK(cudaMemsetAsync(M->d_imre, 0, sizeof(unsigned long long) * 2 * MAXT * nc, M->st));
@@ -623,9 +649,51 @@ void eval_equal_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, boo
     sa.bad = M->d_bad;
     sa.imre = M->d_imre;
     sa.nblk = M->nblk_solve;
+    const Group& g = M->groups[0];
+    if (classes) {
+        sa.classes = 1;
+        sa.V = M->nofs;
+        sa.pair_cls = M->d_pair_ofs;
+        sa.coef = g.d_coef;
+        sa.xi = g.d_xi;
+        sa.Rpair = M->d_Rpair;
+        sa.pair_a = M->d_pa;
+        sa.pair_b = M->d_pb;
+        solve_equal(sa, nc, M->st);
+        CK(cudaGetLastError());
+        if (grad) {
+            GradSink gs{};
+            gs.gen = gensrc_of(M, g, si_alpha, bw);
+            gs.gen.offs = M->d_ofs;
+            gs.gen.vec_pair = M->d_iota;
+            gs.gen.nvpc = M->nofs;
+            gs.partial = M->d_pgrad;
+            gs.nblk = M->nblk_grad;
+            gs.acc_n = M->d + 1;
+            inv_grad(M->lattice, g.geo, M->nofs * nc, M->d_M, M->d_cvoff, M->total_slots, M->nofs, gs, M->d_work,
+                     M->split ? M->d_gen : nullptr, M->tw, M->st);
+            CK(cudaGetLastError());
+        }
+        ClassFinalArgs fa{};
+        fa.P = M->P;
+        fa.V = M->nofs;
+        fa.d = M->d;
+        fa.nblk_solve = M->nblk_solve;
+        fa.nblk_grad = M->nblk_grad;
+        fa.solve_partial = M->d_psolve;
+        fa.grad_partial = grad ? M->d_pgrad : nullptr;
+        fa.Rpair = M->d_Rpair;
+        fa.gamma = M->d_gamma;
+        fa.pair_a = M->d_pa;
+        fa.pair_b = M->d_pb;
+        fa.out = M->d_out;
+        finalize_classes(fa, nc, M->st);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(M->h_res, M->d_res, sizeof(double) * M->res_len, cudaMemcpyDeviceToHost, M->st));
+        return;
+    }
     solve_equal(sa, nc, M->st);
     CK(cudaGetLastError());
-    const Group& g = M->groups[0];
     if (grad) {
         GradSink gs{};
         gs.gen = gensrc_of(M, g, si_alpha, bw);
@@ -817,6 +885,7 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
         M->T = dz->L;
         M->max_cand = max_cand;
         if (const char* e = std::getenv("FMTGP_KAPPA_TABLE")) M->kap_enabled = e[0] != '0';
+        if (const char* e = std::getenv("FMTGP_CLASSES")) M->class_mode = e[0] != '0';
         M->off[0] = 0;
         for (int l = 0; l < M->T; ++l) {
             M->m[l] = dz->m[l];
@@ -989,6 +1058,20 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
         M->d_ofs = dalloc<uint64_t>(uniq.size());
         CK(cudaMemcpy(M->d_pair_ofs, pofs.data(), M->P * sizeof(int), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(M->d_ofs, uniq.data(), uniq.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
+        {
+            std::vector<int> iota(M->P);
+            std::vector<long long> cvo(M->P);
+            for (int i = 0; i < M->P; ++i) iota[i] = i, cvo[i] = (long long)i * M->pslots[0];
+            M->d_iota = dalloc<int>(M->P);
+            M->d_cvoff = dalloc<long long>(M->P);
+            CK(cudaMemcpy(M->d_iota, iota.data(), M->P * sizeof(int), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(M->d_cvoff, cvo.data(), M->P * sizeof(long long), cudaMemcpyHostToDevice));
+            std::vector<double> ones(size_t(max_cand) * M->P, 1.0), zeros(size_t(max_cand) * M->P, 0.0);
+            M->d_ones = dalloc<double>(ones.size());
+            M->d_zeros = dalloc<double>(zeros.size());
+            CK(cudaMemcpy(M->d_ones, ones.data(), ones.size() * sizeof(double), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(M->d_zeros, zeros.data(), zeros.size() * sizeof(double), cudaMemcpyHostToDevice));
+        }
         if (M->equal && !M->lattice && DigGeo::make(M->m[0], M->nofs, M->dgeo, (long long)M->nofs * max_cand)) {
             M->dig = true;
             const DigGeo& g = M->dgeo;
@@ -1009,7 +1092,7 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
         } else {
             M->nblk_solve = 1;
         }
-        M->d_psolve = dalloc<double>(size_t(max_cand) * std::max(M->nblk_solve, 1) * 3);
+        M->d_psolve = dalloc<double>(size_t(max_cand) * std::max(M->nblk_solve, 1) * (3 + M->P));
         // one result block [out | bad | imre] -> a single D2H copy per evaluation
         M->res_len = size_t(max_cand) * (NOUT + 1 + 2 * MAXT) + MAXT;
         M->d_res = dalloc<double>(M->res_len);
@@ -1118,6 +1201,10 @@ int fmtgp_model_destroy(fmtgp_model_t M) {
     F(M->d_counter);
     F(M->d_vec_sum);
     F(M->d_pair_ofs);
+    F(M->d_iota);
+    F(M->d_cvoff);
+    F(M->d_ones);
+    F(M->d_zeros);
     F(M->d_ofs);
     F(M->d_kap);
     F(M->d_laminv);
