@@ -257,6 +257,8 @@ struct fmtgp_model {
     // fmtgp_nll does not write the fit's spectrum / chat (hot loop); they are re-derived from the
     // remembered hyperparameters (incl. the escalated noise scale) when an API call needs them
     bool fit_lazy = false;
+    double* d_scratch = nullptr;  // per-call workspace (posterior queries), grown on demand
+    size_t scratch_len = 0;
     bool class_mode = true;  // nll transforms per pair-offset class (FMTGP_CLASSES=0: per pair)
     double fit_xi_scale = 1.0;
     struct StoredHyper {
@@ -509,6 +511,20 @@ void compute_yhat_tau(fmtgp_model* M) {
         for (int t = 0; t < M->T; ++t) M->tau[t] = y0[t] / std::sqrt(double(M->n[t]));
     }
     M->have_y = true;
+}
+
+// model-owned device workspace (no cudaMalloc / cudaFree — which synchronises — per call)
+double* scratch(fmtgp_model* M, size_t words) {
+    if (words > M->scratch_len) {
+        CK(cudaStreamSynchronize(M->st));
+        if (M->d_scratch) cudaFree(M->d_scratch);
+        M->d_scratch = nullptr;
+        M->scratch_len = 0;
+        const size_t len = std::max(words, M->scratch_len * 2);
+        M->d_scratch = dalloc<double>(len);
+        M->scratch_len = len;
+    }
+    return M->d_scratch;
 }
 
 void take_tau(fmtgp_model* M) {  // after a D2H of the result block
@@ -1201,6 +1217,7 @@ int fmtgp_model_destroy(fmtgp_model_t M) {
     F(M->d_counter);
     F(M->d_vec_sum);
     F(M->d_pair_ofs);
+    F(M->d_scratch);
     F(M->d_iota);
     F(M->d_cvoff);
     F(M->d_ones);
@@ -1563,11 +1580,17 @@ int fmtgp_posterior_mean(fmtgp_model_t M, int task, const double* X, int64_t cou
         CK(cudaSetDevice(M->dev));
         ensure_coefficients(M);
         upload_fit(M);
-        double* dX = dalloc<double>(size_t(count) * M->d);
-        double* dO = dalloc<double>(size_t(count));
-        try {
+        int nsplit;
+        long long chunk;
+        posterior_split(count, M->N, nsplit, chunk);
+        double* dX = scratch(M, size_t(count) * (M->d + 1 + nsplit));
+        double* dO = dX + size_t(count) * M->d;
+        {
             CK(cudaMemcpyAsync(dX, X, sizeof(double) * count * M->d, cudaMemcpyHostToDevice, M->st));
             PostArgs a{};
+            a.part = dO + count;
+            a.nsplit = nsplit;
+            a.chunk = chunk;
             a.lattice = M->lattice;
             a.d = M->d;
             a.T = M->T;
@@ -1596,13 +1619,7 @@ int fmtgp_posterior_mean(fmtgp_model_t M, int task, const double* X, int64_t cou
             CK(cudaGetLastError());
             CK(cudaMemcpyAsync(out, dO, sizeof(double) * count, cudaMemcpyDeviceToHost, M->st));
             CK(cudaStreamSynchronize(M->st));
-        } catch (...) {
-            cudaFree(dX);
-            cudaFree(dO);
-            throw;
         }
-        cudaFree(dX);
-        cudaFree(dO);
     });
 }
 

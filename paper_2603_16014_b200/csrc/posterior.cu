@@ -38,54 +38,90 @@ __device__ __forceinline__ uint64_t point_word(const PostArgs& a, int l, uint64_
 
 constexpr int PM_NT = 128, PM_TILE = 128;
 
+// grid (query blocks, training chunks): each CTA sums one chunk of the training points for its
+// 128 queries into part[chunk][q]; k_post_combine adds the chunks in fixed order (deterministic)
+template <bool LAT, int DC>
 __global__ void __launch_bounds__(PM_NT) k_post_mean(PostArgs a) {
-    __shared__ uint64_t pts[PM_TILE * MAXD];
+    __shared__ uint64_t pts[PM_TILE * DC];
     __shared__ double wts[PM_TILE];
     const long long q = blockIdx.x * (long long)PM_NT + threadIdx.x;
     const bool live = q < a.count;
-    double xq[MAXD];
-    uint64_t xb[MAXD];
+    const int d = a.d;
+    double xq[DC], eta[DC];
+    uint64_t xb[DC];
 #pragma unroll
-    for (int j = 0; j < MAXD; ++j)
-        if (j < a.d) {
-            xq[j] = live ? a.X[q * a.d + j] : 0.0;
-            xb[j] = uint64_t(xq[j] * 0x1p53);  // frac_to_bits (ld_sequences.cpp:55-58)
-        }
+    for (int j = 0; j < DC; ++j) {
+        xq[j] = (j < d && live) ? a.X[q * d + j] : 0.0;
+        xb[j] = uint64_t(xq[j] * 0x1p53);  // frac_to_bits (ld_sequences.cpp:55-58)
+        eta[j] = j < d ? a.eta[j] : 0.0;
+    }
+    const long long g0 = blockIdx.y * a.chunk, g1 = g0 + a.chunk;
     double acc = 0.0;
     for (int l = 0; l < a.T; ++l) {
+        const long long lo = a.off[l] > g0 ? a.off[l] : g0;
+        const long long hi = a.off[l] + a.n[l] < g1 ? a.off[l] + a.n[l] : g1;
+        if (lo >= hi) continue;
         const double Rtl = a.R[a.task * a.T + l];
-        const long long nl = a.n[l];
-        const double* cl = a.c + a.off[l];
-        for (long long base = 0; base < nl; base += PM_TILE) {
+        for (long long base = lo; base < hi; base += PM_TILE) {
             __syncthreads();
-            for (int e = threadIdx.x; e < PM_TILE * a.d; e += PM_NT) {
-                const int r = e / a.d, j = e - r * a.d;
-                if (base + r < nl) pts[r * MAXD + j] = point_word(a, l, base + r, j);
+            const int cnt = int(hi - base < PM_TILE ? hi - base : PM_TILE);
+            for (int e = threadIdx.x; e < cnt * d; e += PM_NT) {
+                const int r = e / d, j = e - r * d;
+                pts[r * DC + j] = point_word(a, l, uint64_t(base + r - a.off[l]), j);
             }
-            for (int r = threadIdx.x; r < PM_TILE; r += PM_NT) wts[r] = base + r < nl ? Rtl * cl[base + r] : 0.0;
+            for (int r = threadIdx.x; r < cnt; r += PM_NT) wts[r] = Rtl * a.c[base + r];
             __syncthreads();
-            const int cnt = int(nl - base < PM_TILE ? nl - base : PM_TILE);
+#pragma unroll 2
             for (int r = 0; r < cnt; ++r) {
                 double prod = a.gamma;
 #pragma unroll
-                for (int j = 0; j < MAXD; ++j)
-                    if (j < a.d) {
-                        const uint64_t pw = pts[r * MAXD + j];
-                        const double base_v = a.lattice ? si_free(xq[j], double(pw) * 0x1p-53, a.si_alpha)
-                                                        : dsi_walsh(xb[j] ^ pw, a.b);
-                        prod *= 1.0 + a.eta[j] * base_v;
+                for (int j = 0; j < DC; ++j)
+                    if (j < d) {
+                        const uint64_t pw = pts[r * DC + j];
+                        const double bv = LAT ? si_free(xq[j], double(pw) * 0x1p-53, a.si_alpha)
+                                              : dsi_walsh(xb[j] ^ pw, a.b);
+                        prod *= 1.0 + eta[j] * bv;
                     }
                 acc = fma(prod, wts[r], acc);
             }
         }
     }
-    if (live) a.out[q] = a.tau + acc;
+    if (live) a.part[blockIdx.y * a.count + q] = acc;
+}
+
+__global__ void k_post_combine(PostArgs a) {
+    const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (q >= a.count) return;
+    double s = 0.0;
+    for (int k = 0; k < a.nsplit; ++k) s += a.part[k * a.count + q];
+    a.out[q] = a.tau + s;
+}
+
+void posterior_split(long long count, long long N, int& nsplit, long long& chunk) {
+    const long long qblocks = (count + PM_NT - 1) / PM_NT;
+    long long want = (4 * 148 + qblocks - 1) / std::max(qblocks, 1ll);
+    const long long tiles = (N + PM_TILE - 1) / PM_TILE;
+    want = std::max(1ll, std::min(want, tiles));
+    chunk = ((tiles + want - 1) / want) * PM_TILE;
+    nsplit = int((N + chunk - 1) / chunk);
 }
 
 void posterior_mean(const PostArgs& a, cudaStream_t s) {
     const long long blocks = (a.count + PM_NT - 1) / PM_NT;
+    if (blocks <= 0) return;
     ProfScope ps("posterior_mean", s);
-    if (blocks > 0) k_post_mean<<<unsigned(blocks), PM_NT, 0, s>>>(a);
+    const dim3 grid(unsigned(blocks), unsigned(a.nsplit));
+    const int dc = a.d <= 4 ? 4 : a.d <= 8 ? 8 : 16;
+    if (a.lattice) {
+        if (dc == 4) k_post_mean<true, 4><<<grid, PM_NT, 0, s>>>(a);
+        else if (dc == 8) k_post_mean<true, 8><<<grid, PM_NT, 0, s>>>(a);
+        else k_post_mean<true, 16><<<grid, PM_NT, 0, s>>>(a);
+    } else {
+        if (dc == 4) k_post_mean<false, 4><<<grid, PM_NT, 0, s>>>(a);
+        else if (dc == 8) k_post_mean<false, 8><<<grid, PM_NT, 0, s>>>(a);
+        else k_post_mean<false, 16><<<grid, PM_NT, 0, s>>>(a);
+    }
+    k_post_combine<<<unsigned((a.count + 255) / 256), 256, 0, s>>>(a);
 }
 
 }  // namespace fmtgp

@@ -19,7 +19,13 @@ struct PostArgs {
     const double* X;         // device [count * d]
     long long count;
     double* out;             // device [count]
+    double* part;            // device [nsplit][count] partial sums (workspace)
+    int nsplit;              // training-point chunks (grid.y)
+    long long chunk;         // global training indices per chunk (multiple of the tile)
 };
+
+// grid shape for `count` queries over N training points: >= ~4 CTAs per SM
+void posterior_split(long long count, long long N, int& nsplit, long long& chunk);
 
 void posterior_mean(const PostArgs& a, cudaStream_t s);
 
