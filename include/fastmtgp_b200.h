@@ -139,6 +139,23 @@ FMTGP_API int fmtgp_nll(fmtgp_model_t model, const fmtgp_hyper* h, int want_grad
 FMTGP_API int fmtgp_nll_batch(fmtgp_model_t model, int ncand, const fmtgp_hyper* h, int want_grad, fmtgp_result* out);
 /* coefficients c = K^-1 (y - E tau) of the last fmtgp_nll call (GpModel::c), host [N] */
 FMTGP_API int fmtgp_coefficients(fmtgp_model_t model, double* c);
+
+/* ---- fit: the reference's iRprop- loop (gp_core.cpp:317-382) driven by the analytic gradient --
+ * Parameter vector theta (ParamPack, gp_core.cpp:243-304): [log gamma, log eta[d], B[L*s] (row-major),
+ * log t[L], and for digital designs log b[4]].  One NLL+gradient evaluation per step instead of the
+ * reference's 2*P_theta+1 loss evaluations; iRprop- constants 0.1 / 1.2 / 0.5 / [1e-6, 1].
+ * loss_trace[k] = best loss after step k; theta_best receives the best parameters; the model is
+ * left refreshed at them (coefficients / posterior / cubature follow). */
+typedef struct fmtgp_fit_report {
+    int steps;
+    int n_params;
+    int escalations;            /* noise escalations of the final refresh              */
+    double final_loss;          /* best loss                                            */
+    double tau[FMTGP_MAX_T];    /* prior means at the best parameters (internal order)  */
+} fmtgp_fit_report;
+FMTGP_API int fmtgp_fit_param_count(fmtgp_model_t model, int s, int* n_params);
+FMTGP_API int fmtgp_fit(fmtgp_model_t model, const fmtgp_hyper* init, int steps, double* theta_best,
+                        double* loss_trace, double* step_seconds, fmtgp_fit_report* report);
 /* posterior_mean_batch (gp_core.cpp:409-421) for the last fmtgp_nll hyperparameters:
  * X host [count * d], task internal index */
 FMTGP_API int fmtgp_posterior_mean(fmtgp_model_t model, int task, const double* X, int64_t count, double* out);

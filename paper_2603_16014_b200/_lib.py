@@ -57,6 +57,11 @@ class CResult(C.Structure):
                 ("xi_scale", C.c_double), ("escalations", C.c_int), ("status", C.c_int)]
 
 
+class CFitReport(C.Structure):
+    _fields_ = [("steps", C.c_int), ("n_params", C.c_int), ("escalations", C.c_int),
+                ("final_loss", C.c_double), ("tau", C.c_double * MAX_T)]
+
+
 _lib = None
 
 _SIGS = {
@@ -77,6 +82,8 @@ _SIGS = {
     "fmtgp_nll": (C.c_int, [C.c_void_p, C.POINTER(CHyper), C.c_int, C.POINTER(CResult)]),
     "fmtgp_nll_batch": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(CHyper), C.c_int, C.POINTER(CResult)]),
     "fmtgp_coefficients": (C.c_int, [C.c_void_p, _dp]),
+    "fmtgp_fit_param_count": (C.c_int, [C.c_void_p, C.c_int, _ip]),
+    "fmtgp_fit": (C.c_int, [C.c_void_p, C.POINTER(CHyper), C.c_int, _dp, _dp, _dp, C.POINTER(CFitReport)]),
     "fmtgp_posterior_mean": (C.c_int, [C.c_void_p, C.c_int, _dp, C.c_int64, _dp]),
     "fmtgp_posterior_var": (C.c_int, [C.c_void_p, C.c_int, _dp, C.c_int64, _dp]),
     "fmtgp_cubature": (C.c_int, [C.c_void_p, _dp, _dp]),

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <chrono>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
@@ -1169,6 +1170,190 @@ struct ProfGuard {
     ~ProfGuard() { g_prof = prev; }
 };
 
+// fmtgp_nll without the C-ABI guard: one refresh + loss (+ gradient) with escalation; the fit's
+// spectrum / chat are re-derived lazily when a later call needs them.
+void nll_public(fmtgp_model* M, const fmtgp_hyper* h, bool grad, fmtgp_result* out) {
+    M->fit_lazy = false;
+    nll_batch_impl(M, 1, h, grad, out, /*keep_chat=*/!M->equal);
+    if (out->status != FMTGP_OK) {
+        if (out->status == FMTGP_ERR_SCHUR) throw Fail{FMTGP_ERR_SCHUR, "noise escalation schedule exhausted"};
+        throw Fail{out->status, "invert_and_logdet: non-real Schur complement"};
+    }
+    remember_hyper(M, h);
+    if (M->equal) {
+        M->fit_h.store(h, M->d, M->T);
+        M->fit_xi_scale = out->xi_scale;
+        M->fit_lazy = true;
+    }
+    M->have_fit = true;
+    M->have_c = false;
+    M->have_spec = true;
+    M->have_inv = false;
+}
+
+// Hyperparameters as the reference's ParamPack (gp_core.cpp:243-304): log gamma, log eta, B, log t,
+// log b (digital).  Owns its arrays; view() is a fmtgp_hyper over them.
+struct PackedHyper {
+    int d, L, s, dig;
+    std::vector<double> eta, B, t, xi;
+    fmtgp_hyper h{};
+    PackedHyper(const fmtgp_model* M, const fmtgp_hyper* init)
+        : d(M->d), L(M->T), s(init->s), dig(!M->lattice), eta(init->eta, init->eta + M->d),
+          B(init->B, init->B + size_t(M->T) * init->s), t(init->t, init->t + M->T), xi(init->xi, init->xi + M->T) {
+        h = *init;
+        rebind();
+    }
+    void rebind() {
+        h.eta = eta.data();
+        h.B = B.data();
+        h.t = t.data();
+        h.xi = xi.data();
+        h.s = s;
+    }
+    int count() const { return 1 + d + L * s + L + (dig ? 4 : 0); }
+    std::vector<double> pack() const {
+        std::vector<double> th;
+        th.push_back(std::log(h.gamma));
+        for (double v : eta) th.push_back(std::log(v));
+        for (double v : B) th.push_back(v);
+        for (double v : t) th.push_back(std::log(v));
+        if (dig)
+            for (int a = 0; a < 4; ++a) th.push_back(std::log(h.b[a]));
+        return th;
+    }
+    void unpack(const std::vector<double>& th) {
+        int k = 0;
+        h.gamma = std::exp(th[k++]);
+        for (auto& v : eta) v = std::exp(th[k++]);
+        for (auto& v : B) v = th[k++];
+        for (auto& v : t) v = std::exp(th[k++]);
+        if (dig)
+            for (int a = 0; a < 4; ++a) h.b[a] = std::exp(th[k++]);
+        rebind();
+    }
+};
+
+// loss at the packed point (guarded_loss, gp_core.cpp:306-313: escalation failure -> +inf), with
+// the gradient w.r.t. theta when grad != nullptr.  Walsh weights: the DSI base kernel is linear in
+// b, so with a single non-zero order b_k d/dlog b_k = sum_j eta_j d/deta_j exactly; a zero weight
+// sits at log 0 = -inf where the reference's difference quotient is not finite (gradient 0); with
+// several non-zero orders the log b_k components use the reference's own central difference.
+double fit_loss(fmtgp_model* M, PackedHyper& P, const std::vector<double>& th, std::vector<double>* grad) {
+    if (grad && !M->equal) {
+        // unequal n: no analytic gradient yet -> the reference's own central
+        // difference on theta (gp_core.cpp:341-351), every evaluation on the device
+        const double f0 = fit_loss(M, P, th, nullptr);
+        grad->assign(th.size(), 0.0);
+        for (size_t i = 0; i < th.size(); ++i) {
+            const double hstep = 1e-4 * std::max(1.0, std::abs(th[i]));
+            std::vector<double> tp = th;
+            tp[i] = th[i] + hstep;
+            const double fp = fit_loss(M, P, tp, nullptr);
+            tp[i] = th[i] - hstep;
+            const double fm = fit_loss(M, P, tp, nullptr);
+            (*grad)[i] = (std::isfinite(fp) && std::isfinite(fm)) ? (fp - fm) / (2.0 * hstep) : 0.0;
+        }
+        P.unpack(th);
+        return f0;
+    }
+    P.unpack(th);
+    fmtgp_result r{};
+    try {
+        nll_batch_impl(M, 1, &P.h, grad != nullptr, &r, false);
+    } catch (const Fail& f) {  // unequal n reports an exhausted escalation by throwing
+        if (f.code != FMTGP_ERR_SCHUR) throw;
+        r.status = FMTGP_ERR_SCHUR;
+    }
+    if (r.status == FMTGP_ERR_NONREAL) throw Fail{FMTGP_ERR_NONREAL, "invert_and_logdet: non-real Schur complement"};
+    const bool ok = r.status == FMTGP_OK && std::isfinite(r.nll);
+    if (!grad) return ok ? r.nll : INFINITY;
+    grad->assign(th.size(), 0.0);
+    if (!ok) return INFINITY;
+    auto& g = *grad;
+    int k = 0;
+    g[k++] = P.h.gamma * r.dgamma;
+    double eta_deta = 0.0;
+    for (int j = 0; j < P.d; ++j) {
+        g[k++] = P.eta[j] * r.deta[j];
+        eta_deta += P.eta[j] * r.deta[j];
+    }
+    for (int l = 0; l < P.L; ++l)
+        for (int q = 0; q < P.s; ++q) g[k++] = r.dB[l * P.s + q];
+    for (int l = 0; l < P.L; ++l) g[k++] = P.t[l] * r.dt[l];
+    if (P.dig) {
+        int nz = 0;
+        for (int a = 0; a < 4; ++a) nz += P.h.b[a] != 0.0;
+        if (nz == 1) {
+            for (int a = 0; a < 4; ++a) g[k + a] = P.h.b[a] != 0.0 ? eta_deta : 0.0;
+        } else {
+            const std::vector<double> base = th;
+            for (int a = 0; a < 4; ++a) {
+                if (P.h.b[a] == 0.0) continue;
+                const double hstep = 1e-4 * std::max(1.0, std::abs(base[k + a]));
+                std::vector<double> tp = base;
+                tp[k + a] = base[k + a] + hstep;
+                const double fp = fit_loss(M, P, tp, nullptr);
+                tp[k + a] = base[k + a] - hstep;
+                const double fm = fit_loss(M, P, tp, nullptr);
+                g[k + a] = (std::isfinite(fp) && std::isfinite(fm)) ? (fp - fm) / (2.0 * hstep) : 0.0;
+            }
+            P.unpack(base);
+        }
+    }
+    return r.nll;
+}
+
+// fit (gp_core.cpp:317-382): iRprop- on theta.  The loss at the updated theta is the value the
+// next step's gradient evaluation returns, so each step costs one NLL+gradient evaluation.
+void fit_impl(fmtgp_model* M, const fmtgp_hyper* init, int steps, double* theta_best, double* loss_trace,
+              double* step_seconds, fmtgp_fit_report* rep) {
+    using clock = std::chrono::steady_clock;
+    PackedHyper P(M, init);
+    std::vector<double> theta = P.pack();
+    const int np = int(theta.size());
+    std::vector<double> grad, grad_prev(np, 0.0), step(np, 0.1);
+    constexpr double kUp = 1.2, kDown = 0.5, kMax = 1.0, kMin = 1e-6;
+    double cur = fit_loss(M, P, theta, &grad);
+    if (!std::isfinite(cur)) throw Fail{FMTGP_ERR_INVALID, "fit: initial loss is not finite"};
+    double best = cur;
+    std::vector<double> best_theta = theta;
+    for (int it = 0; it < steps; ++it) {
+        const auto tic = clock::now();
+        for (int i = 0; i < np; ++i) {
+            double gi = grad[i];
+            const double sgn = gi * grad_prev[i];
+            if (sgn > 0.0) {
+                step[i] = std::min(step[i] * kUp, kMax);
+            } else if (sgn < 0.0) {
+                step[i] = std::max(step[i] * kDown, kMin);
+                gi = 0.0;  // iRprop-: skip the update after a sign flip
+            }
+            if (gi > 0.0) theta[i] -= step[i];
+            else if (gi < 0.0) theta[i] += step[i];
+            grad_prev[i] = gi;
+        }
+        // the loss at the new theta; its gradient drives the next step (not needed after the last)
+        cur = fit_loss(M, P, theta, it + 1 < steps ? &grad : nullptr);
+        if (cur < best) {
+            best = cur;
+            best_theta = theta;
+        }
+        loss_trace[it] = best;
+        if (step_seconds) step_seconds[it] = std::chrono::duration<double>(clock::now() - tic).count();
+    }
+    P.unpack(best_theta);
+    fmtgp_result r{};
+    nll_public(M, &P.h, false, &r);  // model.refresh() at the best parameters
+    if (theta_best)
+        for (int i = 0; i < np; ++i) theta_best[i] = best_theta[i];
+    std::memset(rep, 0, sizeof(*rep));
+    rep->steps = steps;
+    rep->n_params = np;
+    rep->escalations = r.escalations;
+    rep->final_loss = best;
+    for (int l = 0; l < M->T; ++l) rep->tau[l] = r.tau[l];
+}
+
 // ===================================================================== C ABI
 extern "C" {
 
@@ -1526,22 +1711,25 @@ int fmtgp_nll(fmtgp_model_t M, const fmtgp_hyper* h, int want_grad, fmtgp_result
         ProfGuard pg_(M);
         if (!M || !h || !out) invalid("nll: null argument");
         CK(cudaSetDevice(M->dev));
-        M->fit_lazy = false;
-        nll_batch_impl(M, 1, h, want_grad != 0, out, /*keep_chat=*/!M->equal);
-        if (out->status != FMTGP_OK) {
-            if (out->status == FMTGP_ERR_SCHUR) throw Fail{FMTGP_ERR_SCHUR, "noise escalation schedule exhausted"};
-            throw Fail{out->status, "invert_and_logdet: non-real Schur complement"};
-        }
-        remember_hyper(M, h);
-        if (M->equal) {
-            M->fit_h.store(h, M->d, M->T);
-            M->fit_xi_scale = out->xi_scale;
-            M->fit_lazy = true;
-        }
-        M->have_fit = true;
-        M->have_c = false;
-        M->have_spec = true;
-        M->have_inv = false;
+        nll_public(M, h, want_grad != 0, out);
+    });
+}
+
+int fmtgp_fit_param_count(fmtgp_model_t M, int s, int* n) {
+    return guarded([&] {
+        if (!M || !n || s < 0) invalid("fit_param_count: bad argument");
+        *n = 1 + M->d + M->T * s + M->T + (M->lattice ? 0 : 4);
+    });
+}
+
+int fmtgp_fit(fmtgp_model_t M, const fmtgp_hyper* init, int steps, double* theta_best, double* loss_trace,
+              double* step_seconds, fmtgp_fit_report* rep) {
+    return guarded([&] {
+        ProfGuard pg_(M);
+        if (!M || !init || !rep || steps < 0 || (steps > 0 && !loss_trace)) invalid("fit: bad argument");
+        CK(cudaSetDevice(M->dev));
+        validate_hyper(M, init);
+        fit_impl(M, init, steps, theta_best, loss_trace, step_seconds, rep);
     });
 }
 

@@ -59,6 +59,18 @@ def _result(r: CResult, dz: Design, hp: Hyper) -> Dict:
                 xi_scale=r.xi_scale, escalations=r.escalations, status=r.status)
 
 
+def unpack_theta(theta: np.ndarray, like: Hyper, digital: bool) -> Hyper:
+    """ParamPack::unpack (gp_core.cpp:289-303): log gamma, log eta, B, log t, [log b]."""
+    d, (L, s) = like.eta.size, like.B.shape
+    k = 0
+    gamma = float(np.exp(theta[k])); k += 1
+    eta = np.exp(theta[k:k + d]); k += d
+    B = np.array(theta[k:k + L * s]).reshape(L, s); k += L * s
+    t = np.exp(theta[k:k + L]); k += L
+    b = tuple(np.exp(theta[k:k + 4])) if digital else like.b
+    return Hyper(gamma=gamma, eta=eta, B=B, t=t, xi=like.xi.copy(), si_alpha=like.si_alpha, b=b)
+
+
 class Model:
     """Device-resident design + observations + workspace (one per GPU / dataset)."""
 
@@ -171,6 +183,25 @@ class Model:
         res = (CResult * n)()
         check(self.lib.fmtgp_nll_batch(self.h, n, arr, int(grad), res))
         return [_result(res[i], self.design, hps[i]) for i in range(n)]
+
+    def fit(self, hp: Hyper, steps: int) -> Dict:
+        """The reference's `fit` (iRprop- over ParamPack, gp_core.cpp:317-382) with the analytic
+        gradient: one NLL+gradient evaluation per step.  Returns the best hyperparameters, the
+        packed theta, the best-so-far loss trace and per-step seconds; the model is left
+        refreshed at the best point."""
+        ch, keep = _chyper(hp)
+        n = C.c_int()
+        check(self.lib.fmtgp_fit_param_count(self.h, int(hp.B.shape[1]), C.byref(n)))
+        theta = np.empty(n.value)
+        trace = np.empty(max(steps, 1))
+        secs = np.empty(max(steps, 1))
+        rep = _lib.CFitReport()
+        check(self.lib.fmtgp_fit(self.h, C.byref(ch), int(steps), dptr(theta), dptr(trace), dptr(secs),
+                                 C.byref(rep)))
+        best = unpack_theta(theta, hp, self.design.kind == 1)
+        self.hyper = best
+        return dict(hyper=best, theta=theta, loss_trace=trace[:steps].copy(), step_seconds=secs[:steps].copy(),
+                    final_loss=rep.final_loss, escalations=rep.escalations, tau=np.array(rep.tau[:self.design.L]))
 
     def coefficients(self) -> np.ndarray:
         c = np.empty(self.design.N)

@@ -119,6 +119,31 @@ def test_gradient_vs_reference_fd(ref, Model, kind, m):
     assert abs(r["dgamma"] - fd["gamma"]) <= 1e-6 * max(1.0, abs(fd["gamma"]))
 
 
+@pytest.mark.parametrize("case", [(LATTICE, [6, 6], None), (DIGITAL, [6, 6, 6], (0.0, 0.0, 0.0, 1.0)),
+                                  (DIGITAL, [5, 5], (0.5, 0.2, 0.1, 1.0)), (LATTICE, [6, 4], None)],
+                         ids=["lattice", "digital-order4", "digital-mixed-b", "lattice-unequal"])
+def test_fit_matches_reference(ref, Model, case):
+    """iRprop- fit (gp_core.cpp:317-382): the analytic-gradient loop follows the reference's
+    FD-gradient trajectory (the update uses gradient signs only); best-so-far loss trace within
+    the NLL tolerance at every step.  Unequal n uses the reference's own difference quotient."""
+    kind, m, b = case
+    dz, hp, y = instance(kind, m)
+    if b is not None:
+        hp.b = b
+    steps = 6
+    M = Model(dz)
+    M.set_y(y)
+    out = M.fit(hp, steps)
+    final_ref, trace_ref = ref.Model(dz, hp, y).fit(steps)
+    tol = 1e-8 * dz.N
+    assert np.all(np.abs(out["loss_trace"] - trace_ref) <= tol + 1e-9 * np.abs(trace_ref)), (out["loss_trace"], trace_ref)
+    assert abs(out["final_loss"] - final_ref) <= tol + 1e-9 * abs(final_ref)
+    assert np.all(np.diff(out["loss_trace"]) <= 0)
+    # the model is left refreshed at the best point
+    r = M.nll(out["hyper"], grad=False)
+    assert abs(r["nll"] - out["final_loss"]) <= tol
+
+
 @pytest.mark.parametrize("kind", [LATTICE, DIGITAL], ids=["lattice", "digital"])
 @pytest.mark.parametrize("m", [[3], [4, 4], [6, 6, 6], [5, 3], [6, 4, 4, 2]], ids=lambda m: "m" + "-".join(map(str, m)))
 def test_posterior_and_cubature(ref, Model, kind, m):

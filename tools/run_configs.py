@@ -61,6 +61,13 @@ def main():
         if cfg in (1, 2, 4):
             r, best, med = timed(lambda: M.nll(inst.hyper, grad=True))
             out.update(nll=r["nll"], logdet=r["logdet"], deta=list(r["deta"]), fit_s_best=best, fit_s_med=med)
+        if cfg in (1, 2, 4):  # the iRprop- fit loop, seconds per optimisation step
+            M.profile(False)
+            steps = 20 if cfg != 4 else 5
+            f = M.fit(inst.hyper, steps)
+            out.update(fit_steps=steps, fit_step_s_med=float(np.median(f["step_seconds"])),
+                       fit_final_loss=f["final_loss"], fit_loss_first=float(f["loss_trace"][0]))
+            M.profile(True)
         if cfg == 1:
             c = M.coefficients()
             pm, b2, m2 = timed(lambda: np.stack([M.posterior_mean(t, inst.X_test) for t in range(dz.L)]))
