@@ -286,7 +286,7 @@ def main():
     e2e_value = world * 1e3 * args.steps / e2e_ms
     hyper_bytes = 8 * (dz.d + 1 + P + 2 * P)
     h2d = 8 * dz.N + hyper_bytes
-    d2h = 8 * (4 + 16 + 64) + 8  # result record + status words
+    d2h = 8 * ((4 + 16 + 64) + 1 + 2 * 8 + 8)  # result block: record, bad flag, non-real maxima, tau (model.cu res_len)
 
     if rank != 0:
         if dist:
