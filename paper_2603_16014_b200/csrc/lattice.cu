@@ -1,0 +1,483 @@
+// Equal-n lattice fit in three fused kernels — see lattice.cuh.
+#include "lattice.cuh"
+
+namespace fmtgp {
+
+constexpr int LAT_NT = 512;            // 16 complex per thread per FFT stage, 2^13-element tiles
+constexpr int LAT_TILE_LOG = 13;
+constexpr int LAT_MID_SMEM = 200 * 1024;
+
+bool LatGeo::make(int m, int V, int T, int d, LatGeo& g) {
+    if (m < 17 || m > 28 || T < 1 || T > 4 || V < 1 || d < 1 || d > MAXD) return false;
+    g.m = m;
+    g.lt = m - 1;
+    // row length: all V class rows of one frequency block in smem, <= 512 threads of 16 elements
+    int l2cap = 0;
+    while (l2cap < LAT_TILE_LOG && (long long)V << (l2cap + 1) <= (1 << LAT_TILE_LOG) &&
+           (long long)V * padded_len(2 << l2cap) * 16 <= LAT_MID_SMEM)
+        ++l2cap;
+    int l2 = std::min(l2cap, std::max(g.lt - LAT_TILE_LOG, (g.lt + 1) / 2));
+    const int l1 = g.lt - l2;
+    if (l2 < 1 || l1 < 1 || l1 > LAT_TILE_LOG) return false;
+    g.l1 = l1;
+    g.l2 = l2;
+    g.lc = std::min(LAT_TILE_LOG - l1, l2);
+    g.nblk_col = (1 << l2) >> g.lc;
+    return true;
+}
+
+Geo LatGeo::slot_geo() const {
+    Geo s{};
+    s.m = m;
+    s.lt = lt;
+    s.two = 1;
+    s.l1 = l1;
+    s.l2 = l2;
+    s.cap = std::max(l1, l2);
+    s.C = 1 << (s.cap - l1);
+    return s;
+}
+
+// ------------------------------------------------------------------ generator on the fly
+// Lattice coordinate of real DFT-order index i against the class offset (lattice_word in
+// generator.cuh, ld_sequences.cpp:31-53): with off = oh 2^(53-m) + olo (olo < 2^(53-m)),
+//   D = ((i g + oh) mod 2^m) 2^(53-m) + olo,   x = D 2^-53 = t 2^-m + olo 2^-53  (exact in fp64),
+// so the 64-bit multiply / shift / mask chain becomes one 32-bit IMAD + LOP and one DFMA.
+// u = min(x, 1 - x) is exact and equals the reference's min(D, 2^53 - D) 2^-53 (kernels.cpp:28-32).
+template <int DC>
+struct LatGen {
+    uint32_t gm[DC], oh[DC];
+    double ol[DC], eta[DC];
+    double gam, inv_n;
+    uint32_t mask;
+    int d;
+    __device__ __forceinline__ void init(const LatArgs& a, int c, int o) {
+        d = a.d;
+        mask = (a.m >= 32) ? 0xffffffffu : ((1u << a.m) - 1u);
+        inv_n = pow2i(-a.m);
+        gam = __ldg(a.gamma + c);
+        const int sh = DIGITAL_BITS - a.m;
+#pragma unroll
+        for (int j = 0; j < DC; ++j) {
+            if (j < d) {
+                const uint64_t off = __ldg(a.cofs + size_t(o) * MAXD + j) & MASK53;
+                gm[j] = uint32_t(__ldg(a.g + j)) & mask;
+                oh[j] = uint32_t(off >> sh) & mask;
+                ol[j] = double(off & ((uint64_t(1) << sh) - 1)) * 0x1p-53;
+                eta[j] = __ldg(a.eta + size_t(c) * d + j);
+            } else {
+                gm[j] = oh[j] = 0u;
+                ol[j] = eta[j] = 0.0;
+            }
+        }
+    }
+};
+
+template <int ALPHA>
+__device__ __forceinline__ double lat_kappa(uint32_t t, double inv_n, double ol) {
+    const double x = fma(double(t), inv_n, ol);
+    const double u = fmin(x, 1.0 - x);
+    constexpr double pi2 = 9.869604401089358618834491;
+    if constexpr (ALPHA == 1) return 2.0 * pi2 * (u * (u - 1.0) + 1.0 / 6.0);
+    const double b4 = ((u - 2.0) * u + 1.0) * u * u - 1.0 / 30.0;
+    return -(2.0 / 3.0) * pi2 * pi2 * b4;
+}
+
+// q(i) = gamma prod_j (1 + eta_j kappa_j)  (SpatialKernel, kernels.cpp:91-103)
+template <int DC, int ALPHA>
+__device__ __forceinline__ double lat_q(const LatGen<DC>& G, uint32_t i) {
+    double prod = G.gam;
+#pragma unroll
+    for (int j = 0; j < DC; ++j)
+        if (j < G.d) {
+            const double k = lat_kappa<ALPHA>((i * G.gm[j] + G.oh[j]) & G.mask, G.inv_n, G.ol[j]);
+            prod *= 1.0 + G.eta[j] * k;
+        }
+    return prod;
+}
+
+// acc_j += W dq/deta_j (prefix / suffix products: 1 + eta kappa may vanish)
+template <int DC, int ALPHA>
+__device__ __forceinline__ void lat_dq_acc(const LatGen<DC>& G, uint32_t i, double W, double* acc) {
+    double kap[DC], f[DC];
+#pragma unroll
+    for (int j = 0; j < DC; ++j)
+        if (j < G.d) {
+            kap[j] = lat_kappa<ALPHA>((i * G.gm[j] + G.oh[j]) & G.mask, G.inv_n, G.ol[j]);
+            f[j] = 1.0 + G.eta[j] * kap[j];
+        }
+    double pre = G.gam * W;
+    double dq[DC];
+#pragma unroll
+    for (int j = 0; j < DC; ++j)
+        if (j < G.d) {
+            dq[j] = pre * kap[j];
+            pre *= f[j];
+        }
+    double suf = 1.0;
+#pragma unroll
+    for (int j = DC - 1; j >= 0; --j)
+        if (j < G.d) {
+            acc[j] = fma(dq[j], suf, acc[j]);
+            suf *= f[j];
+        }
+}
+
+// ------------------------------------------------------------------ L1: generator x column FFT
+template <int NT, int DC, int ALPHA>
+__global__ void __launch_bounds__(NT) k_lat_col_fwd(LatArgs a, int l1, int l2, int lc) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double2* sm = reinterpret_cast<double2*>(smraw);
+    constexpr auto S = sidx<true>;
+    const int v = blockIdx.y, c = v / a.V, o = v - c * a.V;
+    const int C = 1 << lc, N1 = 1 << l1, ld = padded_len(N1), tile = C << l1;
+    const uint32_t c0 = uint32_t(blockIdx.x) << lc;
+    LatGen<DC> G;
+    G.init(a, c, o);
+    for (int e = threadIdx.x; e < tile; e += NT) {
+        const int j1 = e >> lc, cc = e & (C - 1);
+        const uint32_t j = (uint32_t(j1) << l2) + c0 + uint32_t(cc);
+        sm[cc * ld + S(j1)] = make_double2(lat_q<DC, ALPHA>(G, 2u * j), lat_q<DC, ALPHA>(G, 2u * j + 1u));
+    }
+    pdl_trigger();
+    // zero the per-fit flags once per fit (L2 / L3 run after this kernel)
+    if (blockIdx.x == 0 && blockIdx.y == 0) {
+        for (int t = threadIdx.x; t < a.nc; t += NT) a.bad[t] = 0x7f7f7f7f;
+        for (int t = threadIdx.x; t < a.nc * MAXT * 2; t += NT) a.imre[t] = 0ull;
+    }
+    __syncthreads();
+    smem_fft<NT, true>(sm, l1, C, ld, -1, a.tw);
+    double2* out = a.Y + size_t(v) * a.half;
+    const int lt = l1 + l2;
+    for (int e = threadIdx.x; e < tile; e += NT) {
+        const int k1 = e >> lc, cc = e & (C - 1);
+        const uint64_t j2 = c0 + uint32_t(cc);
+        out[((long long)k1 << l2) + j2] = cmul(sm[cc * ld + S(k1)], twiddle(a.tw, j2 * uint64_t(k1), lt));
+    }
+}
+
+// ------------------------------------------------------------------ L2: row FFT + solve + inverse row FFT
+__device__ __forceinline__ int lat_row_of(int q, int rank, int N1) {
+    if (q == 0) return rank == 0 ? 0 : N1 / 2;
+    return rank == 0 ? q : N1 - q;
+}
+
+template <int NT, int T>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArgs a, int l1, int l2) {
+    constexpr int P = T * (T + 1) / 2;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double2* sm = reinterpret_cast<double2*>(smraw);  // [V][padded N2]
+    constexpr auto S = sidx<true>;
+    __shared__ double s_coef[P], s_xi[P], s_wR[P];
+    __shared__ int s_cls[P];
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = int(cl.block_rank());
+    const int q = blockIdx.x >> 1, c = blockIdx.y, V = a.V;
+    const int N1 = 1 << l1, N2 = 1 << l2, lds = padded_len(N2), lt = l1 + l2;
+    const int row = lat_row_of(q, rank, N1);
+    const long long half = a.half;
+    double2* Yc = a.Y + size_t(c) * V * half;
+    const double2* yh = a.yhat;
+    // prologue independent of L1 (overlaps its tail under programmatic dependent launch)
+    if (threadIdx.x < P) {
+        const int p = threadIdx.x;
+        s_coef[p] = __ldg(a.coef + size_t(c) * P + p);
+        s_xi[p] = __ldg(a.xi + size_t(c) * P + p);
+        s_wR[p] = (a.pair_a[p] == a.pair_b[p] ? 1.0 : 2.0) * __ldg(a.Rpair + size_t(c) * P + p);
+        s_cls[p] = a.pair_ofs[p];
+    }
+    pdl_wait();
+    pdl_trigger();
+    for (int e = threadIdx.x; e < (V << l2); e += NT) {
+        const int oo = e >> l2, k2 = e & (N2 - 1);
+        cp_async16(&sm[oo * lds + S(k2)], &Yc[size_t(oo) * half + ((long long)row << l2) + k2]);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    smem_fft<NT, true>(sm, l2, V, lds, -1, a.tw);
+    cl.sync();  // both rows transformed: partner rows readable over DSMEM
+
+    // frequency pairs (k, N' - k): one thread owns both slots (reads, solves, writes back)
+    const bool selfrow = q == 0;  // rows 0 and N1/2 pair with themselves
+    double2* rem = cl.map_shared_rank(sm, rank ^ 1);
+    const int rowA = selfrow ? row : q, rowB = selfrow ? row : N1 - q;
+    double2* bufA = (selfrow || rank == 0) ? sm : rem;
+    double2* bufB = (selfrow || rank == 1) ? sm : rem;
+    int p0, p1;
+    if (selfrow) {
+        p0 = 0;
+        p1 = rank == 0 ? N2 / 2 + 1 : N2 / 2;
+    } else {
+        p0 = rank * (N2 / 2);
+        p1 = p0 + N2 / 2;
+    }
+    const bool grad = a.want_grad != 0;
+    double acc[2 + P];
+#pragma unroll
+    for (int x = 0; x < 2 + P; ++x) acc[x] = 0.0;
+    double imx[T], rex[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) imx[t] = rex[t] = 0.0;
+    long long first_bad = 0x7f7f7f7fll;
+#pragma unroll 1
+    for (int p = p0 + int(threadIdx.x); p < p1; p += NT) {
+        const int k2a = p;
+        const int k2b = selfrow ? (rank == 0 ? ((N2 - p) & (N2 - 1)) : (N2 - 1 - p)) : (N2 - 1 - p);
+        const long long kA = rowA + ((long long)k2a << l1);
+        const long long slA = ((long long)rowA << l2) + k2a, slB = ((long long)rowB << l2) + k2b;
+        if (kA == 0) {
+            // packed slot 0: frequency 0 (.x) and Nyquist (.y), two real systems; tau zeroes the
+            // frequency-0 residual (gp_core.cpp:67-88) — k_solve_class's p == 0 branch
+            double H0[P], HN[P], A0[P], AN[P], r0[T], rN[T], c0v[T], cN[T], I0[P], IN[P], l0, lN, q0, qN;
+#pragma unroll
+            for (int x = 0; x < P; ++x) {
+                const double2 z = sm[s_cls[x] * lds + S(0)];
+                H0[x] = z.x + z.y;
+                HN[x] = z.x - z.y;
+                A0[x] = fma(s_coef[x], H0[x], s_xi[x]);
+                AN[x] = fma(s_coef[x], HN[x], s_xi[x]);
+            }
+#pragma unroll
+            for (int t = 0; t < T; ++t) r0[t] = 0.0, rN[t] = yh[size_t(t) * half].y;
+            const int st0 = ldl_solve<T, false>(A0, r0, grad, l0, q0, c0v, I0, imx, rex);
+            const int stN = ldl_solve<T, false>(AN, rN, grad, lN, qN, cN, IN, imx, rex);
+            if (st0 == 1 || stN == 1) first_bad = 0;
+            acc[0] += l0 + lN;
+            acc[1] += q0 + qN;
+            if (grad) {
+                double M0[P], MN[P];
+                int x = 0;
+#pragma unroll
+                for (int i = 0; i < T; ++i)
+#pragma unroll
+                    for (int j = i; j < T; ++j, ++x) {
+                        M0[x] = I0[x] - c0v[i] * c0v[j];
+                        MN[x] = IN[x] - cN[i] * cN[j];
+                    }
+#pragma unroll
+                for (int y = 0; y < P; ++y) acc[2 + y] += M0[y] * H0[y] + MN[y] * HN[y];
+#pragma unroll
+                for (int o = 0; o < P; ++o) {
+                    if (o >= V) break;
+                    double z0 = 0.0, zN = 0.0;
+#pragma unroll
+                    for (int y = 0; y < P; ++y)
+                        if (s_cls[y] == o) z0 = fma(s_wR[y], M0[y], z0), zN = fma(s_wR[y], MN[y], zN);
+                    sm[o * lds + S(0)] = make_double2(0.5 * (z0 + zN), 0.5 * (z0 - zN));  // inverse pre, k = 0
+                }
+            }
+            continue;
+        }
+        const bool self = slA == slB;  // k = N'/2 (row 0, k2 = N2/2)
+        const double2 wA = twiddle(a.tw, uint64_t(kA), a.m);
+        const double2 wB = make_double2(-wA.x, wA.y);  // exp(-2 pi i (N' - k)/n) = -conj(wA)
+        double2 HA[P], HB[P];
+#pragma unroll
+        for (int x = 0; x < P; ++x) {
+            const int o = s_cls[x];
+            const double2 za = bufA[o * lds + S(k2a)], zb = bufB[o * lds + S(k2b)];
+            HA[x] = r2c_post(za, zb, wA);
+            HB[x] = r2c_post(zb, za, wB);
+        }
+        double2 ZA[P], ZB[P];
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+            if (side == 1 && self) break;
+            const double2* H = side == 0 ? HA : HB;
+            const long long sl = side == 0 ? slA : slB;
+            double2 A[P], r[T], ch[T], Ai[P];
+#pragma unroll
+            for (int x = 0; x < P; ++x) A[x] = make_double2(fma(s_coef[x], H[x].x, s_xi[x]), s_coef[x] * H[x].y);
+#pragma unroll
+            for (int t = 0; t < T; ++t) r[t] = yh[size_t(t) * half + sl];
+            double ld, qd;
+            const int st = ldl_solve<T, true>(A, r, grad, ld, qd, ch, Ai, imx, rex);
+            if (st == 1 && sl < first_bad) first_bad = sl;
+            acc[0] += 2.0 * ld;  // slot k >= 1 stands for frequencies k and n - k
+            acc[1] += 2.0 * qd;
+            if (grad) {
+                double2 Mq[P];
+                int x = 0;
+#pragma unroll
+                for (int i = 0; i < T; ++i)
+#pragma unroll
+                    for (int j = i; j < T; ++j, ++x) Mq[x] = csub(Ai[x], cmulc(ch[i], ch[j]));
+#pragma unroll
+                for (int y = 0; y < P; ++y) acc[2 + y] += 2.0 * (Mq[y].x * H[y].x + Mq[y].y * H[y].y);
+#pragma unroll
+                for (int o = 0; o < P; ++o) {
+                    double2 z = make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int y = 0; y < P; ++y)
+                        if (s_cls[y] == o) z = make_double2(fma(s_wR[y], Mq[y].x, z.x), fma(s_wR[y], Mq[y].y, z.y));
+                    if (side == 0) ZA[o] = z;
+                    else ZB[o] = z;
+                }
+            }
+        }
+        if (grad) {
+            // inverse real-FFT pre-processing of the class adjoints, written back in place
+#pragma unroll
+            for (int o = 0; o < P; ++o) {
+                if (o >= V) break;
+                if (self) {
+                    bufA[o * lds + S(k2a)] = c2r_pre(ZA[o], ZA[o], wA);
+                } else {
+                    bufA[o * lds + S(k2a)] = c2r_pre(ZA[o], ZB[o], wA);
+                    bufB[o * lds + S(k2b)] = c2r_pre(ZB[o], ZA[o], wB);
+                }
+            }
+        }
+    }
+    cl.sync();  // every DSMEM access of the cluster is done
+
+    __shared__ double redv[(NT / 32) * (2 + P)];
+    block_sum_vec<NT, 2 + P>(acc, redv);
+    if (threadIdx.x == 0) {
+        double* pm = a.part_mid + (size_t(c) * N1 + blockIdx.x) * (2 + P);
+#pragma unroll
+        for (int x = 0; x < 2 + P; ++x) pm[x] = acc[x];
+    }
+    if (first_bad != 0x7f7f7f7fll) atomicMin(a.bad + c, int(first_bad));
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+        double vi = imx[t], vr = rex[t];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            vi = fmax(vi, __shfl_xor_sync(0xffffffffu, vi, o));
+            vr = fmax(vr, __shfl_xor_sync(0xffffffffu, vr, o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicMax(a.imre + ((size_t)c * MAXT + t) * 2 + 0, (unsigned long long)__double_as_longlong(vi));
+            atomicMax(a.imre + ((size_t)c * MAXT + t) * 2 + 1, (unsigned long long)__double_as_longlong(vr));
+        }
+    }
+    if (!grad) return;
+    smem_fft<NT, true>(sm, l2, V, lds, +1, a.tw);  // block_sum_vec's barriers ordered the writes
+    for (int e = threadIdx.x; e < (V << l2); e += NT) {
+        const int oo = e >> l2, j2 = e & (N2 - 1);
+        Yc[size_t(oo) * half + ((long long)row << l2) + j2] =
+            cmulc(sm[oo * lds + S(j2)], twiddle(a.tw, uint64_t(j2) * uint64_t(row), lt));
+    }
+}
+
+// ------------------------------------------------------------------ L3: inverse column FFT -> gradient dot
+template <int NT, int DC, int ALPHA>
+__global__ void __launch_bounds__(NT) k_lat_col_inv(LatArgs a, int l1, int l2, int lc) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double2* sm = reinterpret_cast<double2*>(smraw);
+    constexpr auto S = sidx<true>;
+    __shared__ int s_last;
+    const int v = blockIdx.y, c = v / a.V, o = v - c * a.V;
+    const int C = 1 << lc, N1 = 1 << l1, ld = padded_len(N1), tile = C << l1;
+    const uint32_t c0 = uint32_t(blockIdx.x) << lc;
+    LatGen<DC> G;
+    G.init(a, c, o);  // independent of L2: overlaps its tail
+    pdl_wait();
+    const double2* x = a.Y + size_t(v) * a.half;
+    for (int e = threadIdx.x; e < tile; e += NT) {
+        const int k1 = e >> lc, cc = e & (C - 1);
+        cp_async16(&sm[cc * ld + S(k1)], &x[((long long)k1 << l2) + c0 + cc]);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    smem_fft<NT, true>(sm, l1, C, ld, +1, a.tw);
+    double acc[DC];
+#pragma unroll
+    for (int j = 0; j < DC; ++j) acc[j] = 0.0;
+    for (int e = threadIdx.x; e < tile; e += NT) {
+        const int j1 = e >> lc, cc = e & (C - 1);
+        const uint32_t j = (uint32_t(j1) << l2) + c0 + uint32_t(cc);
+        const double2 z = sm[cc * ld + S(j1)];  // W(2j) = 2 Re z, W(2j+1) = 2 Im z
+        lat_dq_acc<DC, ALPHA>(G, 2u * j, 2.0 * z.x, acc);
+        lat_dq_acc<DC, ALPHA>(G, 2u * j + 1u, 2.0 * z.y, acc);
+    }
+    const int nblk = gridDim.x;
+    __shared__ double redv[(NT / 32) * DC];
+    block_sum_vec<NT, DC>(acc, redv);
+    if (threadIdx.x == 0) {
+        double* out = a.part_dot + (size_t(v) * nblk + blockIdx.x) * (MAXD + 1);
+#pragma unroll
+        for (int j = 0; j < DC; ++j)
+            if (j < a.d) out[j] = acc[j];
+    }
+    // last-CTA reduction (one acq_rel ticket per candidate over its V * nblk CTAs), fixed order
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned ticket = atom_add_acq_rel_gpu(a.counter + c, 1u);
+        s_last = ticket == unsigned(a.V * nblk) - 1;
+        if (s_last) a.counter[c] = 0;  // self-reset for the next replay
+    }
+    __syncthreads();
+    if (!s_last) return;
+    ClassSums t{};
+    t.P = a.P;
+    t.V = a.V;
+    t.d = a.d;
+    t.nrows = N1;  // L2 CTAs per candidate
+    t.nblk = nblk;
+    t.dstride = MAXD + 1;
+    t.mid = a.part_mid + size_t(c) * t.nrows * (2 + a.P);
+    t.dot = a.part_dot + size_t(c) * a.V * nblk * (MAXD + 1);
+    t.pair_a = a.pair_a;
+    t.pair_b = a.pair_b;
+    t.Rpair = a.Rpair + size_t(c) * a.P;
+    t.gamma = __ldg(a.gamma + c);
+    t.out = a.out + size_t(c) * NOUT;
+    class_sums_out<NT>(t);
+}
+
+// ------------------------------------------------------------------ launcher
+template <class K>
+static void set_smem_lat(K kern, size_t bytes) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+}
+
+template <int DC, int ALPHA>
+static void lat_cols(const LatGeo& g, const LatArgs& a, size_t sm_col, bool inverse, cudaStream_t s) {
+    const dim3 grid(g.nblk_col, a.V * a.nc);
+    if (!inverse) {
+        auto k = k_lat_col_fwd<LAT_NT, DC, ALPHA>;
+        set_smem_lat(k, sm_col);
+        ProfScope ps("lat_col_fwd", s);
+        k<<<grid, LAT_NT, sm_col, s>>>(a, g.l1, g.l2, g.lc);
+    } else {
+        auto k = k_lat_col_inv<LAT_NT, DC, ALPHA>;
+        set_smem_lat(k, sm_col);
+        ProfScope ps("lat_col_inv", s);
+        CK_LAUNCH(launch_pdl(k, grid, dim3(LAT_NT), sm_col, s, true, a, g.l1, g.l2, g.lc));
+    }
+}
+
+template <int ALPHA>
+static void lat_cols_d(const LatGeo& g, const LatArgs& a, size_t sm_col, bool inverse, cudaStream_t s) {
+    if (a.d <= 4) lat_cols<4, ALPHA>(g, a, sm_col, inverse, s);
+    else if (a.d <= 8) lat_cols<8, ALPHA>(g, a, sm_col, inverse, s);
+    else lat_cols<16, ALPHA>(g, a, sm_col, inverse, s);
+}
+
+template <int T>
+static void lat_mid_launch(const LatGeo& g, const LatArgs& a, cudaStream_t s) {
+    const size_t sm = size_t(a.V) * padded_len(1 << g.l2) * sizeof(double2);
+    auto k = k_lat_mid<LAT_NT, T>;
+    set_smem_lat(k, sm);
+    ProfScope ps("lat_mid", s);
+    CK_LAUNCH(launch_pdl(k, dim3(1u << g.l1, a.nc), dim3(LAT_NT), sm, s, true, a, g.l1, g.l2));
+}
+
+void lat_fit(const LatGeo& g, const LatArgs& a, cudaStream_t s) {
+    const size_t sm_col = size_t(1 << g.lc) * padded_len(1 << g.l1) * sizeof(double2);
+    if (a.si_alpha == 1) lat_cols_d<1>(g, a, sm_col, false, s);
+    else lat_cols_d<2>(g, a, sm_col, false, s);
+    switch (a.T) {
+        case 1: lat_mid_launch<1>(g, a, s); break;
+        case 2: lat_mid_launch<2>(g, a, s); break;
+        case 3: lat_mid_launch<3>(g, a, s); break;
+        default: lat_mid_launch<4>(g, a, s); break;
+    }
+    if (!a.want_grad) return;
+    if (a.si_alpha == 1) lat_cols_d<1>(g, a, sm_col, true, s);
+    else lat_cols_d<2>(g, a, sm_col, true, s);
+}
+
+}  // namespace fmtgp

@@ -1,0 +1,64 @@
+// Equal-n rank-1-lattice (SI / real FFT) fit in three fused kernels — the configuration-4 hot path.
+//
+//   L1 k_lat_col_fwd : generator q_o(2j), q_o(2j+1) on the fly (32-bit lattice arithmetic, exact)
+//                      packed as z(j) = q(2j) + i q(2j+1) x column FFT x four-step twiddle, one
+//                      vector per pair-offset CLASS o (all diagonal pairs share offset 0)
+//   L2 k_lat_mid     : 2-CTA cluster owning the Hermitian partner rows (r, N1 - r): row FFT of every
+//                      class, real-FFT post-processing of each frequency PAIR (k, N' - k) by one
+//                      thread (own + partner smem over DSMEM), per-frequency T x T LDL^H solve
+//                      (logdet, quad, M = Lam^-1 - chat chat^H, Parseval dR partials, class adjoints
+//                      Z_o), inverse pre-processing written back in place, inverse row FFT
+//   L3 k_lat_col_inv : inverse column FFT -> W -> dot with dq_o/deta (generator on the fly) ->
+//                      partials; the last CTA reduces everything into the result record
+//
+// The arithmetic per frequency is k_solve_class's (kernels.cu) and the transforms are the
+// generic two-pass ones (passes.cuh) — what changes is that the spectra, the adjoints and the
+// solve never make an HBM round trip between them: per fit the path moves 8n'(V (2 + 2) + T)
+// bytes (n' = n/2 complex slots) instead of the generic path's 8n'(V (6 + 2) + 2T + ...).
+// Reference: fast_gram.cpp:42-89 (build_spectrum), :151-263 (invert_and_logdet, equal n),
+// gp_core.cpp:92-141 + 197-227 (refresh / loss_value), gradient as in DESIGN.md §4.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace fmtgp {
+
+struct LatGeo {
+    int m, lt;       // n = 2^m real points, n' = 2^lt = n/2 complex slots
+    int l1, l2;      // n' = N1 (rows of L2) * N2 (row length); slot of frequency k1 + N1 k2 = k1 N2 + k2
+    int lc;          // log2 columns per L1/L3 CTA (tile 2^(l1 + lc) <= 2^13)
+    int nblk_col;    // L1/L3 CTAs per vector
+    static bool make(int m, int V, int T, int d, LatGeo& g);
+    // the generic-kernel geometry with the same slot layout (yhat, coefficients, seam calls)
+    Geo slot_geo() const;
+};
+
+struct LatArgs {
+    int T, P, V, d, nc, m;
+    long long half;           // n' slots per vector
+    int si_alpha;
+    const uint64_t* g;        // [d] generating vector
+    const uint64_t* cofs;     // [V][MAXD] class offsets (53-bit, Delta_a - Delta_b)
+    const int* pair_ofs;      // [P] pair -> class
+    const double* eta;        // [nc][d]
+    const double* gamma;      // [nc]
+    const double* coef;       // [nc][P]  R_ab
+    const double* xi;         // [nc][P]
+    const double* Rpair;      // [nc][P]
+    const int* pair_a;
+    const int* pair_b;
+    const double2* yhat;      // [T][n'] slot layout
+    double2* Y;               // [nc][V][n'] intermediate
+    double* part_mid;         // [nc][N1][2 + P]
+    double* part_dot;         // [nc][V][nblk_col][MAXD + 1]
+    int* bad;                 // [nc]
+    unsigned long long* imre; // [nc][MAXT][2]
+    unsigned int* counter;    // [nc] last-CTA tickets (self-resetting)
+    double* out;              // [nc][NOUT]
+    const double2* tw;
+    int want_grad;
+};
+
+void lat_fit(const LatGeo& g, const LatArgs& a, cudaStream_t s);
+
+}  // namespace fmtgp

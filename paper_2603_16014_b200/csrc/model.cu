@@ -21,6 +21,7 @@
 #include "../../include/fastmtgp_b200.h"
 #include "kernels.cuh"
 #include "digital.cuh"
+#include "lattice.cuh"
 #include "fold.cuh"
 #include "posterior.cuh"
 #include "unequal.cuh"
@@ -316,6 +317,9 @@ struct fmtgp_model {
     uint64_t* d_ofs = nullptr;  // distinct pair offsets [nofs][MAXD]
     int nofs = 0;
     double* d_kap = nullptr;    // design-time kappa table [nofs][d][n]
+    // fused three-kernel lattice path (lattice.cuh); shares part_mid / part_dot / counter
+    bool lat = false;
+    LatGeo lgeo{};
     double kap_b[4]{};
     bool kap_valid = false;
     bool kap_enabled = true;
@@ -622,6 +626,61 @@ void eval_digital_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, b
     CK(cudaMemcpyAsync(M->h_res, M->d_res, sizeof(double) * M->res_len, cudaMemcpyDeviceToHost, M->st));
 }
 
+// Fused lattice fit (lattice.cuh): three kernels, spectra and adjoints never leave the SMs /
+// L2 between the row FFT, the solve and the inverse row FFT.
+void eval_lattice_body(fmtgp_model* M, int nc, int si_alpha, bool grad) {
+    copy_hyper(M);  // failure flags are zeroed by the first kernel
+    const Group& g = M->groups[0];
+    LatArgs a{};
+    a.T = M->T;
+    a.P = M->P;
+    a.V = M->nofs;
+    a.d = M->d;
+    a.nc = nc;
+    a.m = M->m[0];
+    a.half = M->pslots[0];
+    a.si_alpha = si_alpha;
+    a.g = M->d_g;
+    a.cofs = M->d_ofs;
+    a.pair_ofs = M->d_pair_ofs;
+    a.eta = M->d_eta;
+    a.gamma = M->d_gamma;
+    a.coef = g.d_coef;
+    a.xi = g.d_xi;
+    a.Rpair = M->d_Rpair;
+    a.pair_a = M->d_pa;
+    a.pair_b = M->d_pb;
+    a.yhat = static_cast<const double2*>(M->d_yhat);
+    a.Y = static_cast<double2*>(M->d_work);
+    a.part_mid = M->d_part_mid;
+    a.part_dot = M->d_part_dot;
+    a.bad = M->d_bad;
+    a.imre = M->d_imre;
+    a.counter = M->d_counter;
+    a.out = M->d_out;
+    a.tw = M->tw;
+    a.want_grad = grad;
+    lat_fit(M->lgeo, a, M->st);
+    CK(cudaGetLastError());
+    if (!grad) {
+        FinalArgs fa{};
+        fa.T = M->T;
+        fa.P = M->P;
+        fa.d = M->d;
+        fa.ncand = nc;
+        fa.nblk_solve = 1 << M->lgeo.l1;
+        fa.solve_partial = M->d_part_mid;
+        fa.solve_stride = 2 + M->P;
+        fa.Rpair = M->d_Rpair;
+        fa.gamma = M->d_gamma;
+        fa.pair_a = M->d_pa;
+        fa.pair_b = M->d_pb;
+        fa.out = M->d_out;
+        finalize(fa, M->st);
+    }
+    CK(cudaMemcpyAsync(M->h_res, M->d_res, sizeof(double) * M->res_len, cudaMemcpyDeviceToHost, M->st));
+}
+
 // The design-time kappa table depends on the design and the Walsh order weights only
 // (not on gamma, eta, R, xi): rebuilt when b changes, outside any captured graph.
 void ensure_kappa_table(fmtgp_model* M, int si_alpha, const double* bw) {
@@ -641,6 +700,10 @@ void ensure_kappa_table(fmtgp_model* M, int si_alpha, const double* bw) {
 void eval_equal_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, bool grad, bool keep_chat) {
     if (M->dig) {
         eval_digital_body(M, nc, si_alpha, bw, grad, keep_chat);
+        return;
+    }
+    if (M->lat && !keep_chat) {
+        eval_lattice_body(M, nc, si_alpha, grad);
         return;
     }
     copy_hyper(M);
@@ -967,6 +1030,25 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
         M->d_pb = dalloc<int>(M->P);
         CK(cudaMemcpy(M->d_pa, M->pa.data(), M->P * sizeof(int), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(M->d_pb, M->pb.data(), M->P * sizeof(int), cudaMemcpyHostToDevice));
+        // distinct pair offsets (diagonal pairs share offset 0): the transforms run per class
+        std::vector<int> pofs(M->P);
+        std::vector<uint64_t> uniq;
+        for (int p = 0; p < M->P; ++p) {
+            int found = -1;
+            for (int o = 0; o < M->nofs; ++o)
+                if (std::equal(offs.begin() + size_t(p) * MAXD, offs.begin() + size_t(p + 1) * MAXD,
+                               uniq.begin() + size_t(o) * MAXD))
+                    found = o;
+            if (found < 0) {
+                uniq.insert(uniq.end(), offs.begin() + size_t(p) * MAXD, offs.begin() + size_t(p + 1) * MAXD);
+                found = M->nofs++;
+            }
+            pofs[p] = found;
+        }
+        M->d_pair_ofs = dalloc<int>(M->P);
+        M->d_ofs = dalloc<uint64_t>(uniq.size());
+        CK(cudaMemcpy(M->d_pair_ofs, pofs.data(), M->P * sizeof(int), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(M->d_ofs, uniq.data(), uniq.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
         // transform geometry per length: tiles sized from all vectors of that length
         {
             long long tot[28] = {0};
@@ -977,6 +1059,13 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
             }
             for (int mm = 0; mm < 28; ++mm) M->geo_m[mm] = Geo::make(mm, M->lattice, tot[mm]);
             M->split = all <= (1ll << 22);
+            // fused lattice path: its row split becomes the slot layout of every vector of that length
+            const char* lf = std::getenv("FMTGP_LAT_FUSED");
+            if (M->equal && M->lattice && M->class_mode && !(lf && lf[0] == '0') &&
+                LatGeo::make(M->m[0], M->nofs, M->T, M->d, M->lgeo)) {
+                M->lat = true;
+                M->geo_m[M->m[0]] = M->lgeo.slot_geo();
+            }
         }
         // groups of pairs by generating-task length
         size_t work = 0;
@@ -1056,25 +1145,6 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
         M->d_lam = dalloc<char>(size_t(max_cand) * M->total_slots * es);
         M->d_laminv = dalloc<char>(size_t(M->total_slots) * es);
         M->d_chat = dalloc<char>(size_t(M->task_slots) * es);
-        // distinct pair offsets (diagonal pairs share offset 0): the transforms run per class
-        std::vector<int> pofs(M->P);
-        std::vector<uint64_t> uniq;
-        for (int p = 0; p < M->P; ++p) {
-            int found = -1;
-            for (int o = 0; o < M->nofs; ++o)
-                if (std::equal(offs.begin() + size_t(p) * MAXD, offs.begin() + size_t(p + 1) * MAXD,
-                               uniq.begin() + size_t(o) * MAXD))
-                    found = o;
-            if (found < 0) {
-                uniq.insert(uniq.end(), offs.begin() + size_t(p) * MAXD, offs.begin() + size_t(p + 1) * MAXD);
-                found = M->nofs++;
-            }
-            pofs[p] = found;
-        }
-        M->d_pair_ofs = dalloc<int>(M->P);
-        M->d_ofs = dalloc<uint64_t>(uniq.size());
-        CK(cudaMemcpy(M->d_pair_ofs, pofs.data(), M->P * sizeof(int), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(M->d_ofs, uniq.data(), uniq.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
         {
             std::vector<int> iota(M->P);
             std::vector<long long> cvo(M->P);
@@ -1099,6 +1169,13 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
             M->d_vec_sum = dalloc<double>(size_t(max_cand) * M->nofs * (MAXD + 1));
             const size_t kbytes = size_t(M->nofs) * M->d * (size_t(1) << M->m[0]) * sizeof(double);
             if (kbytes <= (size_t(1) << 30)) M->d_kap = dalloc<double>(kbytes / sizeof(double));
+        }
+        if (M->lat) {
+            const LatGeo& g = M->lgeo;
+            M->d_part_mid = dalloc<double>(size_t(max_cand) * (size_t(1) << g.l1) * (2 + M->P));
+            M->d_part_dot = dalloc<double>(size_t(max_cand) * M->nofs * g.nblk_col * (MAXD + 1));
+            M->d_counter = dalloc<unsigned int>(size_t(max_cand) * (1 + M->nofs));
+            CK(cudaMemset(M->d_counter, 0, sizeof(unsigned int) * max_cand * (1 + M->nofs)));
         }
         if (M->equal) {
             M->d_M = dalloc<char>(size_t(max_cand) * M->total_slots * es);
