@@ -183,6 +183,8 @@ __global__ void __launch_bounds__(NT) k_dig_mid(DigArgs a, int l2) {
 #pragma unroll
     for (int t = 0; t < T; ++t) imx[t] = rex[t] = 0.0;
     int first_bad = 0x7f7f7f7f;
+    double lpm = 1.0;  // running pivot product lpm * 2^lpe: one log per thread (ldl_core)
+    int lpe = 0;
 #pragma unroll 1
     for (int u = 0, k2 = threadIdx.x; k2 < N2; ++u, k2 += NT) {
         const long long k = base + k2;
@@ -201,10 +203,9 @@ __global__ void __launch_bounds__(NT) k_dig_mid(DigArgs a, int l2) {
                 if (u == w) rv = rpre[w][t];
             r[t] = u < KPT ? rv : (k == 0 ? 0.0 : __ldg(a.yhat + size_t(t) * n + k));
         }
-        double ld, qd;
-        const int st = ldl_solve<T, false>(A, r, a.want_grad != 0, ld, qd, ch, Ai, imx, rex);
+        double qd;
+        const int st = ldl_core<T, false>(A, r, a.want_grad != 0, lpm, lpe, qd, ch, Ai, imx, rex);
         if (st == 1 && int(k) < first_bad) first_bad = int(k);
-        acc[0] += ld;
         acc[1] += qd;
         if (a.want_grad) {
             double Mq[P];
@@ -224,6 +225,7 @@ __global__ void __launch_bounds__(NT) k_dig_mid(DigArgs a, int l2) {
             for (int t = 0; t < T; ++t) a.chat_out[size_t(t) * n + k] = ch[t];
         }
     }
+    acc[0] = log_of(lpm, lpe);
     __shared__ double redv[(NT / 32) * (2 + P)];
     block_sum_vec<NT, 2 + P>(acc, redv);
     const int nrows = gridDim.x;
@@ -248,7 +250,6 @@ template <int NT, int D>
 __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2, int lc, int nrows) {
     extern __shared__ __align__(16) double sm[];
     __shared__ GenSmem<D> tab;
-    __shared__ double red[32];
     __shared__ int s_last;
     const int v = blockIdx.y, c = v / a.V, o = v - c * a.V;
     const int C = 1 << lc, N1 = 1 << l1, ld = padded_len(N1);

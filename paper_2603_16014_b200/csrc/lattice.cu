@@ -43,84 +43,100 @@ Geo LatGeo::slot_geo() const {
 // generator.cuh, ld_sequences.cpp:31-53): with off = oh 2^(53-m) + olo (olo < 2^(53-m)),
 //   D = ((i g + oh) mod 2^m) 2^(53-m) + olo,   x = D 2^-53 = t 2^-m + olo 2^-53  (exact in fp64),
 // so the 64-bit multiply / shift / mask chain becomes one 32-bit IMAD + LOP and one DFMA.
-// u = min(x, 1 - x) is exact and equals the reference's min(D, 2^53 - D) 2^-53 (kernels.cpp:28-32).
-template <int DC>
+// The Bernoulli kernels are polynomials in w = x^2 - x = -u (1 - u), symmetric under
+// u -> 1 - u, so the reference's symmetrisation u = min(x, 1 - x) (kernels.cpp:28-32) is implied:
+//   B2: kappa = 2 pi^2 (u^2 - u + 1/6)            = ka w + kb,       ka = 2 pi^2,      kb = pi^2 / 3
+//   B4: kappa = -(2/3) pi^4 (u^2 (u - 1)^2 - 1/30) = ka w^2 + kb,     ka = -(2/3) pi^4, kb = pi^4 / 45
+// and f = 1 + eta kappa = A + B v with v = w (B2) or w^2 (B4), A = 1 + eta kb, B = eta ka:
+// two DFMAs per dimension after x.  Dimensions are padded to the register cap DC with A = 1,
+// B = 0 (f = 1 exactly), so the unrolled loops carry no per-dimension predicates.
+template <int ALPHA>
+struct LatPoly {
+    static constexpr double pi2 = 9.869604401089358618834491;
+    static constexpr double ka = ALPHA == 1 ? 2.0 * pi2 : -(2.0 / 3.0) * pi2 * pi2;
+    static constexpr double kb = ALPHA == 1 ? pi2 / 3.0 : pi2 * pi2 / 45.0;
+};
+
+template <int DC, int ALPHA>
 struct LatGen {
     uint32_t gm[DC], oh[DC];
-    double ol[DC], eta[DC];
+    double ol[DC], A[DC], B[DC];
     double gam, inv_n;
     uint32_t mask;
-    int d;
     __device__ __forceinline__ void init(const LatArgs& a, int c, int o) {
-        d = a.d;
         mask = (a.m >= 32) ? 0xffffffffu : ((1u << a.m) - 1u);
         inv_n = pow2i(-a.m);
         gam = __ldg(a.gamma + c);
         const int sh = DIGITAL_BITS - a.m;
 #pragma unroll
         for (int j = 0; j < DC; ++j) {
-            if (j < d) {
+            if (j < a.d) {
                 const uint64_t off = __ldg(a.cofs + size_t(o) * MAXD + j) & MASK53;
+                const double eta = __ldg(a.eta + size_t(c) * a.d + j);
                 gm[j] = uint32_t(__ldg(a.g + j)) & mask;
                 oh[j] = uint32_t(off >> sh) & mask;
                 ol[j] = double(off & ((uint64_t(1) << sh) - 1)) * 0x1p-53;
-                eta[j] = __ldg(a.eta + size_t(c) * d + j);
+                A[j] = fma(eta, LatPoly<ALPHA>::kb, 1.0);
+                B[j] = eta * LatPoly<ALPHA>::ka;
             } else {
                 gm[j] = oh[j] = 0u;
-                ol[j] = eta[j] = 0.0;
+                ol[j] = B[j] = 0.0;
+                A[j] = 1.0;
             }
+        }
+    }
+    // v_j = w (B2) or w^2 (B4) of dimension j at real DFT-order index i
+    __device__ __forceinline__ double v(int j, uint32_t i) const {
+        const uint32_t t = (i * gm[j] + oh[j]) & mask;
+        const double x = fma(double(t), inv_n, ol[j]);
+        const double w = fma(x, x, -x);
+        return ALPHA == 1 ? w : w * w;
+    }
+    // q(i) = gamma prod_j (1 + eta_j kappa_j)  (SpatialKernel, kernels.cpp:91-103)
+    __device__ __forceinline__ double q(uint32_t i) const {
+        double prod = gam;
+#pragma unroll
+        for (int j = 0; j < DC; ++j) prod *= fma(B[j], v(j, i), A[j]);
+        return prod;
+    }
+    // acc_j += W dq/deta_j = W gamma kappa_j prod_{k != j} f_k  (prefix / suffix products: f may vanish)
+    __device__ __forceinline__ void dq_acc(uint32_t i, double W, double* acc) const {
+        double vv[DC], f[DC];
+#pragma unroll
+        for (int j = 0; j < DC; ++j) {
+            vv[j] = v(j, i);
+            f[j] = fma(B[j], vv[j], A[j]);
+        }
+        double pre = gam * W;
+        double dq[DC];
+#pragma unroll
+        for (int j = 0; j < DC; ++j) {
+            dq[j] = pre * fma(LatPoly<ALPHA>::ka, vv[j], LatPoly<ALPHA>::kb);
+            pre *= f[j];
+        }
+        double suf = 1.0;
+#pragma unroll
+        for (int j = DC - 1; j >= 0; --j) {
+            acc[j] = fma(dq[j], suf, acc[j]);
+            suf *= f[j];
         }
     }
 };
 
-template <int ALPHA>
-__device__ __forceinline__ double lat_kappa(uint32_t t, double inv_n, double ol) {
-    const double x = fma(double(t), inv_n, ol);
-    const double u = fmin(x, 1.0 - x);
-    constexpr double pi2 = 9.869604401089358618834491;
-    if constexpr (ALPHA == 1) return 2.0 * pi2 * (u * (u - 1.0) + 1.0 / 6.0);
-    const double b4 = ((u - 2.0) * u + 1.0) * u * u - 1.0 / 30.0;
-    return -(2.0 / 3.0) * pi2 * pi2 * b4;
-}
+// Four-step twiddles without per-element table reads: a thread's elements are u = 0, 1, ... NT
+// apart, so exp(-2 pi i j (t0 + u s) / 2^L) = base * step_u with base = w^(j t0) per thread and
+// step_u = w^(j s u) from a small per-CTA smem table — both exact table products (<= 2 ulp), all
+// loads issued at kernel start where the generator / FFT hides their latency.
+constexpr int LAT_STEPS = 16;  // elements per thread per vector (EPT at NT = 512)
 
-// q(i) = gamma prod_j (1 + eta_j kappa_j)  (SpatialKernel, kernels.cpp:91-103)
-template <int DC, int ALPHA>
-__device__ __forceinline__ double lat_q(const LatGen<DC>& G, uint32_t i) {
-    double prod = G.gam;
-#pragma unroll
-    for (int j = 0; j < DC; ++j)
-        if (j < G.d) {
-            const double k = lat_kappa<ALPHA>((i * G.gm[j] + G.oh[j]) & G.mask, G.inv_n, G.ol[j]);
-            prod *= 1.0 + G.eta[j] * k;
-        }
-    return prod;
-}
-
-// acc_j += W dq/deta_j (prefix / suffix products: 1 + eta kappa may vanish)
-template <int DC, int ALPHA>
-__device__ __forceinline__ void lat_dq_acc(const LatGen<DC>& G, uint32_t i, double W, double* acc) {
-    double kap[DC], f[DC];
-#pragma unroll
-    for (int j = 0; j < DC; ++j)
-        if (j < G.d) {
-            kap[j] = lat_kappa<ALPHA>((i * G.gm[j] + G.oh[j]) & G.mask, G.inv_n, G.ol[j]);
-            f[j] = 1.0 + G.eta[j] * kap[j];
-        }
-    double pre = G.gam * W;
-    double dq[DC];
-#pragma unroll
-    for (int j = 0; j < DC; ++j)
-        if (j < G.d) {
-            dq[j] = pre * kap[j];
-            pre *= f[j];
-        }
-    double suf = 1.0;
-#pragma unroll
-    for (int j = DC - 1; j >= 0; --j)
-        if (j < G.d) {
-            acc[j] = fma(dq[j], suf, acc[j]);
-            suf *= f[j];
-        }
+// column kernels: thread t owns column cc = t & (C-1), rows k1 = (t >> lc) + u (NT >> lc)
+__device__ __forceinline__ void col_steps(double2* s_step, const double2* __restrict__ tw, uint32_t c0, int lc,
+                                          int NT, int L) {
+    const int C = 1 << lc;
+    for (int t = threadIdx.x; t < C * LAT_STEPS; t += NT) {
+        const int cc = t / LAT_STEPS, u = t - cc * LAT_STEPS;
+        s_step[t] = twiddle(tw, uint64_t(c0 + cc) * uint64_t((NT >> lc) * u), L);
+    }
 }
 
 // ------------------------------------------------------------------ L1: generator x column FFT
@@ -132,12 +148,32 @@ __global__ void __launch_bounds__(NT) k_lat_col_fwd(LatArgs a, int l1, int l2, i
     const int v = blockIdx.y, c = v / a.V, o = v - c * a.V;
     const int C = 1 << lc, N1 = 1 << l1, ld = padded_len(N1), tile = C << l1;
     const uint32_t c0 = uint32_t(blockIdx.x) << lc;
-    LatGen<DC> G;
+    __shared__ double2 s_step[32 * LAT_STEPS];
+    const int lt = l1 + l2;
+    col_steps(s_step, a.tw, c0, lc, NT, lt);
+    const int tcc = threadIdx.x & (C - 1);
+    const double2 tbase = twiddle(a.tw, uint64_t(c0 + tcc) * uint64_t(threadIdx.x >> lc), lt);
+    LatGen<DC, ALPHA> G;
     G.init(a, c, o);
-    for (int e = threadIdx.x; e < tile; e += NT) {
-        const int j1 = e >> lc, cc = e & (C - 1);
-        const uint32_t j = (uint32_t(j1) << l2) + c0 + uint32_t(cc);
-        sm[cc * ld + S(j1)] = make_double2(lat_q<DC, ALPHA>(G, 2u * j), lat_q<DC, ALPHA>(G, 2u * j + 1u));
+    int done = 0;
+    if ((l1 & 3) == 1) {
+        // first (twiddle-free) radix-2 Stockham level fused into the generation: no radix-2 tail stage
+        const int H = N1 >> 1;
+        for (int e = threadIdx.x; e < (C << (l1 - 1)); e += NT) {
+            const int jj = e >> lc, cc = e & (C - 1);
+            const uint32_t j0 = (uint32_t(jj) << l2) + c0 + uint32_t(cc), j1 = j0 + (uint32_t(H) << l2);
+            const double2 x0 = make_double2(G.q(2u * j0), G.q(2u * j0 + 1u));
+            const double2 x1 = make_double2(G.q(2u * j1), G.q(2u * j1 + 1u));
+            sm[cc * ld + S(2 * jj)] = cadd(x0, x1);
+            sm[cc * ld + S(2 * jj + 1)] = csub(x0, x1);
+        }
+        done = 1;
+    } else {
+        for (int e = threadIdx.x; e < tile; e += NT) {
+            const int j1 = e >> lc, cc = e & (C - 1);
+            const uint32_t j = (uint32_t(j1) << l2) + c0 + uint32_t(cc);
+            sm[cc * ld + S(j1)] = make_double2(G.q(2u * j), G.q(2u * j + 1u));
+        }
     }
     pdl_trigger();
     // zero the per-fit flags once per fit (L2 / L3 run after this kernel)
@@ -146,13 +182,16 @@ __global__ void __launch_bounds__(NT) k_lat_col_fwd(LatArgs a, int l1, int l2, i
         for (int t = threadIdx.x; t < a.nc * MAXT * 2; t += NT) a.imre[t] = 0ull;
     }
     __syncthreads();
-    smem_fft<NT, true>(sm, l1, C, ld, -1, a.tw);
+    smem_fft_from<NT, true>(sm, l1, done, C, ld, -1, a.tw);
     double2* out = a.Y + size_t(v) * a.half;
-    const int lt = l1 + l2;
-    for (int e = threadIdx.x; e < tile; e += NT) {
-        const int k1 = e >> lc, cc = e & (C - 1);
-        const uint64_t j2 = c0 + uint32_t(cc);
-        out[((long long)k1 << l2) + j2] = cmul(sm[cc * ld + S(k1)], twiddle(a.tw, j2 * uint64_t(k1), lt));
+    const double2* st = s_step + tcc * LAT_STEPS;
+#pragma unroll 4
+    for (int u = 0; u < LAT_STEPS; ++u) {
+        const int e = threadIdx.x + u * NT;
+        if (e < tile) {
+            const int k1 = e >> lc;
+            out[((long long)k1 << l2) + c0 + tcc] = cmul(sm[tcc * ld + S(k1)], cmul(tbase, st[u]));
+        }
     }
 }
 
@@ -178,14 +217,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
     const long long half = a.half;
     double2* Yc = a.Y + size_t(c) * V * half;
     const double2* yh = a.yhat;
-    // prologue independent of L1 (overlaps its tail under programmatic dependent launch)
+    // frequency pairs (k, N' - k): one thread owns both slots (reads, solves, writes back)
+    const bool selfrow = q == 0;  // rows 0 and N1/2 pair with themselves
+    const int rowA = selfrow ? row : q, rowB = selfrow ? row : N1 - q;
+    int p0, p1;
+    if (selfrow) {
+        p0 = 0;
+        p1 = rank == 0 ? N2 / 2 + 1 : N2 / 2;
+    } else {
+        p0 = rank * (N2 / 2);
+        p1 = p0 + N2 / 2;
+    }
+    // prologue independent of L1 (overlaps its tail under programmatic dependent launch):
+    // coefficients, and the twiddles as per-thread bases x per-CTA step tables (see col_steps)
+    __shared__ double2 s_rstep[LAT_STEPS], s_ostep[LAT_STEPS];
     if (threadIdx.x < P) {
         const int p = threadIdx.x;
         s_coef[p] = __ldg(a.coef + size_t(c) * P + p);
         s_xi[p] = __ldg(a.xi + size_t(c) * P + p);
         s_wR[p] = (a.pair_a[p] == a.pair_b[p] ? 1.0 : 2.0) * __ldg(a.Rpair + size_t(c) * P + p);
         s_cls[p] = a.pair_ofs[p];
+    } else if (threadIdx.x >= 32 && threadIdx.x < 32 + LAT_STEPS) {
+        const int u = threadIdx.x - 32;
+        s_rstep[u] = twiddle(a.tw, uint64_t(u) * uint64_t(NT) * uint64_t(N1), a.m);  // r2c: w_n^k
+        s_ostep[u] = twiddle(a.tw, uint64_t(u) * uint64_t(NT) * uint64_t(row), lt);  // four-step
     }
+    const double2 rbase = twiddle(a.tw, uint64_t(rowA) + uint64_t(p0 + int(threadIdx.x)) * uint64_t(N1), a.m);
+    const double2 obase = twiddle(a.tw, uint64_t(threadIdx.x) * uint64_t(row), lt);
     pdl_wait();
     pdl_trigger();
     for (int e = threadIdx.x; e < (V << l2); e += NT) {
@@ -197,20 +255,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
     smem_fft<NT, true>(sm, l2, V, lds, -1, a.tw);
     cl.sync();  // both rows transformed: partner rows readable over DSMEM
 
-    // frequency pairs (k, N' - k): one thread owns both slots (reads, solves, writes back)
-    const bool selfrow = q == 0;  // rows 0 and N1/2 pair with themselves
     double2* rem = cl.map_shared_rank(sm, rank ^ 1);
-    const int rowA = selfrow ? row : q, rowB = selfrow ? row : N1 - q;
     double2* bufA = (selfrow || rank == 0) ? sm : rem;
     double2* bufB = (selfrow || rank == 1) ? sm : rem;
-    int p0, p1;
-    if (selfrow) {
-        p0 = 0;
-        p1 = rank == 0 ? N2 / 2 + 1 : N2 / 2;
-    } else {
-        p0 = rank * (N2 / 2);
-        p1 = p0 + N2 / 2;
-    }
     const bool grad = a.want_grad != 0;
     double acc[2 + P];
 #pragma unroll
@@ -219,8 +266,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
 #pragma unroll
     for (int t = 0; t < T; ++t) imx[t] = rex[t] = 0.0;
     long long first_bad = 0x7f7f7f7fll;
+    double lpm = 1.0;  // running pivot product of the slots k >= 1 (weight 2): one log per thread
+    int lpe = 0;
 #pragma unroll 1
-    for (int p = p0 + int(threadIdx.x); p < p1; p += NT) {
+    for (int p = p0 + int(threadIdx.x), it = 0; p < p1; p += NT, ++it) {
         const int k2a = p;
         const int k2b = selfrow ? (rank == 0 ? ((N2 - p) & (N2 - 1)) : (N2 - 1 - p)) : (N2 - 1 - p);
         const long long kA = rowA + ((long long)k2a << l1);
@@ -269,7 +318,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
             continue;
         }
         const bool self = slA == slB;  // k = N'/2 (row 0, k2 = N2/2)
-        const double2 wA = twiddle(a.tw, uint64_t(kA), a.m);
+        const double2 wA = cmul(rbase, s_rstep[it]);  // exp(-2 pi i k / n)
         const double2 wB = make_double2(-wA.x, wA.y);  // exp(-2 pi i (N' - k)/n) = -conj(wA)
         double2 HA[P], HB[P];
 #pragma unroll
@@ -290,11 +339,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
             for (int x = 0; x < P; ++x) A[x] = make_double2(fma(s_coef[x], H[x].x, s_xi[x]), s_coef[x] * H[x].y);
 #pragma unroll
             for (int t = 0; t < T; ++t) r[t] = yh[size_t(t) * half + sl];
-            double ld, qd;
-            const int st = ldl_solve<T, true>(A, r, grad, ld, qd, ch, Ai, imx, rex);
+            double qd;
+            const int st = ldl_core<T, true>(A, r, grad, lpm, lpe, qd, ch, Ai, imx, rex);
             if (st == 1 && sl < first_bad) first_bad = sl;
-            acc[0] += 2.0 * ld;  // slot k >= 1 stands for frequencies k and n - k
-            acc[1] += 2.0 * qd;
+            acc[1] += 2.0 * qd;  // slot k >= 1 stands for frequencies k and n - k
             if (grad) {
                 double2 Mq[P];
                 int x = 0;
@@ -330,6 +378,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
         }
     }
     cl.sync();  // every DSMEM access of the cluster is done
+    acc[0] += 2.0 * log_of(lpm, lpe);
 
     __shared__ double redv[(NT / 32) * (2 + P)];
     block_sum_vec<NT, 2 + P>(acc, redv);
@@ -354,10 +403,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
     }
     if (!grad) return;
     smem_fft<NT, true>(sm, l2, V, lds, +1, a.tw);  // block_sum_vec's barriers ordered the writes
-    for (int e = threadIdx.x; e < (V << l2); e += NT) {
-        const int oo = e >> l2, j2 = e & (N2 - 1);
-        Yc[size_t(oo) * half + ((long long)row << l2) + j2] =
-            cmulc(sm[oo * lds + S(j2)], twiddle(a.tw, uint64_t(j2) * uint64_t(row), lt));
+#pragma unroll 1
+    for (int u = 0; u < LAT_STEPS; ++u) {
+        const int j2 = int(threadIdx.x) + u * NT;
+        if (j2 >= N2) break;
+        const double2 w = cmul(obase, s_ostep[u]);
+        for (int oo = 0; oo < V; ++oo)
+            Yc[size_t(oo) * half + ((long long)row << l2) + j2] = cmulc(sm[oo * lds + S(j2)], w);
     }
 }
 
@@ -371,17 +423,45 @@ __global__ void __launch_bounds__(NT) k_lat_col_inv(LatArgs a, int l1, int l2, i
     const int v = blockIdx.y, c = v / a.V, o = v - c * a.V;
     const int C = 1 << lc, N1 = 1 << l1, ld = padded_len(N1), tile = C << l1;
     const uint32_t c0 = uint32_t(blockIdx.x) << lc;
-    LatGen<DC> G;
+    LatGen<DC, ALPHA> G;
     G.init(a, c, o);  // independent of L2: overlaps its tail
     pdl_wait();
     const double2* x = a.Y + size_t(v) * a.half;
-    for (int e = threadIdx.x; e < tile; e += NT) {
-        const int k1 = e >> lc, cc = e & (C - 1);
-        cp_async16(&sm[cc * ld + S(k1)], &x[((long long)k1 << l2) + c0 + cc]);
+    int done = 0;
+    if ((l1 & 3) == 1) {
+        // first (twiddle-free) radix-2 level fused into the load: no radix-2 tail stage; all of a
+        // thread's loads are issued before the first butterfly
+        constexpr int PB = LAT_STEPS / 2;
+        const int H = N1 >> 1, npair = C << (l1 - 1);
+        double2 x0[PB], x1[PB];
+#pragma unroll
+        for (int u = 0; u < PB; ++u) {
+            const int e = threadIdx.x + u * NT;
+            if (e < npair) {
+                const int jj = e >> lc, cc = e & (C - 1);
+                x0[u] = __ldcs(&x[((long long)jj << l2) + c0 + cc]);
+                x1[u] = __ldcs(&x[((long long)(jj + H) << l2) + c0 + cc]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < PB; ++u) {
+            const int e = threadIdx.x + u * NT;
+            if (e < npair) {
+                const int jj = e >> lc, cc = e & (C - 1);
+                sm[cc * ld + S(2 * jj)] = cadd(x0[u], x1[u]);
+                sm[cc * ld + S(2 * jj + 1)] = csub(x0[u], x1[u]);
+            }
+        }
+        done = 1;
+    } else {
+        for (int e = threadIdx.x; e < tile; e += NT) {
+            const int k1 = e >> lc, cc = e & (C - 1);
+            cp_async16(&sm[cc * ld + S(k1)], &x[((long long)k1 << l2) + c0 + cc]);
+        }
+        cp_async_wait_all();
     }
-    cp_async_wait_all();
     __syncthreads();
-    smem_fft<NT, true>(sm, l1, C, ld, +1, a.tw);
+    smem_fft_from<NT, true>(sm, l1, done, C, ld, +1, a.tw);
     double acc[DC];
 #pragma unroll
     for (int j = 0; j < DC; ++j) acc[j] = 0.0;
@@ -389,8 +469,8 @@ __global__ void __launch_bounds__(NT) k_lat_col_inv(LatArgs a, int l1, int l2, i
         const int j1 = e >> lc, cc = e & (C - 1);
         const uint32_t j = (uint32_t(j1) << l2) + c0 + uint32_t(cc);
         const double2 z = sm[cc * ld + S(j1)];  // W(2j) = 2 Re z, W(2j+1) = 2 Im z
-        lat_dq_acc<DC, ALPHA>(G, 2u * j, 2.0 * z.x, acc);
-        lat_dq_acc<DC, ALPHA>(G, 2u * j + 1u, 2.0 * z.y, acc);
+        G.dq_acc(2u * j, 2.0 * z.x, acc);
+        G.dq_acc(2u * j + 1u, 2.0 * z.y, acc);
     }
     const int nblk = gridDim.x;
     __shared__ double redv[(NT / 32) * DC];
@@ -451,7 +531,8 @@ static void lat_cols(const LatGeo& g, const LatArgs& a, size_t sm_col, bool inve
 
 template <int ALPHA>
 static void lat_cols_d(const LatGeo& g, const LatArgs& a, size_t sm_col, bool inverse, cudaStream_t s) {
-    if (a.d <= 4) lat_cols<4, ALPHA>(g, a, sm_col, inverse, s);
+    if (a.d <= 2) lat_cols<2, ALPHA>(g, a, sm_col, inverse, s);
+    else if (a.d <= 4) lat_cols<4, ALPHA>(g, a, sm_col, inverse, s);
     else if (a.d <= 8) lat_cols<8, ALPHA>(g, a, sm_col, inverse, s);
     else lat_cols<16, ALPHA>(g, a, sm_col, inverse, s);
 }

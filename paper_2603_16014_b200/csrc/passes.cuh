@@ -304,10 +304,12 @@ __device__ __forceinline__ double2 c2r_pre(double2 Ak, double2 Ap, double2 wk) {
 // Hermitian LDL^H of A (upper pairs, row by row), T <= 8.  Pivots are the diagonal Schur
 // complements of Algorithm 1 (fast_gram.cpp:167-178): logdet = sum log d_s.
 // Returns 0 ok, 1 non-positive pivot (SchurBreakdown), 2 non-real diagonal (FastMtgpError).
+// ldl_core multiplies the pivots into a running product pm * 2^pe (pm frexp-normalised, so no
+// pivot range can overflow it): a kernel that solves many frequencies takes ONE log at the end.
 template <int T, bool CX>
-__device__ __forceinline__ int ldl_solve(const typename Sc<CX>::T* A, const typename Sc<CX>::T* r, bool want_inv,
-                                         double& logdet, double& quad, typename Sc<CX>::T* chat,
-                                         typename Sc<CX>::T* Ainv, double* imx, double* rex) {
+__device__ __forceinline__ int ldl_core(const typename Sc<CX>::T* A, const typename Sc<CX>::T* r, bool want_inv,
+                                        double& pm, int& pe, double& quad, typename Sc<CX>::T* chat,
+                                        typename Sc<CX>::T* Ainv, double* imx, double* rex) {
     using S = Sc<CX>;
     using V = typename S::T;
     V L[T][T];
@@ -315,10 +317,6 @@ __device__ __forceinline__ int ldl_solve(const typename Sc<CX>::T* A, const type
     int status = 0;
     // pair index of (a,b), a <= b, row by row (fast_gram.cpp:35-40)
     auto pidx = [](int a, int b) { return a * T - a * (a - 1) / 2 + (b - a); };
-    // log det = log(prod of pivots): one log per frequency; the running product is kept
-    // normalised (frexp) so no pivot range can overflow it
-    double pm = 1.0;
-    int pe = 0;
 #pragma unroll
     for (int s = 0; s < T; ++s) {
         double dd = S::re(A[pidx(s, s)]);
@@ -345,7 +343,6 @@ __device__ __forceinline__ int ldl_solve(const typename Sc<CX>::T* A, const type
             L[i][s] = S::scale(acc, dinv[s]);
         }
     }
-    logdet = log(pm) + double(pe) * 0.69314718055994530942;
     // z = L^-1 r, quad = sum |z|^2 / d
     V z[T];
     quad = 0.0;
@@ -395,6 +392,20 @@ __device__ __forceinline__ int ldl_solve(const typename Sc<CX>::T* A, const type
             }
     }
     return status;
+}
+
+__device__ __forceinline__ double log_of(double pm, int pe) { return log(pm) + double(pe) * 0.69314718055994530942; }
+
+// One frequency: logdet = sum log d_s.
+template <int T, bool CX>
+__device__ __forceinline__ int ldl_solve(const typename Sc<CX>::T* A, const typename Sc<CX>::T* r, bool want_inv,
+                                         double& logdet, double& quad, typename Sc<CX>::T* chat,
+                                         typename Sc<CX>::T* Ainv, double* imx, double* rex) {
+    double pm = 1.0;
+    int pe = 0;
+    const int st = ldl_core<T, CX>(A, r, want_inv, pm, pe, quad, chat, Ainv, imx, rex);
+    logdet = log_of(pm, pe);
+    return st;
 }
 
 // --------------------------------------------------------------------- split-mode generator helpers

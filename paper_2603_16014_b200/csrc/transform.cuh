@@ -180,9 +180,12 @@ __device__ __forceinline__ void fft_stage(double2* buf, int logN, int ns_log, in
 
 // Full unnormalised DFT of nvec vectors of length 2^logN in smem (natural order).
 // Caller must __syncthreads() before (data in place); returns synchronised.
+// Stages from `done` on (the first `done` radix-2 levels already applied, e.g. fused into a
+// kernel's load phase: x[2j] = a_j + a_{j+N/2}, x[2j+1] = a_j - a_{j+N/2}, the twiddle-free
+// Stockham radix-2 stage with ns_log = 0).
 template <int NT, bool PADDED = false>
-__device__ void smem_fft(double2* buf, int logN, int nvec, int vstride, int dir, const double2* __restrict__ tw) {
-    int done = 0;
+__device__ void smem_fft_from(double2* buf, int logN, int done, int nvec, int vstride, int dir,
+                              const double2* __restrict__ tw) {
     while (done < logN) {
         const int left = logN - done;
         if (left >= 4) {
@@ -199,6 +202,11 @@ __device__ void smem_fft(double2* buf, int logN, int nvec, int vstride, int dir,
             done += 1;
         }
     }
+}
+
+template <int NT, bool PADDED = false>
+__device__ void smem_fft(double2* buf, int logN, int nvec, int vstride, int dir, const double2* __restrict__ tw) {
+    smem_fft_from<NT, PADDED>(buf, logN, 0, nvec, vstride, dir, tw);
 }
 
 template <int NT, int R, int RL, bool PADDED = false>
