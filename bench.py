@@ -125,7 +125,11 @@ def algorithmic_bytes(kernel: str, inst, P: int, T: int) -> float:
         "inv_row_dig": 2 * P * vec, "inv_row_lat": 2 * P * vec,  # read M, write intermediate
         "inv_col_dig": P * vec, "inv_col_lat": P * vec,  # read intermediate, dot in registers
         "inv_small_dig": P * vec, "inv_small_lat": P * vec,
-        "finalize": 0.0,
+        "finalize": 0.0, "dig_finalize": 0.0,
+        # fused lattice path (lattice.cuh): n/2 complex slots of 16 B = 8n bytes per vector
+        "lat_col_fwd": V * vec,  # generator on the fly -> intermediate out
+        "lat_mid": (2 * V + T) * vec,  # intermediate + yhat in; inverse-row intermediate out
+        "lat_col_inv": V * vec,  # intermediate in, gradient dot in registers
     }
     return table.get(kernel, 0.0)
 

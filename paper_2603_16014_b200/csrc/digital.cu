@@ -261,6 +261,7 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
     // column is loaded and transformed
     if (a.kap) load_kappa_tile<NT, D>(kbuf, a.kap + size_t(o) * D * n, n, l1, l2, lc, c0);
     pdl_wait();
+    if (a.tail != 1) pdl_trigger();  // separate finalize kernel: let its CTA become resident now
     for (int e = threadIdx.x; e < tile; e += NT) {
         const int k1 = e >> lc, cc = e & (C - 1);
         cp_async8(&sm[cc * ld + sidx<true>(k1)], &x[((long long)k1 << l2) + c0 + cc]);
@@ -321,6 +322,7 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
 #pragma unroll
         for (int j = 0; j <= D; ++j) out[j == D ? MAXD : j] = acc[j];
     }
+    if (a.tail != 1) return;  // k_dig_finalize reduces the partials
     // last-CTA reduction: one acq_rel ticket per candidate over its V * nblk CTAs (the release
     // publishes this CTA's partial, the last arrival's acquire sees all of them); fixed
     // summation order => deterministic
@@ -365,6 +367,29 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
     t.gamma = __ldg(a.gamma + c);
     t.out = a.out + size_t(c) * NOUT;
     class_sums_out<NT>(t);
+}
+
+// ------------------------------------------------------------------ finalize as its own kernel
+// (DigArgs::tail != 1): one CTA per candidate; under programmatic dependent launch it is resident
+// (prologue done) while K3 runs and reduces as soon as K3's partials are visible.
+__global__ void __launch_bounds__(256) k_dig_finalize(DigArgs a, int nrows, int nblk) {
+    const int c = blockIdx.x;
+    ClassSums t{};
+    t.P = a.P;
+    t.V = a.V;
+    t.d = a.d;
+    t.nrows = nrows;
+    t.nblk = nblk;
+    t.dstride = MAXD + 1;
+    t.mid = a.part_mid + size_t(c) * nrows * (2 + a.P);
+    t.dot = a.part_dot + size_t(c) * a.V * nblk * (MAXD + 1);
+    t.pair_a = a.pair_a;
+    t.pair_b = a.pair_b;
+    t.Rpair = a.Rpair + size_t(c) * a.P;
+    t.gamma = __ldg(a.gamma + c);
+    t.out = a.out + size_t(c) * NOUT;
+    pdl_wait();
+    class_sums_out<256>(t);
 }
 
 // ------------------------------------------------------------------ launcher
@@ -420,6 +445,10 @@ void dig_fit(const DigGeo& g, const DigArgs& a, cudaStream_t s) {
             CK_LAUNCH(launch_pdl(k3, gcol, dim3(NT), sm_col, s, true, a, g.l1, g.l2, g.lc, nrows));
         })
     })
+    if (a.tail != 1) {
+        ProfScope ps("dig_finalize", s);
+        CK_LAUNCH(launch_pdl(k_dig_finalize, dim3(a.nc), dim3(256), 0, s, a.tail == 2, a, nrows, g.nblk_col));
+    }
 }
 
 }  // namespace fmtgp

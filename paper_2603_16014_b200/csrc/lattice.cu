@@ -201,7 +201,22 @@ __device__ __forceinline__ int lat_row_of(int q, int rank, int N1) {
     return rank == 0 ? q : N1 - q;
 }
 
-template <int NT, int T>
+// Class of pair y (row-by-row pair order) when every task has its own shift (the BASELINE
+// designs): all diagonal pairs share offset 0 (class 0), every off-diagonal pair is its own class.
+template <int T>
+__host__ __device__ constexpr int cls_distinct(int y) {
+    int q = 0, off = 0;
+    for (int a = 0; a < T; ++a)
+        for (int b = a; b < T; ++b, ++q) {
+            if (q == y) return a == b ? 0 : 1 + off;
+            if (a != b) ++off;
+        }
+    return 0;
+}
+
+// DIST: the class map is cls_distinct<T> (compile time: no per-pair class selects); otherwise
+// it comes from LatArgs::pair_ofs.
+template <int NT, int T, bool DIST>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArgs a, int l1, int l2) {
     constexpr int P = T * (T + 1) / 2;
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -211,12 +226,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
     __shared__ int s_cls[P];
     cg::cluster_group cl = cg::this_cluster();
     const int rank = int(cl.block_rank());
-    const int q = blockIdx.x >> 1, c = blockIdx.y, V = a.V;
+    const int q = blockIdx.x >> 1, c = blockIdx.y, V = DIST ? P - T + 1 : a.V;
+    auto cls = [&](int y) { return DIST ? cls_distinct<T>(y) : s_cls[y]; };
     const int N1 = 1 << l1, N2 = 1 << l2, lds = padded_len(N2), lt = l1 + l2;
     const int row = lat_row_of(q, rank, N1);
     const long long half = a.half;
     double2* Yc = a.Y + size_t(c) * V * half;
-    const double2* yh = a.yhat;
     // frequency pairs (k, N' - k): one thread owns both slots (reads, solves, writes back)
     const bool selfrow = q == 0;  // rows 0 and N1/2 pair with themselves
     const int rowA = selfrow ? row : q, rowB = selfrow ? row : N1 - q;
@@ -244,6 +259,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
     }
     const double2 rbase = twiddle(a.tw, uint64_t(rowA) + uint64_t(p0 + int(threadIdx.x)) * uint64_t(N1), a.m);
     const double2 obase = twiddle(a.tw, uint64_t(threadIdx.x) * uint64_t(row), lt);
+    const double2* yh = a.yhat;
+    auto partner = [&](int p) { return selfrow ? (rank == 0 ? ((N2 - p) & (N2 - 1)) : (N2 - 1 - p)) : (N2 - 1 - p); };
+    // yhat of the thread's next pair is loaded one iteration ahead (its latency hides behind a solve)
+    double2 yA[T], yB[T];
+    {
+        const int p = p0 + int(threadIdx.x);
+        if (p < p1) {
+            const long long sa = ((long long)rowA << l2) + p, sb = ((long long)rowB << l2) + partner(p);
+#pragma unroll
+            for (int t = 0; t < T; ++t) yA[t] = yh[size_t(t) * half + sa], yB[t] = yh[size_t(t) * half + sb];
+        }
+    }
     pdl_wait();
     pdl_trigger();
     for (int e = threadIdx.x; e < (V << l2); e += NT) {
@@ -271,23 +298,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
 #pragma unroll 1
     for (int p = p0 + int(threadIdx.x), it = 0; p < p1; p += NT, ++it) {
         const int k2a = p;
-        const int k2b = selfrow ? (rank == 0 ? ((N2 - p) & (N2 - 1)) : (N2 - 1 - p)) : (N2 - 1 - p);
+        const int k2b = partner(p);
         const long long kA = rowA + ((long long)k2a << l1);
         const long long slA = ((long long)rowA << l2) + k2a, slB = ((long long)rowB << l2) + k2b;
+        double2 rA[T], rB[T];
+#pragma unroll
+        for (int t = 0; t < T; ++t) rA[t] = yA[t], rB[t] = yB[t];
+        if (p + NT < p1) {
+            const long long sa = slA + NT, sb = ((long long)rowB << l2) + partner(p + NT);
+#pragma unroll
+            for (int t = 0; t < T; ++t) yA[t] = yh[size_t(t) * half + sa], yB[t] = yh[size_t(t) * half + sb];
+        }
         if (kA == 0) {
             // packed slot 0: frequency 0 (.x) and Nyquist (.y), two real systems; tau zeroes the
             // frequency-0 residual (gp_core.cpp:67-88) — k_solve_class's p == 0 branch
             double H0[P], HN[P], A0[P], AN[P], r0[T], rN[T], c0v[T], cN[T], I0[P], IN[P], l0, lN, q0, qN;
 #pragma unroll
             for (int x = 0; x < P; ++x) {
-                const double2 z = sm[s_cls[x] * lds + S(0)];
+                const double2 z = sm[cls(x) * lds + S(0)];
                 H0[x] = z.x + z.y;
                 HN[x] = z.x - z.y;
                 A0[x] = fma(s_coef[x], H0[x], s_xi[x]);
                 AN[x] = fma(s_coef[x], HN[x], s_xi[x]);
             }
 #pragma unroll
-            for (int t = 0; t < T; ++t) r0[t] = 0.0, rN[t] = yh[size_t(t) * half].y;
+            for (int t = 0; t < T; ++t) r0[t] = 0.0, rN[t] = rA[t].y;
             const int st0 = ldl_solve<T, false>(A0, r0, grad, l0, q0, c0v, I0, imx, rex);
             const int stN = ldl_solve<T, false>(AN, rN, grad, lN, qN, cN, IN, imx, rex);
             if (st0 == 1 || stN == 1) first_bad = 0;
@@ -311,7 +346,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
                     double z0 = 0.0, zN = 0.0;
 #pragma unroll
                     for (int y = 0; y < P; ++y)
-                        if (s_cls[y] == o) z0 = fma(s_wR[y], M0[y], z0), zN = fma(s_wR[y], MN[y], zN);
+                        if (cls(y) == o) z0 = fma(s_wR[y], M0[y], z0), zN = fma(s_wR[y], MN[y], zN);
                     sm[o * lds + S(0)] = make_double2(0.5 * (z0 + zN), 0.5 * (z0 - zN));  // inverse pre, k = 0
                 }
             }
@@ -323,7 +358,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
         double2 HA[P], HB[P];
 #pragma unroll
         for (int x = 0; x < P; ++x) {
-            const int o = s_cls[x];
+            const int o = cls(x);
             const double2 za = bufA[o * lds + S(k2a)], zb = bufB[o * lds + S(k2b)];
             HA[x] = r2c_post(za, zb, wA);
             HB[x] = r2c_post(zb, za, wB);
@@ -338,7 +373,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
 #pragma unroll
             for (int x = 0; x < P; ++x) A[x] = make_double2(fma(s_coef[x], H[x].x, s_xi[x]), s_coef[x] * H[x].y);
 #pragma unroll
-            for (int t = 0; t < T; ++t) r[t] = yh[size_t(t) * half + sl];
+            for (int t = 0; t < T; ++t) r[t] = side == 0 ? rA[t] : rB[t];
             double qd;
             const int st = ldl_core<T, true>(A, r, grad, lpm, lpe, qd, ch, Ai, imx, rex);
             if (st == 1 && sl < first_bad) first_bad = sl;
@@ -357,7 +392,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
                     double2 z = make_double2(0.0, 0.0);
 #pragma unroll
                     for (int y = 0; y < P; ++y)
-                        if (s_cls[y] == o) z = make_double2(fma(s_wR[y], Mq[y].x, z.x), fma(s_wR[y], Mq[y].y, z.y));
+                        if (cls(y) == o) z = make_double2(fma(s_wR[y], Mq[y].x, z.x), fma(s_wR[y], Mq[y].y, z.y));
                     if (side == 0) ZA[o] = z;
                     else ZB[o] = z;
                 }
@@ -540,7 +575,7 @@ static void lat_cols_d(const LatGeo& g, const LatArgs& a, size_t sm_col, bool in
 template <int T>
 static void lat_mid_launch(const LatGeo& g, const LatArgs& a, cudaStream_t s) {
     const size_t sm = size_t(a.V) * padded_len(1 << g.l2) * sizeof(double2);
-    auto k = k_lat_mid<LAT_NT, T>;
+    auto k = a.distinct ? k_lat_mid<LAT_NT, T, true> : k_lat_mid<LAT_NT, T, false>;
     set_smem_lat(k, sm);
     ProfScope ps("lat_mid", s);
     CK_LAUNCH(launch_pdl(k, dim3(1u << g.l1, a.nc), dim3(LAT_NT), sm, s, true, a, g.l1, g.l2));

@@ -57,6 +57,7 @@ struct LatArgs {
     double* out;              // [nc][NOUT]
     const double2* tw;
     int want_grad;
+    int distinct;             // pair_ofs is the all-shifts-distinct map (cls_distinct in lattice.cu)
 };
 
 void lat_fit(const LatGeo& g, const LatArgs& a, cudaStream_t s);

@@ -310,6 +310,7 @@ struct fmtgp_model {
     unsigned int* d_counter = nullptr;
     double* d_vec_sum = nullptr;
     int* d_pair_ofs = nullptr;
+    std::vector<int> h_pair_ofs;
     int* d_iota = nullptr;           // [P] 0..P-1 (class vector -> class offset row)
     long long* d_cvoff = nullptr;    // [P] slot offset of class vector o (o * pslots)
     double* d_ones = nullptr;        // [max_cand * P]
@@ -320,6 +321,7 @@ struct fmtgp_model {
     // fused three-kernel lattice path (lattice.cuh); shares part_mid / part_dot / counter
     bool lat = false;
     LatGeo lgeo{};
+    int dig_tail = 1;  // digital K3 finalize mode (DigArgs::tail), FMTGP_DIG_TAIL
     double kap_b[4]{};
     bool kap_valid = false;
     bool kap_enabled = true;
@@ -605,6 +607,7 @@ void eval_digital_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, b
     a.vec_sum = M->d_vec_sum;
     a.out = M->d_out;
     a.want_grad = grad;
+    a.tail = M->dig_tail;
     dig_fit(M->dgeo, a, M->st);
     CK(cudaGetLastError());
     if (!grad) {
@@ -660,6 +663,11 @@ void eval_lattice_body(fmtgp_model* M, int nc, int si_alpha, bool grad) {
     a.out = M->d_out;
     a.tw = M->tw;
     a.want_grad = grad;
+    a.distinct = M->nofs == M->P - M->T + 1;
+    for (int p = 0, off = 0; p < M->P && a.distinct; ++p) {
+        const int want = M->pa[p] == M->pb[p] ? 0 : 1 + off++;
+        if (M->h_pair_ofs[p] != want) a.distinct = 0;
+    }
     lat_fit(M->lgeo, a, M->st);
     CK(cudaGetLastError());
     if (!grad) {
@@ -966,6 +974,7 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
         M->max_cand = max_cand;
         if (const char* e = std::getenv("FMTGP_KAPPA_TABLE")) M->kap_enabled = e[0] != '0';
         if (const char* e = std::getenv("FMTGP_CLASSES")) M->class_mode = e[0] != '0';
+        if (const char* e = std::getenv("FMTGP_DIG_TAIL")) M->dig_tail = std::atoi(e);
         M->off[0] = 0;
         for (int l = 0; l < M->T; ++l) {
             M->m[l] = dz->m[l];
@@ -1045,6 +1054,7 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
             }
             pofs[p] = found;
         }
+        M->h_pair_ofs = pofs;
         M->d_pair_ofs = dalloc<int>(M->P);
         M->d_ofs = dalloc<uint64_t>(uniq.size());
         CK(cudaMemcpy(M->d_pair_ofs, pofs.data(), M->P * sizeof(int), cudaMemcpyHostToDevice));
