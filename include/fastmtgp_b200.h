@@ -164,6 +164,28 @@ FMTGP_API int fmtgp_posterior_var(fmtgp_model_t model, int task, const double* X
 /* multitask_cubature (cubature.cpp:52-75): mu [L], Sigma [L * L] (internal order) */
 FMTGP_API int fmtgp_cubature(fmtgp_model_t model, double* mu, double* Sigma);
 
+/* ---- frequency-sharded lattice fit over `world` ranks -----------------
+ * No reference counterpart (the reference is single-process): the config-4 extension.  Each rank
+ * holds a model of the full design (y replicated, fmtgp_model_set_y) and runs three phases on
+ * its stream; between them the caller moves the exchange blocks with an all-to-all of equal
+ * chunks (world blocks of exchange_elems / world complex values, block h goes to rank h):
+ *   begin(Y)  generator x column FFT of this rank's column blocks into Y
+ *   all-to-all Y -> Y2
+ *   mid(Y2)   row FFT + per-frequency solve + inverse row FFT of this rank's row clusters, in place
+ *   all-to-all Y2 -> Y3
+ *   end(Y3)   inverse column FFT + gradient dot; rec = [NOUT sums | first bad slot | non-real maxima]
+ * The caller combines the ranks' records (sum the first NOUT entries in rank order, min of the
+ * bad slot, max of the maxima) and calls finish for the fmtgp_result (status SCHUR -> escalate
+ * xi_scale x10 as fmtgp_nll does, gp_core.cpp:98-127). */
+#define FMTGP_SHARD_REC_LEN (4 + FMTGP_MAX_D + FMTGP_MAX_T * FMTGP_MAX_T + 1 + 2 * FMTGP_MAX_T)
+FMTGP_API int fmtgp_shard_setup(fmtgp_model_t model, int rank, int world, int64_t* exchange_elems);
+FMTGP_API int fmtgp_shard_begin(fmtgp_model_t model, const fmtgp_hyper* h, int want_grad, double xi_scale,
+                                void* Y);
+FMTGP_API int fmtgp_shard_mid(fmtgp_model_t model, void* Y2);
+FMTGP_API int fmtgp_shard_end(fmtgp_model_t model, const void* Y3, double* rec);
+FMTGP_API int fmtgp_shard_finish(fmtgp_model_t model, const fmtgp_hyper* h, const double* rec, int want_grad,
+                                 double xi_scale, int escalations, fmtgp_result* out);
+
 /* ---- measurement: per-kernel CUDA-event timing on the model's stream ---------------- */
 FMTGP_API int fmtgp_profile_enable(fmtgp_model_t model, int on);  /* also resets the tallies */
 /* idx-th kernel name seen since enable, its summed device ms and launch count;

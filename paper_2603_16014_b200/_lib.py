@@ -13,6 +13,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libfmtgp_b200.so")
+SHARD_REC_LEN = 4 + 16 + 8 * 8 + 1 + 2 * 8  # FMTGP_SHARD_REC_LEN
 MAX_D = 16
 MAX_T = 8
 
@@ -87,6 +88,12 @@ _SIGS = {
     "fmtgp_posterior_mean": (C.c_int, [C.c_void_p, C.c_int, _dp, C.c_int64, _dp]),
     "fmtgp_posterior_var": (C.c_int, [C.c_void_p, C.c_int, _dp, C.c_int64, _dp]),
     "fmtgp_cubature": (C.c_int, [C.c_void_p, _dp, _dp]),
+    "fmtgp_shard_setup": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int64)]),
+    "fmtgp_shard_begin": (C.c_int, [C.c_void_p, C.POINTER(CHyper), C.c_int, C.c_double, C.c_void_p]),
+    "fmtgp_shard_mid": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "fmtgp_shard_end": (C.c_int, [C.c_void_p, C.c_void_p, _dp]),
+    "fmtgp_shard_finish": (C.c_int, [C.c_void_p, C.POINTER(CHyper), _dp, C.c_int, C.c_double, C.c_int,
+                                     C.POINTER(CResult)]),
     "fmtgp_profile_enable": (C.c_int, [C.c_void_p, C.c_int]),
     "fmtgp_profile_read": (C.c_int, [C.c_void_p, C.c_int, C.c_char_p, C.c_int, _dp, _ip]),
 }

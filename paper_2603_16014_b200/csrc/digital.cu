@@ -3,6 +3,15 @@
 
 namespace fmtgp {
 
+// FMTGP_TRACE: first-entry / last-exit globaltimer marks per kernel phase (slot: min or max)
+__device__ __forceinline__ void dig_trace(unsigned long long* tr, int slot, bool is_min) {
+    if (!tr || threadIdx.x != 0) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (is_min) atomicMin(tr + slot, t);
+    else atomicMax(tr + slot, t);
+}
+
 bool DigGeo::make(int m, int P, DigGeo& g, long long total_vecs) {
     if (m < 1 || P < 1) return false;
     // row length: all P (= class count V) rows of one frequency block in <= 64 KB of smem
@@ -85,6 +94,7 @@ template <int NT, int D>
 __global__ void __launch_bounds__(NT, 3) k_dig_col_fwd(DigArgs a, int l1, int l2, int lc) {
     extern __shared__ __align__(16) double sm[];
     __shared__ GenSmem<D> tab;
+    dig_trace(a.trace, 0, true);
     const int v = blockIdx.y, c = v / a.V, o = v - c * a.V;
     const int C = 1 << lc, N1 = 1 << l1, ld = padded_len(N1);
     const long long c0 = (long long)blockIdx.x << lc, n = a.n;
@@ -139,6 +149,7 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_fwd(DigArgs a, int l1, int l2
         const int k1 = e >> lc, cc = e & (C - 1);
         out[((long long)k1 << l2) + c0 + cc] = sm[cc * ld + sidx<true>(k1)];
     }
+    dig_trace(a.trace, 1, false);
 }
 
 // ------------------------------------------------------------------ K2: row FWHT + solve + inverse row FWHT
@@ -168,7 +179,9 @@ __global__ void __launch_bounds__(NT) k_dig_mid(DigArgs a, int l2) {
         for (int t = 0; t < T; ++t)
             rpre[u][t] = (k2 < N2 && base + k2 != 0) ? __ldg(a.yhat + size_t(t) * n + base + k2) : 0.0;
     }
+    dig_trace(a.trace, 2, true);
     pdl_wait();
+    dig_trace(a.trace, 3, true);
     pdl_trigger();
     for (int e = threadIdx.x; e < (V << l2); e += NT) {
         const int o = e >> l2, k2 = e & (N2 - 1);
@@ -243,6 +256,7 @@ __global__ void __launch_bounds__(NT) k_dig_mid(DigArgs a, int l2) {
         const int o = e >> l2, k2 = e & (N2 - 1);
         Yc[size_t(o) * n + base + k2] = sm[o * lds + sidx<true>(k2)];
     }
+    dig_trace(a.trace, 4, false);
 }
 
 // ------------------------------------------------------------------ K3: column FWHT -> W -> gradient dot
@@ -259,8 +273,10 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
     double* kbuf = sm + kbuf_offset(C, ld);
     // the kappa tile does not depend on K2: it streams in while K2 finishes (PDL) and while the
     // column is loaded and transformed
+    dig_trace(a.trace, 5, true);
     if (a.kap) load_kappa_tile<NT, D>(kbuf, a.kap + size_t(o) * D * n, n, l1, l2, lc, c0);
     pdl_wait();
+    dig_trace(a.trace, 6, true);
     if (a.tail != 1) pdl_trigger();  // separate finalize kernel: let its CTA become resident now
     for (int e = threadIdx.x; e < tile; e += NT) {
         const int k1 = e >> lc, cc = e & (C - 1);
@@ -322,6 +338,7 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
 #pragma unroll
         for (int j = 0; j <= D; ++j) out[j == D ? MAXD : j] = acc[j];
     }
+    dig_trace(a.trace, 7, false);
     if (a.tail != 1) return;  // k_dig_finalize reduces the partials
     // last-CTA reduction: one acq_rel ticket per candidate over its V * nblk CTAs (the release
     // publishes this CTA's partial, the last arrival's acquire sees all of them); fixed
@@ -334,6 +351,7 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
     }
     __syncthreads();
     if (!s_last) return;
+    dig_trace(a.trace, 8, false);
     // stage every partial into the (now free) dynamic smem with all copies in flight: the tail is
     // one L2 round trip instead of a chain of dependent ones
     const int S = 2 + a.P;
@@ -352,7 +370,9 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
         cp_async_wait_all();
     }
     __syncthreads();
+    dig_trace(a.trace, 9, false);
     ClassSums t{};
+    t.T = a.T;
     t.P = a.P;
     t.V = a.V;
     t.d = D;
@@ -367,6 +387,8 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
     t.gamma = __ldg(a.gamma + c);
     t.out = a.out + size_t(c) * NOUT;
     class_sums_out<NT>(t);
+    __syncthreads();
+    dig_trace(a.trace, 10, false);
 }
 
 // ------------------------------------------------------------------ finalize as its own kernel
@@ -375,6 +397,7 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
 __global__ void __launch_bounds__(256) k_dig_finalize(DigArgs a, int nrows, int nblk) {
     const int c = blockIdx.x;
     ClassSums t{};
+    t.T = a.T;
     t.P = a.P;
     t.V = a.V;
     t.d = a.d;

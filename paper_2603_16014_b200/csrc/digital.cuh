@@ -55,6 +55,7 @@ struct DigArgs {
     double* vec_sum;          // [nc][V][MAXD+1] per-class gradient sums
     double* out;              // [nc][NOUT]
     int want_grad;
+    unsigned long long* trace = nullptr;  // FMTGP_TRACE diagnostics: globaltimer marks (see dig_trace)
     int tail = 1;             // 1: last CTA of K3 reduces; 0: separate finalize kernel; 2: same, PDL-launched
 };
 

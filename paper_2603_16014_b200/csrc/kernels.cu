@@ -1074,6 +1074,7 @@ __global__ void __launch_bounds__(256) k_finalize_classes(ClassFinalArgs a) {
         return;
     }
     ClassSums t{};
+    t.T = a.T;
     t.P = a.P;
     t.V = a.V;
     t.d = a.d;

@@ -173,7 +173,8 @@ __device__ void finalize_candidate(const FinalArgs& a, int c) {
                 out[OUT_DR + pb * MAXT + pa] = 0.5 * dRp;
             }
         }
-        out[OUT_DGAMMA] = dgam / a.gamma[c];
+        (void)dgam;
+        out[OUT_DGAMMA] = 0.0;  // formed on the host from the dR record (finish_results)
         for (int j = 0; j < MAXD; ++j) out[OUT_DETA + j] = deta[j];
     }
 }
@@ -191,7 +192,7 @@ __device__ void finalize_candidate(const FinalArgs& a, int c) {
 // Kept out of line and small: in the digital path it is the last CTA's tail, whose
 // instructions come from DRAM after an L2 flush.
 struct ClassSums {
-    int P, V, d, nrows, nblk, dstride;
+    int T, P, V, d, nrows, nblk, dstride;
     const double* mid;
     const double* dot;
     const int* pair_a;
@@ -203,15 +204,11 @@ struct ClassSums {
 
 template <int NT>
 __device__ __noinline__ void class_sums_out(const ClassSums& t) {
+    // Short code on purpose: in the fused kernels this runs in ONE CTA after every other CTA
+    // finished (FMTGP_TRACE measured it: 6.0 us with the previous per-output branch ladder and a
+    // device fp64 division, 3.0 us now).
     __shared__ double res[2 + MAXP + MAXP * MAXD];
-    __shared__ double sR[MAXP];
-    __shared__ int spa[MAXP], spb[MAXP];
     const int S = 2 + t.P, Q = S + t.V * t.d;
-    if (threadIdx.x < t.P) {
-        spa[threadIdx.x] = t.pair_a[threadIdx.x];
-        spb[threadIdx.x] = t.pair_b[threadIdx.x];
-        sR[threadIdx.x] = t.Rpair[threadIdx.x];
-    }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll 1
     for (int q = warp; q < Q; q += NT / 32) {
@@ -223,46 +220,45 @@ __device__ __noinline__ void class_sums_out(const ClassSums& t) {
             const int o = (q - S) / t.d, j = (q - S) - o * t.d;
             base = t.dot + size_t(o) * t.nblk * t.dstride + j, stride = t.dstride, count = t.nblk;
         }
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        double s0 = 0.0, s1 = 0.0;
         int b = lane;
 #pragma unroll 1
-        for (; b + 96 < count; b += 128) {
+        for (; b + 32 < count; b += 64) {
             s0 += base[size_t(b) * stride];
             s1 += base[size_t(b + 32) * stride];
-            s2 += base[size_t(b + 64) * stride];
-            s3 += base[size_t(b + 96) * stride];
         }
-#pragma unroll 1
-        for (; b < count; b += 32) s0 += base[size_t(b) * stride];
-        double s = (s0 + s1) + (s2 + s3);
+        if (b < count) s0 += base[size_t(b) * stride];
+        double sum = s0 + s1;
 #pragma unroll
-        for (int o2 = 16; o2 > 0; o2 >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o2);
-        if (lane == 0) res[q] = s;
+        for (int o2 = 16; o2 > 0; o2 >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o2);
+        if (lane == 0) res[q] = sum;
     }
     __syncthreads();
 #pragma unroll 1
-    for (int x = threadIdx.x; x < NOUT; x += NT) {
-        double v = 0.0;
-        if (x == OUT_LOGDET) v = res[0];
-        else if (x == OUT_QUAD) v = res[1];
-        else if (x == OUT_NLL) v = res[0] + res[1];  // rT c + logdet (gp_core.cpp:207-211)
-        else if (x >= OUT_DETA && x < OUT_DETA + MAXD) {
-            const int j = x - OUT_DETA;
-            if (j < t.d)
+    for (int x = threadIdx.x; x < NOUT; x += NT) {  // NT may be below NOUT (small column tiles)
+    double v = 0.0;
+    if (x < OUT_NLL) {
+        v = res[x];
+    } else if (x == OUT_NLL) {
+        v = res[0] + res[1];  // rT c + logdet (gp_core.cpp:207-211)
+    } else if (x == OUT_DGAMMA) {
+        // dNLL/dgamma = sum_ab R_ab G_ab / gamma (q is linear in gamma): formed on the host from
+        // the dR record (finish_results), like dB = 2 G B and dt = diag G
+    } else if (x < OUT_DR) {
+        const int j = x - OUT_DETA;
 #pragma unroll 1
-                for (int o = 0; o < t.V; ++o) v += res[S + o * t.d + j];
-        } else if (x >= OUT_DR && x < OUT_DR + MAXT * MAXT) {
-            const int a = (x - OUT_DR) / MAXT, b = (x - OUT_DR) % MAXT;
-#pragma unroll 1
-            for (int p = 0; p < t.P; ++p)
-                if ((spa[p] == a && spb[p] == b) || (spa[p] == b && spb[p] == a))
-                    v = res[2 + p];  // diagonal dNLL/dR_aa; off-diagonal G_ab = G_ba = (2 res) / 2
-        } else if (x == OUT_DGAMMA) {
-#pragma unroll 1
-            for (int p = 0; p < t.P; ++p) v += sR[p] * (spa[p] == spb[p] ? 1.0 : 2.0) * res[2 + p];
-            v /= t.gamma;
+        for (int o = 0; o < t.V && j < t.d; ++o) v += res[S + o * t.d + j];
+    } else {
+        // G_ab = G_ba = dNLL/dR_pair (diagonal) or its half-sum convention (2 res) / 2
+        int a = (x - OUT_DR) / MAXT, b = (x - OUT_DR) - a * MAXT;
+        if (a > b) {
+            const int tmp = a;
+            a = b;
+            b = tmp;
         }
-        t.out[x] = v;
+        if (b < t.T) v = res[2 + a * t.T - a * (a - 1) / 2 + (b - a)];
+    }
+    t.out[x] = v;
     }
 }
 
@@ -274,7 +270,7 @@ __device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v
 
 // Class-layout finalize as its own kernel (generic equal-n path): one CTA per candidate.
 struct ClassFinalArgs {
-    int P, V, d, nblk_solve, nblk_grad;
+    int T, P, V, d, nblk_solve, nblk_grad;
     const double* solve_partial;  // [ncand][nblk_solve][2 + P]
     const double* grad_partial;   // [ncand][V][nblk_grad][MAXD + 1] (nullptr: no gradient)
     const double* Rpair;          // [ncand][P]

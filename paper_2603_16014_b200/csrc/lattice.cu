@@ -139,6 +139,24 @@ __device__ __forceinline__ void col_steps(double2* s_step, const double2* __rest
     }
 }
 
+// ------------------------------------------------------------------ exchange-block layout
+// Row k1 -> (owner rank h, local row i): cluster q = min(k1, N1 - k1) (rows 0 and N1/2 form
+// cluster 0), side = 1 for the upper row of the pair.
+__device__ __forceinline__ int row_owner(int k1, int N1, int QP, int& i) {
+    int q, side;
+    if (k1 == 0) q = 0, side = 0;
+    else if (k1 == (N1 >> 1)) q = 0, side = 1;
+    else if (k1 < (N1 >> 1)) q = k1, side = 0;
+    else q = N1 - k1, side = 1;
+    const int h = q / QP;
+    i = 2 * (q - h * QP) + side;
+    return h;
+}
+// element (row owner h, class o, local row i, local column jl) of candidate c's exchange blocks
+__device__ __forceinline__ size_t xaddr(const LatArgs& a, int c, int h, int o, int i, int jl) {
+    return size_t(c) * a.V * a.half + ((size_t(h) * a.V + o) * a.R + i) * a.WC + jl;
+}
+
 // ------------------------------------------------------------------ L1: generator x column FFT
 template <int NT, int DC, int ALPHA>
 __global__ void __launch_bounds__(NT) k_lat_col_fwd(LatArgs a, int l1, int l2, int lc) {
@@ -147,7 +165,7 @@ __global__ void __launch_bounds__(NT) k_lat_col_fwd(LatArgs a, int l1, int l2, i
     constexpr auto S = sidx<true>;
     const int v = blockIdx.y, c = v / a.V, o = v - c * a.V;
     const int C = 1 << lc, N1 = 1 << l1, ld = padded_len(N1), tile = C << l1;
-    const uint32_t c0 = uint32_t(blockIdx.x) << lc;
+    const uint32_t c0 = uint32_t(a.rank * a.ncb + blockIdx.x) << lc;  // global first column
     __shared__ double2 s_step[32 * LAT_STEPS];
     const int lt = l1 + l2;
     col_steps(s_step, a.tw, c0, lc, NT, lt);
@@ -183,14 +201,16 @@ __global__ void __launch_bounds__(NT) k_lat_col_fwd(LatArgs a, int l1, int l2, i
     }
     __syncthreads();
     smem_fft_from<NT, true>(sm, l1, done, C, ld, -1, a.tw);
-    double2* out = a.Y + size_t(v) * a.half;
     const double2* st = s_step + tcc * LAT_STEPS;
+    const int jl = int(c0) + tcc - a.rank * a.WC;
 #pragma unroll 4
     for (int u = 0; u < LAT_STEPS; ++u) {
         const int e = threadIdx.x + u * NT;
         if (e < tile) {
             const int k1 = e >> lc;
-            out[((long long)k1 << l2) + c0 + tcc] = cmul(sm[tcc * ld + S(k1)], cmul(tbase, st[u]));
+            int i;
+            const int h = row_owner(k1, N1, a.QP, i);
+            a.Y[xaddr(a, c, h, o, i, jl)] = cmul(sm[tcc * ld + S(k1)], cmul(tbase, st[u]));
         }
     }
 }
@@ -226,12 +246,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
     __shared__ int s_cls[P];
     cg::cluster_group cl = cg::this_cluster();
     const int rank = int(cl.block_rank());
-    const int q = blockIdx.x >> 1, c = blockIdx.y, V = DIST ? P - T + 1 : a.V;
+    const int q = a.rank * a.QP + (blockIdx.x >> 1), c = blockIdx.y, V = DIST ? P - T + 1 : a.V;
+    const int li = blockIdx.x;  // local row index of this CTA's row in the exchange blocks
     auto cls = [&](int y) { return DIST ? cls_distinct<T>(y) : s_cls[y]; };
     const int N1 = 1 << l1, N2 = 1 << l2, lds = padded_len(N2), lt = l1 + l2;
     const int row = lat_row_of(q, rank, N1);
     const long long half = a.half;
-    double2* Yc = a.Y + size_t(c) * V * half;
     // frequency pairs (k, N' - k): one thread owns both slots (reads, solves, writes back)
     const bool selfrow = q == 0;  // rows 0 and N1/2 pair with themselves
     const int rowA = selfrow ? row : q, rowB = selfrow ? row : N1 - q;
@@ -275,7 +295,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
     pdl_trigger();
     for (int e = threadIdx.x; e < (V << l2); e += NT) {
         const int oo = e >> l2, k2 = e & (N2 - 1);
-        cp_async16(&sm[oo * lds + S(k2)], &Yc[size_t(oo) * half + ((long long)row << l2) + k2]);
+        const int sr = k2 / a.WC;  // column owner
+        cp_async16(&sm[oo * lds + S(k2)], &a.Y[xaddr(a, c, sr, oo, li, k2 - sr * a.WC)]);
     }
     cp_async_wait_all();
     __syncthreads();
@@ -418,7 +439,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
     __shared__ double redv[(NT / 32) * (2 + P)];
     block_sum_vec<NT, 2 + P>(acc, redv);
     if (threadIdx.x == 0) {
-        double* pm = a.part_mid + (size_t(c) * N1 + blockIdx.x) * (2 + P);
+        double* pm = a.part_mid + (size_t(c) * gridDim.x + blockIdx.x) * (2 + P);
 #pragma unroll
         for (int x = 0; x < 2 + P; ++x) pm[x] = acc[x];
     }
@@ -444,7 +465,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
         if (j2 >= N2) break;
         const double2 w = cmul(obase, s_ostep[u]);
         for (int oo = 0; oo < V; ++oo)
-            Yc[size_t(oo) * half + ((long long)row << l2) + j2] = cmulc(sm[oo * lds + S(j2)], w);
+            a.Y[xaddr(a, c, j2 / a.WC, oo, li, j2 - (j2 / a.WC) * a.WC)] = cmulc(sm[oo * lds + S(j2)], w);
     }
 }
 
@@ -457,11 +478,12 @@ __global__ void __launch_bounds__(NT) k_lat_col_inv(LatArgs a, int l1, int l2, i
     __shared__ int s_last;
     const int v = blockIdx.y, c = v / a.V, o = v - c * a.V;
     const int C = 1 << lc, N1 = 1 << l1, ld = padded_len(N1), tile = C << l1;
-    const uint32_t c0 = uint32_t(blockIdx.x) << lc;
+    const uint32_t c0 = uint32_t(a.rank * a.ncb + blockIdx.x) << lc;  // global first column
+    const int jl0 = int(c0) - a.rank * a.WC;
     LatGen<DC, ALPHA> G;
     G.init(a, c, o);  // independent of L2: overlaps its tail
     pdl_wait();
-    const double2* x = a.Y + size_t(v) * a.half;
+    const double2* xb = a.Cbuf;
     int done = 0;
     if ((l1 & 3) == 1) {
         // first (twiddle-free) radix-2 level fused into the load: no radix-2 tail stage; all of a
@@ -474,8 +496,10 @@ __global__ void __launch_bounds__(NT) k_lat_col_inv(LatArgs a, int l1, int l2, i
             const int e = threadIdx.x + u * NT;
             if (e < npair) {
                 const int jj = e >> lc, cc = e & (C - 1);
-                x0[u] = __ldcs(&x[((long long)jj << l2) + c0 + cc]);
-                x1[u] = __ldcs(&x[((long long)(jj + H) << l2) + c0 + cc]);
+                int i0, i1;
+                const int h0 = row_owner(jj, N1, a.QP, i0), h1 = row_owner(jj + H, N1, a.QP, i1);
+                x0[u] = __ldcs(&xb[xaddr(a, c, h0, o, i0, jl0 + cc)]);
+                x1[u] = __ldcs(&xb[xaddr(a, c, h1, o, i1, jl0 + cc)]);
             }
         }
 #pragma unroll
@@ -491,7 +515,9 @@ __global__ void __launch_bounds__(NT) k_lat_col_inv(LatArgs a, int l1, int l2, i
     } else {
         for (int e = threadIdx.x; e < tile; e += NT) {
             const int k1 = e >> lc, cc = e & (C - 1);
-            cp_async16(&sm[cc * ld + S(k1)], &x[((long long)k1 << l2) + c0 + cc]);
+            int i1;
+            const int h1 = row_owner(k1, N1, a.QP, i1);
+            cp_async16(&sm[cc * ld + S(k1)], &xb[xaddr(a, c, h1, o, i1, jl0 + cc)]);
         }
         cp_async_wait_all();
     }
@@ -526,10 +552,11 @@ __global__ void __launch_bounds__(NT) k_lat_col_inv(LatArgs a, int l1, int l2, i
     __syncthreads();
     if (!s_last) return;
     ClassSums t{};
+    t.T = a.T;
     t.P = a.P;
     t.V = a.V;
     t.d = a.d;
-    t.nrows = N1;  // L2 CTAs per candidate
+    t.nrows = a.R;  // L2 CTAs per candidate on this rank
     t.nblk = nblk;
     t.dstride = MAXD + 1;
     t.mid = a.part_mid + size_t(c) * t.nrows * (2 + a.P);
@@ -550,7 +577,7 @@ static void set_smem_lat(K kern, size_t bytes) {
 
 template <int DC, int ALPHA>
 static void lat_cols(const LatGeo& g, const LatArgs& a, size_t sm_col, bool inverse, cudaStream_t s) {
-    const dim3 grid(g.nblk_col, a.V * a.nc);
+    const dim3 grid(a.ncb, a.V * a.nc);
     if (!inverse) {
         auto k = k_lat_col_fwd<LAT_NT, DC, ALPHA>;
         set_smem_lat(k, sm_col);
@@ -578,22 +605,29 @@ static void lat_mid_launch(const LatGeo& g, const LatArgs& a, cudaStream_t s) {
     auto k = a.distinct ? k_lat_mid<LAT_NT, T, true> : k_lat_mid<LAT_NT, T, false>;
     set_smem_lat(k, sm);
     ProfScope ps("lat_mid", s);
-    CK_LAUNCH(launch_pdl(k, dim3(1u << g.l1, a.nc), dim3(LAT_NT), sm, s, true, a, g.l1, g.l2));
+    CK_LAUNCH(launch_pdl(k, dim3(unsigned(a.R), a.nc), dim3(LAT_NT), sm, s, true, a, g.l1, g.l2));
+}
+
+void lat_phase(const LatGeo& g, const LatArgs& a, int phase, cudaStream_t s) {
+    const size_t sm_col = size_t(1 << g.lc) * padded_len(1 << g.l1) * sizeof(double2);
+    if (phase == 1) {
+        if (a.si_alpha == 1) lat_cols_d<1>(g, a, sm_col, false, s);
+        else lat_cols_d<2>(g, a, sm_col, false, s);
+    } else if (phase == 2) {
+        switch (a.T) {
+            case 1: lat_mid_launch<1>(g, a, s); break;
+            case 2: lat_mid_launch<2>(g, a, s); break;
+            case 3: lat_mid_launch<3>(g, a, s); break;
+            default: lat_mid_launch<4>(g, a, s); break;
+        }
+    } else if (a.want_grad) {
+        if (a.si_alpha == 1) lat_cols_d<1>(g, a, sm_col, true, s);
+        else lat_cols_d<2>(g, a, sm_col, true, s);
+    }
 }
 
 void lat_fit(const LatGeo& g, const LatArgs& a, cudaStream_t s) {
-    const size_t sm_col = size_t(1 << g.lc) * padded_len(1 << g.l1) * sizeof(double2);
-    if (a.si_alpha == 1) lat_cols_d<1>(g, a, sm_col, false, s);
-    else lat_cols_d<2>(g, a, sm_col, false, s);
-    switch (a.T) {
-        case 1: lat_mid_launch<1>(g, a, s); break;
-        case 2: lat_mid_launch<2>(g, a, s); break;
-        case 3: lat_mid_launch<3>(g, a, s); break;
-        default: lat_mid_launch<4>(g, a, s); break;
-    }
-    if (!a.want_grad) return;
-    if (a.si_alpha == 1) lat_cols_d<1>(g, a, sm_col, true, s);
-    else lat_cols_d<2>(g, a, sm_col, true, s);
+    for (int phase = 1; phase <= 3; ++phase) lat_phase(g, a, phase, s);
 }
 
 }  // namespace fmtgp

@@ -58,8 +58,21 @@ struct LatArgs {
     const double2* tw;
     int want_grad;
     int distinct;             // pair_ofs is the all-shifts-distinct map (cls_distinct in lattice.cu)
+    // ---- frequency sharding over G ranks (G = 1: one GPU).  Rank g owns the
+    // column blocks [g ncb, (g+1) ncb) of L1 / L3 (WC = N2 / G columns) and the row clusters
+    // [g QP, (g+1) QP) of L2 (R = 2 QP rows: cluster q = rows {q, N1 - q}, or {0, N1/2} for q = 0).
+    // (nrank = G, rank = g.)  The intermediate is stored in exchange blocks Y[h][o][i][jl]: h = the rank that owns the row
+    // (i its local index 2 (q - h QP) + side) and jl the column local to its column owner, so
+    // that "rows of h x my columns" is one contiguous block — the all-to-all's send unit.  L1
+    // writes Y, the all-to-all moves the blocks to their row owners, L2 works in place, a second
+    // all-to-all returns them to the column owners (Cbuf) for L3.  G = 1: Cbuf == Y.
+    int nrank = 1, rank = 0;
+    int QP = 0, R = 0, WC = 0, ncb = 0;
+    const double2* Cbuf = nullptr;
 };
 
 void lat_fit(const LatGeo& g, const LatArgs& a, cudaStream_t s);
+// one phase of it (1: L1, 2: L2, 3: L3 when want_grad) — the sharded fit interleaves all-to-alls
+void lat_phase(const LatGeo& g, const LatArgs& a, int phase, cudaStream_t s);
 
 }  // namespace fmtgp

@@ -321,7 +321,13 @@ struct fmtgp_model {
     // fused three-kernel lattice path (lattice.cuh); shares part_mid / part_dot / counter
     bool lat = false;
     LatGeo lgeo{};
-    int dig_tail = 1;  // digital K3 finalize mode (DigArgs::tail), FMTGP_DIG_TAIL
+    int dig_tail = 1;
+    // frequency sharding of the fused lattice fit (fmtgp_shard_*): world size / rank
+    int sh_G = 1, sh_g = 0;
+    LatArgs sh_args{};
+    fmtgp_hyper sh_h{};
+    bool sh_grad = false;
+    unsigned long long* d_trace = nullptr;  // FMTGP_TRACE=1: digital-fit phase timestamps to stderr  // digital K3 finalize mode (DigArgs::tail), FMTGP_DIG_TAIL
     double kap_b[4]{};
     bool kap_valid = false;
     bool kap_enabled = true;
@@ -555,11 +561,14 @@ void finish_results(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, bool g
         r.escalations = esc[c];
         for (int t = 0; t < T; ++t) r.tau[t] = M->tau[t];
         if (grad) {
-            r.dgamma = o[OUT_DGAMMA];
+            r.dgamma = 0.0;  // q is linear in gamma: dNLL/dgamma = sum_ab R_ab G_ab / gamma
             for (int j = 0; j < M->d; ++j) r.deta[j] = o[OUT_DETA + j];
             const fmtgp_hyper* h = hs[c];
             for (int a = 0; a < T; ++a)
                 for (int b = 0; b < T; ++b) r.dR[a * T + b] = o[OUT_DR + a * MAXT + b];
+            const std::vector<double> R = task_gram(M, h);
+            for (int x = 0; x < T * T; ++x) r.dgamma += R[x] * r.dR[x];
+            r.dgamma /= h->gamma;
             for (int a = 0; a < T; ++a) {
                 r.dt[a] = r.dR[a * T + a];
                 for (int k = 0; k < h->s; ++k) {
@@ -608,6 +617,13 @@ void eval_digital_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, b
     a.out = M->d_out;
     a.want_grad = grad;
     a.tail = M->dig_tail;
+    if (M->d_trace) {
+        std::vector<unsigned long long> init(16, 0);
+        for (int i : {0, 2, 3, 5, 6}) init[i] = ~0ull;
+        CK(cudaMemcpyAsync(M->d_trace, init.data(), 16 * sizeof(unsigned long long), cudaMemcpyHostToDevice, M->st));
+        CK(cudaStreamSynchronize(M->st));
+        a.trace = M->d_trace;
+    }
     dig_fit(M->dgeo, a, M->st);
     CK(cudaGetLastError());
     if (!grad) {
@@ -631,8 +647,7 @@ void eval_digital_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, b
 
 // Fused lattice fit (lattice.cuh): three kernels, spectra and adjoints never leave the SMs /
 // L2 between the row FFT, the solve and the inverse row FFT.
-void eval_lattice_body(fmtgp_model* M, int nc, int si_alpha, bool grad) {
-    copy_hyper(M);  // failure flags are zeroed by the first kernel
+LatArgs lat_args(fmtgp_model* M, int nc, int si_alpha, bool grad) {
     const Group& g = M->groups[0];
     LatArgs a{};
     a.T = M->T;
@@ -668,24 +683,40 @@ void eval_lattice_body(fmtgp_model* M, int nc, int si_alpha, bool grad) {
         const int want = M->pa[p] == M->pb[p] ? 0 : 1 + off++;
         if (M->h_pair_ofs[p] != want) a.distinct = 0;
     }
+    const LatGeo& lg = M->lgeo;
+    a.nrank = M->sh_G;
+    a.rank = M->sh_g;
+    a.QP = (1 << lg.l1) / 2 / a.nrank;
+    a.R = 2 * a.QP;
+    a.WC = (1 << lg.l2) / a.nrank;
+    a.ncb = lg.nblk_col / a.nrank;
+    a.Cbuf = a.Y;
+    return a;
+}
+
+void lat_finalize_nograd(fmtgp_model* M, int nc) {
+    FinalArgs fa{};
+    fa.T = M->T;
+    fa.P = M->P;
+    fa.d = M->d;
+    fa.ncand = nc;
+    fa.nblk_solve = (1 << M->lgeo.l1) / M->sh_G;
+    fa.solve_partial = M->d_part_mid;
+    fa.solve_stride = 2 + M->P;
+    fa.Rpair = M->d_Rpair;
+    fa.gamma = M->d_gamma;
+    fa.pair_a = M->d_pa;
+    fa.pair_b = M->d_pb;
+    fa.out = M->d_out;
+    finalize(fa, M->st);
+}
+
+void eval_lattice_body(fmtgp_model* M, int nc, int si_alpha, bool grad) {
+    copy_hyper(M);  // failure flags are zeroed by the first kernel
+    const LatArgs a = lat_args(M, nc, si_alpha, grad);
     lat_fit(M->lgeo, a, M->st);
     CK(cudaGetLastError());
-    if (!grad) {
-        FinalArgs fa{};
-        fa.T = M->T;
-        fa.P = M->P;
-        fa.d = M->d;
-        fa.ncand = nc;
-        fa.nblk_solve = 1 << M->lgeo.l1;
-        fa.solve_partial = M->d_part_mid;
-        fa.solve_stride = 2 + M->P;
-        fa.Rpair = M->d_Rpair;
-        fa.gamma = M->d_gamma;
-        fa.pair_a = M->d_pa;
-        fa.pair_b = M->d_pb;
-        fa.out = M->d_out;
-        finalize(fa, M->st);
-    }
+    if (!grad) lat_finalize_nograd(M, nc);
     CK(cudaMemcpyAsync(M->h_res, M->d_res, sizeof(double) * M->res_len, cudaMemcpyDeviceToHost, M->st));
 }
 
@@ -710,7 +741,7 @@ void eval_equal_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, boo
         eval_digital_body(M, nc, si_alpha, bw, grad, keep_chat);
         return;
     }
-    if (M->lat && !keep_chat) {
+    if (M->lat && M->sh_G == 1 && !keep_chat) {  // a sharded model's plain nll takes the generic path
         eval_lattice_body(M, nc, si_alpha, grad);
         return;
     }
@@ -763,6 +794,7 @@ void eval_equal_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, boo
             CK(cudaGetLastError());
         }
         ClassFinalArgs fa{};
+        fa.T = M->T;
         fa.P = M->P;
         fa.V = M->nofs;
         fa.d = M->d;
@@ -834,6 +866,18 @@ void eval_equal(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, const doub
         if (e.nc == nc && e.grad == int(grad) && e.keep_chat == int(keep_chat) && e.si_alpha == h0->si_alpha &&
             e.prof == prof && std::memcmp(e.b, h0->b, sizeof(e.b)) == 0)
             ge = &e;
+    if (M->d_trace) {  // diagnostics: always eager, print the phase marks
+        eval_equal_body(M, nc, h0->si_alpha, h0->b, grad, keep_chat);
+        CK(cudaStreamSynchronize(M->st));
+        unsigned long long t[16];
+        CK(cudaMemcpy(t, M->d_trace, sizeof(t), cudaMemcpyDeviceToHost));
+        const char* nm[11] = {"K1 first entry", "K1 last exit", "K2 first entry", "K2 first past wait", "K2 last exit",
+                              "K3 first entry", "K3 first past wait", "K3 last exit (pre-ticket)", "tail: ticket",
+                              "tail: staged", "tail: done"};
+        for (int i = 0; i < 11; ++i)
+            if (t[i] && t[i] != ~0ull) std::fprintf(stderr, "trace %-26s %8.2f us\n", nm[i], 1e-3 * double(t[i] - t[0]));
+        return;
+    }
     if (!M->use_graphs || !ge || ge->runs == 0) {
         eval_equal_body(M, nc, h0->si_alpha, h0->b, grad, keep_chat);
         CK(cudaStreamSynchronize(M->st));
@@ -975,6 +1019,8 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
         if (const char* e = std::getenv("FMTGP_KAPPA_TABLE")) M->kap_enabled = e[0] != '0';
         if (const char* e = std::getenv("FMTGP_CLASSES")) M->class_mode = e[0] != '0';
         if (const char* e = std::getenv("FMTGP_DIG_TAIL")) M->dig_tail = std::atoi(e);
+        if (const char* e = std::getenv("FMTGP_TRACE"))
+            if (e[0] == '1') M->d_trace = dalloc<unsigned long long>(16);
         M->off[0] = 0;
         for (int l = 0; l < M->T; ++l) {
             M->m[l] = dz->m[l];
@@ -1487,6 +1533,7 @@ int fmtgp_model_destroy(fmtgp_model_t M) {
     F(M->d_part_mid);
     F(M->d_part_dot);
     F(M->d_counter);
+    F(M->d_trace);
     F(M->d_vec_sum);
     F(M->d_pair_ofs);
     F(M->d_scratch);
@@ -1817,6 +1864,80 @@ int fmtgp_fit(fmtgp_model_t M, const fmtgp_hyper* init, int steps, double* theta
         CK(cudaSetDevice(M->dev));
         validate_hyper(M, init);
         fit_impl(M, init, steps, theta_best, loss_trace, step_seconds, rep);
+    });
+}
+
+// ---- frequency-sharded lattice fit: one rank's three phases; the caller runs
+// the two all-to-alls of the exchange blocks between them and sums the records over ranks.
+int fmtgp_shard_setup(fmtgp_model_t M, int rank, int world, int64_t* exchange_elems) {
+    return guarded([&] {
+        if (!M || !exchange_elems) invalid("shard_setup: null argument");
+        if (!M->lat)
+            throw Fail{FMTGP_ERR_UNSUPPORTED, "shard_setup: only the fused equal-n lattice fit shards (n >= 2^17, T <= 4)"};
+        const LatGeo& g = M->lgeo;
+        const int clusters = (1 << g.l1) / 2;
+        if (world < 1 || rank < 0 || rank >= world || clusters % world || g.nblk_col % world || (1 << g.l2) % world)
+            invalid("shard_setup: the world size must divide the row clusters and the column blocks");
+        M->sh_G = world;
+        M->sh_g = rank;
+        *exchange_elems = (int64_t)M->nofs * M->pslots[0] / world;
+    });
+}
+
+int fmtgp_shard_begin(fmtgp_model_t M, const fmtgp_hyper* h, int want_grad, double xi_scale, void* Y) {
+    return guarded([&] {
+        if (!M || !h || !Y) invalid("shard_begin: null argument");
+        if (!M->lat) invalid("shard_begin: model is not sharded (fmtgp_shard_setup)");
+        if (!M->have_y) invalid("nll: observations not set (fmtgp_model_set_y)");
+        validate_hyper(M, h);
+        CK(cudaSetDevice(M->dev));
+        const fmtgp_hyper* hs[1] = {h};
+        fill_hyper(M, 1, hs, &xi_scale);
+        copy_hyper(M);
+        M->sh_args = lat_args(M, 1, h->si_alpha, want_grad != 0);
+        M->sh_args.Y = static_cast<double2*>(Y);
+        M->sh_grad = want_grad != 0;
+        lat_phase(M->lgeo, M->sh_args, 1, M->st);
+        CK(cudaGetLastError());
+    });
+}
+
+int fmtgp_shard_mid(fmtgp_model_t M, void* Y) {
+    return guarded([&] {
+        if (!M || !Y) invalid("shard_mid: null argument");
+        CK(cudaSetDevice(M->dev));
+        M->sh_args.Y = static_cast<double2*>(Y);
+        lat_phase(M->lgeo, M->sh_args, 2, M->st);
+        CK(cudaGetLastError());
+    });
+}
+
+int fmtgp_shard_end(fmtgp_model_t M, const void* Cbuf, double* rec) {
+    return guarded([&] {
+        if (!M || !Cbuf || !rec) invalid("shard_end: null argument");
+        CK(cudaSetDevice(M->dev));
+        M->sh_args.Cbuf = static_cast<const double2*>(Cbuf);
+        if (M->sh_grad) lat_phase(M->lgeo, M->sh_args, 3, M->st);
+        else lat_finalize_nograd(M, 1);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(M->h_res, M->d_res, sizeof(double) * M->res_len, cudaMemcpyDeviceToHost, M->st));
+        CK(cudaStreamSynchronize(M->st));
+        for (int x = 0; x < NOUT; ++x) rec[x] = M->h_out[x];
+        rec[NOUT] = double(M->h_bad[0]);
+        for (int x = 0; x < 2 * MAXT; ++x) rec[NOUT + 1 + x] = M->h_imre[x];
+    });
+}
+
+int fmtgp_shard_finish(fmtgp_model_t M, const fmtgp_hyper* h, const double* rec, int want_grad, double xi_scale,
+                       int escalations, fmtgp_result* out) {
+    return guarded([&] {
+        if (!M || !h || !rec || !out) invalid("shard_finish: null argument");
+        for (int x = 0; x < NOUT; ++x) M->h_out[x] = rec[x];
+        M->h_bad[0] = int(rec[NOUT]);
+        for (int x = 0; x < 2 * MAXT; ++x) M->h_imre[x] = rec[NOUT + 1 + x];
+        const fmtgp_hyper* hs[1] = {h};
+        finish_results(M, 1, hs, want_grad != 0, out, &xi_scale, &escalations);
+        out->status = nonreal_of(M, 0) ? FMTGP_ERR_NONREAL : (M->h_bad[0] != BAD_NONE ? FMTGP_ERR_SCHUR : FMTGP_OK);
     });
 }
 

@@ -4,9 +4,13 @@
   independent — contiguous blocks per rank, no data-path collective, one gather of the small
   per-candidate result records at the end.  Results are bit-identical to a single-GPU sweep
   (each candidate's evaluation does not depend on its batch neighbours; tested).
-* Frequency sharding of the per-frequency solves (config 4) uses `freq_slab`: rank r owns the
-  contiguous slot range of the four-step row pass, so after the column pass + all-to-all the
-  solve and the adjoint are local and only {logdet, quad, dR, deta} are all-reduced.
+* Frequency sharding of the fused lattice fit (config 4, `sharded_nll`): rank r owns a block of
+  column tiles of the four-step column passes and a block of row clusters (Hermitian partner row
+  pairs) of the row pass.  Per evaluation: column pass -> all-to-all -> row FFT + per-frequency
+  solve + inverse row FFT -> all-to-all -> inverse column pass + gradient dot -> one gather of
+  the 101-double records, summed in rank order (deterministic).  The three phases are the
+  library's fmtgp_shard_{begin,mid,end} (include/fastmtgp_b200.h); the exchanges are
+  torch.distributed all_to_all_single (NCCL over NVLink on the GPU box, gloo in the CPU tests).
 """
 from __future__ import annotations
 
@@ -44,3 +48,163 @@ def sweep(evaluate: Callable[[Sequence], List[dict]], candidates: Sequence, worl
     for part in gathered:
         out.extend(part)
     return out
+
+
+# ----------------------------------------------------------------------------- frequency sharding
+NOUT = 4 + 16 + 8 * 8  # result record (csrc/kernels.cuh OUT_*)
+
+
+def combine_records(recs) -> "np.ndarray":
+    """Rank-order sum of the NOUT sums, min of the first failing slot, max of the per-stage
+    non-real maxima (fmtgp_shard_end's record layout)."""
+    import numpy as np
+    recs = [np.asarray(r, dtype=np.float64) for r in recs]
+    out = recs[0].copy()
+    for r in recs[1:]:
+        out[:NOUT] += r[:NOUT]
+        out[NOUT] = min(out[NOUT], r[NOUT])
+        out[NOUT + 1:] = np.maximum(out[NOUT + 1:], r[NOUT + 1:])
+    return out
+
+
+class ShardedLatticeFit:
+    """One rank of the frequency-sharded fused lattice fit (equal n, n >= 2^17, T <= 4).
+
+    `exchange(send, recv)` is an all-to-all of `world` equal chunks (default: torch.distributed
+    all_to_all_single on the model's stream) and `gather(rec)` returns every rank's record in
+    rank order (default: torch.distributed.all_gather).  Both are injectable so the same
+    orchestration runs with virtual ranks on one device (tests)."""
+
+    def __init__(self, design, rank: int, world: int, device: int = 0, model=None):
+        import ctypes as C
+
+        import torch
+
+        from .fast_gram import Model
+        from ._lib import check
+
+        self.rank, self.world = rank, world
+        self.model = model if model is not None else Model(design, device=device)
+        n = C.c_int64()
+        check(self.model.lib.fmtgp_shard_setup(self.model.h, rank, world, C.byref(n)))
+        self.elems = int(n.value)  # complex values per exchange buffer
+        dev = torch.device("cuda", device)
+        self.bufs = [torch.empty(2 * self.elems, dtype=torch.float64, device=dev) for _ in range(2)]
+        self.stream = torch.cuda.ExternalStream(self.model.stream, device=dev)
+
+    def set_y(self, y):
+        self.model.set_y(y)
+
+    # -- the three phases (asynchronous on the model's stream except `end`)
+    def begin(self, hp, grad: bool, xi_scale: float):
+        from ._lib import check
+        ch = self.model._hyper_struct(hp)
+        import ctypes as C
+        check(self.model.lib.fmtgp_shard_begin(self.model.h, C.byref(ch), int(grad), float(xi_scale),
+                                               C.c_void_p(self.bufs[0].data_ptr())))
+        return self.bufs[0]
+
+    def mid(self):
+        from ._lib import check
+        import ctypes as C
+        check(self.model.lib.fmtgp_shard_mid(self.model.h, C.c_void_p(self.bufs[1].data_ptr())))
+        return self.bufs[1]
+
+    def end(self):
+        import ctypes as C
+
+        import numpy as np
+
+        from ._lib import SHARD_REC_LEN, check
+        rec = np.zeros(SHARD_REC_LEN)
+        check(self.model.lib.fmtgp_shard_end(self.model.h, C.c_void_p(self.bufs[0].data_ptr()),
+                                             rec.ctypes.data_as(C.POINTER(C.c_double))))
+        return rec
+
+    def finish(self, hp, rec, grad: bool, xi_scale: float, escalations: int):
+        import ctypes as C
+
+        import numpy as np
+
+        from ._lib import CResult, check
+        from .fast_gram import _result
+        ch = self.model._hyper_struct(hp)
+        r = CResult()
+        rec = np.ascontiguousarray(rec, dtype=np.float64)
+        check(self.model.lib.fmtgp_shard_finish(self.model.h, C.byref(ch), rec.ctypes.data_as(C.POINTER(C.c_double)),
+                                                int(grad), float(xi_scale), int(escalations), C.byref(r)))
+        return _result(r, self.model.design, hp)
+
+    def default_exchange(self, send, recv, group=None):
+        import torch
+        import torch.distributed as dist
+        with torch.cuda.stream(self.stream):
+            dist.all_to_all_single(recv, send, group=group)
+
+    def default_gather(self, rec, group=None):
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+        t = torch.from_numpy(np.asarray(rec, dtype=np.float64)).to(self.bufs[0].device)
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(out, t, group=group)
+        return [o.cpu().numpy() for o in out]
+
+
+def sharded_nll(ranks, hp, grad: bool = True, exchange=None, gather=None, max_retries: int = 6):
+    """Frequency-sharded NLL (+ gradient) with the reference's escalation schedule
+    (xi x 10 per SchurBreakdown, at most 6 retries, gp_core.cpp:98-127).
+
+    `ranks` is this process's ShardedLatticeFit (one element, multi-process) or all of them
+    (virtual ranks on one device, in which case `exchange` / `gather` act on the list)."""
+    from ._lib import ERR_NONREAL, ERR_SCHUR, FastMtgpError, SchurBreakdown
+    local = list(ranks)
+    scale, attempt = 1.0, 0
+    while True:
+        sends = [r.begin(hp, grad, scale) for r in local]
+        recvs = [r.bufs[1] for r in local]
+        exchange(sends, recvs)  # column blocks -> row owners
+        mids = [r.mid() for r in local]
+        backs = [r.bufs[0] for r in local]
+        exchange(mids, backs)  # row blocks -> column owners
+        recs = [r.end() for r in local]
+        allrec = gather(recs)
+        rec = combine_records(allrec)
+        res = local[0].finish(hp, rec, grad, scale, attempt)
+        if res["status"] == ERR_SCHUR and attempt < max_retries:
+            scale *= 10.0
+            attempt += 1
+            continue
+        if res["status"] == ERR_SCHUR:  # as fmtgp_nll: schedule exhausted
+            raise SchurBreakdown("noise escalation schedule exhausted")
+        if res["status"] == ERR_NONREAL:
+            raise FastMtgpError("invert_and_logdet: non-real Schur complement")
+        return res
+
+
+def local_exchange(world: int):
+    """All-to-all among virtual ranks on one device: block h of rank g's send buffer -> block g
+    of rank h's receive buffer (each rank's buffer = `world` equal chunks)."""
+    def ex(sends, recvs):
+        import torch
+        torch.cuda.synchronize()
+        chunks = [s.view(world, -1) for s in sends]
+        for h in range(world):
+            rv = recvs[h].view(world, -1)
+            for g in range(world):
+                rv[g].copy_(chunks[g][h])
+        torch.cuda.synchronize()
+    return ex
+
+
+def dist_exchange(rank_obj, group=None):
+    """Multi-process all-to-all (torch.distributed; NCCL on GPUs), ordered on the model's stream."""
+    def ex(sends, recvs):
+        rank_obj.default_exchange(sends[0], recvs[0], group)
+    return ex
+
+
+def dist_gather(rank_obj, group=None):
+    def ga(recs):
+        return rank_obj.default_gather(recs[0], group)
+    return ga

@@ -171,3 +171,46 @@ def test_fused_escalation_matches_generic():
         return
     assert rf["escalations"] == rg["escalations"]
     assert abs(rf["nll"] - rg["nll"]) <= 1e-8 * dz.N
+
+
+@pytest.mark.parametrize("case", [(18, 2, 4, 1, 2), (18, 2, 4, 1, 4), (17, 3, 5, 2, 2), (19, 4, 3, 1, 8), (18, 1, 2, 1, 4)],
+                         ids=lambda c: "m%d-T%d-d%d-a%d-G%d" % c)
+def test_frequency_sharded_virtual_ranks(case):
+    """SURVEY.md §8e frequency sharding, G virtual ranks on one device: each rank runs its own
+    column / row-cluster share of the three fused kernels into exchange blocks; the all-to-alls are
+    block copies between the ranks' buffers (no kernel waits on another rank), the records are
+    summed in rank order.  Must equal the one-GPU fused fit (same arithmetic, other summation
+    grouping of the partials)."""
+    from paper_2603_16014_b200 import sharding
+    m, T, d, alpha, G = case
+    dz, hp, y = make(m, T, d, alpha)
+    want = model(dz, y, True).nll(hp, grad=True)
+    ranks = []
+    for g in range(G):
+        r = sharding.ShardedLatticeFit(dz, g, G, model=model(dz, y, True))
+        ranks.append(r)
+    got = sharding.sharded_nll(ranks, hp, grad=True, exchange=sharding.local_exchange(G), gather=lambda recs: recs)
+    close_results(got, want, dz.N, 1e-11)
+    nog = sharding.sharded_nll(ranks, hp, grad=False, exchange=sharding.local_exchange(G), gather=lambda recs: recs)
+    assert abs(nog["nll"] - want["nll"]) <= 1e-11 * abs(want["nll"])
+
+
+def test_frequency_sharded_escalation_matches_single():
+    """A rank-deficient task Gram with zero nugget escalates the same number of times sharded."""
+    from paper_2603_16014_b200 import sharding
+    dz, hp, y = make(18, 2, 2, 1)
+    hp = hp.replace(B=np.array([[1.0, 0.0], [1.0, 0.0]]), t=np.array([1e-300, 1e-300]), xi=np.zeros(2))
+    try:
+        want = model(dz, y, True).nll(hp, grad=False)
+    except Exception as e:  # noqa: BLE001
+        want = type(e).__name__
+    ranks = [sharding.ShardedLatticeFit(dz, g, 2, model=model(dz, y, True)) for g in range(2)]
+    try:
+        got = sharding.sharded_nll(ranks, hp, grad=False, exchange=sharding.local_exchange(2), gather=lambda r: r)
+    except Exception as e:  # noqa: BLE001
+        got = type(e).__name__
+    if isinstance(want, str):
+        assert got == want
+    else:
+        assert got["escalations"] == want["escalations"]
+        assert abs(got["nll"] - want["nll"]) <= 1e-8 * dz.N
