@@ -12,7 +12,7 @@ __device__ __forceinline__ void dig_trace(unsigned long long* tr, int slot, bool
     else atomicMax(tr + slot, t);
 }
 
-bool DigGeo::make(int m, int P, DigGeo& g, long long total_vecs) {
+bool DigGeo::make(int m, int P, DigGeo& g, long long total_vecs, int d) {
     if (m < 1 || P < 1) return false;
     // row length: all P (= class count V) rows of one frequency block in <= 64 KB of smem
     int l2max = 0;
@@ -26,6 +26,7 @@ bool DigGeo::make(int m, int P, DigGeo& g, long long total_vecs) {
     // column tile: >= ~4 CTAs per SM over all vectors, 2^10..2^11 elements, <= 2^(l1 + l2)
     int tl = 11;
     if (total_vecs > 0 && ((total_vecs << m) >> tl) < 4 * 148) tl = 10;
+    if (d > 4) tl = 10;  // kappa tile d * 2^tl doubles: keep >= 2 CTAs per SM (config 5: d = 10)
     tl = std::max(tl, g.l1);
     g.lc = std::min(tl - g.l1, l2);
     if (g.lc < 0) return false;
@@ -95,59 +96,67 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_fwd(DigArgs a, int l1, int l2
     extern __shared__ __align__(16) double sm[];
     __shared__ GenSmem<D> tab;
     dig_trace(a.trace, 0, true);
-    const int v = blockIdx.y, c = v / a.V, o = v - c * a.V;
+    // candidate group: the CTA evaluates candidates [cb, ce) against one kappa tile (read once)
+    const int o = blockIdx.y % a.V, cb = (blockIdx.y / a.V) * a.cpb, ce = min(a.nc, cb + a.cpb);
     const int C = 1 << lc, N1 = 1 << l1, ld = padded_len(N1);
     const long long c0 = (long long)blockIdx.x << lc, n = a.n;
-    double eta[D];
-#pragma unroll
-    for (int j = 0; j < D; ++j) eta[j] = __ldg(a.eta + size_t(c) * D + j);
-    const double gam = __ldg(a.gamma + c);
-    GenSrc g{};
-    uint64_t off[D];
-    if (!a.kap) {
-        g.sp = a.sp;
-        g.pg = a.pg;
-        g.eta = a.eta;
-        gen_smem_init<D>(tab, g, c);
-#pragma unroll
-        for (int j = 0; j < D; ++j) off[j] = __ldg(a.cofs + size_t(o) * MAXD + j);
-        __syncthreads();
-    }
     const double* kp = a.kap ? a.kap + size_t(o) * D * n : nullptr;
     const int tile = C << l1;
+    double* kbuf = sm + kbuf_offset(C, ld);
     if (kp) {
         // design-time kappa tile -> smem with cp.async (no register staging)
-        double* kbuf = sm + kbuf_offset(C, ld);
         load_kappa_tile<NT, D>(kbuf, kp, n, l1, l2, lc, c0);
         cp_async_wait_all();
-        __syncthreads();
-        for (int e = threadIdx.x; e < tile; e += NT) {
-            double kappa[D];
+    }
+    uint64_t off[D];
+    if (!kp) {
 #pragma unroll
-            for (int j = 0; j < D; ++j) kappa[j] = kbuf[j * tile + e];
-            sm[(e & (C - 1)) * ld + sidx<true>(e >> lc)] = product_kernel_d<D, false>(kappa, eta, gam, nullptr);
-        }
-    } else {
-        for (int e = threadIdx.x; e < tile; e += NT) {
-            const int j1 = e >> lc, cc = e & (C - 1);
-            const long long i = ((long long)j1 << l2) + c0 + cc;
-            double kappa[D];
-            kappa_d<D>(g, tab, off, uint64_t(i), kappa);
-            sm[cc * ld + sidx<true>(j1)] = product_kernel_d<D, false>(kappa, eta, gam, nullptr);
-        }
+        for (int j = 0; j < D; ++j) off[j] = __ldg(a.cofs + size_t(o) * MAXD + j);
     }
-    pdl_trigger();
-    // zero the per-fit flags once per fit (K2 / K3 run after this kernel)
-    if (blockIdx.x == 0 && blockIdx.y == 0) {
-        for (int t = threadIdx.x; t < a.nc; t += NT) a.bad[t] = 0x7f7f7f7f;
-        for (int t = threadIdx.x; t < a.nc * MAXT * 2; t += NT) a.imre[t] = 0ull;
-    }
-    __syncthreads();
-    smem_wht<NT, true>(sm, l1, C, ld);
-    double* out = a.Y + size_t(v) * n;
-    for (int e = threadIdx.x; e < (C << l1); e += NT) {
-        const int k1 = e >> lc, cc = e & (C - 1);
-        out[((long long)k1 << l2) + c0 + cc] = sm[cc * ld + sidx<true>(k1)];
+#pragma unroll 1
+    for (int c = cb; c < ce; ++c) {
+        double eta[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) eta[j] = __ldg(a.eta + size_t(c) * D + j);
+        const double gam = __ldg(a.gamma + c);
+        GenSrc g{};
+        __syncthreads();  // previous candidate's store phase is done with sm / tab
+        if (kp) {
+            for (int e = threadIdx.x; e < tile; e += NT) {
+                double kappa[D];
+#pragma unroll
+                for (int j = 0; j < D; ++j) kappa[j] = kbuf[j * tile + e];
+                sm[(e & (C - 1)) * ld + sidx<true>(e >> lc)] = product_kernel_d<D, false>(kappa, eta, gam, nullptr);
+            }
+        } else {
+            g.sp = a.sp;
+            g.pg = a.pg;
+            g.eta = a.eta;
+            gen_smem_init<D>(tab, g, c);
+            __syncthreads();
+            for (int e = threadIdx.x; e < tile; e += NT) {
+                const int j1 = e >> lc, cc = e & (C - 1);
+                const long long i = ((long long)j1 << l2) + c0 + cc;
+                double kappa[D];
+                kappa_d<D>(g, tab, off, uint64_t(i), kappa);
+                sm[cc * ld + sidx<true>(j1)] = product_kernel_d<D, false>(kappa, eta, gam, nullptr);
+            }
+        }
+        if (c == cb) {
+            pdl_trigger();
+            // zero the per-fit flags once per fit (K2 / K3 run after this kernel)
+            if (blockIdx.x == 0 && blockIdx.y == 0) {
+                for (int t = threadIdx.x; t < a.nc; t += NT) a.bad[t] = 0x7f7f7f7f;
+                for (int t = threadIdx.x; t < a.nc * MAXT * 2; t += NT) a.imre[t] = 0ull;
+            }
+        }
+        __syncthreads();
+        smem_wht<NT, true>(sm, l1, C, ld);
+        double* out = a.Y + (size_t(c) * a.V + o) * n;
+        for (int e = threadIdx.x; e < (C << l1); e += NT) {
+            const int k1 = e >> lc, cc = e & (C - 1);
+            out[((long long)k1 << l2) + c0 + cc] = sm[cc * ld + sidx<true>(k1)];
+        }
     }
     dig_trace(a.trace, 1, false);
 }
@@ -265,10 +274,11 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
     extern __shared__ __align__(16) double sm[];
     __shared__ GenSmem<D> tab;
     __shared__ int s_last;
-    const int v = blockIdx.y, c = v / a.V, o = v - c * a.V;
+    // candidate group: the CTA evaluates candidates [cb, ce) against one kappa tile (read once)
+    const int o = blockIdx.y % a.V, cb = (blockIdx.y / a.V) * a.cpb, ce = min(a.nc, cb + a.cpb);
+    const int c = cb;  // the last-CTA tail (tail == 1) runs only with one candidate per CTA
     const int C = 1 << lc, N1 = 1 << l1, ld = padded_len(N1);
     const long long c0 = (long long)blockIdx.x << lc, n = a.n;
-    const double* x = a.Y + size_t(v) * n;
     const int tile = C << l1;
     double* kbuf = sm + kbuf_offset(C, ld);
     // the kappa tile does not depend on K2: it streams in while K2 finishes (PDL) and while the
@@ -278,65 +288,74 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
     pdl_wait();
     dig_trace(a.trace, 6, true);
     if (a.tail != 1) pdl_trigger();  // separate finalize kernel: let its CTA become resident now
-    for (int e = threadIdx.x; e < tile; e += NT) {
-        const int k1 = e >> lc, cc = e & (C - 1);
-        cp_async8(&sm[cc * ld + sidx<true>(k1)], &x[((long long)k1 << l2) + c0 + cc]);
-    }
-    double eta[D];
-#pragma unroll
-    for (int j = 0; j < D; ++j) eta[j] = __ldg(a.eta + size_t(c) * D + j);
-    const double gam = __ldg(a.gamma + c);
-    GenSrc g{};
     uint64_t off[D];
     if (!a.kap) {
-        g.sp = a.sp;
-        g.pg = a.pg;
-        g.eta = a.eta;
-        gen_smem_init<D>(tab, g, c);
 #pragma unroll
         for (int j = 0; j < D; ++j) off[j] = __ldg(a.cofs + size_t(o) * MAXD + j);
     }
     const double* kp = a.kap ? a.kap + size_t(o) * D * n : nullptr;
-    double acc[D + 1];
-#pragma unroll
-    for (int j = 0; j <= D; ++j) acc[j] = 0.0;
-    if (kp) {
-        cp_async_wait_all();
-        __syncthreads();
-        smem_wht<NT, true>(sm, l1, C, ld);
-        for (int e = threadIdx.x; e < tile; e += NT) {
-            const double W = sm[(e & (C - 1)) * ld + sidx<true>(e >> lc)];  // W = H M, natural index
-            double kappa[D], dq[D];
-#pragma unroll
-            for (int j = 0; j < D; ++j) kappa[j] = kbuf[j * tile + e];
-            const double q = product_kernel_d<D, true>(kappa, eta, gam, dq);
-#pragma unroll
-            for (int j = 0; j < D; ++j) acc[j] = fma(W, dq[j], acc[j]);
-            acc[D] = fma(W, q, acc[D]);
-        }
-    } else {
-        cp_async_wait_all();
-        __syncthreads();
-        smem_wht<NT, true>(sm, l1, C, ld);
-        for (int e = threadIdx.x; e < tile; e += NT) {
-            const int j1 = e >> lc, cc = e & (C - 1);
-            const long long i = ((long long)j1 << l2) + c0 + cc;
-            const double W = sm[cc * ld + sidx<true>(j1)];
-            double kappa[D], dq[D];
-            kappa_d<D>(g, tab, off, uint64_t(i), kappa);
-            const double q = product_kernel_d<D, true>(kappa, eta, gam, dq);
-#pragma unroll
-            for (int j = 0; j < D; ++j) acc[j] = fma(W, dq[j], acc[j]);
-            acc[D] = fma(W, q, acc[D]);
-        }
-    }
     const int nblk = gridDim.x;
-    double* out = a.part_dot + (size_t(v) * nblk + blockIdx.x) * (MAXD + 1);
-    __shared__ double redv[(NT / 32) * (D + 1)];
-    block_sum_vec<NT, D + 1>(acc, redv);
-    if (threadIdx.x == 0) {
+    __shared__ double redv[(NT / 32) * D];
+    // candidate groups double-buffer the column tile: candidate c + 1's tile streams in while c is
+    // transformed and reduced (second buffer after the kappa tile)
+    double* tiles[2] = {sm, kbuf + (a.kap ? D * tile : 0) + 2};
+    auto load_tile = [&](double* dst, int cand) {
+        const double* x = a.Y + (size_t(cand) * a.V + o) * n;
+        for (int e = threadIdx.x; e < tile; e += NT) {
+            const int k1 = e >> lc, cc = e & (C - 1);
+            cp_async8(&dst[cc * ld + sidx<true>(k1)], &x[((long long)k1 << l2) + c0 + cc]);
+        }
+    };
+    load_tile(tiles[0], cb);
+    GenSrc g{};
+    if (!kp) {  // XOR tables of the digital net (candidate-independent)
+        g.sp = a.sp;
+        g.pg = a.pg;
+        g.eta = a.eta;
+        gen_smem_init<D>(tab, g, cb, /*load_eta=*/false);
+    }
+#pragma unroll 1
+    for (int cc2 = cb; cc2 < ce; ++cc2) {
+        double* tb = tiles[(cc2 - cb) & 1];
+        double eta[D];
 #pragma unroll
-        for (int j = 0; j <= D; ++j) out[j == D ? MAXD : j] = acc[j];
+        for (int j = 0; j < D; ++j) eta[j] = __ldg(a.eta + size_t(cc2) * D + j);
+        const double gam = __ldg(a.gamma + cc2);
+        double acc[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) acc[j] = 0.0;
+        cp_async_wait_all();  // this candidate's tile (and, first time, the kappa tile)
+        __syncthreads();      // ... visible to all; the previous candidate is done with the other buffer
+        if (cc2 + 1 < ce) load_tile(tiles[(cc2 + 1 - cb) & 1], cc2 + 1);
+        smem_wht<NT, true>(tb, l1, C, ld);
+        if (kp) {
+            for (int e = threadIdx.x; e < tile; e += NT) {
+                const double W = tb[(e & (C - 1)) * ld + sidx<true>(e >> lc)];  // W = H M, natural index
+                double kappa[D], dq[D];
+#pragma unroll
+                for (int j = 0; j < D; ++j) kappa[j] = kbuf[j * tile + e];
+                product_kernel_d<D, true>(kappa, eta, gam, dq);
+#pragma unroll
+                for (int j = 0; j < D; ++j) acc[j] = fma(W, dq[j], acc[j]);
+            }
+        } else {
+            for (int e = threadIdx.x; e < tile; e += NT) {
+                const int j1 = e >> lc, cc = e & (C - 1);
+                const long long i = ((long long)j1 << l2) + c0 + cc;
+                const double W = tb[cc * ld + sidx<true>(j1)];
+                double kappa[D], dq[D];
+                kappa_d<D>(g, tab, off, uint64_t(i), kappa);
+                product_kernel_d<D, true>(kappa, eta, gam, dq);
+#pragma unroll
+                for (int j = 0; j < D; ++j) acc[j] = fma(W, dq[j], acc[j]);
+            }
+        }
+        block_sum_vec<NT, D>(acc, redv);
+        if (threadIdx.x == 0) {
+            double* out = a.part_dot + ((size_t(cc2) * a.V + o) * nblk + blockIdx.x) * (MAXD + 1);
+#pragma unroll
+            for (int j = 0; j < D; ++j) out[j] = acc[j];
+        }
     }
     dig_trace(a.trace, 7, false);
     if (a.tail != 1) return;  // k_dig_finalize reduces the partials
@@ -435,10 +454,11 @@ static void mid_launch(const DigGeo& g, const DigArgs& a, size_t sm, cudaStream_
 void dig_fit(const DigGeo& g, const DigArgs& a, cudaStream_t s) {
     const int C = 1 << g.lc;
     // K1/K3 dynamic smem: column tile (+ kappa tile); K3's last CTA reuses it to stage partials
-    const size_t tile_words = size_t(kbuf_offset(C, padded_len(1 << g.l1))) + (a.kap ? size_t(a.d) << (g.l1 + g.lc) : 0);
+    const size_t tile_words = size_t(kbuf_offset(C, padded_len(1 << g.l1))) + (a.kap ? size_t(a.d) << (g.l1 + g.lc) : 0) +
+                              (a.cpb > 1 ? size_t(C) * padded_len(1 << g.l1) + 2 : 0);  // K3's second column tile
     const size_t stage_words = ((size_t(1 << g.l1) * (2 + a.P) + 1) & ~size_t(1)) + size_t(a.V) * g.nblk_col * a.d;
     const size_t sm_col = std::max(tile_words, stage_words) * sizeof(double);
-    const dim3 gcol(g.nblk_col, a.V * a.nc);
+    const dim3 gcol(g.nblk_col, a.V * ((a.nc + a.cpb - 1) / a.cpb));
     FM_D_DISPATCH(a.d, {
         FM_NT_DISPATCH(g.nt_col, {
             auto k1 = k_dig_col_fwd<NT, D>;

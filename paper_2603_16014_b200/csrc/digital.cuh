@@ -24,7 +24,7 @@ struct DigGeo {
     int lc;          // log2 columns per K1/K3 CTA (tile = 2^(l1 + lc) <= 2^11)
     int nt_col, nt_mid;
     int nblk_col;    // K1/K3 CTAs per vector
-    static bool make(int m, int V, DigGeo& g, long long total_vecs = 0);  // V rows per K2 CTA
+    static bool make(int m, int V, DigGeo& g, long long total_vecs = 0, int d = 0);  // V rows per K2 CTA
 };
 
 struct DigArgs {
@@ -56,6 +56,7 @@ struct DigArgs {
     double* out;              // [nc][NOUT]
     int want_grad;
     unsigned long long* trace = nullptr;  // FMTGP_TRACE diagnostics: globaltimer marks (see dig_trace)
+    int cpb = 1;              // candidates per K1/K3 CTA (the kappa tile is read once per CTA)
     int tail = 1;             // 1: last CTA of K3 reduces; 0: separate finalize kernel; 2: same, PDL-launched
 };
 

@@ -617,6 +617,16 @@ void eval_digital_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, b
     a.out = M->d_out;
     a.want_grad = grad;
     a.tail = M->dig_tail;
+    // candidate batches: one kappa tile per CTA serves a group of candidates (config 5 reads the
+    // design-time table once per group instead of once per candidate); groups keep >= 2 CTAs per SM
+    if (nc > 1 && a.kap) {
+        const long long ctas = (long long)M->dgeo.nblk_col * a.V;
+        int groups = int(std::max<long long>(1, (2 * 148 + ctas - 1) / ctas));
+        groups = std::min(groups, nc);
+        a.cpb = (nc + groups - 1) / groups;
+        if (const char* e = std::getenv("FMTGP_DIG_CPB")) a.cpb = std::max(1, std::min(nc, std::atoi(e)));
+    }
+    if (a.cpb > 1) a.tail = 2;  // per-candidate finalize kernel (the last-CTA tail is per CTA)
     if (M->d_trace) {
         std::vector<unsigned long long> init(16, 0);
         for (int i : {0, 2, 3, 5, 6}) init[i] = ~0ull;
@@ -1215,7 +1225,7 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
             CK(cudaMemcpy(M->d_ones, ones.data(), ones.size() * sizeof(double), cudaMemcpyHostToDevice));
             CK(cudaMemcpy(M->d_zeros, zeros.data(), zeros.size() * sizeof(double), cudaMemcpyHostToDevice));
         }
-        if (M->equal && !M->lattice && DigGeo::make(M->m[0], M->nofs, M->dgeo, (long long)M->nofs * max_cand)) {
+        if (M->equal && !M->lattice && DigGeo::make(M->m[0], M->nofs, M->dgeo, (long long)M->nofs * max_cand, M->d)) {
             M->dig = true;
             const DigGeo& g = M->dgeo;
             M->d_part_mid = dalloc<double>(size_t(max_cand) * (size_t(1) << g.l1) * (2 + M->P));
