@@ -1,4 +1,6 @@
 // Equal-n digital-net fit in three fused kernels — see digital.cuh.
+#include <cstdlib>
+
 #include "digital.cuh"
 
 namespace fmtgp {
@@ -27,6 +29,7 @@ bool DigGeo::make(int m, int P, DigGeo& g, long long total_vecs, int d) {
     int tl = 11;
     if (total_vecs > 0 && ((total_vecs << m) >> tl) < 4 * 148) tl = 10;
     if (d > 4) tl = 10;  // kappa tile d * 2^tl doubles: keep >= 2 CTAs per SM (config 5: d = 10)
+    if (const char* e = std::getenv("FMTGP_DIG_TL")) tl = std::max(8, std::min(11, std::atoi(e)));  // tuning
     tl = std::max(tl, g.l1);
     g.lc = std::min(tl - g.l1, l2);
     if (g.lc < 0) return false;
