@@ -153,6 +153,9 @@ typedef struct fmtgp_fit_report {
     double final_loss;          /* best loss                                            */
     double tau[FMTGP_MAX_T];    /* prior means at the best parameters (internal order)  */
 } fmtgp_fit_report;
+/* GCV loss (loss_value(model, LossKind::gcv), gp_core.cpp:213-226): ||c||^2 / (tr K^-1)^2 with the
+ * reference's escalation; equal n only (FMTGP_ERR_UNSUPPORTED otherwise).  num / tr optional. */
+FMTGP_API int fmtgp_gcv(fmtgp_model_t model, const fmtgp_hyper* h, double* loss, double* num, double* tr);
 FMTGP_API int fmtgp_fit_param_count(fmtgp_model_t model, int s, int* n_params);
 FMTGP_API int fmtgp_fit(fmtgp_model_t model, const fmtgp_hyper* init, int steps, double* theta_best,
                         double* loss_trace, double* step_seconds, fmtgp_fit_report* report);

@@ -88,6 +88,7 @@ _SIGS = {
     "fmtgp_posterior_mean": (C.c_int, [C.c_void_p, C.c_int, _dp, C.c_int64, _dp]),
     "fmtgp_posterior_var": (C.c_int, [C.c_void_p, C.c_int, _dp, C.c_int64, _dp]),
     "fmtgp_cubature": (C.c_int, [C.c_void_p, _dp, _dp]),
+    "fmtgp_gcv": (C.c_int, [C.c_void_p, C.POINTER(CHyper), _dp, _dp, _dp]),
     "fmtgp_shard_setup": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int64)]),
     "fmtgp_shard_begin": (C.c_int, [C.c_void_p, C.POINTER(CHyper), C.c_int, C.c_double, C.c_void_p]),
     "fmtgp_shard_mid": (C.c_int, [C.c_void_p, C.c_void_p]),

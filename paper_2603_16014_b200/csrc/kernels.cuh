@@ -205,11 +205,13 @@ struct ClassSums {
 template <int NT>
 __device__ __noinline__ void class_sums_out(const ClassSums& t) {
     // Short code on purpose: in the fused kernels this runs in ONE CTA after every other CTA
-    // finished (FMTGP_TRACE measured it: 6.0 us with the previous per-output branch ladder and a
-    // device fp64 division, 3.0 us now).
+    // finished, with cold instruction lines (FMTGP_TRACE: 6.0 us with the previous per-output
+    // branch ladder and a device fp64 division).
     __shared__ double res[2 + MAXP + MAXP * MAXD];
     const int S = 2 + t.P, Q = S + t.V * t.d;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // compact loops: the tail's time is instruction fetch (a 4-quantity ILP variant of this loop
+    // measured 5.1 us against 4.1 us for this one — more code, more cold lines)
 #pragma unroll 1
     for (int q = warp; q < Q; q += NT / 32) {
         const double* base;
@@ -220,16 +222,10 @@ __device__ __noinline__ void class_sums_out(const ClassSums& t) {
             const int o = (q - S) / t.d, j = (q - S) - o * t.d;
             base = t.dot + size_t(o) * t.nblk * t.dstride + j, stride = t.dstride, count = t.nblk;
         }
-        double s0 = 0.0, s1 = 0.0;
-        int b = lane;
+        double sum = 0.0;
 #pragma unroll 1
-        for (; b + 32 < count; b += 64) {
-            s0 += base[size_t(b) * stride];
-            s1 += base[size_t(b + 32) * stride];
-        }
-        if (b < count) s0 += base[size_t(b) * stride];
-        double sum = s0 + s1;
-#pragma unroll
+        for (int b = lane; b < count; b += 32) sum += base[size_t(b) * stride];
+#pragma unroll 1
         for (int o2 = 16; o2 > 0; o2 >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o2);
         if (lane == 0) res[q] = sum;
     }

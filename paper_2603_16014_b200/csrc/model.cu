@@ -1859,6 +1859,40 @@ int fmtgp_nll(fmtgp_model_t M, const fmtgp_hyper* h, int want_grad, fmtgp_result
     });
 }
 
+// GCV loss (loss_value with LossKind::gcv, gp_core.cpp:213-226) = ||c||^2 / (tr K^-1)^2 at the
+// refreshed (escalated) nugget.  Equal n only: there the tau_GCV normal equations
+// (HH^ tau = E^T K^-2 y, gp_core.cpp:84-87) collapse at frequency 0 to the sample mean, i.e. the
+// NMLL tau, so c is the fit's coefficient vector.  Composed of the seam calls (refresh,
+// coefficients, build + invert at the escalated nugget, trace_inverse).
+int fmtgp_gcv(fmtgp_model_t M, const fmtgp_hyper* h, double* loss, double* num, double* tr) {
+    int rc = guarded([&] {
+        if (!M || !h || !loss) invalid("gcv: null argument");
+        if (!M->equal) throw Fail{FMTGP_ERR_UNSUPPORTED, "gcv: unequal sample sizes not implemented"};
+    });
+    if (rc) return rc;
+    fmtgp_result r{};
+    if ((rc = fmtgp_nll(M, h, 0, &r))) return rc;
+    std::vector<double> c(size_t(M->N));
+    if ((rc = fmtgp_coefficients(M, c.data()))) return rc;
+    std::vector<double> xi(h->xi, h->xi + M->T);
+    for (int t = 0; t < M->T; ++t) {
+        xi[t] = h->xi[t] * r.xi_scale;
+        if (r.xi_scale > 1.0 && h->xi[t] == 0.0) xi[t] = 1e-12 * r.xi_scale;  // gp_core.cpp:103-105
+    }
+    fmtgp_hyper h2 = *h;
+    h2.xi = xi.data();
+    double ld = 0.0, trace = 0.0;
+    if ((rc = fmtgp_build_spectrum(M, &h2))) return rc;
+    if ((rc = fmtgp_invert_and_logdet(M, &ld))) return rc;
+    if ((rc = fmtgp_trace_inverse(M, &trace))) return rc;
+    double s = 0.0;
+    for (double v : c) s += v * v;
+    *loss = s / (trace * trace);
+    if (num) *num = s;
+    if (tr) *tr = trace;
+    return FMTGP_OK;
+}
+
 int fmtgp_fit_param_count(fmtgp_model_t M, int s, int* n) {
     return guarded([&] {
         if (!M || !n || s < 0) invalid("fit_param_count: bad argument");

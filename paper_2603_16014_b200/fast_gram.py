@@ -172,6 +172,15 @@ class Model:
         self.hyper = hp
         return _result(r, self.design, hp)
 
+    def gcv(self, hp: Hyper) -> Dict:
+        """GCV loss ||c||^2 / (tr K^-1)^2 (loss_value with LossKind::gcv, gp_core.cpp:213-226);
+        equal sample sizes."""
+        ch = self._hyper_struct(hp)
+        loss, num, tr = C.c_double(), C.c_double(), C.c_double()
+        check(self.lib.fmtgp_gcv(self.h, C.byref(ch), C.byref(loss), C.byref(num), C.byref(tr)))
+        self.hyper = hp
+        return {"gcv": loss.value, "num": num.value, "trace": tr.value}
+
     def nll_batch(self, hps: Sequence[Hyper], grad: bool = True) -> List[Dict]:
         n = len(hps)
         arr = (CHyper * n)()

@@ -258,3 +258,27 @@ def test_full_size_configs(ref, Model, cfg):
         X = inst.X_test[:256]
         for t in range(inst.design.L):
             assert rel(M.posterior_mean(t, X), rm.posterior_mean(t, X)) <= 1e-10
+
+
+@pytest.mark.parametrize("kind", [LATTICE, DIGITAL], ids=["lattice", "digital"])
+@pytest.mark.parametrize("m", [[3], [5, 5], [6, 6, 6], [9, 9], [12, 12]], ids=lambda m: "m" + "-".join(map(str, m)))
+def test_gcv_matches_reference(ref, Model, kind, m):
+    """GCV loss (gp_core.cpp:213-226) vs the reference's loss_value(model, gcv): ||c||^2 carries
+    the solve's parity floor (relative), tr K^-1 is a per-frequency sum (1e-10)."""
+    dz, hp, y = instance(kind, m)
+    M = Model(dz)
+    M.set_y(y)
+    g = M.gcv(hp)
+    want = ref.Model(dz, hp, y).loss(1)
+    floor = cond_floor(dz, ref.build_spectrum(dz, hp))
+    assert abs(g["gcv"] - want) <= 2 * floor * abs(want) + 1e-300
+    assert abs(g["gcv"] - g["num"] / g["trace"] ** 2) <= 1e-14 * abs(g["gcv"])
+
+
+def test_gcv_unequal_unsupported(Model):
+    from paper_2603_16014_b200.fast_gram import Unsupported
+    dz, hp, y = instance(LATTICE, [3, 2])
+    M = Model(dz)
+    M.set_y(y)
+    with pytest.raises(Unsupported):
+        M.gcv(hp)
