@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_fwd(DigArgs a, int l1, int l2
         }
     }
     dig_trace(a.trace, 1, false);
+    dig_trace(a.trace, 11, true);
 }
 
 // ------------------------------------------------------------------ K2: row FWHT + solve + inverse row FWHT
@@ -269,6 +270,7 @@ __global__ void __launch_bounds__(NT) k_dig_mid(DigArgs a, int l2) {
         Yc[size_t(o) * n + base + k2] = sm[o * lds + sidx<true>(k2)];
     }
     dig_trace(a.trace, 4, false);
+    dig_trace(a.trace, 12, true);
 }
 
 // ------------------------------------------------------------------ K3: column FWHT -> W -> gradient dot
@@ -288,6 +290,11 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
     // column is loaded and transformed
     dig_trace(a.trace, 5, true);
     if (a.kap) load_kappa_tile<NT, D>(kbuf, a.kap + size_t(o) * D * n, n, l1, l2, lc, c0);
+    // hyperparameters of the first candidate before the wait (they may live in mapped host memory)
+    double eta_nx[D], gam_nx;
+#pragma unroll
+    for (int j = 0; j < D; ++j) eta_nx[j] = __ldg(a.eta + size_t(cb) * D + j);
+    gam_nx = __ldg(a.gamma + cb);
     pdl_wait();
     dig_trace(a.trace, 6, true);
     if (a.tail != 1) pdl_trigger();  // separate finalize kernel: let its CTA become resident now
@@ -322,8 +329,13 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
         double* tb = tiles[(cc2 - cb) & 1];
         double eta[D];
 #pragma unroll
-        for (int j = 0; j < D; ++j) eta[j] = __ldg(a.eta + size_t(cc2) * D + j);
-        const double gam = __ldg(a.gamma + cc2);
+        for (int j = 0; j < D; ++j) eta[j] = eta_nx[j];
+        const double gam = gam_nx;
+        if (cc2 + 1 < ce) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) eta_nx[j] = __ldg(a.eta + size_t(cc2 + 1) * D + j);
+            gam_nx = __ldg(a.gamma + cc2 + 1);
+        }
         double acc[D];
 #pragma unroll
         for (int j = 0; j < D; ++j) acc[j] = 0.0;
@@ -361,6 +373,7 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
         }
     }
     dig_trace(a.trace, 7, false);
+    dig_trace(a.trace, 13, true);
     if (a.tail != 1) return;  // k_dig_finalize reduces the partials
     // last-CTA reduction: one acq_rel ticket per candidate over its V * nblk CTAs (the release
     // publishes this CTA's partial, the last arrival's acquire sees all of them); fixed
@@ -407,8 +420,10 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
     t.pair_b = a.pair_b;
     t.Rpair = a.Rpair + size_t(c) * a.P;
     t.gamma = __ldg(a.gamma + c);
-    t.out = a.out + size_t(c) * NOUT;
+    t.out = (a.zc_res ? a.zc_res : a.out) + size_t(c) * NOUT;
     class_sums_out<NT>(t);
+    if (a.zc_res)  // flags (K2's atomics, complete before this grid started) and tau words
+        for (int i = a.res_flags_off + threadIdx.x; i < a.res_len; i += NT) a.zc_res[i] = a.res_dev[i];
     __syncthreads();
     dig_trace(a.trace, 10, false);
 }

@@ -56,6 +56,11 @@ struct DigArgs {
     double* out;              // [nc][NOUT]
     int want_grad;
     unsigned long long* trace = nullptr;  // FMTGP_TRACE diagnostics: globaltimer marks (see dig_trace)
+    // zero-copy result record (tail == 1): the last CTA writes the record straight into the
+    // mapped pinned host block and copies the flags / tau words after it (no D2H copy node)
+    double* zc_res = nullptr;     // mapped host result block (device alias), nullptr: off
+    const double* res_dev = nullptr;  // the device result block (flags / tau source)
+    int res_flags_off = 0, res_len = 0;  // doubles before the flags / whole block
     int cpb = 1;              // candidates per K1/K3 CTA (the kappa tile is read once per CTA)
     int tail = 1;             // 1: last CTA of K3 reduces; 0: separate finalize kernel; 2: same, PDL-launched
 };

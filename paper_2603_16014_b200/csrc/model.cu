@@ -322,6 +322,8 @@ struct fmtgp_model {
     bool lat = false;
     LatGeo lgeo{};
     int dig_tail = 1;
+    bool zero_copy = true;  // FMTGP_ZERO_COPY=0: D2H copy node instead of the mapped record
+    bool zero_copy_hyper = false;  // FMTGP_ZERO_COPY_HYPER=1: kernels read the pinned hyper block
     // frequency sharding of the fused lattice fit (fmtgp_shard_*): world size / rank
     int sh_G = 1, sh_g = 0;
     LatArgs sh_args{};
@@ -582,8 +584,15 @@ void finish_results(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, bool g
 }
 
 // Fused digital fit (digital.cuh): three kernels, spectra never leave L2 between them.
+// host alias of a pointer into the device hyperparameter block (pinned = mapped under UVA)
+const double* hyper_host(const fmtgp_model* M, const double* dptr) { return M->h_hyp + (dptr - M->d_hyp); }
+
 void eval_digital_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, bool grad, bool keep_chat) {
-    copy_hyper(M);  // failure flags are zeroed by the first kernel
+    // zero-copy hyperparameters: with one candidate the kernels read the pinned host block
+    // directly (a few dozen doubles, loaded in prologues that overlap the previous kernel) and the
+    // graph has no H2D copy node; failure flags are zeroed by the first kernel
+    const bool zch = M->zero_copy_hyper && nc == 1 && !keep_chat;
+    if (!zch) copy_hyper(M);
     const Group& g = M->groups[0];
     DigArgs a{};
     a.T = M->T;
@@ -616,6 +625,13 @@ void eval_digital_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, b
     a.vec_sum = M->d_vec_sum;
     a.out = M->d_out;
     a.want_grad = grad;
+    if (zch) {
+        a.eta = hyper_host(M, M->d_eta);
+        a.gamma = hyper_host(M, M->d_gamma);
+        a.coef = hyper_host(M, g.d_coef);
+        a.xi = hyper_host(M, g.d_xi);
+        a.Rpair = hyper_host(M, M->d_Rpair);
+    }
     a.tail = M->dig_tail;
     // candidate batches: one kappa tile per CTA serves a group of candidates (config 5 reads the
     // design-time table once per group instead of once per candidate); groups keep >= 2 CTAs per SM
@@ -627,15 +643,23 @@ void eval_digital_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, b
         if (const char* e = std::getenv("FMTGP_DIG_CPB")) a.cpb = std::max(1, std::min(nc, std::atoi(e)));
     }
     if (a.cpb > 1) a.tail = 2;  // per-candidate finalize kernel (the last-CTA tail is per CTA)
+    const bool zc = grad && a.tail == 1 && nc == 1 && M->zero_copy && !keep_chat;
+    if (zc) {
+        a.zc_res = M->h_res;  // pinned = mapped (UVA): the same pointer on the device
+        a.res_dev = M->d_res;
+        a.res_flags_off = int(size_t(M->max_cand) * NOUT);
+        a.res_len = int(M->res_len);
+    }
     if (M->d_trace) {
         std::vector<unsigned long long> init(16, 0);
-        for (int i : {0, 2, 3, 5, 6}) init[i] = ~0ull;
+        for (int i : {0, 2, 3, 5, 6, 11, 12, 13}) init[i] = ~0ull;
         CK(cudaMemcpyAsync(M->d_trace, init.data(), 16 * sizeof(unsigned long long), cudaMemcpyHostToDevice, M->st));
         CK(cudaStreamSynchronize(M->st));
         a.trace = M->d_trace;
     }
     dig_fit(M->dgeo, a, M->st);
     CK(cudaGetLastError());
+    if (zc) return;  // the record is already in the host block
     if (!grad) {
         FinalArgs fa{};
         fa.T = M->T;
@@ -881,10 +905,10 @@ void eval_equal(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, const doub
         CK(cudaStreamSynchronize(M->st));
         unsigned long long t[16];
         CK(cudaMemcpy(t, M->d_trace, sizeof(t), cudaMemcpyDeviceToHost));
-        const char* nm[11] = {"K1 first entry", "K1 last exit", "K2 first entry", "K2 first past wait", "K2 last exit",
+        const char* nm[14] = {"K1 first entry", "K1 last exit", "K2 first entry", "K2 first past wait", "K2 last exit",
                               "K3 first entry", "K3 first past wait", "K3 last exit (pre-ticket)", "tail: ticket",
-                              "tail: staged", "tail: done"};
-        for (int i = 0; i < 11; ++i)
+                              "tail: staged", "tail: done", "K1 first exit", "K2 first exit", "K3 first exit"};
+        for (int i = 0; i < 14; ++i)
             if (t[i] && t[i] != ~0ull) std::fprintf(stderr, "trace %-26s %8.2f us\n", nm[i], 1e-3 * double(t[i] - t[0]));
         return;
     }
@@ -1029,6 +1053,8 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
         if (const char* e = std::getenv("FMTGP_KAPPA_TABLE")) M->kap_enabled = e[0] != '0';
         if (const char* e = std::getenv("FMTGP_CLASSES")) M->class_mode = e[0] != '0';
         if (const char* e = std::getenv("FMTGP_DIG_TAIL")) M->dig_tail = std::atoi(e);
+        if (const char* e = std::getenv("FMTGP_ZERO_COPY")) M->zero_copy = e[0] != '0';
+        if (const char* e = std::getenv("FMTGP_ZERO_COPY_HYPER")) M->zero_copy_hyper = e[0] != '0';
         if (const char* e = std::getenv("FMTGP_TRACE"))
             if (e[0] == '1') M->d_trace = dalloc<unsigned long long>(16);
         M->off[0] = 0;
