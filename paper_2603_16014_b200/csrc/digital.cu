@@ -5,6 +5,15 @@
 
 namespace fmtgp {
 
+thread_local std::vector<DigLaunchRec>* dig_rec = nullptr;
+
+// hyperparameters of candidate c (kernel parameters when use_hv, else the device block)
+template <int D>
+__device__ __forceinline__ double hv_eta(const DigArgs& a, int c, int j) {
+    return a.use_hv ? a.hv.eta[j] : __ldg(a.eta + size_t(c) * D + j);
+}
+__device__ __forceinline__ double hv_gamma(const DigArgs& a, int c) { return a.use_hv ? a.hv.gamma : __ldg(a.gamma + c); }
+
 // FMTGP_TRACE: first-entry / last-exit globaltimer marks per kernel phase (slot: min or max)
 __device__ __forceinline__ void dig_trace(unsigned long long* tr, int slot, bool is_min) {
     if (!tr || threadIdx.x != 0) return;
@@ -120,8 +129,8 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_fwd(DigArgs a, int l1, int l2
     for (int c = cb; c < ce; ++c) {
         double eta[D];
 #pragma unroll
-        for (int j = 0; j < D; ++j) eta[j] = __ldg(a.eta + size_t(c) * D + j);
-        const double gam = __ldg(a.gamma + c);
+        for (int j = 0; j < D; ++j) eta[j] = hv_eta<D>(a, c, j);
+        const double gam = hv_gamma(a, c);
         GenSrc g{};
         __syncthreads();  // previous candidate's store phase is done with sm / tab
         if (kp) {
@@ -178,9 +187,9 @@ __global__ void __launch_bounds__(NT) k_dig_mid(DigArgs a, int l2) {
     // prologue independent of K1 (overlaps its tail under programmatic dependent launch)
     if (threadIdx.x < P) {
         const int q = threadIdx.x;
-        s_coef[q] = __ldg(a.coef + size_t(c) * P + q);
-        s_xi[q] = __ldg(a.xi + size_t(c) * P + q);
-        s_wR[q] = (a.pair_a[q] == a.pair_b[q] ? 1.0 : 2.0) * __ldg(a.Rpair + size_t(c) * P + q);
+        s_coef[q] = a.use_hv ? a.hv.coef[q] : __ldg(a.coef + size_t(c) * P + q);
+        s_xi[q] = a.use_hv ? a.hv.xi[q] : __ldg(a.xi + size_t(c) * P + q);
+        s_wR[q] = (a.pair_a[q] == a.pair_b[q] ? 1.0 : 2.0) * (a.use_hv ? a.hv.Rpair[q] : __ldg(a.Rpair + size_t(c) * P + q));
         s_cls[q] = a.pair_ofs[q];
     }
     constexpr int KPT = T <= 4 ? 2 : 1;  // frequencies per thread held in the yhat prefetch
@@ -293,8 +302,8 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
     // hyperparameters of the first candidate before the wait (they may live in mapped host memory)
     double eta_nx[D], gam_nx;
 #pragma unroll
-    for (int j = 0; j < D; ++j) eta_nx[j] = __ldg(a.eta + size_t(cb) * D + j);
-    gam_nx = __ldg(a.gamma + cb);
+    for (int j = 0; j < D; ++j) eta_nx[j] = hv_eta<D>(a, cb, j);
+    gam_nx = hv_gamma(a, cb);
     pdl_wait();
     dig_trace(a.trace, 6, true);
     if (a.tail != 1) pdl_trigger();  // separate finalize kernel: let its CTA become resident now
@@ -333,8 +342,8 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
         const double gam = gam_nx;
         if (cc2 + 1 < ce) {
 #pragma unroll
-            for (int j = 0; j < D; ++j) eta_nx[j] = __ldg(a.eta + size_t(cc2 + 1) * D + j);
-            gam_nx = __ldg(a.gamma + cc2 + 1);
+            for (int j = 0; j < D; ++j) eta_nx[j] = hv_eta<D>(a, cc2 + 1, j);
+            gam_nx = hv_gamma(a, cc2 + 1);
         }
         double acc[D];
 #pragma unroll
@@ -419,7 +428,7 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
     t.pair_a = a.pair_a;
     t.pair_b = a.pair_b;
     t.Rpair = a.Rpair + size_t(c) * a.P;
-    t.gamma = __ldg(a.gamma + c);
+    t.gamma = 0.0;  // unused by class_sums_out (dNLL/dgamma is formed on the host)
     t.out = (a.zc_res ? a.zc_res : a.out) + size_t(c) * NOUT;
     class_sums_out<NT>(t);
     if (a.zc_res)  // flags (K2's atomics, complete before this grid started) and tau words
@@ -446,7 +455,7 @@ __global__ void __launch_bounds__(256) k_dig_finalize(DigArgs a, int nrows, int 
     t.pair_a = a.pair_a;
     t.pair_b = a.pair_b;
     t.Rpair = a.Rpair + size_t(c) * a.P;
-    t.gamma = __ldg(a.gamma + c);
+    t.gamma = 0.0;  // unused by class_sums_out (dNLL/dgamma is formed on the host)
     t.out = a.out + size_t(c) * NOUT;
     pdl_wait();
     class_sums_out<256>(t);
@@ -466,6 +475,7 @@ static void mid_launch(const DigGeo& g, const DigArgs& a, size_t sm, cudaStream_
         set_smem_dig(k, sm);
         ProfScope ps("dig_mid", s);
         CK_LAUNCH(launch_pdl(k, grid, dim3(NT), sm, s, true, a, g.l2));
+        if (dig_rec) dig_rec->push_back({reinterpret_cast<const void*>(k), grid, dim3(NT), sm, a, {g.l2}, 1});
     })
 }
 
@@ -483,6 +493,8 @@ void dig_fit(const DigGeo& g, const DigArgs& a, cudaStream_t s) {
             set_smem_dig(k1, sm_col);
             ProfScope ps("dig_col_fwd", s);
             k1<<<gcol, NT, sm_col, s>>>(a, g.l1, g.l2, g.lc);
+            if (dig_rec)
+                dig_rec->push_back({reinterpret_cast<const void*>(k1), gcol, dim3(NT), sm_col, a, {g.l1, g.l2, g.lc}, 3});
         })
     })
     const size_t sm_mid = size_t(a.V) * padded_len(1 << g.l2) * sizeof(double);
@@ -504,11 +516,17 @@ void dig_fit(const DigGeo& g, const DigArgs& a, cudaStream_t s) {
             set_smem_dig(k3, sm_col);
             ProfScope ps("dig_col_inv", s);
             CK_LAUNCH(launch_pdl(k3, gcol, dim3(NT), sm_col, s, true, a, g.l1, g.l2, g.lc, nrows));
+            if (dig_rec)
+                dig_rec->push_back(
+                    {reinterpret_cast<const void*>(k3), gcol, dim3(NT), sm_col, a, {g.l1, g.l2, g.lc, nrows}, 4});
         })
     })
     if (a.tail != 1) {
         ProfScope ps("dig_finalize", s);
         CK_LAUNCH(launch_pdl(k_dig_finalize, dim3(a.nc), dim3(256), 0, s, a.tail == 2, a, nrows, g.nblk_col));
+        if (dig_rec)
+            dig_rec->push_back({reinterpret_cast<const void*>(k_dig_finalize), dim3(a.nc), dim3(256), 0, a,
+                                {nrows, g.nblk_col}, 2});
     }
 }
 

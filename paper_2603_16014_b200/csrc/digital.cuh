@@ -15,6 +15,8 @@
 // fused four-step of SURVEY.md §8d (8n(6P+T) bytes instead of 8n(8P+T)).
 #pragma once
 
+#include <vector>
+
 #include "kernels.cuh"
 
 namespace fmtgp {
@@ -25,6 +27,14 @@ struct DigGeo {
     int nt_col, nt_mid;
     int nblk_col;    // K1/K3 CTAs per vector
     static bool make(int m, int V, DigGeo& g, long long total_vecs = 0, int d = 0);  // V rows per K2 CTA
+};
+
+// Hyperparameter values carried in the kernel parameters (one candidate): no H2D copy node in
+// the fit's graph; the captured kernel nodes are re-parameterised per fit (dig_graph_update).
+struct DigHyperVals {
+    double eta[MAXD];
+    double gamma;
+    double coef[MAXP], xi[MAXP], Rpair[MAXP];
 };
 
 struct DigArgs {
@@ -61,7 +71,9 @@ struct DigArgs {
     double* zc_res = nullptr;     // mapped host result block (device alias), nullptr: off
     const double* res_dev = nullptr;  // the device result block (flags / tau source)
     int res_flags_off = 0, res_len = 0;  // doubles before the flags / whole block
-    int cpb = 1;              // candidates per K1/K3 CTA (the kappa tile is read once per CTA)
+    int cpb = 1;
+    int use_hv = 0;           // hyperparameters from hv (candidate 0) instead of the pointers
+    DigHyperVals hv;              // candidates per K1/K3 CTA (the kappa tile is read once per CTA)
     int tail = 1;             // 1: last CTA of K3 reduces; 0: separate finalize kernel; 2: same, PDL-launched
 };
 
@@ -69,5 +81,17 @@ struct DigArgs {
 void dig_kappa_table(const Spatial& sp, const PointGen& pg, const uint64_t* d_ofs /*[nofs][MAXD]*/, int nofs,
                      long long n, double* kap, cudaStream_t s);
 void dig_fit(const DigGeo& g, const DigArgs& a, cudaStream_t s);
+
+// Launch records of dig_fit (set `dig_rec` before a stream capture): the kernels all take DigArgs
+// first, so a captured graph can be re-parameterised with new hyperparameter values.
+struct DigLaunchRec {
+    const void* func;
+    dim3 grid, block;
+    size_t smem;
+    DigArgs a;
+    int ints[4];
+    int nints;
+};
+extern thread_local std::vector<DigLaunchRec>* dig_rec;
 
 }  // namespace fmtgp

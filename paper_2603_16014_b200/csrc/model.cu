@@ -298,6 +298,11 @@ struct fmtgp_model {
         int runs = 0;
         cudaGraphExec_t exec = nullptr;
         std::vector<EventProfiler::Rec> recs;
+        // fused digital fit with hyperparameters in the kernel parameters: the captured launches
+        // and their nodes, re-parameterised before every replay (no H2D copy node)
+        cudaGraph_t graph = nullptr;
+        std::vector<DigLaunchRec> dig_recs;
+        std::vector<cudaGraphNode_t> dig_nodes;
     };
     std::vector<GraphEntry> graphs;
     bool use_graphs = true;
@@ -324,6 +329,7 @@ struct fmtgp_model {
     int dig_tail = 1;
     bool zero_copy = true;  // FMTGP_ZERO_COPY=0: D2H copy node instead of the mapped record
     bool zero_copy_hyper = false;  // FMTGP_ZERO_COPY_HYPER=1: kernels read the pinned hyper block
+    bool hv_params = true;         // FMTGP_HV_PARAMS=0: H2D copy node instead of kernel-parameter values
     // frequency sharding of the fused lattice fit (fmtgp_shard_*): world size / rank
     int sh_G = 1, sh_g = 0;
     LatArgs sh_args{};
@@ -587,12 +593,30 @@ void finish_results(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, bool g
 // host alias of a pointer into the device hyperparameter block (pinned = mapped under UVA)
 const double* hyper_host(const fmtgp_model* M, const double* dptr) { return M->h_hyp + (dptr - M->d_hyp); }
 
+// one-candidate fused digital fits carry the hyperparameters in the kernel parameters
+bool dig_use_hv(const fmtgp_model* M, int nc, bool keep_chat) {
+    return M->dig && M->hv_params && nc == 1 && !keep_chat && !M->zero_copy_hyper;
+}
+
+// candidate 0's values from the filled host block (fill_hyper)
+void fill_hv(const fmtgp_model* M, DigHyperVals& hv) {
+    const Group& g = M->groups[0];
+    for (int j = 0; j < M->d; ++j) hv.eta[j] = hyper_host(M, M->d_eta)[j];
+    hv.gamma = hyper_host(M, M->d_gamma)[0];
+    for (int p = 0; p < M->P; ++p) {
+        hv.coef[p] = hyper_host(M, g.d_coef)[p];
+        hv.xi[p] = hyper_host(M, g.d_xi)[p];
+        hv.Rpair[p] = hyper_host(M, M->d_Rpair)[p];
+    }
+}
+
 void eval_digital_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, bool grad, bool keep_chat) {
     // zero-copy hyperparameters: with one candidate the kernels read the pinned host block
     // directly (a few dozen doubles, loaded in prologues that overlap the previous kernel) and the
     // graph has no H2D copy node; failure flags are zeroed by the first kernel
     const bool zch = M->zero_copy_hyper && nc == 1 && !keep_chat;
-    if (!zch) copy_hyper(M);
+    const bool hv = dig_use_hv(M, nc, keep_chat);
+    if (!zch && !hv) copy_hyper(M);
     const Group& g = M->groups[0];
     DigArgs a{};
     a.T = M->T;
@@ -625,6 +649,10 @@ void eval_digital_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, b
     a.vec_sum = M->d_vec_sum;
     a.out = M->d_out;
     a.want_grad = grad;
+    if (hv) {
+        a.use_hv = 1;
+        fill_hv(M, a.hv);
+    }
     if (zch) {
         a.eta = hyper_host(M, M->d_eta);
         a.gamma = hyper_host(M, M->d_gamma);
@@ -933,19 +961,61 @@ void eval_equal(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, const doub
     if (!ge->exec) {
         cudaGraph_t graph = nullptr;
         M->prof.capture_list = &ge->recs;
+        const bool hv = dig_use_hv(M, nc, keep_chat);
+        ge->dig_recs.clear();
+        if (hv) dig_rec = &ge->dig_recs;
         CK(cudaStreamBeginCapture(M->st, cudaStreamCaptureModeThreadLocal));
         try {
             eval_equal_body(M, nc, h0->si_alpha, h0->b, grad, keep_chat);
         } catch (...) {
+            dig_rec = nullptr;
             cudaStreamEndCapture(M->st, &graph);
             if (graph) cudaGraphDestroy(graph);
             M->prof.capture_list = nullptr;
             throw;
         }
+        dig_rec = nullptr;
         CK(cudaStreamEndCapture(M->st, &graph));
         M->prof.capture_list = nullptr;
         CK(cudaGraphInstantiate(&ge->exec, graph, 0));
-        cudaGraphDestroy(graph);
+        if (hv) {
+            // the kernel node of every recorded launch (each kernel appears once in this graph)
+            size_t cnt = 0;
+            CK(cudaGraphGetNodes(graph, nullptr, &cnt));
+            std::vector<cudaGraphNode_t> nodes(cnt);
+            CK(cudaGraphGetNodes(graph, nodes.data(), &cnt));
+            ge->dig_nodes.assign(ge->dig_recs.size(), nullptr);
+            for (cudaGraphNode_t nd : nodes) {
+                cudaGraphNodeType ty;
+                CK(cudaGraphNodeGetType(nd, &ty));
+                if (ty != cudaGraphNodeTypeKernel) continue;
+                cudaKernelNodeParams kp{};
+                CK(cudaGraphKernelNodeGetParams(nd, &kp));
+                for (size_t i = 0; i < ge->dig_recs.size(); ++i)
+                    if (ge->dig_recs[i].func == kp.func) ge->dig_nodes[i] = nd;
+            }
+            for (cudaGraphNode_t nd : ge->dig_nodes)
+                if (!nd) throw Fail{FMTGP_ERR_CUDA, "graph: captured digital kernel node not found"};
+            ge->graph = graph;  // node handles stay valid with the template graph
+        } else {
+            cudaGraphDestroy(graph);
+        }
+    }
+    if (!ge->dig_recs.empty()) {  // this fit's hyperparameter values into the captured kernels
+        DigHyperVals hvv{};
+        fill_hv(M, hvv);
+        for (size_t i = 0; i < ge->dig_recs.size(); ++i) {
+            DigLaunchRec& r = ge->dig_recs[i];
+            r.a.hv = hvv;
+            void* args[5] = {&r.a, &r.ints[0], &r.ints[1], &r.ints[2], &r.ints[3]};
+            cudaKernelNodeParams kp{};
+            kp.func = const_cast<void*>(r.func);
+            kp.gridDim = r.grid;
+            kp.blockDim = r.block;
+            kp.sharedMemBytes = static_cast<unsigned>(r.smem);
+            kp.kernelParams = args;
+            CK(cudaGraphExecKernelNodeSetParams(ge->exec, ge->dig_nodes[i], &kp));
+        }
     }
     ++M->spec_version;
     CK(cudaGraphLaunch(ge->exec, M->st));
@@ -1055,6 +1125,7 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
         if (const char* e = std::getenv("FMTGP_DIG_TAIL")) M->dig_tail = std::atoi(e);
         if (const char* e = std::getenv("FMTGP_ZERO_COPY")) M->zero_copy = e[0] != '0';
         if (const char* e = std::getenv("FMTGP_ZERO_COPY_HYPER")) M->zero_copy_hyper = e[0] != '0';
+        if (const char* e = std::getenv("FMTGP_HV_PARAMS")) M->hv_params = e[0] != '0';
         if (const char* e = std::getenv("FMTGP_TRACE"))
             if (e[0] == '1') M->d_trace = dalloc<unsigned long long>(16);
         M->off[0] = 0;
@@ -1559,8 +1630,10 @@ int fmtgp_model_destroy(fmtgp_model_t M) {
     F(M->d_y);
     F(M->d_yhat);
     F(M->d_hyp);
-    for (auto& ge : M->graphs)
+    for (auto& ge : M->graphs) {
         if (ge.exec) cudaGraphExecDestroy(ge.exec);
+        if (ge.graph) cudaGraphDestroy(ge.graph);
+    }
     if (M->h_hyp) cudaFreeHost(M->h_hyp);
     F(M->d_lam);
     F(M->d_M);
