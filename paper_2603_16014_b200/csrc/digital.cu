@@ -433,6 +433,13 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
     class_sums_out<NT>(t);
     if (a.zc_res)  // flags (K2's atomics, complete before this grid started) and tau words
         for (int i = a.res_flags_off + threadIdx.x; i < a.res_len; i += NT) a.zc_res[i] = a.res_dev[i];
+    if (a.done_flag) {
+        __syncthreads();  // every record word of this CTA is written ...
+        if (threadIdx.x == 0) {
+            __threadfence_system();  // ... and ordered before the completion word (cumulative fence)
+            *a.done_flag = a.seq;
+        }
+    }
     __syncthreads();
     dig_trace(a.trace, 10, false);
 }

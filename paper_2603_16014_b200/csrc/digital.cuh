@@ -71,6 +71,10 @@ struct DigArgs {
     double* zc_res = nullptr;     // mapped host result block (device alias), nullptr: off
     const double* res_dev = nullptr;  // the device result block (flags / tau source)
     int res_flags_off = 0, res_len = 0;  // doubles before the flags / whole block
+    // completion word in mapped host memory: after the record (system fence) the last CTA stores
+    // `seq`, and the host returns as soon as it sees it instead of waiting for the graph to retire
+    volatile unsigned long long* done_flag = nullptr;
+    unsigned long long seq = 0;
     int cpb = 1;
     int use_hv = 0;           // hyperparameters from hv (candidate 0) instead of the pointers
     DigHyperVals hv;              // candidates per K1/K3 CTA (the kappa tile is read once per CTA)

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -330,6 +331,8 @@ struct fmtgp_model {
     bool zero_copy = true;  // FMTGP_ZERO_COPY=0: D2H copy node instead of the mapped record
     bool zero_copy_hyper = false;  // FMTGP_ZERO_COPY_HYPER=1: kernels read the pinned hyper block
     bool hv_params = true;         // FMTGP_HV_PARAMS=0: H2D copy node instead of kernel-parameter values
+    volatile unsigned long long* h_done = nullptr;  // completion word (pinned, mapped), see DigArgs
+    unsigned long long done_seq = 0;
     // frequency sharding of the fused lattice fit (fmtgp_shard_*): world size / rank
     int sh_G = 1, sh_g = 0;
     LatArgs sh_args{};
@@ -673,6 +676,7 @@ void eval_digital_body(fmtgp_model* M, int nc, int si_alpha, const double* bw, b
     if (a.cpb > 1) a.tail = 2;  // per-candidate finalize kernel (the last-CTA tail is per CTA)
     const bool zc = grad && a.tail == 1 && nc == 1 && M->zero_copy && !keep_chat;
     if (zc) {
+        if (hv) a.done_flag = M->h_done;  // the host spins on it (eval_equal)
         a.zc_res = M->h_res;  // pinned = mapped (UVA): the same pointer on the device
         a.res_dev = M->d_res;
         a.res_flags_off = int(size_t(M->max_cand) * NOUT);
@@ -1001,12 +1005,16 @@ void eval_equal(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, const doub
             cudaGraphDestroy(graph);
         }
     }
+    bool spin = false;
+    const unsigned long long seq = ++M->done_seq;
     if (!ge->dig_recs.empty()) {  // this fit's hyperparameter values into the captured kernels
         DigHyperVals hvv{};
         fill_hv(M, hvv);
         for (size_t i = 0; i < ge->dig_recs.size(); ++i) {
             DigLaunchRec& r = ge->dig_recs[i];
             r.a.hv = hvv;
+            r.a.seq = seq;
+            if (r.a.done_flag) spin = true;
             void* args[5] = {&r.a, &r.ints[0], &r.ints[1], &r.ints[2], &r.ints[3]};
             cudaKernelNodeParams kp{};
             kp.func = const_cast<void*>(r.func);
@@ -1019,7 +1027,21 @@ void eval_equal(fmtgp_model* M, int nc, const fmtgp_hyper* const* hs, const doub
     }
     ++M->spec_version;
     CK(cudaGraphLaunch(ge->exec, M->st));
-    CK(cudaStreamSynchronize(M->st));
+    if (spin && !prof) {
+        // the record is complete once the completion word carries this fit's sequence number;
+        // the graph retires asynchronously (stream order protects every later call).  A fault or a
+        // stall past ~2 s falls back to the stream synchronisation, which reports it.
+        const auto t0 = std::chrono::steady_clock::now();
+        while (*M->h_done != seq) {
+            if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(2)) {
+                CK(cudaStreamSynchronize(M->st));
+                break;
+            }
+        }
+        std::atomic_thread_fence(std::memory_order_acquire);
+    } else {
+        CK(cudaStreamSynchronize(M->st));
+    }
     if (prof) M->prof.add_graph(ge->recs);
     ge->runs++;
 }
@@ -1354,6 +1376,12 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
         M->res_len = size_t(max_cand) * (NOUT + 1 + 2 * MAXT) + MAXT;
         M->d_res = dalloc<double>(M->res_len);
         CK(cudaMallocHost(reinterpret_cast<void**>(&M->h_res), sizeof(double) * M->res_len));
+        {
+            void* p = nullptr;
+            CK(cudaMallocHost(&p, 64));
+            std::memset(p, 0, 64);
+            M->h_done = static_cast<volatile unsigned long long*>(p);
+        }
         M->d_tau_raw = M->d_res + size_t(max_cand) * (NOUT + 1 + 2 * MAXT);
         M->h_tau_raw = M->h_res + size_t(max_cand) * (NOUT + 1 + 2 * MAXT);
         CK(cudaEventCreateWithFlags(&M->ev_h2d, cudaEventDisableTiming));
@@ -1635,6 +1663,7 @@ int fmtgp_model_destroy(fmtgp_model_t M) {
         if (ge.graph) cudaGraphDestroy(ge.graph);
     }
     if (M->h_hyp) cudaFreeHost(M->h_hyp);
+    if (M->h_done) cudaFreeHost(const_cast<unsigned long long*>(M->h_done));
     F(M->d_lam);
     F(M->d_M);
     F(M->d_work);
