@@ -104,7 +104,7 @@ def offset_classes(dz) -> int:
     return len(seen)
 
 
-def algorithmic_bytes(kernel: str, inst, P: int, T: int) -> float:
+def algorithmic_bytes(kernel: str, inst, P: int, T: int, nc: int = 1) -> float:
     """Minimal HBM bytes one launch of `kernel` must move for this workload (8-byte words;
     SURVEY.md §8d per-kernel split).  Real (digital) slots are 8 B, lattice
     half-spectrum slots 16 B for n/2 of them: either way 8n bytes per vector.  Transforms run
@@ -114,10 +114,11 @@ def algorithmic_bytes(kernel: str, inst, P: int, T: int) -> float:
     n = dz.n[0]
     vec = 8.0 * n
     V = offset_classes(dz)
+    # nc candidates per launch (config 5: 64): the kappa table and yhat are read once per launch
     table = {
-        "dig_col_fwd": V * (1 + dz.d) * vec,  # kappa table in, intermediate out
-        "dig_mid": (2 * V + T) * vec,  # intermediate + yhat in; Z (class adjoints) out
-        "dig_col_inv": V * (1 + dz.d) * vec,  # intermediate + kappa table in
+        "dig_col_fwd": V * (nc + dz.d) * vec,  # kappa table in, intermediate out
+        "dig_mid": (2 * V * nc + T) * vec,  # intermediate + yhat in; Z (class adjoints) out
+        "dig_col_inv": V * (nc + dz.d) * vec,  # intermediate + kappa table in
         "fwd_col_dig": P * vec, "fwd_col_lat": P * vec,  # generator on the fly -> write intermediate
         "fwd_row_dig": 2 * P * vec, "fwd_row_lat": 2 * P * vec,  # read intermediate, write spectra
         "fwd_small_dig": P * vec, "fwd_small_lat": P * vec,  # write spectra
@@ -198,10 +199,12 @@ def main():
     P, T = dz.L * (dz.L + 1) // 2, dz.L
     grad_params = dz.d + hp.B.size + T + 1  # eta, w, v, gamma
     workload = {1: "config1", 2: "config2: T=3 d=5 n=2^16 scrambled digital net, order-4 Walsh DSI kernel",
-                3: "config3", 4: "config4: T=2 d=4 n=2^26 lattice B2", 5: "config5"}[args.config]
+                3: "config3", 4: "config4: T=2 d=4 n=2^26 lattice B2",
+                5: "config5: T=4 d=10 n=2^18 digital order-4 Walsh, 256-candidate sweep per step"}[args.config]
     config = {"workload": workload, "N": dz.N, "T": T, "d": dz.d, "n": dz.n[0],
               "outputs": "NLL, logdet, dNLL/d(eta, w, v, gamma)", "l2": "flushed before every step (512 MiB write)",
-              "parallelism": ("frequency-sharded (2 NCCL all-to-alls per fit)" if args.config == 4 else "replicas")
+              "parallelism": {4: "frequency-sharded (2 NCCL all-to-alls per fit)",
+                              5: "candidate-sharded (gather of the records)"}.get(args.config, "replicas")
               if args.gpus > 1 else "single"}
 
     if args.impl == "reference":
@@ -233,11 +236,11 @@ def main():
 
     from paper_2603_16014_b200.fast_gram import Model
 
-    model = Model(dz, device=local_rank)
+    model = Model(dz, device=local_rank, max_candidates=64 if args.config == 5 else 1)
     model.set_y(inst.y)
     stream = torch.cuda.ExternalStream(model.stream, device=torch.device("cuda", local_rank))
-    sharded = args.config == 4 and world > 1
-    if sharded:
+    sharded = (args.config == 4 and world > 1) or args.config == 5  # one job-wide unit per step
+    if args.config == 4 and world > 1:
         # config 4 at N > 1: the frequency-sharded fit — one fit per step over all
         # ranks (strong scaling): column pass -> NCCL all-to-all -> row pass + solve -> all-to-all ->
         # inverse column pass + gradient dot -> gather of the 101-double records
@@ -258,6 +261,25 @@ def main():
             def profile_read(self):
                 return model.profile_read()
         fitter = _Sharded()
+    elif args.config == 5:
+        # config 5: one step = the 256-candidate sweep (NLL + full gradient each), candidates
+        # sharded over the ranks (strong scaling, no data-path collective)
+        from paper_2603_16014_b200 import sharding
+
+        class _Sweep:
+            def nll(self, h, grad=True):
+                res = sharding.sweep(lambda cs: model.nll_batch(cs, grad=grad), inst.candidates, world, rank)
+                return res[0]
+
+            def set_y(self, y):
+                model.set_y(y)
+
+            def profile(self, on=True):
+                model.profile(on)
+
+            def profile_read(self):
+                return model.profile_read()
+        fitter = _Sweep()
     else:
         fitter = model
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local_rank}")
@@ -299,7 +321,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    value = (1 if sharded else world) * 1e3 / ms_per_step  # sharded: one fit over all ranks
+    per_step = len(inst.candidates) if args.config == 5 else 1  # fits per step (config 5: the sweep)
+    value = per_step * (1 if sharded else world) * 1e3 / ms_per_step  # sharded: one unit over all ranks
 
     # ---- end to end through the public API: pinned host y -> device, fit, result -> host
     y_pinned = torch.empty(dz.N, dtype=torch.float64).pin_memory().numpy()
@@ -319,7 +342,7 @@ def main():
         t = torch.tensor([e2e_ms], device=f"cuda:{local_rank}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e_value = (1 if sharded else world) * 1e3 * args.steps / e2e_ms
+    e2e_value = per_step * (1 if sharded else world) * 1e3 * args.steps / e2e_ms
     hyper_bytes = 8 * (dz.d + 1 + P + 2 * P)
     h2d = 8 * dz.N + hyper_bytes
     d2h = 8 * ((4 + 16 + 64) + 1 + 2 * 8 + 8)  # result block: record, bad flag, non-real maxima, tau (model.cu res_len)
@@ -335,11 +358,12 @@ def main():
     dom = max(prof.items(), key=lambda kv: kv[1][0])
     dom_name, (dom_ms, dom_cnt) = dom
     avg_ms = dom_ms / max(dom_cnt, 1)
-    alg = algorithmic_bytes(dom_name, inst, P, T)
+    ncl = 64 if args.config == 5 else 1  # candidates per launch
+    alg = algorithmic_bytes(dom_name, inst, P, T, ncl)
     achieved = alg / (avg_ms * 1e-3) / 1e9 if avg_ms > 0 else 0.0
     kernels = {k: {"avg_us": 1e3 * v[0] / max(v[1], 1), "launches": v[1],
                    "share": v[0] / max(sum(x[0] for x in prof.values()), 1e-12),
-                   "alg_GBps": (algorithmic_bytes(k, inst, P, T) / (1e-3 * v[0] / max(v[1], 1)) / 1e9)
+                   "alg_GBps": (algorithmic_bytes(k, inst, P, T, ncl) / (1e-3 * v[0] / max(v[1], 1)) / 1e9)
                    if v[0] > 0 else None} for k, v in prof.items()}
     roofline = {"bound": "hbm", "kernel": dom_name,
                 "timing": "per-kernel CUDA events on the fit stream, second pass of the same K steps "
