@@ -368,7 +368,7 @@ def main():
     roofline = {"bound": "hbm", "kernel": dom_name,
                 "timing": "per-kernel CUDA events on the fit stream, second pass of the same K steps "
                           f"({1e3 * prof_total_ms / args.steps:.1f} us/step instrumented)", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": ncu_traffic(dom_name), "alg_bytes_per_launch": alg,
+                "frac": achieved / peak, "traffic": ncu_traffic(dom_name) if args.config in (2, 4) else None,  # captured configs "alg_bytes_per_launch": alg,
                 "peak_source": peak_src, "kernels": kernels}
 
     cpu = None
