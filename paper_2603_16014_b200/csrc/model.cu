@@ -245,8 +245,6 @@ struct fmtgp_model {
     double *d_vecA = nullptr, *d_vecB = nullptr;
     void *d_sA = nullptr, *d_sB = nullptr;
     // pinned staging
-    double* h_stage = nullptr;
-    size_t stage_len = 0;
     double* h_out = nullptr;
     int* h_bad = nullptr;
     // equal n: tau_l = yhat_l(0)/sqrt(n) travels with the next fit's result block (no sync in set_y)
@@ -388,13 +386,6 @@ std::vector<double> task_gram(const fmtgp_model* M, const fmtgp_hyper* h) {
     return R;
 }
 
-void ensure_stage(fmtgp_model* M, size_t len) {
-    if (M->stage_len >= len) return;
-    if (M->h_stage) cudaFreeHost(M->h_stage);
-    M->h_stage = nullptr;
-    CK(cudaMallocHost(reinterpret_cast<void**>(&M->h_stage), len * sizeof(double)));
-    M->stage_len = len;
-}
 
 // Fill the pinned hyperparameter block (eta, gamma, Rpair, per-group coef and xi) for nc
 // candidates; xi_scale[c] is the escalation factor of candidate c.  Host-only: the H2D copy
@@ -1693,7 +1684,6 @@ int fmtgp_model_destroy(fmtgp_model_t M) {
     F(M->d_sA);
     F(M->d_sB);
     if (M->uneq) unequal::destroy(M->uneq);
-    if (M->h_stage) cudaFreeHost(M->h_stage);
 
     if (M->st) cudaStreamDestroy(M->st);
     delete M;

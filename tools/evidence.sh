@@ -7,6 +7,8 @@ python -m pytest tests -m gpu -q > gpurun_out/ev_pytest_gpu.log 2>&1; tail -2 gp
 python bench.py > gpurun_out/ev_bench.log 2>&1; tail -1 gpurun_out/ev_bench.log | cut -c1-400
 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/ev_bench_ref.log 2>&1; tail -1 gpurun_out/ev_bench_ref.log | cut -c1-300
 python bench.py --config 4 --steps 5 --warmup 3 > gpurun_out/ev_bench_c4.log 2>&1; tail -1 gpurun_out/ev_bench_c4.log | cut -c1-300
+python bench.py --config 5 --steps 5 --warmup 3 > gpurun_out/ev_bench_c5.log 2>&1; tail -1 gpurun_out/ev_bench_c5.log | cut -c1-300
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/ev_smoke.log 2>&1; tail -1 gpurun_out/ev_smoke.log
 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ev_bench_small.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/ev_launches.csv \
       python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ev_ncu_launch.log 2>&1
