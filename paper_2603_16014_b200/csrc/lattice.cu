@@ -142,19 +142,19 @@ __device__ __forceinline__ void col_steps(double2* s_step, const double2* __rest
 // ------------------------------------------------------------------ exchange-block layout
 // Row k1 -> (owner rank h, local row i): cluster q = min(k1, N1 - k1) (rows 0 and N1/2 form
 // cluster 0), side = 1 for the upper row of the pair.
-__device__ __forceinline__ int row_owner(int k1, int N1, int QP, int& i) {
+__device__ __forceinline__ int row_owner(int k1, int N1, int lqp, int& i) {
     int q, side;
     if (k1 == 0) q = 0, side = 0;
     else if (k1 == (N1 >> 1)) q = 0, side = 1;
     else if (k1 < (N1 >> 1)) q = k1, side = 0;
     else q = N1 - k1, side = 1;
-    const int h = q / QP;
-    i = 2 * (q - h * QP) + side;
+    const int h = q >> lqp;
+    i = 2 * (q - (h << lqp)) + side;
     return h;
 }
 // element (row owner h, class o, local row i, local column jl) of candidate c's exchange blocks
 __device__ __forceinline__ size_t xaddr(const LatArgs& a, int c, int h, int o, int i, int jl) {
-    return size_t(c) * a.V * a.half + ((size_t(h) * a.V + o) * a.R + i) * a.WC + jl;
+    return size_t(c) * a.V * a.half + (((size_t(h) * a.V + o) * a.R + i) << a.lwc) + jl;
 }
 
 // ------------------------------------------------------------------ L1: generator x column FFT
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(NT) k_lat_col_fwd(LatArgs a, int l1, int l2, i
         if (e < tile) {
             const int k1 = e >> lc;
             int i;
-            const int h = row_owner(k1, N1, a.QP, i);
+            const int h = row_owner(k1, N1, a.lqp, i);
             a.Y[xaddr(a, c, h, o, i, jl)] = cmul(sm[tcc * ld + S(k1)], cmul(tbase, st[u]));
         }
     }
@@ -295,8 +295,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
     pdl_trigger();
     for (int e = threadIdx.x; e < (V << l2); e += NT) {
         const int oo = e >> l2, k2 = e & (N2 - 1);
-        const int sr = k2 / a.WC;  // column owner
-        cp_async16(&sm[oo * lds + S(k2)], &a.Y[xaddr(a, c, sr, oo, li, k2 - sr * a.WC)]);
+        const int sr = k2 >> a.lwc;  // column owner
+        cp_async16(&sm[oo * lds + S(k2)], &a.Y[xaddr(a, c, sr, oo, li, k2 & (a.WC - 1))]);
     }
     cp_async_wait_all();
     __syncthreads();
@@ -465,7 +465,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
         if (j2 >= N2) break;
         const double2 w = cmul(obase, s_ostep[u]);
         for (int oo = 0; oo < V; ++oo)
-            a.Y[xaddr(a, c, j2 / a.WC, oo, li, j2 - (j2 / a.WC) * a.WC)] = cmulc(sm[oo * lds + S(j2)], w);
+            a.Y[xaddr(a, c, j2 >> a.lwc, oo, li, j2 & (a.WC - 1))] = cmulc(sm[oo * lds + S(j2)], w);
     }
 }
 
@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(NT) k_lat_col_inv(LatArgs a, int l1, int l2, i
             if (e < npair) {
                 const int jj = e >> lc, cc = e & (C - 1);
                 int i0, i1;
-                const int h0 = row_owner(jj, N1, a.QP, i0), h1 = row_owner(jj + H, N1, a.QP, i1);
+                const int h0 = row_owner(jj, N1, a.lqp, i0), h1 = row_owner(jj + H, N1, a.lqp, i1);
                 x0[u] = __ldcs(&xb[xaddr(a, c, h0, o, i0, jl0 + cc)]);
                 x1[u] = __ldcs(&xb[xaddr(a, c, h1, o, i1, jl0 + cc)]);
             }
@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(NT) k_lat_col_inv(LatArgs a, int l1, int l2, i
         for (int e = threadIdx.x; e < tile; e += NT) {
             const int k1 = e >> lc, cc = e & (C - 1);
             int i1;
-            const int h1 = row_owner(k1, N1, a.QP, i1);
+            const int h1 = row_owner(k1, N1, a.lqp, i1);
             cp_async16(&sm[cc * ld + S(k1)], &xb[xaddr(a, c, h1, o, i1, jl0 + cc)]);
         }
         cp_async_wait_all();

@@ -68,6 +68,7 @@ struct LatArgs {
     // all-to-all returns them to the column owners (Cbuf) for L3.  G = 1: Cbuf == Y.
     int nrank = 1, rank = 0;
     int QP = 0, R = 0, WC = 0, ncb = 0;
+    int lwc = 0, lqp = 0;     // log2 WC, log2 QP (world sizes are powers of two): no integer division
     const double2* Cbuf = nullptr;
 };
 

@@ -746,6 +746,8 @@ LatArgs lat_args(fmtgp_model* M, int nc, int si_alpha, bool grad) {
     a.QP = (1 << lg.l1) / 2 / a.nrank;
     a.R = 2 * a.QP;
     a.WC = (1 << lg.l2) / a.nrank;
+    while ((1 << a.lwc) < a.WC) ++a.lwc;
+    while ((1 << a.lqp) < a.QP) ++a.lqp;
     a.ncb = lg.nblk_col / a.nrank;
     a.Cbuf = a.Y;
     return a;
@@ -2038,8 +2040,9 @@ int fmtgp_shard_setup(fmtgp_model_t M, int rank, int world, int64_t* exchange_el
             throw Fail{FMTGP_ERR_UNSUPPORTED, "shard_setup: only the fused equal-n lattice fit shards (n >= 2^17, T <= 4)"};
         const LatGeo& g = M->lgeo;
         const int clusters = (1 << g.l1) / 2;
-        if (world < 1 || rank < 0 || rank >= world || clusters % world || g.nblk_col % world || (1 << g.l2) % world)
-            invalid("shard_setup: the world size must divide the row clusters and the column blocks");
+        if (world < 1 || (world & (world - 1)) || rank < 0 || rank >= world || clusters % world ||
+            g.nblk_col % world || (1 << g.l2) % world)
+            invalid("shard_setup: the world size must be a power of two dividing the row clusters and column blocks");
         M->sh_G = world;
         M->sh_g = rank;
         *exchange_elems = (int64_t)M->nofs * M->pslots[0] / world;
