@@ -132,6 +132,12 @@ class Session {
         check(fmtgp_nll(h_, &h, grad ? 1 : 0, &r));
         return r;
     }
+    // loss_value(model, LossKind::gcv)  gp_core.cpp:213-226 (equal n)
+    double gcv(const fmtgp_hyper& h) {
+        double loss = 0.0;
+        check(fmtgp_gcv(h_, &h, &loss, nullptr, nullptr));
+        return loss;
+    }
     std::vector<double> coefficients() {
         std::vector<double> c(dz_.N());
         check(fmtgp_coefficients(h_, c.data()));
