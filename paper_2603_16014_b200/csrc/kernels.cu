@@ -647,8 +647,52 @@ void fwd_array(int lattice, const Geo& g, int nvec, const ArraySrc& src, const S
     fwd_impl(lattice, g, nvec, src, snk, work, tw, s);
 }
 
+// Lattice query column with compile-time dimension cap and Bernoulli order: 32-bit exact lattice
+// coordinate (x_p = t 2^-m + sh_lo 2^-53, the same value as QuerySrc's 64-bit chain), the
+// reference's floating difference for the query coordinate (kernel_against_data,
+// gp_core.cpp:386-397), no integer division per element when a group holds one task.
+template <int DC, int ALPHA>
+struct QuerySrcLat {
+    QuerySrc q;
+    __device__ __forceinline__ double operator()(int v, uint64_t idx) const {
+        const int qi = q.ntg == 1 ? v : v / q.ntg;
+        const int l = __ldg(q.vec_task + (v - qi * q.ntg));
+        const int sb = DIGITAL_BITS - q.m;
+        const uint32_t mask = (1u << q.m) - 1u;
+        const double inv_n = pow2i(-q.m);
+        double prod = q.gamma;
+#pragma unroll
+        for (int j = 0; j < DC; ++j) {
+            if (j < q.d) {
+                const uint64_t sh = __ldg(q.shifts + l * q.d + j);
+                const uint32_t t = (uint32_t(idx) * uint32_t(__ldg(q.g + j)) + uint32_t(sh >> sb)) & mask;
+                const double xp = fma(double(t), inv_n, double(sh & ((uint64_t(1) << sb) - 1)) * 0x1p-53);
+                const double diff = __ldg(q.X + (long long)qi * q.d + j) - xp;
+                const double u1 = diff - floor(diff), u2 = -diff - floor(-diff);
+                double u = fmin(u1, u2);
+                if (u >= 1.0) u = 0.0;
+                constexpr double pi2 = 9.869604401089358618834491;
+                const double base = ALPHA == 1 ? 2.0 * pi2 * (u * (u - 1.0) + 1.0 / 6.0)
+                                               : -(2.0 / 3.0) * pi2 * pi2 * (((u - 2.0) * u + 1.0) * u * u - 1.0 / 30.0);
+                prod *= 1.0 + __ldg(q.eta + j) * base;
+            }
+        }
+        return __ldg(q.Rrow + l) * prod;
+    }
+};
+
 void fwd_query(int lattice, const Geo& g, int nvec, const QuerySrc& src, const ScaleSink& snk, void* work,
                const double2* tw, cudaStream_t s) {
+    if (lattice && src.m >= 1 && src.m <= 31) {
+        const bool a1 = src.si_alpha == 1;
+        if (src.d <= 4) a1 ? fwd_impl(1, g, nvec, QuerySrcLat<4, 1>{src}, snk, work, tw, s)
+                           : fwd_impl(1, g, nvec, QuerySrcLat<4, 2>{src}, snk, work, tw, s);
+        else if (src.d <= 8) a1 ? fwd_impl(1, g, nvec, QuerySrcLat<8, 1>{src}, snk, work, tw, s)
+                                : fwd_impl(1, g, nvec, QuerySrcLat<8, 2>{src}, snk, work, tw, s);
+        else a1 ? fwd_impl(1, g, nvec, QuerySrcLat<16, 1>{src}, snk, work, tw, s)
+                : fwd_impl(1, g, nvec, QuerySrcLat<16, 2>{src}, snk, work, tw, s);
+        return;
+    }
     fwd_impl(lattice, g, nvec, src, snk, work, tw, s);
 }
 
