@@ -315,6 +315,7 @@ __device__ __forceinline__ int ldl_core(const typename Sc<CX>::T* A, const typen
     V L[T][T];
     double dinv[T], piv[T];
     int status = 0;
+    double pprod = 1.0;  // this frequency's pivot product (T <= 8 covariance pivots: no overflow)
     // pair index of (a,b), a <= b, row by row (fast_gram.cpp:35-40)
     auto pidx = [](int a, int b) { return a * T - a * (a - 1) / 2 + (b - a); };
 #pragma unroll
@@ -332,9 +333,7 @@ __device__ __forceinline__ int ldl_core(const typename Sc<CX>::T* A, const typen
         if constexpr (CX) rex[s] = fmax(rex[s], dd);
         piv[s] = dd;
         dinv[s] = 1.0 / dd;
-        int e;
-        pm = frexp(pm * dd, &e);
-        pe += e;
+        pprod *= dd;
 #pragma unroll
         for (int i = s + 1; i < T; ++i) {
             V acc = S::conj(A[pidx(s, i)]);
@@ -342,6 +341,11 @@ __device__ __forceinline__ int ldl_core(const typename Sc<CX>::T* A, const typen
             for (int k = 0; k < s; ++k) acc = S::sub(acc, S::scale(S::mulc(L[i][k], L[s][k]), piv[k]));
             L[i][s] = S::scale(acc, dinv[s]);
         }
+    }
+    {
+        int e;
+        pm = frexp(pm * pprod, &e);  // one renormalisation per frequency
+        pe += e;
     }
     // z = L^-1 r, quad = sum |z|^2 / d
     V z[T];
