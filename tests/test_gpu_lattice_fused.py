@@ -214,3 +214,31 @@ def test_frequency_sharded_escalation_matches_single():
     else:
         assert got["escalations"] == want["escalations"]
         assert abs(got["nll"] - want["nll"]) <= 1e-8 * dz.N
+
+
+def _random_cases(n, seed=2024):
+    rng = np.random.default_rng(seed)
+    cases = []
+    for _ in range(n):
+        T = int(rng.integers(1, 5))
+        shared = [t for t in range(1, T) if rng.random() < 0.3] or None
+        cases.append((int(rng.integers(17, 20)), T, int(rng.integers(1, 17)), int(rng.integers(1, 3)),
+                      shared, int(2 ** rng.integers(0, 3)), int(rng.integers(1, 1000))))
+    return cases
+
+
+@pytest.mark.parametrize("case", _random_cases(12), ids=lambda c: "m%d-T%d-d%d-a%d-G%d-s%d" % (c[0], c[1], c[2], c[3], c[5], c[6]))
+def test_fused_random_shapes(case):
+    """Seeded random shapes (T, d across every register cap, both Bernoulli orders, shared shifts,
+    virtual-rank sharding): fused == generic path within the solve floor."""
+    from paper_2603_16014_b200 import sharding
+    m, T, d, alpha, shared, G, seed = case
+    dz, hp, y = make(m, T, d, alpha, seed=seed, shared=shared)
+    Mg = model(dz, y, False)
+    want = Mg.nll(hp, grad=True)
+    floor = floor_of(Mg, dz, hp)
+    got = model(dz, y, True).nll(hp, grad=True)
+    close_results(got, want, dz.N, floor)
+    ranks = [sharding.ShardedLatticeFit(dz, g, G, model=model(dz, y, True)) for g in range(G)]
+    sh = sharding.sharded_nll(ranks, hp, grad=True, exchange=sharding.local_exchange(G), gather=lambda r: r)
+    close_results(sh, want, dz.N, floor)
