@@ -1340,6 +1340,14 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
         if (M->equal && !M->lattice && DigGeo::make(M->m[0], M->nofs, M->dgeo, (long long)M->nofs * max_cand, M->d)) {
             M->dig = true;
             const DigGeo& g = M->dgeo;
+            // the fused kernels always stage the class vectors in d_work (column pass -> row
+            // pass), also where the generic geometry of this length is single-pass and sized none
+            const size_t need = size_t(max_cand) * M->nofs * (size_t(1) << M->m[0]);
+            if (M->work_elems < need) {
+                if (M->d_work) cudaFree(M->d_work);
+                M->d_work = dalloc<char>(need * sizeof(double));
+                M->work_elems = need;
+            }
             M->d_part_mid = dalloc<double>(size_t(max_cand) * (size_t(1) << g.l1) * (2 + M->P));
             M->d_part_dot = dalloc<double>(size_t(max_cand) * M->nofs * g.nblk_col * (MAXD + 1));
             M->d_counter = dalloc<unsigned int>(size_t(max_cand) * (1 + M->nofs));
