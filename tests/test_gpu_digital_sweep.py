@@ -42,3 +42,14 @@ def test_digital_random_shapes_sequential(ref):
         for h, rb in zip(cands, M.nll_batch(cands, grad=True)):
             rs = M.nll(h, grad=True)
             assert rs["nll"] == rb["nll"] and np.array_equal(rs["deta"], rb["deta"])
+
+
+def test_all_paths_random_shapes(ref):
+    """tools/sweep_general.py's checks on 30 seeded shapes (lattice / digital, equal / unequal n,
+    T <= 8, d <= 16, shared shifts): NLL, coefficients, posterior mean / variance, cubature."""
+    import subprocess
+    import sys
+    out = subprocess.run([sys.executable, "tools/sweep_general.py", "30", "31"], capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "bad 0" in out.stdout, out.stdout[-3000:]
