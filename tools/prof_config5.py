@@ -11,7 +11,8 @@ from paper_2603_16014_b200.fast_gram import Model  # noqa: E402
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 3
 inst = configs.make(5)
-M = Model(inst.design, max_candidates=64)
+mc = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else 64
+M = Model(inst.design, max_candidates=mc)
 M.set_y(inst.y)
 ts = []
 for _ in range(reps):
