@@ -153,6 +153,9 @@ def test_fused_then_seam_calls_consistent(ref):
     mu, S = M.cubature()
     mu_r, S_r = rm.cubature()
     assert np.linalg.norm(mu - mu_r) <= floor * np.linalg.norm(mu_r)
+    pv = M.posterior_var(0, X[:3])  # the fused slot layout through the variance fold
+    want_v = np.array([rm.posterior_cov(0, X[q], 0, X[q]) for q in range(3)])
+    assert np.abs(pv - want_v).max() <= 1e-6 * max(1.0, np.abs(want_v).max())
 
 
 def test_fused_escalation_matches_generic():
