@@ -14,7 +14,12 @@
 """
 from __future__ import annotations
 
+import ctypes as C
 from typing import Callable, List, Sequence, Tuple
+
+import numpy as np
+
+from ._lib import ERR_NONREAL, ERR_SCHUR, SHARD_REC_LEN, CResult, FastMtgpError, SchurBreakdown, check
 
 
 def shard_range(n: int, world: int, rank: int) -> Tuple[int, int]:
@@ -57,7 +62,6 @@ NOUT = 4 + 16 + 8 * 8  # result record (csrc/kernels.cuh OUT_*)
 def combine_records(recs) -> "np.ndarray":
     """Rank-order sum of the NOUT sums, min of the first failing slot, max of the per-stage
     non-real maxima (fmtgp_shard_end's record layout)."""
-    import numpy as np
     recs = [np.asarray(r, dtype=np.float64) for r in recs]
     out = recs[0].copy()
     for r in recs[1:]:
@@ -76,12 +80,9 @@ class ShardedLatticeFit:
     orchestration runs with virtual ranks on one device (tests)."""
 
     def __init__(self, design, rank: int, world: int, device: int = 0, model=None):
-        import ctypes as C
-
         import torch
 
         from .fast_gram import Model
-        from ._lib import check
 
         self.rank, self.world = rank, world
         self.model = model if model is not None else Model(design, device=device)
@@ -97,37 +98,27 @@ class ShardedLatticeFit:
 
     # -- the three phases (asynchronous on the model's stream except `end`)
     def begin(self, hp, grad: bool, xi_scale: float):
-        from ._lib import check
         ch = self.model._hyper_struct(hp)
-        import ctypes as C
         check(self.model.lib.fmtgp_shard_begin(self.model.h, C.byref(ch), int(grad), float(xi_scale),
                                                C.c_void_p(self.bufs[0].data_ptr())))
         return self.bufs[0]
 
     def mid(self):
-        from ._lib import check
-        import ctypes as C
         check(self.model.lib.fmtgp_shard_mid(self.model.h, C.c_void_p(self.bufs[1].data_ptr())))
         return self.bufs[1]
 
     def end(self):
-        import ctypes as C
 
-        import numpy as np
 
-        from ._lib import SHARD_REC_LEN, check
         rec = np.zeros(SHARD_REC_LEN)
         check(self.model.lib.fmtgp_shard_end(self.model.h, C.c_void_p(self.bufs[0].data_ptr()),
                                              rec.ctypes.data_as(C.POINTER(C.c_double))))
         return rec
 
     def finish(self, hp, rec, grad: bool, xi_scale: float, escalations: int):
-        import ctypes as C
 
-        import numpy as np
 
-        from ._lib import CResult, check
-        from .fast_gram import _result
+        from .fast_gram import _result  # noqa: PLC0415 (fast_gram imports nothing from here)
         ch = self.model._hyper_struct(hp)
         r = CResult()
         rec = np.ascontiguousarray(rec, dtype=np.float64)
@@ -142,7 +133,6 @@ class ShardedLatticeFit:
             dist.all_to_all_single(recv, send, group=group)
 
     def default_gather(self, rec, group=None):
-        import numpy as np
         import torch
         import torch.distributed as dist
         t = torch.from_numpy(np.asarray(rec, dtype=np.float64)).to(self.bufs[0].device)
@@ -157,7 +147,6 @@ def sharded_nll(ranks, hp, grad: bool = True, exchange=None, gather=None, max_re
 
     `ranks` is this process's ShardedLatticeFit (one element, multi-process) or all of them
     (virtual ranks on one device, in which case `exchange` / `gather` act on the list)."""
-    from ._lib import ERR_NONREAL, ERR_SCHUR, FastMtgpError, SchurBreakdown
     local = list(ranks)
     scale, attempt = 1.0, 0
     while True:
