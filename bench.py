@@ -1,18 +1,23 @@
 #!/usr/bin/env python3
 """Benchmark of the fast-MTGP fit hot path (BASELINE.json metric) on B200.
 
-Default workload: BASELINE configs[1] ("config 2"): T=3 tasks, d=5, n=2^16 points per
-task on scrambled digital nets, order-4 Walsh DSI kernel; one step = one fit evaluation
-= NLL + logdet + analytic gradient w.r.t. (eta, w, v, gamma), inputs resident in HBM.
+Default workload: BASELINE config 4 -- the largest single-GPU configuration, on which the
+north-star's HBM-roofline target is stated: T=2 tasks, d=4, n=2^26 points per task on a rank-1
+lattice (N = 2^27), B2 kernel; one step = one fit evaluation = NLL + logdet + analytic gradient
+w.r.t. (eta, w, v, gamma), inputs resident in HBM.  `--config 2|5` runs the other configs.
 
 Timing: W warm-up steps, then K steps each bracketed by CUDA events on the library's
 stream; L2 is flushed (512 MiB write) before every timed step, outside the events; the
 step times are summed, barrier + synchronize on both sides, max over ranks.
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config 2]
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config 4]
 
-N > 1 (torchrun, NCCL): the fit does not shard (configs 1-2 are
-"replicas only"), so every rank runs an independent replica and value = N x fits/s.
+N > 1 (one process per GPU; `--gpus N` self-launches torchrun when WORLD_SIZE is unset):
+config 4 runs the frequency-sharded fit (SURVEY.md §8e, strong scaling), config 5 shards the
+candidates, configs 1-2 run independent replicas (value = N x fits/s).
+
+Reference arm (`--impl reference`): the reference's own `fit` (oracle/_ref, built from the
+unmodified reference sources) on the host cores, its own per-step timer; see cpu_reference.
 """
 from __future__ import annotations
 
@@ -135,92 +140,136 @@ def algorithmic_bytes(kernel: str, inst, P: int, T: int, nc: int = 1) -> float:
     return table.get(kernel, 0.0)
 
 
-def ncu_traffic(kernel: str):
-    """dram__bytes_read+write per launch from the committed ncu --set full capture."""
+def ncu_traffic(cfg: int, kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from the committed
+    `ncu --set full` capture of this config (profiles/ncu_traffic.json, written by
+    tools/ncu_summary.py from the capture named there); (None, None) if not captured."""
     path = os.path.join(HERE, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(kernel)
+            d = json.load(f)
+        ent = d.get(f"config{cfg}", {})
+        if kernel in ent:
+            return ent[kernel], ent.get("_source", "profiles/ncu_traffic.json")
     except Exception:
-        return None
+        pass
+    return None, None
 
 
 # ----------------------------------------------------------------------------- reference arm
-def cpu_reference(inst, steps: int, warmup: int, grad_params: int):
-    """Time the reference C++ library itself (oracle/_ref) on host cores: one step = one
-    loss_value (build_spectrum + invert_and_logdet + tau + solve) of the full workload;
-    a fit with the reference's own central-FD gradient costs (1 + 2 P_theta) of them
-    (gp_core.cpp:341-351), so fits/s = 1 / ((1 + 2 P_theta) * t_loss)."""
+# Bounded samples for the CPU reference (one reference fit step at the full config 4 / 5 size takes
+# ~40 min / ~75 s on the host): the same generator, kernel and hyperparameters at 2^m per task,
+# scaled to the full size by N log2 N (the reference's cost is transform-dominated at these
+# shapes, SURVEY.md §8d; checked against one full-size reference loss_value, tools/ref_scaling.py
+# -> profiles/r02_ref_scaling.json).  Configs 1-2 run at full size.
+REF_SAMPLE_M = {4: 18, 5: 14}
+
+
+def nlogn(N: int) -> float:
+    return N * np.log2(N)
+
+
+def cpu_reference(cfg: int, inst, steps: int, warmup: int):
+    """The reference's own fit (gp_core.cpp:317-382) on host cores, timed by the reference's own
+    per-step timer (FitReport::step_seconds): one step = central-FD gradient (2 P_theta calls of
+    loss_value) + iRprop- update + loss at the new theta = the reference's NLL + gradient, our
+    unit of work.  Returns the per-step seconds actually measured and the metric value
+    (fits/s of the full workload; config 5: candidate fits/s)."""
     threads = os.cpu_count() or 1
     os.environ["FASTMTGP_THREADS"] = str(threads)
     from oracle import ref  # test-infrastructure checker / CPU baseline only
-    kind = "reference"
     if not ref.available():
         raise RuntimeError("oracle/_ref not built")
-    model = ref.Model(inst.design, inst.hyper, inst.y)
-    for _ in range(warmup):
-        model.set_hyper(inst.hyper)
-        model.loss(0)
-    ts = []
-    for _ in range(steps):
-        model.set_hyper(inst.hyper)  # invalidate caches: full refresh every step
-        t0 = time.perf_counter()
-        model.loss(0)
-        ts.append(time.perf_counter() - t0)
-    t_loss = statistics.median(ts)
-    evals = 1 + 2 * grad_params
-    return {"value": 1.0 / (evals * t_loss), "unit": "fits/s", "cores": threads, "kind": kind,
-            "sample": f"{len(ts)} x reference loss_value at N = {inst.design.N} (median {t_loss * 1e3:.1f} ms); "
-                      f"fit = {evals} loss evaluations (central-FD gradient over {grad_params} parameters)",
-            "t_loss_s": t_loss}
+    from paper_2603_16014_b200 import configs
+    dz = inst.design
+    m_s = REF_SAMPLE_M.get(cfg)
+    if m_s is not None and m_s < dz.m[0]:
+        sample = configs.make(cfg, m=[m_s] * dz.L, **({"n_cand": 1} if cfg == 5 else {}))
+        scale = nlogn(dz.N) / nlogn(sample.design.N)
+    else:
+        sample, scale = inst, 1.0
+    model = ref.Model(sample.design, sample.hyper, sample.y)
+    secs, n_params, _ = ref.fit_timed(model, warmup + steps)
+    timed = secs[warmup:]
+    t_step = float(np.mean(timed))
+    what = (f"reference fit (gp_core.cpp:317-382), {len(timed)} timed iRprop- steps after {warmup} warm-up, each "
+            f"= central-FD gradient over {n_params} parameters ({2 * n_params} loss_value calls) + update + "
+            f"loss at the new theta; mean {t_step:.3f} s/step at N = {sample.design.N}")
+    if scale != 1.0:
+        what += (f"; sample 2^{m_s} per task, scaled by N log2 N (x{scale:.1f}) to N = {dz.N} "
+                 f"(validation: profiles/r02_ref_scaling.json)")
+    if cfg == 5:
+        what += "; one candidate per step (value = candidate fits/s)"
+    return {"value": 1.0 / (t_step * scale), "unit": "fits/s", "cores": threads, "kind": "reference",
+            "sample": what, "t_step_s": t_step, "scale": scale, "n_params": n_params}
 
 
 # ----------------------------------------------------------------------------- main
+WORKLOADS = {1: "config1: T=2 d=2 n=2^10 lattice B2",
+             2: "config2: T=3 d=5 n=2^16 scrambled digital net, order-4 Walsh DSI kernel",
+             3: "config3: T=4 d=8 n=2^20/2^18/2^16/2^14 lattice B4",
+             4: "config4: T=2 d=4 n=2^26 lattice B2 (N = 2^27)",
+             5: "config5: T=4 d=10 n=2^18 digital order-4 Walsh, 256-candidate sweep per step"}
+
+
+def self_launch(args) -> int:
+    """`python bench.py --gpus N` outside torchrun: start N ranks on this node (NCCL over NVLink),
+    one process per GPU, rendezvous on 127.0.0.1; rank 0's JSON line is this process's output."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 4, 5],
+                    help="BASELINE config; default 4 = the largest single-GPU config (headline)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="diagnostics only: skip the L2 flush")
     args = ap.parse_args()
     warmup = max(args.warmup, 3)
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
     from paper_2603_16014_b200 import configs
 
     inst = configs.make(args.config)
     dz, hp = inst.design, inst.hyper
     P, T = dz.L * (dz.L + 1) // 2, dz.L
-    grad_params = dz.d + hp.B.size + T + 1  # eta, w, v, gamma
-    workload = {1: "config1", 2: "config2: T=3 d=5 n=2^16 scrambled digital net, order-4 Walsh DSI kernel",
-                3: "config3", 4: "config4: T=2 d=4 n=2^26 lattice B2",
-                5: "config5: T=4 d=10 n=2^18 digital order-4 Walsh, 256-candidate sweep per step"}[args.config]
-    config = {"workload": workload, "N": dz.N, "T": T, "d": dz.d, "n": dz.n[0],
-              "outputs": "NLL, logdet, dNLL/d(eta, w, v, gamma)", "l2": "flushed before every step (512 MiB write)",
-              "parallelism": {4: "frequency-sharded (2 NCCL all-to-alls per fit)",
-                              5: "candidate-sharded (gather of the records)"}.get(args.config, "replicas")
-              if args.gpus > 1 else "single"}
+    parallelism = "single"
+    if args.gpus > 1:
+        parallelism = {4: f"frequency-sharded over {world} GPUs (2 NCCL all-to-alls per fit)",
+                       5: f"candidate-sharded over {world} GPUs (gather of the records)"}.get(args.config,
+                                                                                      f"{world} replicas")
+    config = {"workload": WORKLOADS[args.config], "N": dz.N, "T": T, "d": dz.d, "n": dz.n[0],
+              "outputs": "NLL, logdet, dNLL/d(eta, w, v, gamma)",
+              "l2": "flushed before every step (512 MiB write)" if not args.no_flush else "not flushed",
+              "parallelism": parallelism}
 
     if args.impl == "reference":
         if rank != 0:
             return
-        if args.config == 4:  # as the cpu_baseline below: 2^20 per task, scaled by N log2 N
-            small = configs.make(4, m=[20, 20])
-            cb = cpu_reference(small, args.steps, warmup, grad_params)
-            f = (dz.N * np.log2(dz.N)) / (small.design.N * np.log2(small.design.N))
-            cb["value"] /= f
-            cb["sample"] += f"; measured at 2 x 2^20 points and scaled by N log2 N (x{f:.1f}) to 2 x 2^26"
-        else:
-            cb = cpu_reference(inst, args.steps, warmup, grad_params)
+        cb = cpu_reference(args.config, inst, args.steps, warmup)
         line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "fits/s", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": warmup, "ms_per_step": 1e3 / cb["value"], "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
+                "steps": args.steps, "warmup": warmup, "ms_per_step": 1e3 * cb["t_step_s"],
+                "ms_per_step_note": "what the reference actually ran per step (the bounded sample); value is "
+                                    "scaled to the full workload as cpu_baseline.sample states",
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": config,
                 "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
                 "e2e": {"value": cb["value"], "unit": "fits/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -365,26 +414,23 @@ def main():
                    "share": v[0] / max(sum(x[0] for x in prof.values()), 1e-12),
                    "alg_GBps": (algorithmic_bytes(k, inst, P, T, ncl) / (1e-3 * v[0] / max(v[1], 1)) / 1e9)
                    if v[0] > 0 else None} for k, v in prof.items()}
+    traffic, traffic_src = ncu_traffic(args.config, dom_name)
+    # whole fit against SURVEY.md §8d's algorithmic bytes 8n(6P + T) (the north-star's 60 % target)
+    b_fit = 8.0 * dz.n[0] * (6 * P + T) * (len(inst.candidates) if args.config == 5 else 1)
+    fit_level = {"alg_bytes": b_fit, "definition": "SURVEY.md 8(d) B_alg = 8n(6P+T) per fit",
+                 "achieved": b_fit / (ms_per_step * 1e-3) / 1e9 * (1 if sharded else world),
+                 "frac": b_fit / (ms_per_step * 1e-3) / 1e9 * (1 if sharded else world) / peak}
     roofline = {"bound": "hbm", "kernel": dom_name,
                 "timing": "per-kernel CUDA events on the fit stream, second pass of the same K steps "
-                          f"({1e3 * prof_total_ms / args.steps:.1f} us/step instrumented)", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": ncu_traffic(dom_name) if args.config in (2, 4) else None,  # captured configs "alg_bytes_per_launch": alg,
-                "peak_source": peak_src, "kernels": kernels}
+                          f"({1e3 * prof_total_ms / args.steps:.1f} us/step instrumented)",
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "alg_bytes_per_launch": alg, "traffic": traffic, "traffic_source": traffic_src,
+                "peak_source": peak_src, "kernels": kernels, "fit": fit_level}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        try:
-            if args.config == 4:
-                # one reference loss at n = 2^26 per task takes minutes: time it at 2^20 per task
-                # and scale by N log2 N (FFT-dominated) — stated in `sample`
-                small = configs.make(4, m=[20, 20])
-                cb = cpu_reference(small, 2, 1, grad_params)
-                n_s, n_f = small.design.N, dz.N
-                f = (n_f * np.log2(n_f)) / (n_s * np.log2(n_s))
-                cb["value"] /= f
-                cb["sample"] += f"; measured at 2 x 2^20 points and scaled by N log2 N (x{f:.1f}) to 2 x 2^26"
-            else:
-                cb = cpu_reference(inst, 3, 1, grad_params)
+        try:  # bounded: 1 warm-up + 2 timed reference fit steps (10-30 s of host work)
+            cb = cpu_reference(args.config, inst, 2, 1)
             cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": "fits/s", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}

@@ -71,6 +71,7 @@ def lib():
         L.ref_model_cubature.argtypes = [C.c_void_p, dp, dp]
         L.ref_model_single_cubature.argtypes = [C.c_void_p, dp, dp]
         L.ref_model_fit.argtypes = [C.c_void_p, C.c_int, dp, dp]
+        L.ref_model_fit_timed.argtypes = [C.c_void_p, C.c_int, dp, dp, dp, C.POINTER(C.c_int)]
         _lib = L
     return _lib
 
@@ -198,6 +199,15 @@ class Model:
         fl = C.c_double()
         _check(lib().ref_model_fit(self.h, steps, C.byref(fl), dptr(trace)))
         return fl.value, trace[:steps]
+
+
+def fit_timed(model: "Model", steps: int):
+    """The reference's own fit (gp_core.cpp:317-382) with its own per-step timer
+    (FitReport::step_seconds): returns (step_seconds[steps], n_params, loss_trace)."""
+    trace, secs = np.empty(max(steps, 1)), np.empty(max(steps, 1))
+    fl, npar = C.c_double(), C.c_int()
+    _check(lib().ref_model_fit_timed(model.h, steps, C.byref(fl), dptr(trace), dptr(secs), C.byref(npar)))
+    return secs[:steps].copy(), npar.value, trace[:steps].copy()
 
 
 def nll_fd_grad(dz: Design, hp: Hyper, y: np.ndarray, h_rel: float = 1e-5, richardson: bool = True):

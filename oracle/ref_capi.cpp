@@ -335,6 +335,27 @@ int ref_model_fit(void* h, int steps, double* final_loss, double* trace) {
     });
 }
 
+// fit with the reference's own per-step timer (FitReport::step_seconds, gp_core.cpp:340-372): one
+// step = the central-FD gradient (2 P_theta loss evaluations) + the iRprop- update + the loss at the
+// new theta — the reference's cost of one NLL + gradient.  The CPU baseline of bench.py.
+int ref_model_fit_timed(void* h, int steps, double* final_loss, double* trace, double* step_seconds,
+                        int* n_params) {
+    return guarded([&] {
+        auto& m = static_cast<RefModel*>(h)->model;
+        FitReport rep = fit(m, steps, LossKind::nmll);
+        *final_loss = rep.final_loss;
+        for (std::size_t i = 0; i < rep.loss_trace.size(); ++i) {
+            if (trace) trace[i] = rep.loss_trace[i];
+            if (step_seconds) step_seconds[i] = rep.step_seconds[i];
+        }
+        if (n_params) {
+            // ParamPack::layout (gp_core.cpp:243-304): log gamma, log eta, B, log t, log b (DSI)
+            *n_params = 1 + m.design.d + int(m.hyper.B.rows() * m.hyper.B.cols()) + m.design.L +
+                        (m.family == KernelFamily::dsi_digital ? 4 : 0);
+        }
+    });
+}
+
 int ref_thread_count() { return thread_count(); }
 
 }  // extern "C"

@@ -1072,21 +1072,39 @@ void nll_batch_impl(fmtgp_model* M, int nc, const fmtgp_hyper* hin, bool grad, f
     std::vector<double> scale(nc, 1.0);
     std::vector<int> esc(nc, 0);
     std::vector<int> status(nc, FMTGP_OK);
+    // one launch serves candidates of one base kernel only: the Walsh order weights b (digital) or
+    // the Bernoulli order (lattice) select the kernel code and the design-time kappa table, so
+    // candidates are grouped by them (stable) and every group is evaluated on its own
+    auto same_kernel = [&](int x, int y) {
+        return M->lattice ? hin[x].si_alpha == hin[y].si_alpha : std::memcmp(hin[x].b, hin[y].b, sizeof(hin[x].b)) == 0;
+    };
+    {
+        std::vector<int> grouped;
+        std::vector<char> used(nc, 0);
+        for (int c = 0; c < nc; ++c) {
+            if (used[c]) continue;
+            for (int e = c; e < nc; ++e)
+                if (!used[e] && same_kernel(c, e)) used[e] = 1, grouped.push_back(e);
+        }
+        todo.swap(grouped);
+    }
     for (int attempt = 0; !todo.empty(); ++attempt) {
-        for (size_t base = 0; base < todo.size(); base += M->max_cand) {
-            const int cnt = int(std::min<size_t>(M->max_cand, todo.size() - base));
-            std::vector<const fmtgp_hyper*> hs(cnt);
-            std::vector<double> sc(cnt);
-            std::vector<int> es(cnt);
-            for (int i = 0; i < cnt; ++i) {
+        for (size_t base = 0, cnt = 0; base < todo.size(); base += cnt) {
+            cnt = 1;
+            while (base + cnt < todo.size() && int(cnt) < M->max_cand && same_kernel(todo[base], todo[base + cnt])) ++cnt;
+            const int nb = int(cnt);
+            std::vector<const fmtgp_hyper*> hs(nb);
+            std::vector<double> sc(nb);
+            std::vector<int> es(nb);
+            for (int i = 0; i < nb; ++i) {
                 hs[i] = hin + todo[base + i];
                 sc[i] = scale[todo[base + i]];
                 es[i] = attempt;
             }
-            eval_equal(M, cnt, hs.data(), sc.data(), grad, keep_chat && todo[base] == 0 && cnt == 1);
-            std::vector<fmtgp_result> tmp(cnt);
-            finish_results(M, cnt, hs.data(), grad, tmp.data(), sc.data(), es.data());
-            for (int i = 0; i < cnt; ++i) {
+            eval_equal(M, nb, hs.data(), sc.data(), grad, keep_chat && todo[base] == 0 && nb == 1);
+            std::vector<fmtgp_result> tmp(nb);
+            finish_results(M, nb, hs.data(), grad, tmp.data(), sc.data(), es.data());
+            for (int i = 0; i < nb; ++i) {
                 const int c = todo[base + i];
                 out[c] = tmp[i];
                 if (nonreal_of(M, i)) status[c] = FMTGP_ERR_NONREAL;
@@ -1537,7 +1555,21 @@ double fit_loss(fmtgp_model* M, PackedHyper& P, const std::vector<double>& th, s
     const bool ok = r.status == FMTGP_OK && std::isfinite(r.nll);
     if (!grad) return ok ? r.nll : INFINITY;
     grad->assign(th.size(), 0.0);
-    if (!ok) return INFINITY;
+    if (!ok) {
+        // infeasible point (escalation exhausted): the reference still differences its guarded
+        // loss here and moves off it where a probe is finite (gp_core.cpp:343-351)
+        for (size_t i = 0; i < th.size(); ++i) {
+            const double hstep = 1e-4 * std::max(1.0, std::abs(th[i]));
+            std::vector<double> tp = th;
+            tp[i] = th[i] + hstep;
+            const double fp = fit_loss(M, P, tp, nullptr);
+            tp[i] = th[i] - hstep;
+            const double fm = fit_loss(M, P, tp, nullptr);
+            (*grad)[i] = (std::isfinite(fp) && std::isfinite(fm)) ? (fp - fm) / (2.0 * hstep) : 0.0;
+        }
+        P.unpack(th);
+        return INFINITY;
+    }
     auto& g = *grad;
     int k = 0;
     g[k++] = P.h.gamma * r.dgamma;

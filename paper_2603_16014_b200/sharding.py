@@ -20,6 +20,7 @@ from typing import Callable, List, Sequence, Tuple
 import numpy as np
 
 from ._lib import ERR_NONREAL, ERR_SCHUR, SHARD_REC_LEN, CResult, FastMtgpError, SchurBreakdown, check
+from .fast_gram import _result
 
 
 def shard_range(n: int, world: int, rank: int) -> Tuple[int, int]:
@@ -108,17 +109,12 @@ class ShardedLatticeFit:
         return self.bufs[1]
 
     def end(self):
-
-
         rec = np.zeros(SHARD_REC_LEN)
         check(self.model.lib.fmtgp_shard_end(self.model.h, C.c_void_p(self.bufs[0].data_ptr()),
                                              rec.ctypes.data_as(C.POINTER(C.c_double))))
         return rec
 
     def finish(self, hp, rec, grad: bool, xi_scale: float, escalations: int):
-
-
-        from .fast_gram import _result  # noqa: PLC0415 (fast_gram imports nothing from here)
         ch = self.model._hyper_struct(hp)
         r = CResult()
         rec = np.ascontiguousarray(rec, dtype=np.float64)

@@ -1,0 +1,165 @@
+"""GPU parity at the BASELINE.json configuration SHAPES (VERDICT r01 "Next round" item 1).
+
+Every kernel instantiation the bench and the sweeps run is checked against the reference:
+  * config-2 shape (digital, T=3, d=5, order-4 Walsh b = e4, rank-2 task factor): the exact-D
+    fused kernels k_dig_col_fwd / k_dig_mid / k_dig_col_inv<*, 5>;
+  * config-5 shape (digital, T=4, d=10, K_task = L L^T + 0.05 I): k_dig_col_inv<*, 10> through
+    fmtgp_nll_batch, once with one candidate per CTA and once with candidate groups (cpb > 1:
+    the double-buffered column tiles + the per-candidate finalize kernel);
+  * config-4 shape (lattice, T=2, d=4, B2, eta = 0.8, rank-1 w): the fused lattice path L1-L3;
+  * the same generators at (or near) full size against the reference's loss_value.
+
+The reference has no gradient (it differences its loss, gp_core.cpp:341-351): gradients are
+compared with Richardson-extrapolated central differences of the reference NLL
+(oracle.ref.nll_fd_grad; two step sizes agree to ~1e-9 relative at these shapes, so the 1e-7
+bound below is the FD floor with a margin, not a loosened tolerance).  NLL / logdet: absolute
+1e-8 N (BASELINE north_star).
+"""
+import numpy as np
+import pytest
+
+from paper_2603_16014_b200 import configs
+
+pytestmark = pytest.mark.gpu
+
+FD_REL = 1e-7
+
+
+@pytest.fixture(scope="module")
+def Model():
+    from paper_2603_16014_b200.fast_gram import Model as M
+    return M
+
+
+def check_grad(r, fd, N):
+    assert abs(r["nll"] - fd["nll"]) <= 1e-8 * N, (r["nll"], fd["nll"])
+    scale = max(1.0, np.abs(fd["eta"]).max(), np.abs(fd["B"]).max(), np.abs(fd["t"]).max(), abs(fd["gamma"]))
+    for mine, ref_key in (("deta", "eta"), ("dB", "B"), ("dt", "t")):
+        err = np.abs(np.asarray(r[mine]) - np.asarray(fd[ref_key])).max()
+        assert err <= FD_REL * scale, (mine, r[mine], fd[ref_key])
+    assert abs(r["dgamma"] - fd["gamma"]) <= FD_REL * scale
+
+
+@pytest.mark.parametrize("m", [8, 9, 10])
+def test_config2_shape_gradient(ref, Model, m):
+    inst = configs.make(2, m=[m] * 3)
+    M = Model(inst.design)
+    M.set_y(inst.y)
+    r = M.nll(inst.hyper, grad=True)
+    check_grad(r, ref.nll_fd_grad(inst.design, inst.hyper, inst.y), inst.design.N)
+    # the bench replays the captured graph: the replay must give the same bits
+    again = M.nll(inst.hyper, grad=True)
+    assert again["nll"] == r["nll"] and np.array_equal(again["deta"], r["deta"])
+
+
+@pytest.mark.parametrize("cpb", [None, "4"], ids=["one-per-cta", "groups4"])
+def test_config5_shape_gradient(ref, Model, monkeypatch, cpb):
+    if cpb is not None:
+        monkeypatch.setenv("FMTGP_DIG_CPB", cpb)
+    inst = configs.make(5, m=[8] * 4, n_cand=8)
+    M = Model(inst.design, max_candidates=8)
+    M.set_y(inst.y)
+    res = M.nll_batch(inst.candidates, grad=True)
+    for c in (0, 3, 6):
+        check_grad(res[c], ref.nll_fd_grad(inst.design, inst.candidates[c], inst.y), inst.design.N)
+    for h, r in zip(inst.candidates, res):
+        assert abs(r["nll"] - ref.Model(inst.design, h, inst.y).loss(0)) <= 1e-8 * inst.design.N
+
+
+def test_config5_groups_equal_single(Model, monkeypatch):
+    """Candidate groups (cpb = 4) give the same bits as one-candidate evaluations."""
+    inst = configs.make(5, m=[9] * 4, n_cand=8)
+    M1 = Model(inst.design, max_candidates=1)
+    M1.set_y(inst.y)
+    single = [M1.nll(h, grad=True) for h in inst.candidates]
+    monkeypatch.setenv("FMTGP_DIG_CPB", "4")
+    M = Model(inst.design, max_candidates=8)
+    M.set_y(inst.y)
+    batch = M.nll_batch(inst.candidates, grad=True)
+    for a, b in zip(single, batch):
+        assert abs(a["nll"] - b["nll"]) <= 1e-12 * abs(a["nll"])
+        for k in ("deta", "dB", "dt"):
+            assert np.abs(np.asarray(a[k]) - np.asarray(b[k])).max() <= 1e-10 * max(1.0, np.abs(a[k]).max())
+
+
+def test_mixed_kernel_candidates_in_one_batch(ref, Model):
+    """candidates with different Walsh order weights b in one nll_batch are evaluated
+    with their own base kernel (grouped by b), equal to single calls and to the reference."""
+    inst = configs.make(5, m=[7] * 4, n_cand=6)
+    bs = [(0.0, 0.0, 0.0, 1.0), (1.0, 0.0, 0.0, 0.0), (0.5, 0.2, 0.1, 1.0)]
+    cands = [h.replace(b=bs[i % 3]) for i, h in enumerate(inst.candidates)]
+    M = Model(inst.design, max_candidates=6)
+    M.set_y(inst.y)
+    batch = M.nll_batch(cands, grad=True)
+    for h, rb in zip(cands, batch):
+        rs = M.nll(h, grad=True)
+        assert abs(rs["nll"] - rb["nll"]) <= 1e-12 * abs(rs["nll"])
+        assert np.abs(rs["deta"] - rb["deta"]).max() <= 1e-10 * max(1.0, np.abs(rs["deta"]).max())
+        assert abs(rb["nll"] - ref.Model(inst.design, h, inst.y).loss(0)) <= 1e-8 * inst.design.N
+
+
+def test_mixed_bernoulli_order_in_one_batch(ref, Model):
+    inst = configs.make(4, m=[17, 17])
+    cands = [inst.hyper, inst.hyper.replace(si_alpha=2), inst.hyper.replace(eta=inst.hyper.eta * 0.5)]
+    M = Model(inst.design, max_candidates=3)
+    M.set_y(inst.y)
+    batch = M.nll_batch(cands, grad=True)
+    for h, rb in zip(cands, batch):
+        rs = M.nll(h, grad=True)
+        assert abs(rs["nll"] - rb["nll"]) <= 1e-12 * abs(rs["nll"])
+        assert abs(rb["nll"] - ref.Model(inst.design, h, inst.y).loss(0)) <= 1e-8 * inst.design.N
+
+
+@pytest.mark.parametrize("m", [17, 18])
+def test_config4_shape_gradient_fused_lattice(ref, Model, m):
+    inst = configs.make(4, m=[m, m])
+    M = Model(inst.design)
+    M.set_y(inst.y)
+    r = M.nll(inst.hyper, grad=True)
+    check_grad(r, ref.nll_fd_grad(inst.design, inst.hyper, inst.y), inst.design.N)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("m", [22, 23])
+def test_config4_large_vs_reference(ref, Model, m):
+    """Config-4 generator, kernel and hyperparameters at 2 x 2^22 / 2 x 2^23 (the full size
+    2 x 2^26 takes the reference minutes per loss: tools/ref_check_full.py, evidence in profiles/)."""
+    inst = configs.make(4, m=[m, m])
+    M = Model(inst.design)
+    M.set_y(inst.y)
+    r = M.nll(inst.hyper, grad=True)
+    rm = ref.Model(inst.design, inst.hyper, inst.y)
+    want = rm.loss(0)
+    st = rm.state()
+    N = inst.design.N
+    assert abs(r["nll"] - want) <= 1e-8 * N
+    assert abs(r["logdet"] - st["logdet"]) <= 1e-8 * N
+    c = M.coefficients()
+    assert np.linalg.norm(c - st["c"]) <= 1e-10 * np.linalg.norm(st["c"])
+
+
+@pytest.mark.slow
+def test_config5_full_size_candidates_vs_reference(ref, Model):
+    """Eight config-5 candidates at the full n = 2^18 per task (N = 2^20) vs the reference's
+    loss_value, through the batched sweep (candidate groups)."""
+    inst = configs.make(5, n_cand=8)
+    M = Model(inst.design, max_candidates=8)
+    M.set_y(inst.y)
+    res = M.nll_batch(inst.candidates, grad=True)
+    N = inst.design.N
+    rm = ref.Model(inst.design, inst.candidates[0], inst.y)
+    for h, r in zip(inst.candidates, res):
+        rm.set_hyper(h)
+        assert abs(r["nll"] - rm.loss(0)) <= 1e-8 * N
+
+
+@pytest.mark.slow
+def test_config2_full_size_gradient(ref, Model):
+    """Config 2 at full size (3 x 2^16): NLL, logdet, c and the analytic gradient vs central
+    differences of the reference (plain, not Richardson: 60 reference losses)."""
+    inst = configs.make(2)
+    M = Model(inst.design)
+    M.set_y(inst.y)
+    r = M.nll(inst.hyper, grad=True)
+    fd = ref.nll_fd_grad(inst.design, inst.hyper, inst.y, richardson=False)
+    check_grad(r, fd, inst.design.N)

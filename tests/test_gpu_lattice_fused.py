@@ -254,5 +254,7 @@ def test_fused_fit_loop_matches_generic():
     hp = hp.replace(xi=np.full(2, 1e-3))
     a = model(dz, y, True).fit(hp, 5)
     b = model(dz, y, False).fit(hp, 5)
-    tol = 1e-8 * dz.N
-    assert np.all(np.abs(a["loss_trace"] - b["loss_trace"]) <= tol + 1e-9 * np.abs(b["loss_trace"]))
+    # same trajectory: every iRprop- update moves theta by the same signed step, so theta agrees to
+    # rounding (a single sign flip would move a component by >= 1e-6); losses to a relative bound
+    assert np.abs(np.asarray(a["theta"]) - np.asarray(b["theta"])).max() <= 1e-12
+    assert np.all(np.abs(a["loss_trace"] - b["loss_trace"]) <= 1e-10 * np.abs(b["loss_trace"]))
