@@ -100,7 +100,9 @@ def test_mixed_kernel_candidates_in_one_batch(ref, Model):
 
 def test_mixed_bernoulli_order_in_one_batch(ref, Model):
     inst = configs.make(4, m=[17, 17])
-    cands = [inst.hyper, inst.hyper.replace(si_alpha=2), inst.hyper.replace(eta=inst.hyper.eta * 0.5)]
+    # the B4 candidate gets a larger nugget: at 1e-8 the reference's own solve trips its 1e-8
+    # imaginary-residue guard at this size (SURVEY.md §8c caveat 1)
+    cands = [inst.hyper, inst.hyper.replace(si_alpha=2, xi=np.full(2, 1e-3)), inst.hyper.replace(eta=inst.hyper.eta * 0.5)]
     M = Model(inst.design, max_candidates=3)
     M.set_y(inst.y)
     batch = M.nll_batch(cands, grad=True)
