@@ -1,9 +1,10 @@
 // Equal-n lattice fit in three fused kernels — see lattice.cuh.
 #include "lattice.cuh"
+#include "ipfft.cuh"
 
 namespace fmtgp {
 
-constexpr int LAT_NT = 512;            // 16 complex per thread per FFT stage, 2^13-element tiles
+constexpr int LAT_NT = 512;            // one radix-16 group per thread per FFT stage, 2^13-element tiles
 constexpr int LAT_TILE_LOG = 13;
 constexpr int LAT_MID_SMEM = 200 * 1024;
 
@@ -18,7 +19,7 @@ bool LatGeo::make(int m, int V, int T, int d, LatGeo& g) {
         ++l2cap;
     int l2 = std::min(l2cap, std::max(g.lt - LAT_TILE_LOG, (g.lt + 1) / 2));
     const int l1 = g.lt - l2;
-    if (l2 < 1 || l1 < 1 || l1 > LAT_TILE_LOG) return false;
+    if (l2 < 5 || l1 < 5 || l1 > LAT_TILE_LOG) return false;  // in-place FFTs need >= 1 radix-16 stage
     g.l1 = l1;
     g.l2 = l2;
     g.lc = std::min(LAT_TILE_LOG - l1, l2);
@@ -123,22 +124,6 @@ struct LatGen {
     }
 };
 
-// Four-step twiddles without per-element table reads: a thread's elements are u = 0, 1, ... NT
-// apart, so exp(-2 pi i j (t0 + u s) / 2^L) = base * step_u with base = w^(j t0) per thread and
-// step_u = w^(j s u) from a small per-CTA smem table — both exact table products (<= 2 ulp), all
-// loads issued at kernel start where the generator / FFT hides their latency.
-constexpr int LAT_STEPS = 16;  // elements per thread per vector (EPT at NT = 512)
-
-// column kernels: thread t owns column cc = t & (C-1), rows k1 = (t >> lc) + u (NT >> lc)
-__device__ __forceinline__ void col_steps(double2* s_step, const double2* __restrict__ tw, uint32_t c0, int lc,
-                                          int NT, int L) {
-    const int C = 1 << lc;
-    for (int t = threadIdx.x; t < C * LAT_STEPS; t += NT) {
-        const int cc = t / LAT_STEPS, u = t - cc * LAT_STEPS;
-        s_step[t] = twiddle(tw, uint64_t(c0 + cc) * uint64_t((NT >> lc) * u), L);
-    }
-}
-
 // ------------------------------------------------------------------ exchange-block layout
 // Row k1 -> (owner rank h, local row i): cluster q = min(k1, N1 - k1) (rows 0 and N1/2 form
 // cluster 0), side = 1 for the upper row of the pair.
@@ -158,39 +143,31 @@ __device__ __forceinline__ size_t xaddr(const LatArgs& a, int c, int h, int o, i
 }
 
 // ------------------------------------------------------------------ L1: generator x column FFT
+// In-place DIF column FFT (ipfft.cuh) of C = 2^lc columns of N1 = 2^l1 rows (C N1 = 16 NT):
+// stage 0 is fused with the generator (each thread generates its radix-16 group straight into
+// registers), the twiddle-free tail stage with the store of the exchange blocks (row k1 =
+// ip_freq of the position).  The four-step twiddle w_{n'}^(k1 j2) is applied by L2 on its inputs.
 template <int NT, int DC, int ALPHA>
 __global__ void __launch_bounds__(NT) k_lat_col_fwd(LatArgs a, int l1, int l2, int lc) {
     extern __shared__ __align__(16) unsigned char smraw[];
     double2* sm = reinterpret_cast<double2*>(smraw);
     constexpr auto S = sidx<true>;
     const int v = blockIdx.y, c = v / a.V, o = v - c * a.V;
-    const int C = 1 << lc, N1 = 1 << l1, ld = padded_len(N1), tile = C << l1;
+    const int N1 = 1 << l1, ld = padded_len(N1);
     const uint32_t c0 = uint32_t(a.rank * a.ncb + blockIdx.x) << lc;  // global first column
-    __shared__ double2 s_step[32 * LAT_STEPS];
-    const int lt = l1 + l2;
-    col_steps(s_step, a.tw, c0, lc, NT, lt);
-    const int tcc = threadIdx.x & (C - 1);
-    const double2 tbase = twiddle(a.tw, uint64_t(c0 + tcc) * uint64_t(threadIdx.x >> lc), lt);
-    LatGen<DC, ALPHA> G;
-    G.init(a, c, o);
-    int done = 0;
-    if ((l1 & 3) == 1) {
-        // first (twiddle-free) radix-2 Stockham level fused into the generation: no radix-2 tail stage
-        const int H = N1 >> 1;
-        for (int e = threadIdx.x; e < (C << (l1 - 1)); e += NT) {
-            const int jj = e >> lc, cc = e & (C - 1);
-            const uint32_t j0 = (uint32_t(jj) << l2) + c0 + uint32_t(cc), j1 = j0 + (uint32_t(H) << l2);
-            const double2 x0 = make_double2(G.q(2u * j0), G.q(2u * j0 + 1u));
-            const double2 x1 = make_double2(G.q(2u * j1), G.q(2u * j1 + 1u));
-            sm[cc * ld + S(2 * jj)] = cadd(x0, x1);
-            sm[cc * ld + S(2 * jj + 1)] = csub(x0, x1);
-        }
-        done = 1;
-    } else {
-        for (int e = threadIdx.x; e < tile; e += NT) {
-            const int j1 = e >> lc, cc = e & (C - 1);
-            const uint32_t j = (uint32_t(j1) << l2) + c0 + uint32_t(cc);
-            sm[cc * ld + S(j1)] = make_double2(G.q(2u * j), G.q(2u * j + 1u));
+    const IpGeo ig = IpGeo::of(l1);
+    const int M_log = l1 - 4;  // stage-0 stride; also log2 of the 16-position chunks per column
+    const int vec = threadIdx.x >> M_log, j1 = threadIdx.x & ((1 << M_log) - 1);
+    Tw16 t0;
+    t0.load(a.tw, j1, l1);
+    double2 x[16];
+    {
+        LatGen<DC, ALPHA> G;
+        G.init(a, c, o);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const uint32_t J = (uint32_t(j1 + (r << M_log)) << l2) + c0 + uint32_t(vec);
+            x[r] = make_double2(G.q(2u * J), G.q(2u * J + 1u));
         }
     }
     pdl_trigger();
@@ -199,19 +176,30 @@ __global__ void __launch_bounds__(NT) k_lat_col_fwd(LatArgs a, int l1, int l2, i
         for (int t = threadIdx.x; t < a.nc; t += NT) a.bad[t] = 0x7f7f7f7f;
         for (int t = threadIdx.x; t < a.nc * MAXT * 2; t += NT) a.imre[t] = 0ull;
     }
+    dif16_regs(x, t0);
+    {
+        double2* xs = sm + vec * ld;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) xs[S(j1 + (brev_c<16>(r) << M_log))] = x[r];
+    }
     __syncthreads();
-    smem_fft_from<NT, true>(sm, l1, done, C, ld, -1, a.tw);
-    const double2* st = s_step + tcc * LAT_STEPS;
-    const int jl = int(c0) + tcc - a.rank * a.WC;
-#pragma unroll 4
-    for (int u = 0; u < LAT_STEPS; ++u) {
-        const int e = threadIdx.x + u * NT;
-        if (e < tile) {
-            const int k1 = e >> lc;
-            int i;
-            const int h = row_owner(k1, N1, a.lqp, i);
-            a.Y[xaddr(a, c, h, o, i, jl)] = cmul(sm[tcc * ld + S(k1)], cmul(tbase, st[u]));
-        }
+    ip_mid_stages<NT, false>(sm, ig, 1, ig.a16, 1 << lc, ld, a.tw);
+    // tail stage + store: this thread's 16 contiguous positions of column vec2
+    const int vec2 = threadIdx.x >> M_log, p0 = (threadIdx.x & ((1 << M_log) - 1)) << 4;
+    {
+        const double2* xs = sm + vec2 * ld;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) x[r] = xs[S(p0 + r)];
+    }
+    tail_regs(x, ig.rl, -1);
+    const int kb = ip_freq(p0, ig);
+    const int jl = int(c0) + vec2 - a.rank * a.WC;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        const int k1 = kb | ip_freq_lo(tail_out_pos(r, ig.rl), ig);
+        int i;
+        const int h = row_owner(k1, N1, a.lqp, i);
+        a.Y[xaddr(a, c, h, o, i, jl)] = x[r];
     }
 }
 
@@ -236,6 +224,10 @@ __host__ __device__ constexpr int cls_distinct(int y) {
 
 // DIST: the class map is cls_distinct<T> (compile time: no per-pair class selects); otherwise
 // it comes from LatArgs::pair_ofs.
+// Row transforms are in place (ipfft.cuh): DIF stage 0 applies the four-step twiddle
+// w_{n'}^(row j2) to its inputs, the solve walks the DIF output in POSITION order (bank-conflict
+// free; yhat comes in the matching permuted layout, LatArgs::yperm), and the last DIT stage
+// applies the conjugate twiddle on its way to HBM.
 template <int NT, int T, bool DIST>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArgs a, int l1, int l2) {
     constexpr int P = T * (T + 1) / 2;
@@ -244,51 +236,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
     constexpr auto S = sidx<true>;
     __shared__ double s_coef[P], s_xi[P], s_wR[P];
     __shared__ int s_cls[P];
+    __shared__ double2 s_ostep[16];
     cg::cluster_group cl = cg::this_cluster();
     const int rank = int(cl.block_rank());
     const int q = a.rank * a.QP + (blockIdx.x >> 1), c = blockIdx.y, V = DIST ? P - T + 1 : a.V;
     const int li = blockIdx.x;  // local row index of this CTA's row in the exchange blocks
     auto cls = [&](int y) { return DIST ? cls_distinct<T>(y) : s_cls[y]; };
     const int N1 = 1 << l1, N2 = 1 << l2, lds = padded_len(N2), lt = l1 + l2;
+    const IpGeo ig = IpGeo::of(l2);
+    const int M_log = l2 - 4;
     const int row = lat_row_of(q, rank, N1);
     const long long half = a.half;
-    // frequency pairs (k, N' - k): one thread owns both slots (reads, solves, writes back)
     const bool selfrow = q == 0;  // rows 0 and N1/2 pair with themselves
     const int rowA = selfrow ? row : q, rowB = selfrow ? row : N1 - q;
-    int p0, p1;
-    if (selfrow) {
-        p0 = 0;
-        p1 = rank == 0 ? N2 / 2 + 1 : N2 / 2;
-    } else {
-        p0 = rank * (N2 / 2);
-        p1 = p0 + N2 / 2;
-    }
-    // prologue independent of L1 (overlaps its tail under programmatic dependent launch):
-    // coefficients, and the twiddles as per-thread bases x per-CTA step tables (see col_steps)
-    __shared__ double2 s_rstep[LAT_STEPS], s_ostep[LAT_STEPS];
+    // prologue independent of L1 (overlaps its tail under programmatic dependent launch)
     if (threadIdx.x < P) {
         const int p = threadIdx.x;
         s_coef[p] = __ldg(a.coef + size_t(c) * P + p);
         s_xi[p] = __ldg(a.xi + size_t(c) * P + p);
         s_wR[p] = (a.pair_a[p] == a.pair_b[p] ? 1.0 : 2.0) * __ldg(a.Rpair + size_t(c) * P + p);
         s_cls[p] = a.pair_ofs[p];
-    } else if (threadIdx.x >= 32 && threadIdx.x < 32 + LAT_STEPS) {
-        const int u = threadIdx.x - 32;
-        s_rstep[u] = twiddle(a.tw, uint64_t(u) * uint64_t(NT) * uint64_t(N1), a.m);  // r2c: w_n^k
-        s_ostep[u] = twiddle(a.tw, uint64_t(u) * uint64_t(NT) * uint64_t(row), lt);  // four-step
+    } else if (threadIdx.x >= 32 && threadIdx.x < 48) {
+        const int u = threadIdx.x - 32;  // four-step step table: w^(row M u), M = N2 / 16
+        s_ostep[u] = twiddle(a.tw, (uint64_t(u) << M_log) * uint64_t(row), lt);
     }
-    const double2 rbase = twiddle(a.tw, uint64_t(rowA) + uint64_t(p0 + int(threadIdx.x)) * uint64_t(N1), a.m);
-    const double2 obase = twiddle(a.tw, uint64_t(threadIdx.x) * uint64_t(row), lt);
-    const double2* yh = a.yhat;
-    auto partner = [&](int p) { return selfrow ? (rank == 0 ? ((N2 - p) & (N2 - 1)) : (N2 - 1 - p)) : (N2 - 1 - p); };
-    // yhat of the thread's next pair is loaded one iteration ahead (its latency hides behind a solve)
-    double2 yA[T], yB[T];
-    {
-        const int p = p0 + int(threadIdx.x);
-        if (p < p1) {
-            const long long sa = ((long long)rowA << l2) + p, sb = ((long long)rowB << l2) + partner(p);
-#pragma unroll
-            for (int t = 0; t < T; ++t) yA[t] = yh[size_t(t) * half + sa], yB[t] = yh[size_t(t) * half + sb];
+    // this thread's radix-16 group of stage 0 / the last DIT stage: class gvec, offset gj1
+    const bool has_g = int(threadIdx.x) < (V << M_log);
+    const int gvec = threadIdx.x >> M_log, gj1 = threadIdx.x & ((1 << M_log) - 1);
+    double2 obase = twiddle(a.tw, uint64_t(gj1) * uint64_t(row), lt);
+    Tw16 t0;
+    t0.load(a.tw, gj1, l2);
+    // solve iteration space (positions pA of row A; Hermitian partner position pB of row B):
+    //   non-self clusters: rank r takes pA in [r N2/2, (r+1) N2/2), partner N2-1-k2a -> pB = N2-1-pA
+    //   row N1/2 (rank 1 of cluster 0): pA in [0, N2/2), same partner map
+    //   row 0 (rank 0 of cluster 0): partner (N2 - k2a) mod N2 in the same row; every position,
+    //   kept when k2a <= N2/2
+    const bool row0 = selfrow && rank == 0;
+    const int pbeg = (selfrow ? 0 : rank * (N2 / 2)), pend = row0 ? N2 : pbeg + N2 / 2;
+    const double2* yp = a.yperm;
+    // L2-prefetch this CTA's yhat rows (independent of L1)
+    if (threadIdx.x < 2 * T) {
+        const int t = threadIdx.x >> 1, side = threadIdx.x & 1;
+        const long long r0 = side ? rowB : rowA;
+        const long long lo = side ? (row0 ? 0 : N2 - pend) : pbeg, hi = side ? (row0 ? N2 : N2 - pbeg) : pend;
+        const double2* base = yp + size_t(t) * half + (r0 << l2) + lo;
+        const unsigned bytes = unsigned((hi - lo) * sizeof(double2));
+        for (unsigned off = 0; off < bytes; off += 32768u) {
+            const unsigned n = bytes - off < 32768u ? bytes - off : 32768u;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(reinterpret_cast<const char*>(base) + off),
+                         "r"(n)
+                         : "memory");
         }
     }
     pdl_wait();
@@ -300,7 +297,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
     }
     cp_async_wait_all();
     __syncthreads();
-    smem_fft<NT, true>(sm, l2, V, lds, -1, a.tw);
+    if (has_g) {
+        double2* xs = sm + gvec * lds;
+        double2 x[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) x[r] = cmul(xs[S(gj1 + (r << M_log))], cmul(obase, s_ostep[r]));
+        dif16_regs(x, t0);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) xs[S(gj1 + (brev_c<16>(r) << M_log))] = x[r];
+    }
+    __syncthreads();
+    ip_mid_stages<NT, false>(sm, ig, 1, ig.a16, V, lds, a.tw);
+    ip_tail_stage<NT>(sm, ig, V, lds, -1);
     cl.sync();  // both rows transformed: partner rows readable over DSMEM
 
     double2* rem = cl.map_shared_rank(sm, rank ^ 1);
@@ -316,19 +324,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
     long long first_bad = 0x7f7f7f7fll;
     double lpm = 1.0;  // running pivot product of the slots k >= 1 (weight 2): one log per thread
     int lpe = 0;
+    auto partner = [&](int pA, int k2a, int& k2b) {
+        if (row0) {
+            k2b = (N2 - k2a) & (N2 - 1);
+            return ip_pos(k2b, ig);
+        }
+        k2b = N2 - 1 - k2a;
+        return N2 - 1 - pA;
+    };
 #pragma unroll 1
-    for (int p = p0 + int(threadIdx.x), it = 0; p < p1; p += NT, ++it) {
-        const int k2a = p;
-        const int k2b = partner(p);
+    for (int pA = pbeg + int(threadIdx.x); pA < pend; pA += NT) {
+        const int k2a = ip_freq(pA, ig);
+        if (row0 && k2a > N2 / 2) continue;  // its partner's thread owns the pair
+        int k2b;
+        const int pB = partner(pA, k2a, k2b);
         const long long kA = rowA + ((long long)k2a << l1);
         const long long slA = ((long long)rowA << l2) + k2a, slB = ((long long)rowB << l2) + k2b;
         double2 rA[T], rB[T];
 #pragma unroll
-        for (int t = 0; t < T; ++t) rA[t] = yA[t], rB[t] = yB[t];
-        if (p + NT < p1) {
-            const long long sa = slA + NT, sb = ((long long)rowB << l2) + partner(p + NT);
-#pragma unroll
-            for (int t = 0; t < T; ++t) yA[t] = yh[size_t(t) * half + sa], yB[t] = yh[size_t(t) * half + sb];
+        for (int t = 0; t < T; ++t) {
+            rA[t] = yp[size_t(t) * half + ((long long)rowA << l2) + pA];
+            rB[t] = yp[size_t(t) * half + ((long long)rowB << l2) + pB];
         }
         if (kA == 0) {
             // packed slot 0: frequency 0 (.x) and Nyquist (.y), two real systems; tau zeroes the
@@ -374,13 +390,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
             continue;
         }
         const bool self = slA == slB;  // k = N'/2 (row 0, k2 = N2/2)
-        const double2 wA = cmul(rbase, s_rstep[it]);  // exp(-2 pi i k / n)
-        const double2 wB = make_double2(-wA.x, wA.y);  // exp(-2 pi i (N' - k)/n) = -conj(wA)
+        const double2 wA = twiddle(a.tw, uint64_t(kA), a.m);  // exp(-2 pi i k / n)
+        const double2 wB = make_double2(-wA.x, wA.y);          // exp(-2 pi i (N' - k)/n) = -conj(wA)
         double2 HA[P], HB[P];
 #pragma unroll
         for (int x = 0; x < P; ++x) {
             const int o = cls(x);
-            const double2 za = bufA[o * lds + S(k2a)], zb = bufB[o * lds + S(k2b)];
+            const double2 za = bufA[o * lds + S(pA)], zb = bufB[o * lds + S(pB)];
             HA[x] = r2c_post(za, zb, wA);
             HB[x] = r2c_post(zb, za, wB);
         }
@@ -425,10 +441,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
             for (int o = 0; o < P; ++o) {
                 if (o >= V) break;
                 if (self) {
-                    bufA[o * lds + S(k2a)] = c2r_pre(ZA[o], ZA[o], wA);
+                    bufA[o * lds + S(pA)] = c2r_pre(ZA[o], ZA[o], wA);
                 } else {
-                    bufA[o * lds + S(k2a)] = c2r_pre(ZA[o], ZB[o], wA);
-                    bufB[o * lds + S(k2b)] = c2r_pre(ZB[o], ZA[o], wB);
+                    bufA[o * lds + S(pA)] = c2r_pre(ZA[o], ZB[o], wA);
+                    bufB[o * lds + S(pB)] = c2r_pre(ZB[o], ZA[o], wB);
                 }
             }
         }
@@ -458,18 +474,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
         }
     }
     if (!grad) return;
-    smem_fft<NT, true>(sm, l2, V, lds, +1, a.tw);  // block_sum_vec's barriers ordered the writes
-#pragma unroll 1
-    for (int u = 0; u < LAT_STEPS; ++u) {
-        const int j2 = int(threadIdx.x) + u * NT;
-        if (j2 >= N2) break;
-        const double2 w = cmul(obase, s_ostep[u]);
-        for (int oo = 0; oo < V; ++oo)
-            a.Y[xaddr(a, c, j2 >> a.lwc, oo, li, j2 & (a.WC - 1))] = cmulc(sm[oo * lds + S(j2)], w);
+    // inverse row FFT (block_sum_vec's barriers ordered the solve's writes): DIT tail, middle
+    // stages, then stage 0 fused with the conjugate four-step twiddle and the store
+    ip_tail_stage<NT>(sm, ig, V, lds, +1);
+    ip_mid_stages<NT, true>(sm, ig, 1, ig.a16, V, lds, a.tw);
+    if (has_g) {
+        t0.load(a.tw, gj1, l2);
+        obase = twiddle(a.tw, uint64_t(gj1) * uint64_t(row), lt);
+        const double2* xs = sm + gvec * lds;
+        double2 x[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) x[r] = xs[S(gj1 + (r << M_log))];
+        dit16_regs(x, t0);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int j2 = gj1 + (brev_c<16>(r) << M_log);
+            a.Y[xaddr(a, c, j2 >> a.lwc, gvec, li, j2 & (a.WC - 1))] =
+                cmulc(x[r], cmul(obase, s_ostep[brev_c<16>(r)]));
+        }
     }
 }
 
 // ------------------------------------------------------------------ L3: inverse column FFT -> gradient dot
+// In-place DIT: the tail stage is fused with the exchange-block loads, stage 0 with the
+// gradient dot (W(2j) = 2 Re z, W(2j+1) = 2 Im z consumed in registers).
 template <int NT, int DC, int ALPHA>
 __global__ void __launch_bounds__(NT) k_lat_col_inv(LatArgs a, int l1, int l2, int lc) {
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -477,61 +505,54 @@ __global__ void __launch_bounds__(NT) k_lat_col_inv(LatArgs a, int l1, int l2, i
     constexpr auto S = sidx<true>;
     __shared__ int s_last;
     const int v = blockIdx.y, c = v / a.V, o = v - c * a.V;
-    const int C = 1 << lc, N1 = 1 << l1, ld = padded_len(N1), tile = C << l1;
+    const int N1 = 1 << l1, ld = padded_len(N1);
     const uint32_t c0 = uint32_t(a.rank * a.ncb + blockIdx.x) << lc;  // global first column
     const int jl0 = int(c0) - a.rank * a.WC;
-    LatGen<DC, ALPHA> G;
-    G.init(a, c, o);  // independent of L2: overlaps its tail
+    const IpGeo ig = IpGeo::of(l1);
+    const int M_log = l1 - 4;
+    const int tvec = threadIdx.x >> M_log, p0 = (threadIdx.x & ((1 << M_log) - 1)) << 4;
+    const int kb = ip_freq(p0, ig);
     pdl_wait();
-    const double2* xb = a.Cbuf;
-    int done = 0;
-    if ((l1 & 3) == 1) {
-        // first (twiddle-free) radix-2 level fused into the load: no radix-2 tail stage; all of a
-        // thread's loads are issued before the first butterfly
-        constexpr int PB = LAT_STEPS / 2;
-        const int H = N1 >> 1, npair = C << (l1 - 1);
-        double2 x0[PB], x1[PB];
+    double2 x[16];
+    {
+        const double2* xb = a.Cbuf;
 #pragma unroll
-        for (int u = 0; u < PB; ++u) {
-            const int e = threadIdx.x + u * NT;
-            if (e < npair) {
-                const int jj = e >> lc, cc = e & (C - 1);
-                int i0, i1;
-                const int h0 = row_owner(jj, N1, a.lqp, i0), h1 = row_owner(jj + H, N1, a.lqp, i1);
-                x0[u] = __ldcs(&xb[xaddr(a, c, h0, o, i0, jl0 + cc)]);
-                x1[u] = __ldcs(&xb[xaddr(a, c, h1, o, i1, jl0 + cc)]);
-            }
+        for (int r = 0; r < 16; ++r) {
+            const int k1 = kb | ip_freq_lo(r, ig);
+            int i;
+            const int h = row_owner(k1, N1, a.lqp, i);
+            x[r] = __ldcs(&xb[xaddr(a, c, h, o, i, jl0 + tvec)]);
         }
+    }
+    tail_regs(x, ig.rl, +1);
+    {
+        double2* xs = sm + tvec * ld;
 #pragma unroll
-        for (int u = 0; u < PB; ++u) {
-            const int e = threadIdx.x + u * NT;
-            if (e < npair) {
-                const int jj = e >> lc, cc = e & (C - 1);
-                sm[cc * ld + S(2 * jj)] = cadd(x0[u], x1[u]);
-                sm[cc * ld + S(2 * jj + 1)] = csub(x0[u], x1[u]);
-            }
-        }
-        done = 1;
-    } else {
-        for (int e = threadIdx.x; e < tile; e += NT) {
-            const int k1 = e >> lc, cc = e & (C - 1);
-            int i1;
-            const int h1 = row_owner(k1, N1, a.lqp, i1);
-            cp_async16(&sm[cc * ld + S(k1)], &xb[xaddr(a, c, h1, o, i1, jl0 + cc)]);
-        }
-        cp_async_wait_all();
+        for (int r = 0; r < 16; ++r) xs[S(p0 + tail_out_pos(r, ig.rl))] = x[r];
     }
     __syncthreads();
-    smem_fft_from<NT, true>(sm, l1, done, C, ld, +1, a.tw);
+    ip_mid_stages<NT, true>(sm, ig, 1, ig.a16, 1 << lc, ld, a.tw);
+    const int gvec = threadIdx.x >> M_log, gj1 = threadIdx.x & ((1 << M_log) - 1);
+    {
+        Tw16 t0;
+        t0.load(a.tw, gj1, l1);
+        const double2* xs = sm + gvec * ld;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) x[r] = xs[S(gj1 + (r << M_log))];
+        dit16_regs(x, t0);
+    }
     double acc[DC];
 #pragma unroll
     for (int j = 0; j < DC; ++j) acc[j] = 0.0;
-    for (int e = threadIdx.x; e < tile; e += NT) {
-        const int j1 = e >> lc, cc = e & (C - 1);
-        const uint32_t j = (uint32_t(j1) << l2) + c0 + uint32_t(cc);
-        const double2 z = sm[cc * ld + S(j1)];  // W(2j) = 2 Re z, W(2j+1) = 2 Im z
-        G.dq_acc(2u * j, 2.0 * z.x, acc);
-        G.dq_acc(2u * j + 1u, 2.0 * z.y, acc);
+    {
+        LatGen<DC, ALPHA> G;
+        G.init(a, c, o);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const uint32_t J = (uint32_t(gj1 + (brev_c<16>(r) << M_log)) << l2) + c0 + uint32_t(gvec);
+            G.dq_acc(2u * J, 2.0 * x[r].x, acc);  // W(2j) = 2 Re z, W(2j+1) = 2 Im z
+            G.dq_acc(2u * J + 1u, 2.0 * x[r].y, acc);
+        }
     }
     const int nblk = gridDim.x;
     __shared__ double redv[(NT / 32) * DC];
@@ -567,6 +588,22 @@ __global__ void __launch_bounds__(NT) k_lat_col_inv(LatArgs a, int l1, int l2, i
     t.gamma = __ldg(a.gamma + c);
     t.out = a.out + size_t(c) * NOUT;
     class_sums_out<NT>(t);
+}
+
+// yhat in the fused path's row-position order: yperm[t][row][p] = yhat[t][row][ip_freq(p)]
+// (once per dataset, fmtgp_model_set_y)
+__global__ void k_lat_perm(const double2* __restrict__ yh, double2* __restrict__ yp, long long total, int l2) {
+    const IpGeo ig = IpGeo::of(l2);
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long rowbase = e & ~((1ll << l2) - 1);
+        yp[e] = yh[rowbase + ip_freq(int(e & ((1ll << l2) - 1)), ig)];
+    }
+}
+
+void lat_perm_yhat(const LatGeo& g, int T, long long half, const void* yhat, void* yperm, cudaStream_t s) {
+    const long long total = (long long)T * half;
+    k_lat_perm<<<148 * 8, 256, 0, s>>>(static_cast<const double2*>(yhat), static_cast<double2*>(yperm), total, g.l2);
 }
 
 // ------------------------------------------------------------------ launcher

@@ -48,6 +48,7 @@ struct LatArgs {
     const int* pair_a;
     const int* pair_b;
     const double2* yhat;      // [T][n'] slot layout
+    const double2* yperm;     // [T][n'] yhat with each row in DIF position order (lat_perm_yhat)
     double2* Y;               // [nc][V][n'] intermediate
     double* part_mid;         // [nc][N1][2 + P]
     double* part_dot;         // [nc][V][nblk_col][MAXD + 1]
@@ -73,6 +74,8 @@ struct LatArgs {
 };
 
 void lat_fit(const LatGeo& g, const LatArgs& a, cudaStream_t s);
+// yperm[t][row][p] = yhat[t][row][ip_freq(p)] (ipfft.cuh): the row order L2's solve walks in
+void lat_perm_yhat(const LatGeo& g, int T, long long half, const void* yhat, void* yperm, cudaStream_t s);
 // one phase of it (1: L1, 2: L2, 3: L3 when want_grad) — the sharded fit interleaves all-to-alls
 void lat_phase(const LatGeo& g, const LatArgs& a, int phase, cudaStream_t s);
 

@@ -225,6 +225,7 @@ struct fmtgp_model {
     // data
     double* d_y = nullptr;
     void* d_yhat = nullptr;
+    void* d_yperm = nullptr;    // fused lattice path: yhat rows in DIF position order
     bool have_y = false;
     double tau[MAXT]{};
     // per-candidate buffers
@@ -507,6 +508,7 @@ void inverse_vector(fmtgp_model* M, const void* dslots, double* dvec) {
 
 void compute_yhat_tau(fmtgp_model* M) {
     forward_vector(M, M->d_y, M->d_yhat);
+    if (M->lat) lat_perm_yhat(M->lgeo, M->T, M->pslots[0], M->d_yhat, M->d_yperm, M->st);
     // tau: equal n -> tau_l = yhat_l(0) / sqrt(n) (the sample mean, gp_core.cpp:67-88 with
     // V̄ 1 = sqrt(n) e_0); unequal n -> class-0 normal equations at fit time.
     if (M->equal) {
@@ -726,6 +728,7 @@ LatArgs lat_args(fmtgp_model* M, int nc, int si_alpha, bool grad) {
     a.pair_a = M->d_pa;
     a.pair_b = M->d_pb;
     a.yhat = static_cast<const double2*>(M->d_yhat);
+    a.yperm = static_cast<const double2*>(M->d_yperm);
     a.Y = static_cast<double2*>(M->d_work);
     a.part_mid = M->d_part_mid;
     a.part_dot = M->d_part_dot;
@@ -1320,6 +1323,7 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
         }
         M->d_y = dalloc<double>(M->N);
         M->d_yhat = dalloc<char>(M->task_slots * es);
+        if (M->lat) M->d_yperm = dalloc<char>(M->task_slots * es);
         // hyper block: eta [mc*d] | gamma [mc] | Rpair [mc*P] | per group: coef [mc*np] | xi [mc*np]
         {
             size_t len = size_t(max_cand) * (M->d + 1 + M->P);
@@ -1690,6 +1694,7 @@ int fmtgp_model_destroy(fmtgp_model_t M) {
     F(M->d_pb);
     F(M->d_y);
     F(M->d_yhat);
+    F(M->d_yperm);
     F(M->d_hyp);
     for (auto& ge : M->graphs) {
         if (ge.exec) cudaGraphExecDestroy(ge.exec);
