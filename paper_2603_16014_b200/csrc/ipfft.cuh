@@ -1,7 +1,7 @@
 // In-place mixed-radix FFT building blocks for the fused lattice kernels (lattice.cu).
 //
-// A vector of N = 2^LOG complex values (LOG >= 5) is transformed in shared memory by
-// Gentleman-Sande decimation in frequency (DIF, forward) and its exact mirror, decimation in
+// A vector of N = 2^LOG complex values (compile-time LOG >= 5) is transformed in shared memory
+// by Gentleman-Sande decimation in frequency (DIF, forward) and its exact mirror, decimation in
 // time (DIT, inverse).  LOG = 4 A16 + log2(R_last):
 //   * A16 radix-16 stages s = 0 .. A16-1 with stride M_s = 2^(LOG - 4(s+1)) (block 16 M_s):
 //       DIF: x[b 16M + j1 + M j2] (j2 natural) -> 16-point DFT -> * w_{16M}^(j1 k2) -> position
@@ -16,47 +16,49 @@
 // inverse; the DIT input is expected in that same order and its output is natural.
 // Unnormalised, like transform.cuh: DIF computes sum_j x_j e^(-2 pi i jk/N), DIT the conjugate
 // kernel.  Smem addressing is the padded sidx<true> (1 pad per 16 elements): radix-16 stages
-// with M >= 2 and the contiguous 16-position tail groups are bank-conflict free.
+// and the contiguous 16-position tail groups are bank-conflict free, and because a group's
+// base has its low bits below M, sidx(base + r M) = sidx(base) + r M + (r M >> 4): with LOG a
+// template parameter every smem access of a stage is an immediate offset from one pointer.
 #pragma once
 
 #include "transform.cuh"
 
 namespace fmtgp {
 
-struct IpGeo {
-    int log;   // N = 2^log
-    int a16;   // radix-16 stages before the tail
-    int rl;    // log2 R_last (4 when log is a multiple of 4)
-    __host__ __device__ static IpGeo of(int log) {
-        IpGeo g;
-        g.log = log;
-        g.rl = (log & 3) ? (log & 3) : 4;
-        g.a16 = (log - g.rl) >> 2;
-        return g;
+template <int LOG>
+struct Ip {
+    static_assert(LOG >= 5 && LOG <= 13, "in-place FFT length");
+    static constexpr int RL = (LOG & 3) ? (LOG & 3) : 4;  // log2 R_last
+    static constexpr int A16 = (LOG - RL) >> 2;           // radix-16 stages before the tail
+    // frequency held at DIF output position p: digit s of k (base 16, s < A16) sits at position
+    // weight 2^(LOG - 4(s+1)); the tail digit (base R_last) at weight 1
+    static __device__ __forceinline__ int freq(int p) {
+        int k = (p & ((1 << RL) - 1)) << (4 * A16);
+#pragma unroll
+        for (int s = 0; s < A16; ++s) k |= ((p >> (LOG - 4 * (s + 1))) & 15) << (4 * s);
+        return k;
+    }
+    static __device__ __forceinline__ int pos(int k) {
+        int p = k >> (4 * A16);
+#pragma unroll
+        for (int s = 0; s < A16; ++s) p |= ((k >> (4 * s)) & 15) << (LOG - 4 * (s + 1));
+        return p;
+    }
+    // frequency bits of the low 4 position bits: freq(p0 + lo) = freq(p0) | freq_lo(lo) for p0 a
+    // multiple of 16 (the tail digit, then the low bits of radix-16 digit A16-1 at weight R_last)
+    static __host__ __device__ constexpr int freq_lo(int lo) {
+        return ((lo & ((1 << RL) - 1)) << (4 * A16)) | ((lo >> RL) << (4 * (A16 - 1)));
     }
 };
 
-// frequency held at DIF output position p: digit s of k (base 16, s < a16) sits at position
-// weight 2^(log - 4(s+1)); the tail digit (base R_last) at weight 1.
-__device__ __forceinline__ int ip_freq(int p, IpGeo g) {
-    int k = (p & ((1 << g.rl) - 1)) << (4 * g.a16);
-#pragma unroll
-    for (int s = 0; s < 3; ++s)
-        if (s < g.a16) k |= ((p >> (g.log - 4 * (s + 1))) & 15) << (4 * s);
-    return k;
+// smem offset of element r of a group with stride M = 2^ML relative to sidx(base)
+template <int ML>
+__host__ __device__ constexpr int ip_off(int r) {
+    return (r << ML) + ((r << ML) >> 4);
 }
-__device__ __forceinline__ int ip_pos(int k, IpGeo g) {
-    int p = k >> (4 * g.a16);
-#pragma unroll
-    for (int s = 0; s < 3; ++s)
-        if (s < g.a16) p |= ((k >> (4 * s)) & 15) << (g.log - 4 * (s + 1));
-    return p;
-}
-
-// frequency bits of the low 4 position bits: ip_freq(p0 + lo) = ip_freq(p0) | ip_freq_lo(lo) for p0 a
-// multiple of 16 (the tail digit, then the low bits of radix-16 digit a16-1 at position weight R_last)
-__device__ __forceinline__ int ip_freq_lo(int lo, IpGeo g) {
-    return ((lo & ((1 << g.rl) - 1)) << (4 * g.a16)) | ((lo >> g.rl) << (4 * (g.a16 - 1)));
+// exp(-2 pi i t / 2^L), L <= 13: one table read
+__device__ __forceinline__ double2 tw_small(const double2* __restrict__ tab, uint32_t t, int L) {
+    return __ldg(tab + (size_t(L) << TW_BASE_LOG) + (t & ((1u << L) - 1u)));
 }
 
 // w_{2^L}^(j1 k2) for k2 = 1..15 from four table reads (k2 = 1, 4, 8, 12) and at most three
@@ -65,10 +67,10 @@ __device__ __forceinline__ int ip_freq_lo(int lo, IpGeo g) {
 struct Tw16 {
     double2 w1, w4, w8, w12;
     __device__ __forceinline__ void load(const double2* __restrict__ tw, int j1, int L) {
-        w1 = twiddle(tw, uint64_t(j1), L);
-        w4 = twiddle(tw, uint64_t(4 * j1), L);
-        w8 = twiddle(tw, uint64_t(8 * j1), L);
-        w12 = twiddle(tw, uint64_t(12 * j1), L);
+        w1 = tw_small(tw, uint32_t(j1), L);
+        w4 = tw_small(tw, uint32_t(4 * j1), L);
+        w8 = tw_small(tw, uint32_t(8 * j1), L);
+        w12 = tw_small(tw, uint32_t(12 * j1), L);
     }
     // f(k2, w) for k2 = 1..15 in natural order, w = w^(j1 k2)
     template <class F>
@@ -97,75 +99,77 @@ __device__ __forceinline__ void dit16_regs(double2 (&v)[16], const Tw16& t) {
     reg_dft<16>(v, +1);
 }
 
-// Middle radix-16 stages [s0, s1) of nvec vectors (stride ld) on one group per thread per
-// vector-slot; each stage ends with a barrier.  DIF runs s ascending, DIT descending.
-template <int NT, bool DIT>
-__device__ __forceinline__ void ip_mid_stages(double2* sm, IpGeo g, int s0, int s1, int nvec, int ld,
-                                              const double2* __restrict__ tw) {
-    constexpr auto S = sidx<true>;
-    const int gpv_log = g.log - 4;
-    const int total = nvec << gpv_log;
+// One middle radix-16 stage s over nvec vectors (stride ld), then a barrier.
+template <int NT, int LOG, int S_, bool DIT>
+__device__ __forceinline__ void ip_stage(double2* sm, int nvec, int ld, const double2* __restrict__ tw) {
+    constexpr int ML = LOG - 4 * (S_ + 1);
+    constexpr int GPV = LOG - 4;  // log2 groups per vector
+    const int total = nvec << GPV;
 #pragma unroll 1
-    for (int i = 0; i < s1 - s0; ++i) {
-        const int s = DIT ? s1 - 1 - i : s0 + i;
-        const int M_log = g.log - 4 * (s + 1);
-#pragma unroll 1
-        for (int gi = threadIdx.x; gi < total; gi += NT) {
-            const int vec = gi >> gpv_log, q = gi & ((1 << gpv_log) - 1);
-            const int j1 = q & ((1 << M_log) - 1);
-            const int base = ((q >> M_log) << (M_log + 4)) + j1;
-            double2* x = sm + vec * ld;
-            Tw16 t;
-            t.load(tw, j1, M_log + 4);
-            double2 v[16];
+    for (int gi = threadIdx.x; gi < total; gi += NT) {
+        const int vec = gi >> GPV, q = gi & ((1 << GPV) - 1);
+        const int j1 = q & ((1 << ML) - 1);
+        const int base = ((q >> ML) << (ML + 4)) + j1;
+        Tw16 t;
+        t.load(tw, j1, ML + 4);
+        double2* x = sm + vec * ld + sidx<true>(base);
+        double2 v[16];
 #pragma unroll
-            for (int r = 0; r < 16; ++r) v[r] = x[S(base + (r << M_log))];
-            if (DIT) dit16_regs(v, t);
-            else dif16_regs(v, t);
+        for (int r = 0; r < 16; ++r) v[r] = x[ip_off<ML>(r)];
+        if (DIT) dit16_regs(v, t);
+        else dif16_regs(v, t);
 #pragma unroll
-            for (int r = 0; r < 16; ++r) x[S(base + (brev_c<16>(r) << M_log))] = v[r];
-        }
-        __syncthreads();
+        for (int r = 0; r < 16; ++r) x[ip_off<ML>(brev_c<16>(r))] = v[r];
+    }
+    __syncthreads();
+}
+
+// Middle radix-16 stages 1 .. A16-1 (stage 0 is fused by the kernels): DIF ascending, DIT descending.
+template <int NT, int LOG, bool DIT>
+__device__ __forceinline__ void ip_mid_stages(double2* sm, int nvec, int ld, const double2* __restrict__ tw) {
+    constexpr int A = Ip<LOG>::A16;
+    if constexpr (!DIT) {
+        if constexpr (A > 1) ip_stage<NT, LOG, 1, false>(sm, nvec, ld, tw);
+        if constexpr (A > 2) ip_stage<NT, LOG, 2, false>(sm, nvec, ld, tw);
+    } else {
+        if constexpr (A > 2) ip_stage<NT, LOG, 2, true>(sm, nvec, ld, tw);
+        if constexpr (A > 1) ip_stage<NT, LOG, 1, true>(sm, nvec, ld, tw);
     }
 }
 
-// Tail stage (M = 1, radix R = 2^rl, twiddle-free) on 16 contiguous positions held in v:
+// Tail stage (M = 1, radix R = 2^RL, twiddle-free) on 16 contiguous positions held in v:
 // DIF: v natural -> v[c R + r] = Y_c[brev_R(r)]; DIT: v[c R + k2] natural -> y_c[brev_R(r)].
-template <int R>
-__device__ __forceinline__ void tail_regs_r(double2 (&v)[16], int dir) {
+template <int LOG>
+__device__ __forceinline__ void tail_regs(double2 (&v)[16], int dir) {
+    constexpr int R = 1 << Ip<LOG>::RL;
 #pragma unroll
     for (int c = 0; c < 16 / R; ++c) reg_dft<R>(v + c * R, dir);
 }
-__device__ __forceinline__ void tail_regs(double2 (&v)[16], int rl, int dir) {
-    switch (rl) {
-        case 1: tail_regs_r<2>(v, dir); break;
-        case 2: tail_regs_r<4>(v, dir); break;
-        case 3: tail_regs_r<8>(v, dir); break;
-        default: tail_regs_r<16>(v, dir); break;
-    }
-}
 // position offset (within the 16) of output element i of tail_regs
-__device__ __forceinline__ int tail_out_pos(int i, int rl) {
-    const int r = i & ((1 << rl) - 1);
-    return (i & ~((1 << rl) - 1)) + int(__brev(unsigned(r)) >> (32 - rl));
+template <int LOG>
+__host__ __device__ constexpr int tail_out_pos(int i) {
+    constexpr int RL = Ip<LOG>::RL;
+    constexpr int R = 1 << RL;
+    int r = i & (R - 1), b = 0;
+    for (int k = 0; k < RL; ++k) b |= ((r >> k) & 1) << (RL - 1 - k);
+    return (i & ~(R - 1)) + b;
 }
 
 // Tail stage over whole smem vectors: thread owns 16 contiguous positions (conflict-free).
-template <int NT>
-__device__ __forceinline__ void ip_tail_stage(double2* sm, IpGeo g, int nvec, int ld, int dir) {
-    constexpr auto S = sidx<true>;
-    const int cpv_log = g.log - 4;
-    const int total = nvec << cpv_log;
+template <int NT, int LOG>
+__device__ __forceinline__ void ip_tail_stage(double2* sm, int nvec, int ld, int dir) {
+    constexpr int CPV = LOG - 4;
+    const int total = nvec << CPV;
 #pragma unroll 1
     for (int gi = threadIdx.x; gi < total; gi += NT) {
-        const int vec = gi >> cpv_log, p0 = (gi & ((1 << cpv_log) - 1)) << 4;
-        double2* x = sm + vec * ld;
+        const int vec = gi >> CPV, p0 = (gi & ((1 << CPV) - 1)) << 4;
+        double2* x = sm + vec * ld + sidx<true>(p0);
         double2 v[16];
 #pragma unroll
-        for (int r = 0; r < 16; ++r) v[r] = x[S(p0 + r)];
-        tail_regs(v, g.rl, dir);
+        for (int r = 0; r < 16; ++r) v[r] = x[r];
+        tail_regs<LOG>(v, dir);
 #pragma unroll
-        for (int r = 0; r < 16; ++r) x[S(p0 + tail_out_pos(r, g.rl))] = v[r];
+        for (int r = 0; r < 16; ++r) x[tail_out_pos<LOG>(r)] = v[r];
     }
     __syncthreads();
 }

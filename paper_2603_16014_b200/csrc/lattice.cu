@@ -1,10 +1,8 @@
 // Equal-n lattice fit in three fused kernels — see lattice.cuh.
-#include "lattice.cuh"
-#include "ipfft.cuh"
+#include "lattice_kernels.cuh"
 
 namespace fmtgp {
 
-constexpr int LAT_NT = 512;            // one radix-16 group per thread per FFT stage, 2^13-element tiles
 constexpr int LAT_TILE_LOG = 13;
 constexpr int LAT_MID_SMEM = 200 * 1024;
 
@@ -19,7 +17,7 @@ bool LatGeo::make(int m, int V, int T, int d, LatGeo& g) {
         ++l2cap;
     int l2 = std::min(l2cap, std::max(g.lt - LAT_TILE_LOG, (g.lt + 1) / 2));
     const int l1 = g.lt - l2;
-    if (l2 < 5 || l1 < 5 || l1 > LAT_TILE_LOG) return false;  // in-place FFTs need >= 1 radix-16 stage
+    if (l2 < 8 || l1 < 8 || l2 > 13 || l1 > LAT_TILE_LOG) return false;  // instantiated FFT lengths (lat_inst_*.cu)
     g.l1 = l1;
     g.l2 = l2;
     g.lc = std::min(LAT_TILE_LOG - l1, l2);
@@ -39,628 +37,69 @@ Geo LatGeo::slot_geo() const {
     return s;
 }
 
-// ------------------------------------------------------------------ generator on the fly
-// Lattice coordinate of real DFT-order index i against the class offset (lattice_word in
-// generator.cuh, ld_sequences.cpp:31-53): with off = oh 2^(53-m) + olo (olo < 2^(53-m)),
-//   D = ((i g + oh) mod 2^m) 2^(53-m) + olo,   x = D 2^-53 = t 2^-m + olo 2^-53  (exact in fp64),
-// so the 64-bit multiply / shift / mask chain becomes one 32-bit IMAD + LOP and one DFMA.
-// The Bernoulli kernels are polynomials in w = x^2 - x = -u (1 - u), symmetric under
-// u -> 1 - u, so the reference's symmetrisation u = min(x, 1 - x) (kernels.cpp:28-32) is implied:
-//   B2: kappa = 2 pi^2 (u^2 - u + 1/6)            = ka w + kb,       ka = 2 pi^2,      kb = pi^2 / 3
-//   B4: kappa = -(2/3) pi^4 (u^2 (u - 1)^2 - 1/30) = ka w^2 + kb,     ka = -(2/3) pi^4, kb = pi^4 / 45
-// and f = 1 + eta kappa = A + B v with v = w (B2) or w^2 (B4), A = 1 + eta kb, B = eta ka:
-// two DFMAs per dimension after x.  Dimensions are padded to the register cap DC with A = 1,
-// B = 0 (f = 1 exactly), so the unrolled loops carry no per-dimension predicates.
-template <int ALPHA>
-struct LatPoly {
-    static constexpr double pi2 = 9.869604401089358618834491;
-    static constexpr double ka = ALPHA == 1 ? 2.0 * pi2 : -(2.0 / 3.0) * pi2 * pi2;
-    static constexpr double kb = ALPHA == 1 ? pi2 / 3.0 : pi2 * pi2 / 45.0;
-};
-
-template <int DC, int ALPHA>
-struct LatGen {
-    uint32_t gm[DC], oh[DC];
-    double ol[DC], A[DC], B[DC];
-    double gam, inv_n;
-    uint32_t mask;
-    __device__ __forceinline__ void init(const LatArgs& a, int c, int o) {
-        mask = (a.m >= 32) ? 0xffffffffu : ((1u << a.m) - 1u);
-        inv_n = pow2i(-a.m);
-        gam = __ldg(a.gamma + c);
-        const int sh = DIGITAL_BITS - a.m;
-#pragma unroll
-        for (int j = 0; j < DC; ++j) {
-            if (j < a.d) {
-                const uint64_t off = __ldg(a.cofs + size_t(o) * MAXD + j) & MASK53;
-                const double eta = __ldg(a.eta + size_t(c) * a.d + j);
-                gm[j] = uint32_t(__ldg(a.g + j)) & mask;
-                oh[j] = uint32_t(off >> sh) & mask;
-                ol[j] = double(off & ((uint64_t(1) << sh) - 1)) * 0x1p-53;
-                A[j] = fma(eta, LatPoly<ALPHA>::kb, 1.0);
-                B[j] = eta * LatPoly<ALPHA>::ka;
-            } else {
-                gm[j] = oh[j] = 0u;
-                ol[j] = B[j] = 0.0;
-                A[j] = 1.0;
-            }
-        }
-    }
-    // v_j = w (B2) or w^2 (B4) of dimension j at real DFT-order index i
-    __device__ __forceinline__ double v(int j, uint32_t i) const {
-        const uint32_t t = (i * gm[j] + oh[j]) & mask;
-        const double x = fma(double(t), inv_n, ol[j]);
-        const double w = fma(x, x, -x);
-        return ALPHA == 1 ? w : w * w;
-    }
-    // q(i) = gamma prod_j (1 + eta_j kappa_j)  (SpatialKernel, kernels.cpp:91-103)
-    __device__ __forceinline__ double q(uint32_t i) const {
-        double prod = gam;
-#pragma unroll
-        for (int j = 0; j < DC; ++j) prod *= fma(B[j], v(j, i), A[j]);
-        return prod;
-    }
-    // acc_j += W dq/deta_j = W gamma kappa_j prod_{k != j} f_k  (prefix / suffix products: f may vanish)
-    __device__ __forceinline__ void dq_acc(uint32_t i, double W, double* acc) const {
-        double vv[DC], f[DC];
-#pragma unroll
-        for (int j = 0; j < DC; ++j) {
-            vv[j] = v(j, i);
-            f[j] = fma(B[j], vv[j], A[j]);
-        }
-        double pre = gam * W;
-        double dq[DC];
-#pragma unroll
-        for (int j = 0; j < DC; ++j) {
-            dq[j] = pre * fma(LatPoly<ALPHA>::ka, vv[j], LatPoly<ALPHA>::kb);
-            pre *= f[j];
-        }
-        double suf = 1.0;
-#pragma unroll
-        for (int j = DC - 1; j >= 0; --j) {
-            acc[j] = fma(dq[j], suf, acc[j]);
-            suf *= f[j];
-        }
-    }
-};
-
-// ------------------------------------------------------------------ exchange-block layout
-// Row k1 -> (owner rank h, local row i): cluster q = min(k1, N1 - k1) (rows 0 and N1/2 form
-// cluster 0), side = 1 for the upper row of the pair.
-__device__ __forceinline__ int row_owner(int k1, int N1, int lqp, int& i) {
-    int q, side;
-    if (k1 == 0) q = 0, side = 0;
-    else if (k1 == (N1 >> 1)) q = 0, side = 1;
-    else if (k1 < (N1 >> 1)) q = k1, side = 0;
-    else q = N1 - k1, side = 1;
-    const int h = q >> lqp;
-    i = 2 * (q - (h << lqp)) + side;
-    return h;
-}
-// element (row owner h, class o, local row i, local column jl) of candidate c's exchange blocks
-__device__ __forceinline__ size_t xaddr(const LatArgs& a, int c, int h, int o, int i, int jl) {
-    return size_t(c) * a.V * a.half + (((size_t(h) * a.V + o) * a.R + i) << a.lwc) + jl;
-}
-
-// ------------------------------------------------------------------ L1: generator x column FFT
-// In-place DIF column FFT (ipfft.cuh) of C = 2^lc columns of N1 = 2^l1 rows (C N1 = 16 NT):
-// stage 0 is fused with the generator (each thread generates its radix-16 group straight into
-// registers), the twiddle-free tail stage with the store of the exchange blocks (row k1 =
-// ip_freq of the position).  The four-step twiddle w_{n'}^(k1 j2) is applied by L2 on its inputs.
-template <int NT, int DC, int ALPHA>
-__global__ void __launch_bounds__(NT) k_lat_col_fwd(LatArgs a, int l1, int l2, int lc) {
-    extern __shared__ __align__(16) unsigned char smraw[];
-    double2* sm = reinterpret_cast<double2*>(smraw);
-    constexpr auto S = sidx<true>;
-    const int v = blockIdx.y, c = v / a.V, o = v - c * a.V;
-    const int N1 = 1 << l1, ld = padded_len(N1);
-    const uint32_t c0 = uint32_t(a.rank * a.ncb + blockIdx.x) << lc;  // global first column
-    const IpGeo ig = IpGeo::of(l1);
-    const int M_log = l1 - 4;  // stage-0 stride; also log2 of the 16-position chunks per column
-    const int vec = threadIdx.x >> M_log, j1 = threadIdx.x & ((1 << M_log) - 1);
-    Tw16 t0;
-    t0.load(a.tw, j1, l1);
-    double2 x[16];
-    {
-        LatGen<DC, ALPHA> G;
-        G.init(a, c, o);
-#pragma unroll
-        for (int r = 0; r < 16; ++r) {
-            const uint32_t J = (uint32_t(j1 + (r << M_log)) << l2) + c0 + uint32_t(vec);
-            x[r] = make_double2(G.q(2u * J), G.q(2u * J + 1u));
-        }
-    }
-    pdl_trigger();
-    // zero the per-fit flags once per fit (L2 / L3 run after this kernel)
-    if (blockIdx.x == 0 && blockIdx.y == 0) {
-        for (int t = threadIdx.x; t < a.nc; t += NT) a.bad[t] = 0x7f7f7f7f;
-        for (int t = threadIdx.x; t < a.nc * MAXT * 2; t += NT) a.imre[t] = 0ull;
-    }
-    dif16_regs(x, t0);
-    {
-        double2* xs = sm + vec * ld;
-#pragma unroll
-        for (int r = 0; r < 16; ++r) xs[S(j1 + (brev_c<16>(r) << M_log))] = x[r];
-    }
-    __syncthreads();
-    ip_mid_stages<NT, false>(sm, ig, 1, ig.a16, 1 << lc, ld, a.tw);
-    // tail stage + store: this thread's 16 contiguous positions of column vec2
-    const int vec2 = threadIdx.x >> M_log, p0 = (threadIdx.x & ((1 << M_log) - 1)) << 4;
-    {
-        const double2* xs = sm + vec2 * ld;
-#pragma unroll
-        for (int r = 0; r < 16; ++r) x[r] = xs[S(p0 + r)];
-    }
-    tail_regs(x, ig.rl, -1);
-    const int kb = ip_freq(p0, ig);
-    const int jl = int(c0) + vec2 - a.rank * a.WC;
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-        const int k1 = kb | ip_freq_lo(tail_out_pos(r, ig.rl), ig);
-        int i;
-        const int h = row_owner(k1, N1, a.lqp, i);
-        a.Y[xaddr(a, c, h, o, i, jl)] = x[r];
-    }
-}
-
-// ------------------------------------------------------------------ L2: row FFT + solve + inverse row FFT
-__device__ __forceinline__ int lat_row_of(int q, int rank, int N1) {
-    if (q == 0) return rank == 0 ? 0 : N1 / 2;
-    return rank == 0 ? q : N1 - q;
-}
-
-// Class of pair y (row-by-row pair order) when every task has its own shift (the BASELINE
-// designs): all diagonal pairs share offset 0 (class 0), every off-diagonal pair is its own class.
-template <int T>
-__host__ __device__ constexpr int cls_distinct(int y) {
-    int q = 0, off = 0;
-    for (int a = 0; a < T; ++a)
-        for (int b = a; b < T; ++b, ++q) {
-            if (q == y) return a == b ? 0 : 1 + off;
-            if (a != b) ++off;
-        }
-    return 0;
-}
-
-// DIST: the class map is cls_distinct<T> (compile time: no per-pair class selects); otherwise
-// it comes from LatArgs::pair_ofs.
-// Row transforms are in place (ipfft.cuh): DIF stage 0 applies the four-step twiddle
-// w_{n'}^(row j2) to its inputs, the solve walks the DIF output in POSITION order (bank-conflict
-// free; yhat comes in the matching permuted layout, LatArgs::yperm), and the last DIT stage
-// applies the conjugate twiddle on its way to HBM.
-template <int NT, int T, bool DIST>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArgs a, int l1, int l2) {
-    constexpr int P = T * (T + 1) / 2;
-    extern __shared__ __align__(16) unsigned char smraw[];
-    double2* sm = reinterpret_cast<double2*>(smraw);  // [V][padded N2]
-    constexpr auto S = sidx<true>;
-    __shared__ double s_coef[P], s_xi[P], s_wR[P];
-    __shared__ int s_cls[P];
-    __shared__ double2 s_ostep[16];
-    cg::cluster_group cl = cg::this_cluster();
-    const int rank = int(cl.block_rank());
-    const int q = a.rank * a.QP + (blockIdx.x >> 1), c = blockIdx.y, V = DIST ? P - T + 1 : a.V;
-    const int li = blockIdx.x;  // local row index of this CTA's row in the exchange blocks
-    auto cls = [&](int y) { return DIST ? cls_distinct<T>(y) : s_cls[y]; };
-    const int N1 = 1 << l1, N2 = 1 << l2, lds = padded_len(N2), lt = l1 + l2;
-    const IpGeo ig = IpGeo::of(l2);
-    const int M_log = l2 - 4;
-    const int row = lat_row_of(q, rank, N1);
-    const long long half = a.half;
-    const bool selfrow = q == 0;  // rows 0 and N1/2 pair with themselves
-    const int rowA = selfrow ? row : q, rowB = selfrow ? row : N1 - q;
-    // prologue independent of L1 (overlaps its tail under programmatic dependent launch)
-    if (threadIdx.x < P) {
-        const int p = threadIdx.x;
-        s_coef[p] = __ldg(a.coef + size_t(c) * P + p);
-        s_xi[p] = __ldg(a.xi + size_t(c) * P + p);
-        s_wR[p] = (a.pair_a[p] == a.pair_b[p] ? 1.0 : 2.0) * __ldg(a.Rpair + size_t(c) * P + p);
-        s_cls[p] = a.pair_ofs[p];
-    } else if (threadIdx.x >= 32 && threadIdx.x < 48) {
-        const int u = threadIdx.x - 32;  // four-step step table: w^(row M u), M = N2 / 16
-        s_ostep[u] = twiddle(a.tw, (uint64_t(u) << M_log) * uint64_t(row), lt);
-    }
-    // this thread's radix-16 group of stage 0 / the last DIT stage: class gvec, offset gj1
-    const bool has_g = int(threadIdx.x) < (V << M_log);
-    const int gvec = threadIdx.x >> M_log, gj1 = threadIdx.x & ((1 << M_log) - 1);
-    double2 obase = twiddle(a.tw, uint64_t(gj1) * uint64_t(row), lt);
-    Tw16 t0;
-    t0.load(a.tw, gj1, l2);
-    // solve iteration space (positions pA of row A; Hermitian partner position pB of row B):
-    //   non-self clusters: rank r takes pA in [r N2/2, (r+1) N2/2), partner N2-1-k2a -> pB = N2-1-pA
-    //   row N1/2 (rank 1 of cluster 0): pA in [0, N2/2), same partner map
-    //   row 0 (rank 0 of cluster 0): partner (N2 - k2a) mod N2 in the same row; every position,
-    //   kept when k2a <= N2/2
-    const bool row0 = selfrow && rank == 0;
-    const int pbeg = (selfrow ? 0 : rank * (N2 / 2)), pend = row0 ? N2 : pbeg + N2 / 2;
-    const double2* yp = a.yperm;
-    // L2-prefetch this CTA's yhat rows (independent of L1)
-    if (threadIdx.x < 2 * T) {
-        const int t = threadIdx.x >> 1, side = threadIdx.x & 1;
-        const long long r0 = side ? rowB : rowA;
-        const long long lo = side ? (row0 ? 0 : N2 - pend) : pbeg, hi = side ? (row0 ? N2 : N2 - pbeg) : pend;
-        const double2* base = yp + size_t(t) * half + (r0 << l2) + lo;
-        const unsigned bytes = unsigned((hi - lo) * sizeof(double2));
-        for (unsigned off = 0; off < bytes; off += 32768u) {
-            const unsigned n = bytes - off < 32768u ? bytes - off : 32768u;
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(reinterpret_cast<const char*>(base) + off),
-                         "r"(n)
-                         : "memory");
-        }
-    }
-    pdl_wait();
-    pdl_trigger();
-    for (int e = threadIdx.x; e < (V << l2); e += NT) {
-        const int oo = e >> l2, k2 = e & (N2 - 1);
-        const int sr = k2 >> a.lwc;  // column owner
-        cp_async16(&sm[oo * lds + S(k2)], &a.Y[xaddr(a, c, sr, oo, li, k2 & (a.WC - 1))]);
-    }
-    cp_async_wait_all();
-    __syncthreads();
-    if (has_g) {
-        double2* xs = sm + gvec * lds;
-        double2 x[16];
-#pragma unroll
-        for (int r = 0; r < 16; ++r) x[r] = cmul(xs[S(gj1 + (r << M_log))], cmul(obase, s_ostep[r]));
-        dif16_regs(x, t0);
-#pragma unroll
-        for (int r = 0; r < 16; ++r) xs[S(gj1 + (brev_c<16>(r) << M_log))] = x[r];
-    }
-    __syncthreads();
-    ip_mid_stages<NT, false>(sm, ig, 1, ig.a16, V, lds, a.tw);
-    ip_tail_stage<NT>(sm, ig, V, lds, -1);
-    cl.sync();  // both rows transformed: partner rows readable over DSMEM
-
-    double2* rem = cl.map_shared_rank(sm, rank ^ 1);
-    double2* bufA = (selfrow || rank == 0) ? sm : rem;
-    double2* bufB = (selfrow || rank == 1) ? sm : rem;
-    const bool grad = a.want_grad != 0;
-    double acc[2 + P];
-#pragma unroll
-    for (int x = 0; x < 2 + P; ++x) acc[x] = 0.0;
-    double imx[T], rex[T];
-#pragma unroll
-    for (int t = 0; t < T; ++t) imx[t] = rex[t] = 0.0;
-    long long first_bad = 0x7f7f7f7fll;
-    double lpm = 1.0;  // running pivot product of the slots k >= 1 (weight 2): one log per thread
-    int lpe = 0;
-    auto partner = [&](int pA, int k2a, int& k2b) {
-        if (row0) {
-            k2b = (N2 - k2a) & (N2 - 1);
-            return ip_pos(k2b, ig);
-        }
-        k2b = N2 - 1 - k2a;
-        return N2 - 1 - pA;
-    };
-#pragma unroll 1
-    for (int pA = pbeg + int(threadIdx.x); pA < pend; pA += NT) {
-        const int k2a = ip_freq(pA, ig);
-        if (row0 && k2a > N2 / 2) continue;  // its partner's thread owns the pair
-        int k2b;
-        const int pB = partner(pA, k2a, k2b);
-        const long long kA = rowA + ((long long)k2a << l1);
-        const long long slA = ((long long)rowA << l2) + k2a, slB = ((long long)rowB << l2) + k2b;
-        double2 rA[T], rB[T];
-#pragma unroll
-        for (int t = 0; t < T; ++t) {
-            rA[t] = yp[size_t(t) * half + ((long long)rowA << l2) + pA];
-            rB[t] = yp[size_t(t) * half + ((long long)rowB << l2) + pB];
-        }
-        if (kA == 0) {
-            // packed slot 0: frequency 0 (.x) and Nyquist (.y), two real systems; tau zeroes the
-            // frequency-0 residual (gp_core.cpp:67-88) — k_solve_class's p == 0 branch
-            double H0[P], HN[P], A0[P], AN[P], r0[T], rN[T], c0v[T], cN[T], I0[P], IN[P], l0, lN, q0, qN;
-#pragma unroll
-            for (int x = 0; x < P; ++x) {
-                const double2 z = sm[cls(x) * lds + S(0)];
-                H0[x] = z.x + z.y;
-                HN[x] = z.x - z.y;
-                A0[x] = fma(s_coef[x], H0[x], s_xi[x]);
-                AN[x] = fma(s_coef[x], HN[x], s_xi[x]);
-            }
-#pragma unroll
-            for (int t = 0; t < T; ++t) r0[t] = 0.0, rN[t] = rA[t].y;
-            const int st0 = ldl_solve<T, false>(A0, r0, grad, l0, q0, c0v, I0, imx, rex);
-            const int stN = ldl_solve<T, false>(AN, rN, grad, lN, qN, cN, IN, imx, rex);
-            if (st0 == 1 || stN == 1) first_bad = 0;
-            acc[0] += l0 + lN;
-            acc[1] += q0 + qN;
-            if (grad) {
-                double M0[P], MN[P];
-                int x = 0;
-#pragma unroll
-                for (int i = 0; i < T; ++i)
-#pragma unroll
-                    for (int j = i; j < T; ++j, ++x) {
-                        M0[x] = I0[x] - c0v[i] * c0v[j];
-                        MN[x] = IN[x] - cN[i] * cN[j];
-                    }
-#pragma unroll
-                for (int y = 0; y < P; ++y) acc[2 + y] += M0[y] * H0[y] + MN[y] * HN[y];
-#pragma unroll
-                for (int o = 0; o < P; ++o) {
-                    if (o >= V) break;
-                    double z0 = 0.0, zN = 0.0;
-#pragma unroll
-                    for (int y = 0; y < P; ++y)
-                        if (cls(y) == o) z0 = fma(s_wR[y], M0[y], z0), zN = fma(s_wR[y], MN[y], zN);
-                    sm[o * lds + S(0)] = make_double2(0.5 * (z0 + zN), 0.5 * (z0 - zN));  // inverse pre, k = 0
-                }
-            }
-            continue;
-        }
-        const bool self = slA == slB;  // k = N'/2 (row 0, k2 = N2/2)
-        const double2 wA = twiddle(a.tw, uint64_t(kA), a.m);  // exp(-2 pi i k / n)
-        const double2 wB = make_double2(-wA.x, wA.y);          // exp(-2 pi i (N' - k)/n) = -conj(wA)
-        double2 HA[P], HB[P];
-#pragma unroll
-        for (int x = 0; x < P; ++x) {
-            const int o = cls(x);
-            const double2 za = bufA[o * lds + S(pA)], zb = bufB[o * lds + S(pB)];
-            HA[x] = r2c_post(za, zb, wA);
-            HB[x] = r2c_post(zb, za, wB);
-        }
-        double2 ZA[P], ZB[P];
-#pragma unroll
-        for (int side = 0; side < 2; ++side) {
-            if (side == 1 && self) break;
-            const double2* H = side == 0 ? HA : HB;
-            const long long sl = side == 0 ? slA : slB;
-            double2 A[P], r[T], ch[T], Ai[P];
-#pragma unroll
-            for (int x = 0; x < P; ++x) A[x] = make_double2(fma(s_coef[x], H[x].x, s_xi[x]), s_coef[x] * H[x].y);
-#pragma unroll
-            for (int t = 0; t < T; ++t) r[t] = side == 0 ? rA[t] : rB[t];
-            double qd;
-            const int st = ldl_core<T, true>(A, r, grad, lpm, lpe, qd, ch, Ai, imx, rex);
-            if (st == 1 && sl < first_bad) first_bad = sl;
-            acc[1] += 2.0 * qd;  // slot k >= 1 stands for frequencies k and n - k
-            if (grad) {
-                double2 Mq[P];
-                int x = 0;
-#pragma unroll
-                for (int i = 0; i < T; ++i)
-#pragma unroll
-                    for (int j = i; j < T; ++j, ++x) Mq[x] = csub(Ai[x], cmulc(ch[i], ch[j]));
-#pragma unroll
-                for (int y = 0; y < P; ++y) acc[2 + y] += 2.0 * (Mq[y].x * H[y].x + Mq[y].y * H[y].y);
-#pragma unroll
-                for (int o = 0; o < P; ++o) {
-                    double2 z = make_double2(0.0, 0.0);
-#pragma unroll
-                    for (int y = 0; y < P; ++y)
-                        if (cls(y) == o) z = make_double2(fma(s_wR[y], Mq[y].x, z.x), fma(s_wR[y], Mq[y].y, z.y));
-                    if (side == 0) ZA[o] = z;
-                    else ZB[o] = z;
-                }
-            }
-        }
-        if (grad) {
-            // inverse real-FFT pre-processing of the class adjoints, written back in place
-#pragma unroll
-            for (int o = 0; o < P; ++o) {
-                if (o >= V) break;
-                if (self) {
-                    bufA[o * lds + S(pA)] = c2r_pre(ZA[o], ZA[o], wA);
-                } else {
-                    bufA[o * lds + S(pA)] = c2r_pre(ZA[o], ZB[o], wA);
-                    bufB[o * lds + S(pB)] = c2r_pre(ZB[o], ZA[o], wB);
-                }
-            }
-        }
-    }
-    cl.sync();  // every DSMEM access of the cluster is done
-    acc[0] += 2.0 * log_of(lpm, lpe);
-
-    __shared__ double redv[(NT / 32) * (2 + P)];
-    block_sum_vec<NT, 2 + P>(acc, redv);
-    if (threadIdx.x == 0) {
-        double* pm = a.part_mid + (size_t(c) * gridDim.x + blockIdx.x) * (2 + P);
-#pragma unroll
-        for (int x = 0; x < 2 + P; ++x) pm[x] = acc[x];
-    }
-    if (first_bad != 0x7f7f7f7fll) atomicMin(a.bad + c, int(first_bad));
-#pragma unroll
-    for (int t = 0; t < T; ++t) {
-        double vi = imx[t], vr = rex[t];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            vi = fmax(vi, __shfl_xor_sync(0xffffffffu, vi, o));
-            vr = fmax(vr, __shfl_xor_sync(0xffffffffu, vr, o));
-        }
-        if ((threadIdx.x & 31) == 0) {
-            atomicMax(a.imre + ((size_t)c * MAXT + t) * 2 + 0, (unsigned long long)__double_as_longlong(vi));
-            atomicMax(a.imre + ((size_t)c * MAXT + t) * 2 + 1, (unsigned long long)__double_as_longlong(vr));
-        }
-    }
-    if (!grad) return;
-    // inverse row FFT (block_sum_vec's barriers ordered the solve's writes): DIT tail, middle
-    // stages, then stage 0 fused with the conjugate four-step twiddle and the store
-    ip_tail_stage<NT>(sm, ig, V, lds, +1);
-    ip_mid_stages<NT, true>(sm, ig, 1, ig.a16, V, lds, a.tw);
-    if (has_g) {
-        t0.load(a.tw, gj1, l2);
-        obase = twiddle(a.tw, uint64_t(gj1) * uint64_t(row), lt);
-        const double2* xs = sm + gvec * lds;
-        double2 x[16];
-#pragma unroll
-        for (int r = 0; r < 16; ++r) x[r] = xs[S(gj1 + (r << M_log))];
-        dit16_regs(x, t0);
-#pragma unroll
-        for (int r = 0; r < 16; ++r) {
-            const int j2 = gj1 + (brev_c<16>(r) << M_log);
-            a.Y[xaddr(a, c, j2 >> a.lwc, gvec, li, j2 & (a.WC - 1))] =
-                cmulc(x[r], cmul(obase, s_ostep[brev_c<16>(r)]));
-        }
-    }
-}
-
-// ------------------------------------------------------------------ L3: inverse column FFT -> gradient dot
-// In-place DIT: the tail stage is fused with the exchange-block loads, stage 0 with the
-// gradient dot (W(2j) = 2 Re z, W(2j+1) = 2 Im z consumed in registers).
-template <int NT, int DC, int ALPHA>
-__global__ void __launch_bounds__(NT) k_lat_col_inv(LatArgs a, int l1, int l2, int lc) {
-    extern __shared__ __align__(16) unsigned char smraw[];
-    double2* sm = reinterpret_cast<double2*>(smraw);
-    constexpr auto S = sidx<true>;
-    __shared__ int s_last;
-    const int v = blockIdx.y, c = v / a.V, o = v - c * a.V;
-    const int N1 = 1 << l1, ld = padded_len(N1);
-    const uint32_t c0 = uint32_t(a.rank * a.ncb + blockIdx.x) << lc;  // global first column
-    const int jl0 = int(c0) - a.rank * a.WC;
-    const IpGeo ig = IpGeo::of(l1);
-    const int M_log = l1 - 4;
-    const int tvec = threadIdx.x >> M_log, p0 = (threadIdx.x & ((1 << M_log) - 1)) << 4;
-    const int kb = ip_freq(p0, ig);
-    pdl_wait();
-    double2 x[16];
-    {
-        const double2* xb = a.Cbuf;
-#pragma unroll
-        for (int r = 0; r < 16; ++r) {
-            const int k1 = kb | ip_freq_lo(r, ig);
-            int i;
-            const int h = row_owner(k1, N1, a.lqp, i);
-            x[r] = __ldcs(&xb[xaddr(a, c, h, o, i, jl0 + tvec)]);
-        }
-    }
-    tail_regs(x, ig.rl, +1);
-    {
-        double2* xs = sm + tvec * ld;
-#pragma unroll
-        for (int r = 0; r < 16; ++r) xs[S(p0 + tail_out_pos(r, ig.rl))] = x[r];
-    }
-    __syncthreads();
-    ip_mid_stages<NT, true>(sm, ig, 1, ig.a16, 1 << lc, ld, a.tw);
-    const int gvec = threadIdx.x >> M_log, gj1 = threadIdx.x & ((1 << M_log) - 1);
-    {
-        Tw16 t0;
-        t0.load(a.tw, gj1, l1);
-        const double2* xs = sm + gvec * ld;
-#pragma unroll
-        for (int r = 0; r < 16; ++r) x[r] = xs[S(gj1 + (r << M_log))];
-        dit16_regs(x, t0);
-    }
-    double acc[DC];
-#pragma unroll
-    for (int j = 0; j < DC; ++j) acc[j] = 0.0;
-    {
-        LatGen<DC, ALPHA> G;
-        G.init(a, c, o);
-#pragma unroll
-        for (int r = 0; r < 16; ++r) {
-            const uint32_t J = (uint32_t(gj1 + (brev_c<16>(r) << M_log)) << l2) + c0 + uint32_t(gvec);
-            G.dq_acc(2u * J, 2.0 * x[r].x, acc);  // W(2j) = 2 Re z, W(2j+1) = 2 Im z
-            G.dq_acc(2u * J + 1u, 2.0 * x[r].y, acc);
-        }
-    }
-    const int nblk = gridDim.x;
-    __shared__ double redv[(NT / 32) * DC];
-    block_sum_vec<NT, DC>(acc, redv);
-    if (threadIdx.x == 0) {
-        double* out = a.part_dot + (size_t(v) * nblk + blockIdx.x) * (MAXD + 1);
-#pragma unroll
-        for (int j = 0; j < DC; ++j)
-            if (j < a.d) out[j] = acc[j];
-    }
-    // last-CTA reduction (one acq_rel ticket per candidate over its V * nblk CTAs), fixed order
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned ticket = atom_add_acq_rel_gpu(a.counter + c, 1u);
-        s_last = ticket == unsigned(a.V * nblk) - 1;
-        if (s_last) a.counter[c] = 0;  // self-reset for the next replay
-    }
-    __syncthreads();
-    if (!s_last) return;
-    ClassSums t{};
-    t.T = a.T;
-    t.P = a.P;
-    t.V = a.V;
-    t.d = a.d;
-    t.nrows = a.R;  // L2 CTAs per candidate on this rank
-    t.nblk = nblk;
-    t.dstride = MAXD + 1;
-    t.mid = a.part_mid + size_t(c) * t.nrows * (2 + a.P);
-    t.dot = a.part_dot + size_t(c) * a.V * nblk * (MAXD + 1);
-    t.pair_a = a.pair_a;
-    t.pair_b = a.pair_b;
-    t.Rpair = a.Rpair + size_t(c) * a.P;
-    t.gamma = __ldg(a.gamma + c);
-    t.out = a.out + size_t(c) * NOUT;
-    class_sums_out<NT>(t);
-}
-
 // yhat in the fused path's row-position order: yperm[t][row][p] = yhat[t][row][ip_freq(p)]
 // (once per dataset, fmtgp_model_set_y)
-__global__ void k_lat_perm(const double2* __restrict__ yh, double2* __restrict__ yp, long long total, int l2) {
-    const IpGeo ig = IpGeo::of(l2);
+template <int L2>
+__global__ void k_lat_perm(const double2* __restrict__ yh, double2* __restrict__ yp, long long total) {
+    constexpr int l2 = L2;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x) {
         const long long rowbase = e & ~((1ll << l2) - 1);
-        yp[e] = yh[rowbase + ip_freq(int(e & ((1ll << l2) - 1)), ig)];
+        yp[e] = yh[rowbase + Ip<L2>::freq(int(e & ((1ll << l2) - 1)))];
     }
 }
 
 void lat_perm_yhat(const LatGeo& g, int T, long long half, const void* yhat, void* yperm, cudaStream_t s) {
     const long long total = (long long)T * half;
-    k_lat_perm<<<148 * 8, 256, 0, s>>>(static_cast<const double2*>(yhat), static_cast<double2*>(yperm), total, g.l2);
-}
-
-// ------------------------------------------------------------------ launcher
-template <class K>
-static void set_smem_lat(K kern, size_t bytes) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
-}
-
-template <int DC, int ALPHA>
-static void lat_cols(const LatGeo& g, const LatArgs& a, size_t sm_col, bool inverse, cudaStream_t s) {
-    const dim3 grid(a.ncb, a.V * a.nc);
-    if (!inverse) {
-        auto k = k_lat_col_fwd<LAT_NT, DC, ALPHA>;
-        set_smem_lat(k, sm_col);
-        ProfScope ps("lat_col_fwd", s);
-        k<<<grid, LAT_NT, sm_col, s>>>(a, g.l1, g.l2, g.lc);
-    } else {
-        auto k = k_lat_col_inv<LAT_NT, DC, ALPHA>;
-        set_smem_lat(k, sm_col);
-        ProfScope ps("lat_col_inv", s);
-        CK_LAUNCH(launch_pdl(k, grid, dim3(LAT_NT), sm_col, s, true, a, g.l1, g.l2, g.lc));
+    const auto* src = static_cast<const double2*>(yhat);
+    auto* dst = static_cast<double2*>(yperm);
+    switch (g.l2) {
+        case 8: k_lat_perm<8><<<148 * 8, 256, 0, s>>>(src, dst, total); break;
+        case 9: k_lat_perm<9><<<148 * 8, 256, 0, s>>>(src, dst, total); break;
+        case 10: k_lat_perm<10><<<148 * 8, 256, 0, s>>>(src, dst, total); break;
+        case 11: k_lat_perm<11><<<148 * 8, 256, 0, s>>>(src, dst, total); break;
+        case 12: k_lat_perm<12><<<148 * 8, 256, 0, s>>>(src, dst, total); break;
+        default: k_lat_perm<13><<<148 * 8, 256, 0, s>>>(src, dst, total); break;
     }
 }
 
-template <int ALPHA>
-static void lat_cols_d(const LatGeo& g, const LatArgs& a, size_t sm_col, bool inverse, cudaStream_t s) {
-    if (a.d <= 2) lat_cols<2, ALPHA>(g, a, sm_col, inverse, s);
-    else if (a.d <= 4) lat_cols<4, ALPHA>(g, a, sm_col, inverse, s);
-    else if (a.d <= 8) lat_cols<8, ALPHA>(g, a, sm_col, inverse, s);
-    else lat_cols<16, ALPHA>(g, a, sm_col, inverse, s);
+// ------------------------------------------------------------------ dispatch (lat_inst_<L>.cu)
+#define FMTGP_LAT_EXTERN(L)                                                                        \
+    extern template void lat_cols_launch<L>(const LatGeo&, const LatArgs&, bool, cudaStream_t);  \
+    extern template void lat_mid_launch<L>(const LatGeo&, const LatArgs&, cudaStream_t);
+FMTGP_LAT_EXTERN(8)
+FMTGP_LAT_EXTERN(9)
+FMTGP_LAT_EXTERN(10)
+FMTGP_LAT_EXTERN(11)
+FMTGP_LAT_EXTERN(12)
+FMTGP_LAT_EXTERN(13)
+
+static void cols(const LatGeo& g, const LatArgs& a, bool inverse, cudaStream_t s) {
+    switch (g.l1) {
+        case 8: lat_cols_launch<8>(g, a, inverse, s); break;
+        case 9: lat_cols_launch<9>(g, a, inverse, s); break;
+        case 10: lat_cols_launch<10>(g, a, inverse, s); break;
+        case 11: lat_cols_launch<11>(g, a, inverse, s); break;
+        case 12: lat_cols_launch<12>(g, a, inverse, s); break;
+        default: lat_cols_launch<13>(g, a, inverse, s); break;
+    }
 }
 
-template <int T>
-static void lat_mid_launch(const LatGeo& g, const LatArgs& a, cudaStream_t s) {
-    const size_t sm = size_t(a.V) * padded_len(1 << g.l2) * sizeof(double2);
-    auto k = a.distinct ? k_lat_mid<LAT_NT, T, true> : k_lat_mid<LAT_NT, T, false>;
-    set_smem_lat(k, sm);
-    ProfScope ps("lat_mid", s);
-    CK_LAUNCH(launch_pdl(k, dim3(unsigned(a.R), a.nc), dim3(LAT_NT), sm, s, true, a, g.l1, g.l2));
+static void mid(const LatGeo& g, const LatArgs& a, cudaStream_t s) {
+    switch (g.l2) {
+        case 8: lat_mid_launch<8>(g, a, s); break;
+        case 9: lat_mid_launch<9>(g, a, s); break;
+        case 10: lat_mid_launch<10>(g, a, s); break;
+        case 11: lat_mid_launch<11>(g, a, s); break;
+        case 12: lat_mid_launch<12>(g, a, s); break;
+        default: lat_mid_launch<13>(g, a, s); break;
+    }
 }
 
 void lat_phase(const LatGeo& g, const LatArgs& a, int phase, cudaStream_t s) {
-    const size_t sm_col = size_t(1 << g.lc) * padded_len(1 << g.l1) * sizeof(double2);
-    if (phase == 1) {
-        if (a.si_alpha == 1) lat_cols_d<1>(g, a, sm_col, false, s);
-        else lat_cols_d<2>(g, a, sm_col, false, s);
-    } else if (phase == 2) {
-        switch (a.T) {
-            case 1: lat_mid_launch<1>(g, a, s); break;
-            case 2: lat_mid_launch<2>(g, a, s); break;
-            case 3: lat_mid_launch<3>(g, a, s); break;
-            default: lat_mid_launch<4>(g, a, s); break;
-        }
-    } else if (a.want_grad) {
-        if (a.si_alpha == 1) lat_cols_d<1>(g, a, sm_col, true, s);
-        else lat_cols_d<2>(g, a, sm_col, true, s);
-    }
+    if (phase == 1) cols(g, a, false, s);
+    else if (phase == 2) mid(g, a, s);
+    else if (a.want_grad) cols(g, a, true, s);
 }
 
 void lat_fit(const LatGeo& g, const LatArgs& a, cudaStream_t s) {
