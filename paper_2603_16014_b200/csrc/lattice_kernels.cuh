@@ -4,6 +4,8 @@
 #pragma once
 
 #include <cooperative_groups.h>
+#include <algorithm>
+#include <cstdlib>
 
 #include "ipfft.cuh"
 #include "lattice.cuh"
@@ -122,6 +124,22 @@ __device__ __forceinline__ size_t xaddr(const LatArgs& a, int c, int h, int o, i
 // stage 0 is fused with the generator (each thread generates its radix-16 group straight into
 // registers), the twiddle-free tail stage with the store of the exchange blocks (row k1 =
 // ip_freq of the position).  The four-step twiddle w_{n'}^(k1 j2) is applied by L2 on its inputs.
+__device__ __forceinline__ void cluster_arrive_rel() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait_acq() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ unsigned cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned cluster_count() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(r));
+    return r;
+}
+
 template <int NT, int DC, int ALPHA, int L1>
 __global__ void __launch_bounds__(NT) k_lat_col_fwd(LatArgs a, int l2, int lc) {
     using IP = Ip<L1>;
@@ -130,9 +148,19 @@ __global__ void __launch_bounds__(NT) k_lat_col_fwd(LatArgs a, int l2, int lc) {
     constexpr auto S = sidx<true>;
     constexpr int N1 = 1 << L1, ld = padded_len(N1);
     constexpr int M_log = L1 - 4;  // stage-0 stride; also log2 of the 16-position chunks per column
+    cg::cluster_group cl = cg::this_cluster();
+    // K CTAs of a cluster take K adjacent column blocks; after the column FFT each CTA stores a
+    // quarter (1/K) of the rows of ALL K*C columns, reading the other CTAs' columns over DSMEM,
+    // so every row segment written is K*C*16 contiguous bytes instead of 16
+    const int K = int(cluster_count()), crank = int(cluster_rank());
+    int lk = 0;
+    while ((1 << lk) < K) ++lk;
+    const int C = 1 << lc, kcl = lk + lc;
     // thread -> column vec, stage-0 group j1; its tail chunk is positions p0 .. p0+15 of the same column
     const int vec = threadIdx.x >> M_log, j1 = threadIdx.x & ((1 << M_log) - 1), p0 = j1 << 4;
-    const int kb = IP::freq(p0);
+    const double2* src[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) src[r] = r < K ? cl.map_shared_rank(sm, r) : sm;
     Tw16 t0;
     t0.load(a.tw, j1, L1);  // the same for every tile
     // zero the per-fit flags once per fit (L2 / L3 run after this kernel)
@@ -141,13 +169,16 @@ __global__ void __launch_bounds__(NT) k_lat_col_fwd(LatArgs a, int l2, int lc) {
         for (int t = threadIdx.x; t < a.nc * MAXT * 2; t += NT) a.imre[t] = 0ull;
     }
     pdl_trigger();
-    // persistent over (column block, class, candidate) tiles: a tile's scattered exchange-block
+    // persistent over cluster tiles (K column blocks x class x candidate): a tile's exchange-block
     // stores drain while the next tile's generator (registers only) runs
-    const int ntiles = a.ncb * a.V * a.nc;
+    const int ncbk = a.ncb >> lk;
+    const int ntiles = ncbk * a.V * a.nc, nclus = int(gridDim.x) >> lk, cid = int(blockIdx.x) >> lk;
+    cluster_arrive_relaxed();
 #pragma unroll 1
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int bx = tile % a.ncb, v = tile / a.ncb, c = v / a.V, o = v - c * a.V;
-        const uint32_t c0 = uint32_t(a.rank * a.ncb + bx) << lc;  // global first column
+    for (int tile = cid; tile < ntiles; tile += nclus) {
+        const int bk = tile % ncbk, v = tile / ncbk, c = v / a.V, o = v - c * a.V;
+        const int bx = (bk << lk) + crank;
+        const uint32_t c0 = uint32_t(a.rank * a.ncb + bx) << lc;  // global first column of this CTA
         double2 x[16];
         {
             LatGen<DC, ALPHA> G;
@@ -159,30 +190,41 @@ __global__ void __launch_bounds__(NT) k_lat_col_fwd(LatArgs a, int l2, int lc) {
             }
         }
         dif16_regs(x, t0);
-        __syncthreads();  // the previous tile's tail has read smem
+        cluster_wait_acq();  // every CTA of the cluster has read the previous tile out of smem
         {
             double2* xs = sm + vec * ld + S(j1);
 #pragma unroll
             for (int r = 0; r < 16; ++r) xs[ip_off<M_log>(brev_c<16>(r))] = x[r];
         }
         __syncthreads();
-        ip_mid_stages<NT, L1, false>(sm, 1 << lc, ld, a.tw);
-        // tail stage + store
+        ip_mid_stages<NT, L1, false>(sm, C, ld, a.tw);
+        // tail stage, results back in place
         {
-            const double2* xs = sm + vec * ld + S(p0);
+            double2* xs = sm + vec * ld + S(p0);
 #pragma unroll
             for (int r = 0; r < 16; ++r) x[r] = xs[r];
-        }
-        tail_regs<L1>(x, -1);
-        const int jl = int(c0) + vec - a.rank * a.WC;
+            tail_regs<L1>(x, -1);
 #pragma unroll
-        for (int r = 0; r < 16; ++r) {
-            const int k1 = kb | IP::freq_lo(tail_out_pos<L1>(r));
+            for (int r = 0; r < 16; ++r) xs[tail_out_pos<L1>(r)] = x[r];
+        }
+        cl.sync();
+        // transposed store: positions [crank N1/K, (crank+1) N1/K) x the cluster's K*C columns
+        const int jlb = ((a.rank * a.ncb + (bk << lk)) << lc) - a.rank * a.WC;
+#pragma unroll 4
+        for (int u = 0; u < 16; ++u) {
+            const int e = int(threadIdx.x) + u * NT;
+            const int cc = e & ((1 << kcl) - 1);
+            const int p = (crank << (L1 - lk)) + (e >> kcl);
+            const int k1 = IP::freq(p);
             int i;
             const int h = row_owner(k1, N1, a.lqp, i);
-            a.Y[xaddr(a, c, h, o, i, jl)] = x[r];
+            a.Y[xaddr(a, c, h, o, i, jlb + cc)] = src[cc >> lc][(cc & (C - 1)) * ld + S(p)];
         }
+        // relaxed: the remote reads above have completed (their values were stored), and a
+        // release here would wait for every outstanding exchange-block store to drain
+        cluster_arrive_relaxed();
     }
+    cluster_wait_acq();  // no CTA leaves while another still reads its smem
 }
 
 // ------------------------------------------------------------------ L2: row FFT + solve + inverse row FFT
@@ -602,20 +644,78 @@ inline int lat_sm_count() {
     return n;
 }
 
+// column-kernel cluster size (lattice_kernels.cuh k_lat_col_*): K adjacent column blocks per
+// cluster, row segments of K * C * 16 bytes; FMTGP_LAT_CLUSTER overrides (1, 2 or 4)
+inline int lat_cluster_k(int ncb) {
+    static int k = [] {
+        const char* e = std::getenv("FMTGP_LAT_CLUSTER");
+        const int v = e ? std::atoi(e) : 4;
+        return v >= 4 ? 4 : v >= 2 ? 2 : 1;
+    }();
+    int K = k;
+    while (K > 1 && (ncb % K) != 0) K >>= 1;
+    return K;
+}
+
+template <class Kern, class... Args>
+static cudaError_t launch_cluster(Kern kern, int grid, int K, size_t smem, cudaStream_t s, bool pdl, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(LAT_NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = unsigned(K);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+// persistent grid: as many whole clusters as fit at once (one CTA per SM: the tile fills smem)
+template <class Kern>
+static int lat_cluster_grid(Kern kern, int K, size_t smem, int tiles) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(K * 64));
+    cfg.blockDim = dim3(LAT_NT);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = unsigned(K);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclus = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclus, kern, &cfg) != cudaSuccess || nclus <= 0) {
+        cudaGetLastError();
+        nclus = lat_sm_count() / K;
+    }
+    return K * std::max(1, std::min(nclus, tiles));
+}
+
 template <int DC, int ALPHA, int L1>
 static void lat_cols(const LatGeo& g, const LatArgs& a, size_t sm_col, bool inverse, cudaStream_t s) {
-    // persistent: one CTA per SM (the column tile fills its shared memory)
-    const dim3 grid(unsigned(std::min(a.ncb * a.V * a.nc, lat_sm_count())));
+    const int K = lat_cluster_k(a.ncb);
+    const int tiles = (a.ncb / K) * a.V * a.nc;
     if (!inverse) {
         auto k = k_lat_col_fwd<LAT_NT, DC, ALPHA, L1>;
         set_smem_lat(k, sm_col);
+        if (K > 1) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
         ProfScope ps("lat_col_fwd", s);
-        k<<<grid, LAT_NT, sm_col, s>>>(a, g.l2, g.lc);
+        CK_LAUNCH(launch_cluster(k, lat_cluster_grid(k, K, sm_col, tiles), K, sm_col, s, false, a, g.l2, g.lc));
     } else {
+        // inverse: no cluster (the next tile's scattered loads are asynchronous copies that run
+        // under the gradient dot; a DSMEM-transposed variant measured slower)
         auto k = k_lat_col_inv<LAT_NT, DC, ALPHA, L1>;
         set_smem_lat(k, sm_col);
         ProfScope ps("lat_col_inv", s);
-        CK_LAUNCH(launch_pdl(k, grid, dim3(LAT_NT), sm_col, s, true, a, g.l2, g.lc));
+        const int grid = std::min(a.ncb * a.V * a.nc, lat_sm_count());
+        CK_LAUNCH(launch_cluster(k, grid, 1, sm_col, s, true, a, g.l2, g.lc));
     }
 }
 
