@@ -115,6 +115,10 @@ __device__ __forceinline__ int row_owner(int k1, int N1, int lqp, int& i) {
     return h;
 }
 // element (row owner h, class o, local row i, local column jl) of candidate c's exchange blocks
+// offset inside one candidate's blocks (< V n' <= 2^31: 32-bit arithmetic)
+__device__ __forceinline__ unsigned xoff(const LatArgs& a, int h, int o, int i, int jl) {
+    return ((unsigned(h * a.V + o) * unsigned(a.R) + unsigned(i)) << a.lwc) + unsigned(jl);
+}
 __device__ __forceinline__ size_t xaddr(const LatArgs& a, int c, int h, int o, int i, int jl) {
     return size_t(c) * a.V * a.half + (((size_t(h) * a.V + o) * a.R + i) << a.lwc) + jl;
 }
@@ -210,6 +214,7 @@ __global__ void __launch_bounds__(NT) k_lat_col_fwd(LatArgs a, int l2, int lc) {
         cl.sync();
         // transposed store: positions [crank N1/K, (crank+1) N1/K) x the cluster's K*C columns
         const int jlb = ((a.rank * a.ncb + (bk << lk)) << lc) - a.rank * a.WC;
+        double2* Yc = a.Y + size_t(c) * a.V * a.half;
 #pragma unroll 4
         for (int u = 0; u < 16; ++u) {
             const int e = int(threadIdx.x) + u * NT;
@@ -218,7 +223,7 @@ __global__ void __launch_bounds__(NT) k_lat_col_fwd(LatArgs a, int l2, int lc) {
             const int k1 = IP::freq(p);
             int i;
             const int h = row_owner(k1, N1, a.lqp, i);
-            a.Y[xaddr(a, c, h, o, i, jlb + cc)] = src[cc >> lc][(cc & (C - 1)) * ld + S(p)];
+            Yc[xoff(a, h, o, i, jlb + cc)] = src[cc >> lc][(cc & (C - 1)) * ld + S(p)];
         }
         // relaxed: the remote reads above have completed (their values were stored), and a
         // release here would wait for every outstanding exchange-block store to drain
@@ -228,6 +233,39 @@ __global__ void __launch_bounds__(NT) k_lat_col_fwd(LatArgs a, int l2, int lc) {
 }
 
 // ------------------------------------------------------------------ L2: row FFT + solve + inverse row FFT
+// Closed-form 2 x 2 Hermitian solve: ldl_core<2, true>'s outputs (pivots a and det / a, their
+// product det into pm 2^pe, quad = r^H A^-1 r, chat = A^-1 r, A^-1, the non-real / pivot maxima
+// of Algorithm 1's two stages, fast_gram.cpp:167-178) with one reciprocal instead of two and no
+// triangular solves.  A = [A00, A01, A11] (pair order), status 1 on a non-positive pivot.
+__device__ __forceinline__ int herm2_solve(const double2* A, const double2* r, double& pm, int& pe, double& quad,
+                                           double2* chat, double2* Ainv, double* imx, double* rex) {
+    int status = 0;
+    double a = A[0].x;
+    const double d = A[2].x;
+    const double2 b = A[1];
+    imx[0] = fmax(imx[0], fabs(A[0].y));
+    imx[1] = fmax(imx[1], fabs(A[2].y));
+    if (!(a > 0.0)) status = 1, a = 1.0;
+    double det = fma(a, d, -(b.x * b.x + b.y * b.y));  // a * (second pivot)
+    if (!(det > 0.0)) status = 1, det = a;              // second pivot -> 1, as ldl_core
+    const double ip = 1.0 / (a * det);
+    const double idet = a * ip;                          // 1 / det
+    rex[0] = fmax(rex[0], a);
+    rex[1] = fmax(rex[1], det * (det * ip));             // det / a
+    {
+        int e;
+        pm = frexp(pm * det, &e);
+        pe += e;
+    }
+    Ainv[0] = make_double2(d * idet, 0.0);
+    Ainv[1] = make_double2(-b.x * idet, -b.y * idet);
+    Ainv[2] = make_double2(a * idet, 0.0);
+    // chat = A^-1 r: A^-1 = [[d, -b], [-conj b, a]] / det
+    chat[0] = cscale(csub(cscale(r[0], d), cmul(b, r[1])), idet);
+    chat[1] = cscale(csub(cscale(r[1], a), cmulc(r[0], b)), idet);
+    quad = r[0].x * chat[0].x + r[0].y * chat[0].y + r[1].x * chat[1].x + r[1].y * chat[1].y;
+    return status;
+}
 __device__ __forceinline__ int lat_row_of(int q, int rank, int N1) {
     if (q == 0) return rank == 0 ? 0 : N1 / 2;
     return rank == 0 ? q : N1 - q;
@@ -316,10 +354,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
     }
     pdl_wait();
     pdl_trigger();
+    double2* const Yc = a.Y + size_t(c) * a.V * a.half;
     for (int e = threadIdx.x; e < (V << l2); e += NT) {
         const int oo = e >> l2, k2 = e & (N2 - 1);
         const int sr = k2 >> a.lwc;  // column owner
-        cp_async16(&sm[oo * lds + S(k2)], &a.Y[xaddr(a, c, sr, oo, li, k2 & (a.WC - 1))]);
+        cp_async16(&sm[oo * lds + S(k2)], &Yc[xoff(a, sr, oo, li, k2 & (a.WC - 1))]);
     }
     cp_async_wait_all();
     __syncthreads();
@@ -438,7 +477,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
 #pragma unroll
             for (int t = 0; t < T; ++t) r[t] = side == 0 ? rA[t] : rB[t];
             double qd;
-            const int st = ldl_core<T, true>(A, r, grad, lpm, lpe, qd, ch, Ai, imx, rex);
+            int st;
+            if constexpr (T == 2) st = herm2_solve(A, r, lpm, lpe, qd, ch, Ai, imx, rex);
+            else st = ldl_core<T, true>(A, r, grad, lpm, lpe, qd, ch, Ai, imx, rex);
             if (st == 1 && sl < first_bad) first_bad = sl;
             acc[1] += 2.0 * qd;  // slot k >= 1 stands for frequencies k and n - k
             if (grad) {
@@ -515,7 +556,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
             const int j2 = gj1 + (brev_c<16>(r) << M_log);
-            a.Y[xaddr(a, c, j2 >> a.lwc, gvec, li, j2 & (a.WC - 1))] =
+            Yc[xoff(a, j2 >> a.lwc, gvec, li, j2 & (a.WC - 1))] =
                 cmulc(x[r], cmul(obase, s_ostep[brev_c<16>(r)]));
         }
     }
@@ -545,12 +586,13 @@ __global__ void __launch_bounds__(NT) k_lat_col_inv(LatArgs a, int l2, int lc) {
     auto issue = [&](int tile) {
         const int bx = tile % a.ncb, v = tile / a.ncb, c = v / a.V, o = v - c * a.V;
         const int jl = ((a.rank * a.ncb + bx) << lc) + vec - a.rank * a.WC;
+        const double2* Cc = a.Cbuf + size_t(c) * a.V * a.half;
         double2* xs = sm + vec * ld + S(p0);
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
             int i;
             const int h = row_owner(kb | IP::freq_lo(r), N1, a.lqp, i);
-            cp_async16(xs + r, &a.Cbuf[xaddr(a, c, h, o, i, jl)]);
+            cp_async16(xs + r, &Cc[xoff(a, h, o, i, jl)]);
         }
     };
     pdl_wait();
