@@ -127,6 +127,12 @@ FMTGP_API int fmtgp_solve(fmtgp_model_t model, const double* b, double* x);
 FMTGP_API int fmtgp_gram_matvec(fmtgp_model_t model, const double* b, double* out);
 /* extract_pi_h (fast_gram.cpp:311-335): Pi = E^T K^-1 E, [L * L] row-major */
 FMTGP_API int fmtgp_extract_pi(fmtgp_model_t model, double* Pi);
+/* H of extract_pi_h (fast_gram.cpp:311-335, fast_gram.hpp:64-68): H_lk = sqrt(n_l) (Lam^-1)_{N_{l-1}, k n_L},
+ * [L * r] row-major complex (re / im), r = N / n_{L-1} (equal n: r = L) */
+FMTGP_API int fmtgp_extract_h(fmtgp_model_t model, double* H_re, double* H_im);
+/* frequencies [k0, k0 + count) of pair (l <= lp) in natural order (fmtgp_spectrum_read for a range) */
+FMTGP_API int fmtgp_spectrum_read_range(fmtgp_model_t model, int l, int lp, int64_t k0, int64_t count, double* re,
+                                        double* im);
 /* trace_inverse (fast_gram.cpp:301-309) */
 FMTGP_API int fmtgp_trace_inverse(fmtgp_model_t model, double* tr);
 

@@ -18,6 +18,9 @@ from ._cstructs import CDesign, CHyper, dptr, make_cdesign, make_chyper
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_ref", "libfmtgp_ref.so")
+# The same extern "C" shim and the reference's own gp_core / cubature, but with fast_gram.cpp
+# replaced by the B200 drop-in (paper_2603_16014_b200/seam/fast_gram_b200.cpp): `make -C oracle seam`.
+SEAM_PATH = os.path.join(HERE, "_ref", "libfmtgp_seam.so")
 
 
 class RefError(RuntimeError):
@@ -29,10 +32,15 @@ class RefSchurBreakdown(RefError):
 
 
 _lib = None
+_libs = {}
 
 
 def available() -> bool:
     return os.path.exists(LIB_PATH)
+
+
+def seam_available() -> bool:
+    return os.path.exists(SEAM_PATH)
 
 
 def lib():
@@ -40,7 +48,20 @@ def lib():
     if _lib is None:
         if not available():
             raise RefError(f"reference oracle not built: {LIB_PATH} (run make -C oracle ref)")
-        L = C.CDLL(LIB_PATH)
+        _lib = _load(LIB_PATH)
+    return _lib
+
+
+def seam_lib():
+    """The reference's gp_core / cubature over the B200 fast_gram drop-in."""
+    if not seam_available():
+        raise RefError(f"seam library not built: {SEAM_PATH} (run make -C oracle seam)")
+    return _load(SEAM_PATH)
+
+
+def _load(path):
+    if path not in _libs:
+        L = C.CDLL(path)
         P, D = C.POINTER(CDesign), C.POINTER(CHyper)
         dp = C.POINTER(C.c_double)
         L.ref_last_error.restype = C.c_char_p
@@ -60,6 +81,7 @@ def lib():
         L.ref_design_points.argtypes = [P, dp]
         L.ref_build_spectrum.argtypes = [P, D, dp, dp]
         L.ref_invert_solve.argtypes = [P, D, dp, dp, dp, dp, dp, dp]
+        L.ref_pi_h.argtypes = [P, D, dp, dp, dp]
         L.ref_model_create.restype = C.c_void_p
         L.ref_model_create.argtypes = [P, D, dp]
         L.ref_model_free.argtypes = [C.c_void_p]
@@ -72,14 +94,14 @@ def lib():
         L.ref_model_single_cubature.argtypes = [C.c_void_p, dp, dp]
         L.ref_model_fit.argtypes = [C.c_void_p, C.c_int, dp, dp]
         L.ref_model_fit_timed.argtypes = [C.c_void_p, C.c_int, dp, dp, dp, C.POINTER(C.c_int)]
-        _lib = L
-    return _lib
+        _libs[path] = L
+    return _libs[path]
 
 
-def _check(rc: int):
+def _check(rc: int, L=None):
     if rc == 0:
         return
-    msg = lib().ref_last_error().decode()
+    msg = (L or lib()).ref_last_error().decode()
     if rc == 2:
         raise RefSchurBreakdown(msg)
     raise RefError(msg)
@@ -114,13 +136,14 @@ def design_points(dz: Design) -> np.ndarray:
     return out
 
 
-def build_spectrum(dz: Design, hp: Hyper):
+def build_spectrum(dz: Design, hp: Hyper, seam: bool = False):
     """List of complex vectors, pairs (l<=lp) row by row (fast_gram.cpp:35-40)."""
+    L = seam_lib() if seam else lib()
     cd, k1 = make_cdesign(dz)
     ch, k2 = make_chyper(hp)
     lens = [dz.n[l] for l in range(dz.L) for lp in range(l, dz.L)]
     re, im = np.empty(sum(lens)), np.empty(sum(lens))
-    _check(lib().ref_build_spectrum(C.byref(cd), C.byref(ch), dptr(re), dptr(im)))
+    _check(L.ref_build_spectrum(C.byref(cd), C.byref(ch), dptr(re), dptr(im)), L)
     out, o = [], 0
     for n in lens:
         out.append(re[o:o + n] + 1j * im[o:o + n])
@@ -128,43 +151,56 @@ def build_spectrum(dz: Design, hp: Hyper):
     return out
 
 
-def invert_solve(dz: Design, hp: Hyper, b: np.ndarray):
-    """(x = K^-1 b, K b, logdet, trace(K^-1), Pi) through the reference seam."""
+def pi_h(dz: Design, hp: Hyper, seam: bool = False):
+    """(Pi [L, L], H [L, r] complex) of extract_pi_h (fast_gram.cpp:311-335)."""
+    L = seam_lib() if seam else lib()
+    cd, k1 = make_cdesign(dz)
+    ch, k2 = make_chyper(hp)
+    r = dz.N // dz.n[dz.L - 1]
+    Pi, hr, hi = np.empty((dz.L, dz.L)), np.empty((dz.L, r)), np.empty((dz.L, r))
+    _check(L.ref_pi_h(C.byref(cd), C.byref(ch), dptr(Pi), dptr(hr), dptr(hi)), L)
+    return Pi, hr + 1j * hi
+
+
+def invert_solve(dz: Design, hp: Hyper, b: np.ndarray, seam: bool = False, trace: bool = True):
+    """(x = K^-1 b, K b, logdet, trace(K^-1) or None, Pi) through the reference seam."""
+    L = seam_lib() if seam else lib()
     cd, k1 = make_cdesign(dz)
     ch, k2 = make_chyper(hp)
     b = np.ascontiguousarray(b, dtype=np.float64)
     x, kb = np.empty(dz.N), np.empty(dz.N)
     logdet, tr = C.c_double(), C.c_double()
     Pi = np.empty((dz.L, dz.L))
-    _check(lib().ref_invert_solve(C.byref(cd), C.byref(ch), dptr(b), dptr(x), dptr(kb), C.byref(logdet),
-                                  C.byref(tr), dptr(Pi)))
-    return x, kb, logdet.value, tr.value, Pi
+    _check(L.ref_invert_solve(C.byref(cd), C.byref(ch), dptr(b), dptr(x), dptr(kb), C.byref(logdet),
+                              C.byref(tr) if trace else None, dptr(Pi)), L)
+    return x, kb, logdet.value, (tr.value if trace else None), Pi
 
 
 class Model:
     """GpModel (gp_core.hpp:32-56) on the reference library."""
 
-    def __init__(self, dz: Design, hp: Hyper, y: np.ndarray):
+    def __init__(self, dz: Design, hp: Hyper, y: np.ndarray, seam: bool = False):
         self.dz = dz
+        self.L = seam_lib() if seam else lib()
         self._cd, self._k1 = make_cdesign(dz)
         ch, k2 = make_chyper(hp)
         self.y = np.ascontiguousarray(y, dtype=np.float64)
-        self.h = lib().ref_model_create(C.byref(self._cd), C.byref(ch), dptr(self.y))
+        self.h = self.L.ref_model_create(C.byref(self._cd), C.byref(ch), dptr(self.y))
         if not self.h:
-            raise RefError(lib().ref_last_error().decode())
+            raise RefError(self.L.ref_last_error().decode())
 
     def __del__(self):
-        if getattr(self, "h", None) and _lib is not None:
-            _lib.ref_model_free(self.h)
+        if getattr(self, "h", None) and getattr(self, "L", None) is not None:
+            self.L.ref_model_free(self.h)
             self.h = None
 
     def set_hyper(self, hp: Hyper):
         ch, k2 = make_chyper(hp)
-        _check(lib().ref_model_set_hyper(self.h, C.byref(self._cd), C.byref(ch)))
+        _check(self.L.ref_model_set_hyper(self.h, C.byref(self._cd), C.byref(ch)), self.L)
 
     def loss(self, kind: int = 0) -> float:
         v = C.c_double()
-        _check(lib().ref_model_loss(self.h, kind, C.byref(v)))
+        _check(self.L.ref_model_loss(self.h, kind, C.byref(v)), self.L)
         return v.value
 
     def state(self):
@@ -172,32 +208,32 @@ class Model:
         logdet = C.c_double()
         tau, c = np.empty(L), np.empty(N)
         esc = C.c_int()
-        _check(lib().ref_model_state(self.h, C.byref(logdet), dptr(tau), dptr(c), C.byref(esc)))
+        _check(self.L.ref_model_state(self.h, C.byref(logdet), dptr(tau), dptr(c), C.byref(esc)), self.L)
         return dict(logdet=logdet.value, tau=tau, c=c, escalations=esc.value)
 
     def posterior_mean(self, task: int, X: np.ndarray) -> np.ndarray:
         X = np.ascontiguousarray(X, dtype=np.float64)
         out = np.empty(X.shape[0])
-        _check(lib().ref_model_posterior_mean(self.h, task, dptr(X), X.shape[0], dptr(out)))
+        _check(self.L.ref_model_posterior_mean(self.h, task, dptr(X), X.shape[0], dptr(out)), self.L)
         return out
 
     def posterior_cov(self, task: int, x: np.ndarray, task2: int, xp: np.ndarray) -> float:
         x = np.ascontiguousarray(x, dtype=np.float64)
         xp = np.ascontiguousarray(xp, dtype=np.float64)
         v = C.c_double()
-        _check(lib().ref_model_posterior_cov(self.h, task, dptr(x), task2, dptr(xp), C.byref(v)))
+        _check(self.L.ref_model_posterior_cov(self.h, task, dptr(x), task2, dptr(xp), C.byref(v)), self.L)
         return v.value
 
     def cubature(self):
         L = self.dz.L
         mu, S = np.empty(L), np.empty((L, L))
-        _check(lib().ref_model_cubature(self.h, dptr(mu), dptr(S)))
+        _check(self.L.ref_model_cubature(self.h, dptr(mu), dptr(S)), self.L)
         return mu, S
 
     def fit(self, steps: int):
         trace = np.empty(max(steps, 1))
         fl = C.c_double()
-        _check(lib().ref_model_fit(self.h, steps, C.byref(fl), dptr(trace)))
+        _check(self.L.ref_model_fit(self.h, steps, C.byref(fl), dptr(trace)), self.L)
         return fl.value, trace[:steps]
 
 
@@ -206,7 +242,7 @@ def fit_timed(model: "Model", steps: int):
     (FitReport::step_seconds): returns (step_seconds[steps], n_params, loss_trace)."""
     trace, secs = np.empty(max(steps, 1)), np.empty(max(steps, 1))
     fl, npar = C.c_double(), C.c_int()
-    _check(lib().ref_model_fit_timed(model.h, steps, C.byref(fl), dptr(trace), dptr(secs), C.byref(npar)))
+    _check(model.L.ref_model_fit_timed(model.h, steps, C.byref(fl), dptr(trace), dptr(secs), C.byref(npar)), model.L)
     return secs[:steps].copy(), npar.value, trace[:steps].copy()
 
 

@@ -229,11 +229,31 @@ int ref_invert_solve(const RefDesign* rd, const RefHyper* rh, const double* b, d
             std::vector<double> ks = gram_matvec(spec, bv);
             std::memcpy(kb, ks.data(), ks.size() * sizeof(double));
         }
-        if (trace) *trace = trace_inverse(inv);
+        if (trace) *trace = trace_inverse(inv);  // callers pass nullptr to skip it
         if (Pi) {
             PiH ph = extract_pi_h(inv);
             for (int l = 0; l < dz.L; ++l)
                 for (int lp = 0; lp < dz.L; ++lp) Pi[l * dz.L + lp] = ph.Pi(l, lp);
+        }
+    });
+}
+
+// Pi (L x L) and H (L x r row-major, r = N / n_{L-1}) of extract_pi_h (fast_gram.cpp:311-335).
+int ref_pi_h(const RefDesign* rd, const RefHyper* rh, double* Pi, double* H_re, double* H_im) {
+    return guarded([&] {
+        LdDesign dz = make_ld(*rd);
+        Hyperparams h = make_hyper(*rd, *rh);
+        const Eigen::MatrixXd R = task_gram(h.B, h.t);
+        SpatialKernel q = SpatialKernel::from(h, family_of(*rd));
+        BlockSpectrum spec = build_spectrum(dz, R, q, h.xi);
+        BlockInverse inv = invert_and_logdet(spec);
+        PiH ph = extract_pi_h(inv);
+        for (int l = 0; l < dz.L; ++l) {
+            for (int lp = 0; lp < dz.L; ++lp) Pi[l * dz.L + lp] = ph.Pi(l, lp);
+            for (std::size_t k = 0; k < inv.r; ++k) {
+                H_re[l * inv.r + k] = ph.H(l, static_cast<Eigen::Index>(k)).real();
+                H_im[l * inv.r + k] = ph.H(l, static_cast<Eigen::Index>(k)).imag();
+            }
         }
     });
 }

@@ -1990,6 +1990,58 @@ int fmtgp_extract_pi(fmtgp_model_t M, double* Pi) {
     });
 }
 
+int fmtgp_extract_h(fmtgp_model_t M, double* H_re, double* H_im) {
+    return guarded([&] {
+        if (!M || !H_re || !H_im) invalid("extract_h: null argument");
+        if (!M->have_inv) invalid("extract_h: no factorisation");
+        CK(cudaSetDevice(M->dev));
+        if (!M->equal) {
+            unequal::extract_h(M->uneq, M, H_re, H_im);
+            return;
+        }
+        // equal n: r = L, base = n and H_lk = sqrt(n) Lam(0)^-1_lk = Pi_lk / sqrt(n) (real)
+        const int T = M->T;
+        std::vector<double> Pi(size_t(T) * T);
+        const int rc = fmtgp_extract_pi(M, Pi.data());
+        if (rc != FMTGP_OK) throw Fail{rc, fmtgp_last_error()};
+        const double s = 1.0 / std::sqrt(double(M->n[0]));
+        for (int k = 0; k < T * T; ++k) H_re[k] = Pi[k] * s, H_im[k] = 0.0;
+    });
+}
+
+int fmtgp_spectrum_read_range(fmtgp_model_t M, int l, int lp, int64_t k0, int64_t count, double* re, double* im) {
+    return guarded([&] {
+        if (!M || ((!re || !im) && count > 0)) invalid("spectrum_read_range: null argument");
+        if (!M->have_spec) invalid("spectrum_read_range: no spectrum built");
+        ensure_fit_state(M);
+        if (l < 0 || lp < l || lp >= M->T) invalid("pair_index: need 0 <= l <= lp < L");
+        const long long n = M->n[l];
+        if (k0 < 0 || count < 0 || k0 + count > n) invalid("spectrum_read_range: frequency range outside the pair vector");
+        CK(cudaSetDevice(M->dev));
+        const int p = pair_index(M->T, l, lp);
+        const char* base = static_cast<const char*>(M->d_lam) + M->poff[p] * elem_size(M);
+        auto word = [&](long long w) {  // w-th double of the pair's slot vector
+            double v = 0.0;
+            CK(cudaMemcpy(&v, base + w * sizeof(double), sizeof(double), cudaMemcpyDeviceToHost));
+            return v;
+        };
+        const Geo g = M->geo_m[M->m[l]];
+        for (long long k = k0; k < k0 + count; ++k) {
+            const long long o = k - k0;
+            if (!M->lattice || n == 1) {
+                re[o] = word(k), im[o] = 0.0;
+            } else if (k == 0 || k == n / 2) {
+                re[o] = word(k == 0 ? 0 : 1), im[o] = 0.0;
+            } else {
+                const bool mirror = k > n / 2;
+                const long long q = g.pos_of(mirror ? n - k : k);
+                re[o] = word(2 * q);
+                im[o] = mirror ? -word(2 * q + 1) : word(2 * q + 1);
+            }
+        }
+    });
+}
+
 int fmtgp_trace_inverse(fmtgp_model_t M, double* tr) {
     return guarded([&] {
         if (!M || !tr) invalid("trace_inverse: null argument");

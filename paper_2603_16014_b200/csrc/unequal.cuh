@@ -16,6 +16,7 @@ void invert(Plan* P, fmtgp_model* M, double* logdet);
 void apply_inverse(Plan* P, fmtgp_model* M, const void* in_slots, void* out_slots);
 void apply_gram(Plan* P, fmtgp_model* M, const void* in_slots, void* out_slots);
 void extract_pi(Plan* P, fmtgp_model* M, double* Pi);
+void extract_h(Plan* P, fmtgp_model* M, double* Hre, double* Him);
 void coefficients(Plan* P, fmtgp_model* M, double* d_out);
 void posterior_var(Plan* P, fmtgp_model* M, int task, const double* X, int64_t count, double* out);
 void cubature_terms(Plan* P, fmtgp_model* M, double* Pi, double* etc);
