@@ -27,6 +27,20 @@ void init_twiddles(double2* tab, cudaStream_t s) {
     k_init_twiddles<<<dim3(32, 27), 256, 0, s>>>(tab);
 }
 
+// Per-vector binding of a transform source: the column kernels call bind_src(src, v) once per
+// CTA and the result per element, so sources can hoist per-vector constants into registers
+// (QuerySrcLat below); by default the element call is src(v, idx).
+template <class Src>
+struct BoundSrc {
+    const Src& s;
+    int v;
+    __device__ __forceinline__ double operator()(uint64_t idx) const { return s(v, idx); }
+};
+template <class Src>
+__device__ __forceinline__ BoundSrc<Src> bind_src(const Src& s, int v) {
+    return BoundSrc<Src>{s, v};
+}
+
 // ============================================================================ forward, single CTA
 template <int NT, class Src, class Snk>
 __global__ void __launch_bounds__(NT) k_fwd_small_lat(Src src, Snk snk, int m, const double2* __restrict__ tw) {
@@ -39,7 +53,8 @@ __global__ void __launch_bounds__(NT) k_fwd_small_lat(Src src, Snk snk, int m, c
         return;
     }
     const int lp = m - 1, Np = 1 << lp;
-    for (int e = threadIdx.x; e < Np; e += NT) sm[S(e)] = make_double2(src(v, 2ull * e), src(v, 2ull * e + 1));
+    const auto gen = bind_src(src, v);
+    for (int e = threadIdx.x; e < Np; e += NT) sm[S(e)] = make_double2(gen(2ull * e), gen(2ull * e + 1));
     __syncthreads();
     smem_fft<NT, true>(sm, lp, 1, padded_len(Np), -1, tw);
     for (int k = threadIdx.x; k <= Np / 2; k += NT) {
@@ -76,10 +91,11 @@ __global__ void __launch_bounds__(NT) k_fwd_col_lat(Src src, double2* __restrict
     constexpr auto S = sidx<true>;
     const int v = blockIdx.y, C = 1 << lc, N1 = 1 << l1, ld = padded_len(N1);
     const long long c0 = (long long)blockIdx.x << lc;
+    const auto gen = bind_src(src, v);
     for (int e = threadIdx.x; e < (C << l1); e += NT) {
         const int j1 = e >> lc, c = e & (C - 1);
         const uint64_t j = (uint64_t(j1) << l2) + c0 + c;
-        sm[c * ld + S(j1)] = make_double2(src(v, 2 * j), src(v, 2 * j + 1));
+        sm[c * ld + S(j1)] = make_double2(gen(2 * j), gen(2 * j + 1));
     }
     __syncthreads();
     smem_fft<NT, true>(sm, l1, C, ld, -1, tw);
@@ -648,9 +664,13 @@ void fwd_array(int lattice, const Geo& g, int nvec, const ArraySrc& src, const S
 }
 
 // Lattice query column with compile-time dimension cap and Bernoulli order: 32-bit exact lattice
-// coordinate (x_p = t 2^-m + sh_lo 2^-53, the same value as QuerySrc's 64-bit chain), the
-// reference's floating difference for the query coordinate (kernel_against_data,
-// gp_core.cpp:386-397), no integer division per element when a group holds one task.
+// coordinate (x_p = t 2^-m + sh_lo 2^-53, the same value as QuerySrc's 64-bit chain) and the
+// floating difference to the query coordinate (kernel_against_data, gp_core.cpp:386-397).
+// Bound per vector (query, task): every per-dimension constant lives in registers, the element
+// costs per dimension one 32-bit IMAD + LOP, one conversion, diff = (x_q - sh_lo 2^-53) - t 2^-m
+// (one DFMA), u = frac(diff) and the Bernoulli polynomial in w = u^2 - u (symmetric under
+// u -> 1 - u, so the reference's min(frac(d), frac(-d)) of kernels.cpp:28-32 is implied), then
+// f = A + B v as in lattice.cu's LatGen (B2: v = w; B4: v = w^2).
 template <int DC, int ALPHA>
 struct QuerySrcLat {
     QuerySrc q;
@@ -679,7 +699,59 @@ struct QuerySrcLat {
         }
         return __ldg(q.Rrow + l) * prod;
     }
+    struct Bound {
+        uint32_t gm[DC], oh[DC];
+        double c[DC], A[DC], B[DC];
+        double scale, inv_n;
+        uint32_t mask;
+        __device__ __forceinline__ double operator()(uint64_t idx) const {
+            double prod = scale;
+#pragma unroll
+            for (int j = 0; j < DC; ++j) {
+                const uint32_t t = (uint32_t(idx) * gm[j] + oh[j]) & mask;
+                const double diff = fma(-double(t), inv_n, c[j]);
+                const double u = diff - floor(diff);
+                const double w = fma(u, u, -u);
+                prod *= fma(B[j], ALPHA == 1 ? w : w * w, A[j]);
+            }
+            return prod;
+        }
+    };
+    __device__ __forceinline__ Bound bind(int v) const {
+        Bound b;
+        const int qi = q.ntg == 1 ? v : v / q.ntg;
+        const int l = __ldg(q.vec_task + (v - qi * q.ntg));
+        const int sb = DIGITAL_BITS - q.m;
+        b.mask = (1u << q.m) - 1u;
+        b.inv_n = pow2i(-q.m);
+        b.scale = __ldg(q.Rrow + l) * q.gamma;
+        constexpr double pi2 = 9.869604401089358618834491;
+        // base = ka v + kb: B2 2 pi^2 (w + 1/6); B4 -(2/3) pi^4 (w^2 - 1/30)
+        constexpr double ka = ALPHA == 1 ? 2.0 * pi2 : -(2.0 / 3.0) * pi2 * pi2;
+        constexpr double kb = ALPHA == 1 ? pi2 / 3.0 : pi2 * pi2 / 45.0;
+#pragma unroll
+        for (int j = 0; j < DC; ++j) {
+            if (j < q.d) {
+                const uint64_t sh = __ldg(q.shifts + l * q.d + j);
+                const double eta = __ldg(q.eta + j);
+                b.gm[j] = uint32_t(__ldg(q.g + j)) & b.mask;
+                b.oh[j] = uint32_t(sh >> sb) & b.mask;
+                b.c[j] = __ldg(q.X + (long long)qi * q.d + j) - double(sh & ((uint64_t(1) << sb) - 1)) * 0x1p-53;
+                b.A[j] = fma(eta, kb, 1.0);
+                b.B[j] = eta * ka;
+            } else {
+                b.gm[j] = b.oh[j] = 0u;
+                b.c[j] = b.B[j] = 0.0;
+                b.A[j] = 1.0;
+            }
+        }
+        return b;
+    }
 };
+template <int DC, int ALPHA>
+__device__ __forceinline__ typename QuerySrcLat<DC, ALPHA>::Bound bind_src(const QuerySrcLat<DC, ALPHA>& s, int v) {
+    return s.bind(v);
+}
 
 void fwd_query(int lattice, const Geo& g, int nvec, const QuerySrc& src, const ScaleSink& snk, void* work,
                const double2* tw, cudaStream_t s) {

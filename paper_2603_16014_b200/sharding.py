@@ -56,6 +56,24 @@ def sweep(evaluate: Callable[[Sequence], List[dict]], candidates: Sequence, worl
     return out
 
 
+def sharded_posterior_var(evaluate: Callable[[np.ndarray], np.ndarray], X, world: int = 1, rank: int = 0,
+                          group=None) -> np.ndarray:
+    """Posterior variance at the rows of X sharded over `world` ranks (BASELINE config 3, SURVEY.md
+    §8e): the test points are independent — contiguous blocks per rank, `evaluate(X_block)` (e.g.
+    ``lambda Xb: model.posterior_var(task, Xb)``, each rank's model holding the same fit), one
+    all-gather of the variances.  Every rank returns all values in point order, bit-identical to
+    one process (each query's fold is independent of its batch neighbours)."""
+    X = np.asarray(X, dtype=np.float64)
+    start, stop = shard_range(len(X), world, rank)
+    local = np.asarray(evaluate(X[start:stop]), dtype=np.float64) if stop > start else np.empty(0)
+    if world == 1:
+        return local
+    import torch.distributed as dist
+    gathered: List[np.ndarray] = [None] * world  # type: ignore[list-item]
+    dist.all_gather_object(gathered, local, group=group)
+    return np.concatenate(gathered)
+
+
 # ----------------------------------------------------------------------------- frequency sharding
 NOUT = 4 + 16 + 8 * 8  # result record (csrc/kernels.cuh OUT_*)
 

@@ -66,6 +66,42 @@ def test_candidate_sweep_gloo_world2(port):
         assert np.array_equal(np.array(got[r]), np.array(want))
 
 
+def _var_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        X = np.random.default_rng(3).random((37, 8))
+        res = sharding.sharded_posterior_var(_fake_var, X, world=world, rank=rank)
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def _fake_var(Xb):
+    # stands in for Model.posterior_var: a per-point function (the GPU numerics are checked
+    # against the reference in tests/test_gpu_parity.py and test_gpu_seam_dropin.py)
+    return np.cos(Xb).prod(axis=1) - 0.5 * Xb[:, 0]
+
+
+def test_posterior_var_sharding_gloo_world2():
+    """Config-3 test-point sharding: every rank gets all variances in point order,
+    identical to one process."""
+    X = np.random.default_rng(3).random((37, 8))
+    want = sharding.sharded_posterior_var(_fake_var, X)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = _free_port()
+    procs = [ctx.Process(target=_var_worker, args=(r, 2, p, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    for r in range(2):
+        assert np.array_equal(got[r], want)
+
+
 # ----------------------------------------------------------------------------- frequency sharding
 # The orchestration of sharding.sharded_nll (two all-to-alls of exchange blocks + a rank-order
 # record combine + the escalation loop) over real gloo all_to_all_single, world size 2.  The CUDA
