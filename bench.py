@@ -163,6 +163,13 @@ def ncu_traffic(cfg: int, kernel: str):
 # shapes; checked against one full-size reference loss_value, tools/ref_scaling.py
 # -> profiles/r02_ref_scaling.json).  Configs 1-2 run at full size.
 REF_SAMPLE_M = {4: 18, 5: 14}
+# config 3: the reference's own solve throws at full size ("abnormal imaginary residue",
+# fast_gram.cpp:289-296, SURVEY.md §8c caveat 1), so its cost is sampled at n = 2^16..2^10
+# (same generator, kernel, hyperparameters) and scaled by N log2 N: one loss_value (the fit's
+# build + invert + solves) plus REF_C3_QUERIES posterior_cov calls (one solve each,
+# gp_core.cpp:423-445) scaled to the 2^14 test points.
+REF_C3_M = [16, 14, 12, 10]
+REF_C3_QUERIES = 8
 
 
 def nlogn(N: int) -> float:
@@ -182,6 +189,26 @@ def cpu_reference(cfg: int, inst, steps: int, warmup: int):
         raise RuntimeError("oracle/_ref not built")
     from paper_2603_16014_b200 import configs
     dz = inst.design
+    if cfg == 3:
+        import time as _t
+        sample = configs.make(3, m=REF_C3_M, n_test=REF_C3_QUERIES)
+        model = ref.Model(sample.design, sample.hyper, sample.y)
+        model.loss(0)  # warm-up
+        t0 = _t.perf_counter()
+        model.loss(0)
+        t_fit = _t.perf_counter() - t0
+        t0 = _t.perf_counter()
+        for x in sample.X_test:
+            model.posterior_cov(0, x, 0, x)
+        t_q = (_t.perf_counter() - t0) / len(sample.X_test)
+        scale = nlogn(dz.N) / nlogn(sample.design.N)
+        nq = len(inst.X_test)
+        t_step = (t_fit + nq * t_q) * scale
+        what = (f"reference loss_value ({t_fit:.3f} s) + {len(sample.X_test)} posterior_cov calls ({t_q:.4f} s each) "
+                f"at n = 2^{REF_C3_M[0]}..2^{REF_C3_M[-1]} (N = {sample.design.N}; the reference's solve throws at "
+                f"full size, fast_gram.cpp:289-296), {nq} queries, scaled by N log2 N (x{scale:.1f}) to N = {dz.N}")
+        return {"value": 1.0 / t_step, "unit": "fits/s", "cores": threads, "kind": "reference", "sample": what,
+                "t_step_s": (t_fit + len(sample.X_test) * t_q), "scale": scale, "n_params": 0}
     m_s = REF_SAMPLE_M.get(cfg)
     if m_s is not None and m_s < dz.m[0]:
         sample = configs.make(cfg, m=[m_s] * dz.L, **({"n_cand": 1} if cfg == 5 else {}))
@@ -230,7 +257,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 4, 5],
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5],
                     help="BASELINE config; default 4 = the largest single-GPU config (headline)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="diagnostics only: skip the L2 flush")
@@ -256,7 +283,8 @@ def main():
                        5: f"candidate-sharded over {world} GPUs (gather of the records)"}.get(args.config,
                                                                                       f"{world} replicas")
     config = {"workload": WORKLOADS[args.config], "N": dz.N, "T": T, "d": dz.d, "n": dz.n[0],
-              "outputs": "NLL, logdet, dNLL/d(eta, w, v, gamma)",
+              "outputs": ("c, logdet, NLL, posterior variance at 2^14 test points, cubature mu and Sigma "
+                          "(one 'fit' = all of them)") if args.config == 3 else "NLL, logdet, dNLL/d(eta, w, v, gamma)",
               "l2": "flushed before every step (512 MiB write)" if not args.no_flush else "not flushed",
               "parallelism": parallelism}
 
@@ -288,7 +316,7 @@ def main():
     model = Model(dz, device=local_rank, max_candidates=64 if args.config == 5 else 1)
     model.set_y(inst.y)
     stream = torch.cuda.ExternalStream(model.stream, device=torch.device("cuda", local_rank))
-    sharded = (args.config == 4 and world > 1) or args.config == 5  # one job-wide unit per step
+    sharded = (args.config == 4 and world > 1) or args.config in (3, 5)  # one job-wide unit per step
     if args.config == 4 and world > 1:
         # config 4 at N > 1: the frequency-sharded fit — one fit per step over all
         # ranks (strong scaling): column pass -> NCCL all-to-all -> row pass + solve -> all-to-all ->
@@ -329,6 +357,28 @@ def main():
             def profile_read(self):
                 return model.profile_read()
         fitter = _Sweep()
+    elif args.config == 3:
+        # config 3: one step = fit (solve + logdet + NLL, unequal n) + posterior variance at the
+        # 2^14 test points + multitask cubature (BASELINE configs[2] outputs); with N > 1 ranks the
+        # test points are sharded (sharding.sharded_posterior_var)
+        from paper_2603_16014_b200 import sharding
+
+        class _Config3:
+            def nll(self, h, grad=True):
+                r = model.nll(h, grad=False)
+                sharding.sharded_posterior_var(lambda Xb: model.posterior_var(0, Xb), inst.X_test, world, rank)
+                model.cubature()
+                return r
+
+            def set_y(self, y):
+                model.set_y(y)
+
+            def profile(self, on=True):
+                model.profile(on)
+
+            def profile_read(self):
+                return model.profile_read()
+        fitter = _Config3()
     else:
         fitter = model
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local_rank}")
@@ -417,15 +467,30 @@ def main():
     traffic, traffic_src = ncu_traffic(args.config, dom_name)
     # whole fit against SURVEY.md §8d's algorithmic bytes 8n(6P + T) (the north-star's 60 % target)
     b_fit = 8.0 * dz.n[0] * (6 * P + T) * (len(inst.candidates) if args.config == 5 else 1)
-    fit_level = {"alg_bytes": b_fit, "definition": "SURVEY.md 8(d) B_alg = 8n(6P+T) per fit",
+    b_def = "SURVEY.md 8(d) B_alg = 8n(6P+T) per fit"
+    if args.config == 3:  # fit 8(2S + 4N) + variance 16 N Q
+        S_ = sum((T - l) * dz.n[l] for l in range(T))
+        b_fit = 8.0 * (2 * S_ + 4 * dz.N) + 16.0 * dz.N * len(inst.X_test)
+        b_def = "SURVEY.md 8(d) B_alg = 8(2S+4N) (fit) + 16 N Q (posterior variance), S = sum (T-l) n_l"
+    fit_level = {"alg_bytes": b_fit, "definition": b_def,
                  "achieved": b_fit / (ms_per_step * 1e-3) / 1e9 * (1 if sharded else world),
                  "frac": b_fit / (ms_per_step * 1e-3) / 1e9 * (1 if sharded else world) / peak}
+    # fp64 compute roof (SURVEY.md 8(d) approximate fp64 flops per step; peak = the DFMA
+    # microbenchmark tools/micro/fp64_peak.cu on this pool's B200, profiles/r02_fp64_peak.log)
+    fp64_flops = {2: 0.13e9, 3: 0.8e9 + 2.9e12, 4: 39e9, 5: 50e9}.get(args.config)
+    fp64 = None
+    if fp64_flops:
+        fp64_peak = 34.13
+        tf = fp64_flops / (ms_per_step * 1e-3) / 1e12 * (1 if sharded else world)
+        fp64 = {"flops_per_step": fp64_flops, "achieved": tf, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": tf / fp64_peak, "source": "SURVEY.md 8(d) flop estimate; peak measured "
+                                                  "(profiles/r02_fp64_peak.log, DFMA, 2 flops per FMA)"}
     roofline = {"bound": "hbm", "kernel": dom_name,
                 "timing": "per-kernel CUDA events on the fit stream, second pass of the same K steps "
                           f"({1e3 * prof_total_ms / args.steps:.1f} us/step instrumented)",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "alg_bytes_per_launch": alg, "traffic": traffic, "traffic_source": traffic_src,
-                "peak_source": peak_src, "kernels": kernels, "fit": fit_level}
+                "peak_source": peak_src, "kernels": kernels, "fit": fit_level, "fp64": fp64}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:

@@ -207,6 +207,31 @@ def dist_exchange(rank_obj, group=None):
     return ex
 
 
+def host_exchange(rank_obj, group=None):
+    """All-to-all staged through host memory (gloo's CPU all_to_all_single): for process groups
+    without a device transport (the CPU-plumbing tests of the real shard phases)."""
+    def ex(sends, recvs):
+        import torch
+        import torch.distributed as dist
+        torch.cuda.synchronize()
+        s, r = sends[0].cpu(), torch.empty_like(sends[0], device="cpu")
+        dist.all_to_all_single(r, s, group=group)
+        recvs[0].copy_(r)
+        torch.cuda.synchronize()
+    return ex
+
+
+def host_gather(rank_obj, group=None):
+    def ga(recs):
+        import torch
+        import torch.distributed as dist
+        t = torch.from_numpy(np.asarray(recs[0], dtype=np.float64))
+        out = [torch.empty_like(t) for _ in range(rank_obj.world)]
+        dist.all_gather(out, t, group=group)
+        return [o.numpy() for o in out]
+    return ga
+
+
 def dist_gather(rank_obj, group=None):
     def ga(recs):
         return rank_obj.default_gather(recs[0], group)
