@@ -170,6 +170,10 @@ FMTGP_API int fmtgp_fit(fmtgp_model_t model, const fmtgp_hyper* init, int steps,
 FMTGP_API int fmtgp_posterior_mean(fmtgp_model_t model, int task, const double* X, int64_t count, double* out);
 /* posterior variance K((t,x),(t,x)) - k^T K^-1 k (posterior_cov, gp_core.cpp:423-445, x = x') */
 FMTGP_API int fmtgp_posterior_var(fmtgp_model_t model, int task, const double* X, int64_t count, double* out);
+/* posterior_cov (gp_core.cpp:423-445) for count pairs: out[i] = K((task,X[i]),(task2,Xp[i])) - k^T K^-1 k'
+ * (both kernel columns folded forward on the device; X, Xp host [count * d]) */
+FMTGP_API int fmtgp_posterior_cov(fmtgp_model_t model, int task, const double* X, int task2, const double* Xp,
+                                  int64_t count, double* out);
 /* multitask_cubature (cubature.cpp:52-75): mu [L], Sigma [L * L] (internal order) */
 FMTGP_API int fmtgp_cubature(fmtgp_model_t model, double* mu, double* Sigma);
 

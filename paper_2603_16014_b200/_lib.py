@@ -87,6 +87,9 @@ _SIGS = {
     "fmtgp_fit": (C.c_int, [C.c_void_p, C.POINTER(CHyper), C.c_int, _dp, _dp, _dp, C.POINTER(CFitReport)]),
     "fmtgp_posterior_mean": (C.c_int, [C.c_void_p, C.c_int, _dp, C.c_int64, _dp]),
     "fmtgp_posterior_var": (C.c_int, [C.c_void_p, C.c_int, _dp, C.c_int64, _dp]),
+    "fmtgp_posterior_cov": (C.c_int, [C.c_void_p, C.c_int, _dp, C.c_int, _dp, C.c_int64, _dp]),
+    "fmtgp_extract_h": (C.c_int, [C.c_void_p, _dp, _dp]),
+    "fmtgp_spectrum_read_range": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_int64, _dp, _dp]),
     "fmtgp_cubature": (C.c_int, [C.c_void_p, _dp, _dp]),
     "fmtgp_gcv": (C.c_int, [C.c_void_p, C.POINTER(CHyper), _dp, _dp, _dp]),
     "fmtgp_shard_setup": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int64)]),

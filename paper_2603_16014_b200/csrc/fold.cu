@@ -259,6 +259,41 @@ void fold_solve(const FoldDims& D, const void* lam, void* rhs, int nrhs, double*
     }
 }
 
+// cross[q] partials = sum_s sum_i w_i Re(conj(z_q) z_{q+nq}) / d_s over the forward-substituted
+// right-hand sides q and q + nq (posterior covariance k(x)^T K^-1 k(x') = zx^H D^-1 zx')
+template <bool CX>
+__global__ void __launch_bounds__(256) k_fs_cross(FoldDims D, const void* lam_v, const void* rhs_v, int nq,
+                                                  double* part, int nblk) {
+    using S = Sc<CX>;
+    using V = typename S::T;
+    const int q = blockIdx.y;
+    const V* za = static_cast<const V*>(rhs_v) + size_t(q) * D.tot_task;
+    const V* zb = static_cast<const V*>(rhs_v) + size_t(q + nq) * D.tot_task;
+    double acc = 0.0;
+    for (int s = 0; s < D.T; ++s) {
+        const V* lss = static_cast<const V*>(lam_v) + D.poff[D.pid[s][s]];
+        const long long n = D.n[s], H = D.H[s], o = D.toff[s];
+        for (long long i = blockIdx.x * 256ll + threadIdx.x; i < H; i += (long long)gridDim.x * 256) {
+            const V a = za[o + i], b = zb[o + i];
+            double re;
+            if constexpr (CX) re = a.x * b.x + a.y * b.y;
+            else re = a * b;
+            acc += half_weight<CX>(n, i) * re / S::re(lss[i]);
+        }
+    }
+    __shared__ double red[32];
+    acc = block_sum<256>(acc, red);
+    if (threadIdx.x == 0) part[size_t(q) * nblk + blockIdx.x] = acc;
+}
+
+void fold_cross_quad(const FoldDims& D, const void* lam, const void* rhs, int nq, double* part, int nblk,
+                     cudaStream_t s) {
+    ProfScope ps("fold_fs_cross", s);
+    dim3 g(nblk, nq);
+    if (D.lattice) k_fs_cross<true><<<g, 256, 0, s>>>(D, lam, rhs, nq, part, nblk);
+    else k_fs_cross<false><<<g, 256, 0, s>>>(D, lam, rhs, nq, part, nblk);
+}
+
 // ------------------------------------------------------------------ Gram apply (gram_matvec)
 template <bool CX>
 __global__ void __launch_bounds__(256) k_gram_nat(FoldDims D, const void* lam_v, const void* v_v, void* out_v) {

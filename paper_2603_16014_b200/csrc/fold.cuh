@@ -49,6 +49,9 @@ void fold_factor(const FoldDims& D, void* lam, double* partial, int nblk, int* b
 // qpart[r][s][blk]) and optionally back substitution (-> Lam^-1 rhs)
 void fold_solve(const FoldDims& D, const void* lam, void* rhs, int nrhs, double* qpart, int nblk, bool back,
                 cudaStream_t s);
+// part[q][blk]: sum over stages of w Re(conj(z_q) z_{q+nq}) / d of forward-substituted rhs (covariances)
+void fold_cross_quad(const FoldDims& D, const void* lam, const void* rhs, int nq, double* part, int nblk,
+                     cudaStream_t s);
 // out = Lam v (unfolded spectrum, natural layout), one right-hand side
 void fold_gram_apply(const FoldDims& D, const void* lam, const void* v, void* out, cudaStream_t s);
 

@@ -2294,6 +2294,20 @@ int fmtgp_posterior_var(fmtgp_model_t M, int task, const double* X, int64_t coun
     });
 }
 
+int fmtgp_posterior_cov(fmtgp_model_t M, int task, const double* X, int task2, const double* Xp, int64_t count,
+                        double* out) {
+    return guarded([&] {
+        ProfGuard pg_(M);
+        if (!M || (count > 0 && (!X || !Xp || !out))) invalid("posterior_cov: null argument");
+        if (!M->have_fit) invalid("posterior_cov: model not refreshed");
+        ensure_fit_state(M);
+        if (task < 0 || task >= M->T || task2 < 0 || task2 >= M->T) invalid("posterior_cov: task out of range");
+        CK(cudaSetDevice(M->dev));
+        if (!M->uneq) throw Fail{FMTGP_ERR_UNSUPPORTED, "posterior_cov: needs the fold plan"};
+        unequal::posterior_cov(M->uneq, M, task, X, task2, Xp, count, out);
+    });
+}
+
 // multitask_cubature (cubature.cpp:52-75): mu = tau + gamma R (E^T c), Sigma = gamma R - gamma^2 R Pi R
 int fmtgp_cubature(fmtgp_model_t M, double* mu, double* Sigma) {
     return guarded([&] {

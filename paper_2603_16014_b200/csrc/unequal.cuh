@@ -19,5 +19,7 @@ void extract_pi(Plan* P, fmtgp_model* M, double* Pi);
 void extract_h(Plan* P, fmtgp_model* M, double* Hre, double* Him);
 void coefficients(Plan* P, fmtgp_model* M, double* d_out);
 void posterior_var(Plan* P, fmtgp_model* M, int task, const double* X, int64_t count, double* out);
+void posterior_cov(Plan* P, fmtgp_model* M, int task, const double* X, int task2, const double* Xp, int64_t count,
+                   double* out);
 void cubature_terms(Plan* P, fmtgp_model* M, double* Pi, double* etc);
 }  // namespace fmtgp::unequal

@@ -154,6 +154,15 @@ class Model:
         check(self.lib.fmtgp_extract_pi(self.h, dptr(Pi)))
         return Pi
 
+    def extract_pi_h(self):
+        """(Pi [L, L], H [L, r] complex) of extract_pi_h (fast_gram.cpp:311-335), r = N / n_{L-1}."""
+        L = self.design.L
+        r = self.design.N // self.design.n[L - 1]
+        Pi = self.extract_pi()
+        hr, hi = np.empty((L, r)), np.empty((L, r))
+        check(self.lib.fmtgp_extract_h(self.h, dptr(hr), dptr(hi)))
+        return Pi, hr + 1j * hi
+
     def trace_inverse(self) -> float:
         v = C.c_double()
         check(self.lib.fmtgp_trace_inverse(self.h, C.byref(v)))
@@ -236,6 +245,17 @@ class Model:
         check(self.lib.fmtgp_posterior_var(self.h, task, dptr(X), X.shape[0], dptr(out)))
         return out
 
+    def posterior_cov(self, task: int, X: np.ndarray, task2: int, Xp: np.ndarray) -> np.ndarray:
+        """posterior_cov (gp_core.cpp:423-445) for the pairs (X[i], Xp[i]): K((task, x), (task2, x'))
+        - k(x)^T K^-1 k(x'), both kernel columns on the device."""
+        X = np.ascontiguousarray(X, dtype=np.float64).reshape(-1, self.design.d)
+        Xp = np.ascontiguousarray(Xp, dtype=np.float64).reshape(-1, self.design.d)
+        if X.shape != Xp.shape:
+            raise ValueError("posterior_cov: X and Xp need the same shape")
+        out = np.empty(X.shape[0])
+        check(self.lib.fmtgp_posterior_cov(self.h, task, dptr(X), task2, dptr(Xp), X.shape[0], dptr(out)))
+        return out
+
     def cubature(self):
         L = self.design.L
         mu, S = np.empty(L), np.empty((L, L))
@@ -277,8 +297,8 @@ def solve(model: Model, y: np.ndarray) -> np.ndarray:
     return model.solve(y)
 
 
-def extract_pi_h(model: Model) -> np.ndarray:
-    return model.extract_pi()
+def extract_pi_h(model: Model):
+    return model.extract_pi_h()
 
 
 def trace_inverse(model: Model) -> float:

@@ -282,3 +282,23 @@ def test_gcv_unequal_unsupported(Model):
     M.set_y(y)
     with pytest.raises(Unsupported):
         M.gcv(hp)
+
+
+@pytest.mark.parametrize("kind,m", [(LATTICE, [8, 8]), (DIGITAL, [7, 7, 7]), (LATTICE, [9, 7, 5]), (DIGITAL, [6, 4, 4, 2])])
+def test_posterior_cov_cross_terms(ref, Model, kind, m):
+    """posterior_cov(task, x, task2, x') (gp_core.cpp:423-445) with x != x' and task != task2: the
+    device cross term zx^H D^-1 zx' through the fold against the reference (one solve per pair)."""
+    dz, hp, y = instance(kind, m)
+    M = Model(dz)
+    M.set_y(y)
+    M.nll(hp, grad=False)
+    rm = ref.Model(dz, hp, y)
+    rm.loss(0)
+    X = uniform01(41, 3, np.arange(6 * dz.d)).reshape(6, dz.d)
+    Xp = uniform01(43, 5, np.arange(6 * dz.d)).reshape(6, dz.d)
+    t2 = dz.L - 1
+    got = M.posterior_cov(0, X, t2, Xp)
+    want = np.array([rm.posterior_cov(0, X[i], t2, Xp[i]) for i in range(6)])
+    assert np.abs(got - want).max() <= 1e-8 * max(1.0, np.abs(want).max())
+    same = M.posterior_cov(t2, X, t2, X)  # x = x': the variance path
+    assert np.abs(same - M.posterior_var(t2, X)).max() <= 1e-10 * max(1.0, np.abs(same).max())
