@@ -1,0 +1,90 @@
+"""The pybind-surface front-end (paper_2603_16014_b200/fastmtgp.py, bindings.cpp:129-213) and the
+model document I/O (gp_core.cpp:447-508).  CPU tests: design ordering / shift streams, weights,
+document checks; GPU tests: the Model against the reference library on the same design."""
+import json
+
+import numpy as np
+import pytest
+
+from paper_2603_16014_b200 import fastmtgp
+from paper_2603_16014_b200._lib import Unsupported
+from paper_2603_16014_b200.designs import DIGITAL, LATTICE
+
+
+def test_make_design_user_order_and_streams():
+    """Internal order = stable descending size (ld_sequences.cpp:175-176); the shift of a task
+    follows its USER index, so reordering the other tasks does not change it."""
+    d1, i2u1 = fastmtgp.make_design(LATTICE, 3, [5, 7, 5, 6], seed=9)
+    assert i2u1 == [1, 3, 0, 2] and d1.m == [7, 6, 5, 5]
+    d2, i2u2 = fastmtgp.make_design(LATTICE, 3, [5, 7], seed=9)
+    assert i2u2 == [1, 0]
+    assert np.array_equal(d1.shift_bits[0], d2.shift_bits[0])  # both: user task 1
+    assert not np.array_equal(d1.shift_bits[0], d1.shift_bits[2])
+    pts = fastmtgp.design_points("digital", 2, [8, 32, 16], seed=4)
+    assert [p.shape for p in pts] == [(8, 2), (32, 2), (16, 2)]
+    assert all(np.all((p >= 0) & (p < 1)) for p in pts)
+
+
+def test_optimal_weights_formula():
+    rng = np.random.default_rng(1)
+    A = rng.standard_normal((3, 3))
+    Sigma, mu, chi = A @ A.T + np.eye(3), rng.standard_normal(3), np.array([1.0, 0.0, 0.0])
+    w, mse = fastmtgp.optimal_weights(mu, Sigma, chi)
+    # the minimiser of w^T Sigma w + (w.mu - chi.mu)^2 (cubature.cpp weights_mse)
+    f = lambda v: v @ Sigma @ v + (v @ mu - chi @ mu) ** 2  # noqa: E731
+    assert abs(f(w) - mse) <= 1e-12 * max(1.0, abs(mse))
+    for _ in range(5):
+        assert f(w + 1e-3 * rng.standard_normal(3)) >= f(w)
+
+
+def test_reference_document_without_generator_is_rejected():
+    doc = {"kind": "lattice", "family": "si-lattice", "loss": "nmll", "d": 2, "seed": 1, "m": [3],
+           "hyper": {"gamma": 1.0, "eta": [1, 1], "si_alpha": 1, "b": [1, 1, 1, 1], "t": [0.1], "xi": [1e-8],
+                     "tau": [0.0], "lengthscales": [0.25, 0.25], "B": [[0.1]]}, "y": [[0.0] * 8]}
+    with pytest.raises(Unsupported):
+        fastmtgp.Model.from_json(json.dumps(doc))
+
+
+def test_se_dense_is_unsupported():
+    with pytest.raises(Unsupported):
+        fastmtgp.Model("se-dense", 2, [8], 1, [[0.0] * 8])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kernel,n", [("si-lattice", [64, 256]), ("dsi-digital", [32, 128, 32])])
+def test_model_matches_reference(ref, kernel, n):
+    rng = np.random.default_rng(5)
+    y = [rng.standard_normal(v) for v in n]
+    m = fastmtgp.Model(kernel, 3, n, seed=11, y=y, task_rank=1, jitter=1e-6)
+    hi = m._internal(m.hyper)
+    yi = np.concatenate([y[u] for u in m.i2u])
+    rm = ref.Model(m.design, hi, yi)
+    want = rm.loss(0)
+    assert abs(m.loss() - want) <= 1e-8 * m.design.N
+    st = rm.state()
+    assert np.allclose(m.tau(), m._uvec(st["tau"]), rtol=1e-10, atol=1e-12)
+    X = np.random.default_rng(2).random((5, 3))
+    for u in range(len(n)):
+        got = m.posterior_mean_batch(u, X)
+        exp = rm.posterior_mean(m.i2u.index(u), X)
+        assert np.allclose(got, exp, rtol=1e-9, atol=1e-12)
+    c = m.posterior_cov(0, X[0], len(n) - 1, X[1])
+    c_ref = rm.posterior_cov(m.i2u.index(0), X[0], m.i2u.index(len(n) - 1), X[1])
+    assert abs(c - c_ref) <= 1e-8 * max(1.0, abs(c_ref))
+    mu, S = m.cubature()
+    mur, Sr = rm.cubature()
+    assert np.allclose(mu, m._uvec(mur), rtol=1e-9, atol=1e-12)
+    assert np.allclose(S, m._umat(Sr), rtol=1e-8, atol=1e-12)
+
+
+@pytest.mark.gpu
+def test_fit_and_json_round_trip():
+    rng = np.random.default_rng(8)
+    n = [128, 64]
+    m = fastmtgp.Model("si-lattice", 2, n, seed=3, y=[rng.standard_normal(v) for v in n])
+    rep = m.fit(5)
+    assert len(rep["loss_trace"]) == 5 and np.all(np.diff(rep["loss_trace"]) <= 0)
+    doc = m.to_json()
+    m2 = fastmtgp.Model.from_json(doc)
+    assert m2.loss() == pytest.approx(m.loss(), rel=1e-13)
+    assert json.loads(m2.to_json()) == json.loads(doc)
