@@ -133,7 +133,7 @@ FMTGP_API int fmtgp_extract_h(fmtgp_model_t model, double* H_re, double* H_im);
 /* frequencies [k0, k0 + count) of pair (l <= lp) in natural order (fmtgp_spectrum_read for a range) */
 FMTGP_API int fmtgp_spectrum_read_range(fmtgp_model_t model, int l, int lp, int64_t k0, int64_t count, double* re,
                                         double* im);
-/* trace_inverse (fast_gram.cpp:301-309) */
+/* trace_inverse (fast_gram.cpp:301-309); unequal n by selected inversion of the fold */
 FMTGP_API int fmtgp_trace_inverse(fmtgp_model_t model, double* tr);
 
 /* ---- gp_core hot path -------------------------------------------------------------- */
@@ -160,7 +160,8 @@ typedef struct fmtgp_fit_report {
     double tau[FMTGP_MAX_T];    /* prior means at the best parameters (internal order)  */
 } fmtgp_fit_report;
 /* GCV loss (loss_value(model, LossKind::gcv), gp_core.cpp:213-226): ||c||^2 / (tr K^-1)^2 with the
- * reference's escalation; equal n only (FMTGP_ERR_UNSUPPORTED otherwise).  num / tr optional. */
+ * reference's escalation, c = K^-1 (y - E tau_GCV); unequal n through H and the selected-inversion
+ * trace.  num / tr optional. */
 FMTGP_API int fmtgp_gcv(fmtgp_model_t model, const fmtgp_hyper* h, double* loss, double* num, double* tr);
 FMTGP_API int fmtgp_fit_param_count(fmtgp_model_t model, int s, int* n_params);
 FMTGP_API int fmtgp_fit(fmtgp_model_t model, const fmtgp_hyper* init, int steps, double* theta_best,

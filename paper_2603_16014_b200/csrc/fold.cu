@@ -294,6 +294,82 @@ void fold_cross_quad(const FoldDims& D, const void* lam, const void* rhs, int nq
     else k_fs_cross<false><<<g, 256, 0, s>>>(D, lam, rhs, nq, part, nblk);
 }
 
+// ------------------------------------------------------------------ selected inversion (trace of Lam^-1)
+// Lam = U^H D U with U_{(s,i),(a, i mod n_a)} = lam_sa[i] / d_s[i] (the fold's factor).  Z = Lam^-1
+// restricted to the SPECTRUM'S OWN pattern — z_ab[i] = Z_{(a,i),(b, i mod n_b)}, a <= b, the layout
+// of lam — satisfies (Takahashi: Z = D^-1 U^-H + (I - U) Z), for s = T-1 .. 0:
+//   z_sb[i] = -sum_{a>s} lam_sa[i] / d_s[i] * Z_{(a, i mod n_a),(b, i mod n_b)}   (b > s)
+//   z_ss[i] = (1 - sum_{a>s} Re(lam_sa[i] conj(z_sa[i]))) / d_s[i]
+// and every Z entry on the right lies on the pattern again (transposed when n_a < n_b), so the
+// recursion closes in the spectrum's storage: trace(Lam^-1) = sum_s sum_i Re z_ss[i] without
+// Algorithm 1's r x r grid (fast_gram.cpp:151-263, 301-309).  Lattice vectors keep their Hermitian
+// natural half (Z inherits the symmetry of the real-data spectra).
+template <bool CX>
+__device__ __forceinline__ typename Sc<CX>::T zget(const FoldDims& D, const typename Sc<CX>::T* z, int a, long long p,
+                                                   int b, long long q) {
+    using S = Sc<CX>;
+    if (a <= b) return getv<CX>(z + D.poff[D.pid[a][b]], D.n[a], p);
+    return S::conj(getv<CX>(z + D.poff[D.pid[b][a]], D.n[b], q));
+}
+
+template <bool CX>
+__global__ void __launch_bounds__(256) k_selinv_off(FoldDims D, int s, const void* lam_v, void* z_v) {
+    using S = Sc<CX>;
+    using V = typename S::T;
+    const V* lam = static_cast<const V*>(lam_v);
+    V* z = static_cast<V*>(z_v);
+    const int b = s + 1 + blockIdx.y;
+    V* zsb = z + D.poff[D.pid[s][b]];
+    const V* lss = lam + D.poff[D.pid[s][s]];
+    const long long H = D.H[s], nb = D.n[b];
+    for (long long i = blockIdx.x * 256ll + threadIdx.x; i < H; i += (long long)gridDim.x * 256) {
+        V acc = S::zero();
+        for (int a = s + 1; a < D.T; ++a)
+            acc = S::add(acc, S::mul(lam[D.poff[D.pid[s][a]] + i], zget<CX>(D, z, a, i % D.n[a], b, i % nb)));
+        zsb[i] = S::scale(acc, -1.0 / S::re(lss[i]));
+    }
+}
+
+template <bool CX>
+__global__ void __launch_bounds__(256) k_selinv_diag(FoldDims D, int s, const void* lam_v, void* z_v, double* part,
+                                                     int nblk) {
+    using S = Sc<CX>;
+    using V = typename S::T;
+    const V* lam = static_cast<const V*>(lam_v);
+    V* z = static_cast<V*>(z_v);
+    V* zss = z + D.poff[D.pid[s][s]];
+    const V* lss = lam + D.poff[D.pid[s][s]];
+    const long long n = D.n[s], H = D.H[s];
+    double tr = 0.0;
+    for (long long i = blockIdx.x * 256ll + threadIdx.x; i < H; i += (long long)gridDim.x * 256) {
+        double acc = 0.0;
+        for (int a = s + 1; a < D.T; ++a) {
+            const V l = lam[D.poff[D.pid[s][a]] + i], w = z[D.poff[D.pid[s][a]] + i];
+            acc += S::re(S::mulc(l, w));  // Re(l conj(w))
+        }
+        const double v = (1.0 - acc) / S::re(lss[i]);
+        if constexpr (CX) zss[i] = make_double2(v, 0.0);
+        else zss[i] = v;
+        tr += half_weight<CX>(n, i) * v;
+    }
+    __shared__ double red[32];
+    tr = block_sum<256>(tr, red);
+    if (threadIdx.x == 0) part[s * nblk + blockIdx.x] = tr;
+}
+
+void fold_selinv_trace(const FoldDims& D, const void* lam, void* z, double* part, int nblk, cudaStream_t s) {
+    ProfScope ps("fold_selinv", s);
+    for (int st = D.T - 1; st >= 0; --st) {
+        if (st + 1 < D.T) {
+            dim3 g(blocks_for(D.H[st]), D.T - st - 1);
+            if (D.lattice) k_selinv_off<true><<<g, 256, 0, s>>>(D, st, lam, z);
+            else k_selinv_off<false><<<g, 256, 0, s>>>(D, st, lam, z);
+        }
+        if (D.lattice) k_selinv_diag<true><<<nblk, 256, 0, s>>>(D, st, lam, z, part, nblk);
+        else k_selinv_diag<false><<<nblk, 256, 0, s>>>(D, st, lam, z, part, nblk);
+    }
+}
+
 // ------------------------------------------------------------------ Gram apply (gram_matvec)
 template <bool CX>
 __global__ void __launch_bounds__(256) k_gram_nat(FoldDims D, const void* lam_v, const void* v_v, void* out_v) {

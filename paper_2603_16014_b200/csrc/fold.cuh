@@ -52,6 +52,9 @@ void fold_solve(const FoldDims& D, const void* lam, void* rhs, int nrhs, double*
 // part[q][blk]: sum over stages of w Re(conj(z_q) z_{q+nq}) / d of forward-substituted rhs (covariances)
 void fold_cross_quad(const FoldDims& D, const void* lam, const void* rhs, int nq, double* part, int nblk,
                      cudaStream_t s);
+// trace(Lam^-1) by selected inversion on the factor's own pattern: z (tot_pair entries) receives
+// Z = Lam^-1 on that pattern, part[s][blk] the per-stage partial traces
+void fold_selinv_trace(const FoldDims& D, const void* lam, void* z, double* part, int nblk, cudaStream_t s);
 // out = Lam v (unfolded spectrum, natural layout), one right-hand side
 void fold_gram_apply(const FoldDims& D, const void* lam, const void* v, void* out, cudaStream_t s);
 

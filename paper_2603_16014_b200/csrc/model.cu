@@ -2046,8 +2046,11 @@ int fmtgp_trace_inverse(fmtgp_model_t M, double* tr) {
     return guarded([&] {
         if (!M || !tr) invalid("trace_inverse: null argument");
         if (!M->have_inv) invalid("trace_inverse: no factorisation");
-        if (!M->equal) throw Fail{FMTGP_ERR_UNSUPPORTED, "trace_inverse: unequal sample sizes not implemented"};
         CK(cudaSetDevice(M->dev));
+        if (!M->equal) {
+            *tr = unequal::trace_inverse(M->uneq, M);
+            return;
+        }
         const long long ns = M->pslots[0];
         const int T = M->T;
         double acc = 0.0;
@@ -2077,20 +2080,19 @@ int fmtgp_nll(fmtgp_model_t M, const fmtgp_hyper* h, int want_grad, fmtgp_result
 }
 
 // GCV loss (loss_value with LossKind::gcv, gp_core.cpp:213-226) = ||c||^2 / (tr K^-1)^2 at the
-// refreshed (escalated) nugget.  Equal n only: there the tau_GCV normal equations
+// refreshed (escalated) nugget, c = K^-1 (y - E tau_GCV).  Equal n: the tau_GCV normal equations
 // (HH^ tau = E^T K^-2 y, gp_core.cpp:84-87) collapse at frequency 0 to the sample mean, i.e. the
-// NMLL tau, so c is the fit's coefficient vector.  Composed of the seam calls (refresh,
-// coefficients, build + invert at the escalated nugget, trace_inverse).
+// NMLL tau, so c is the fit's coefficient vector.  Unequal n: tau_GCV from H (extract_pi_h) and two
+// solves, the trace by selected inversion of the fold.  Composed of the seam calls.
 int fmtgp_gcv(fmtgp_model_t M, const fmtgp_hyper* h, double* loss, double* num, double* tr) {
     int rc = guarded([&] {
         if (!M || !h || !loss) invalid("gcv: null argument");
-        if (!M->equal) throw Fail{FMTGP_ERR_UNSUPPORTED, "gcv: unequal sample sizes not implemented"};
     });
     if (rc) return rc;
     fmtgp_result r{};
     if ((rc = fmtgp_nll(M, h, 0, &r))) return rc;
     std::vector<double> c(size_t(M->N));
-    if ((rc = fmtgp_coefficients(M, c.data()))) return rc;
+    if (M->equal && (rc = fmtgp_coefficients(M, c.data()))) return rc;
     std::vector<double> xi(h->xi, h->xi + M->T);
     for (int t = 0; t < M->T; ++t) {
         xi[t] = h->xi[t] * r.xi_scale;
@@ -2102,6 +2104,31 @@ int fmtgp_gcv(fmtgp_model_t M, const fmtgp_hyper* h, double* loss, double* num, 
     if ((rc = fmtgp_build_spectrum(M, &h2))) return rc;
     if ((rc = fmtgp_invert_and_logdet(M, &ld))) return rc;
     if ((rc = fmtgp_trace_inverse(M, &trace))) return rc;
+    if (!M->equal) {
+        rc = guarded([&] {
+            const int T = M->T;
+            const long long r_ = M->N / M->n[T - 1];
+            std::vector<double> Hre(size_t(T) * r_), Him(Hre.size()), y(size_t(M->N)), w(y.size()), w2(y.size());
+            int e = fmtgp_extract_h(M, Hre.data(), Him.data());
+            if (e) throw Fail{e, fmtgp_last_error()};
+            CK(cudaMemcpy(y.data(), M->d_y, sizeof(double) * M->N, cudaMemcpyDeviceToHost));
+            if ((e = fmtgp_solve(M, y.data(), w.data())) || (e = fmtgp_solve(M, w.data(), w2.data())))
+                throw Fail{e, fmtgp_last_error()};
+            // HHbar tau = E^T K^-2 y (compute_tau_internal, gp_core.cpp:84-87)
+            std::vector<double> HH(size_t(T) * T, 0.0), rhs(T, 0.0);
+            for (int a = 0; a < T; ++a)
+                for (int b = 0; b < T; ++b)
+                    for (long long k = 0; k < r_; ++k)
+                        HH[a * T + b] += Hre[a * r_ + k] * Hre[b * r_ + k] + Him[a * r_ + k] * Him[b * r_ + k];
+            for (int a = 0; a < T; ++a)
+                for (long long k = M->off[a]; k < M->off[a + 1]; ++k) rhs[a] += w2[k];
+            const std::vector<double> tau = unequal::small_solve(T, HH, rhs);
+            for (int a = 0; a < T; ++a)
+                for (long long k = M->off[a]; k < M->off[a + 1]; ++k) y[k] -= tau[a];
+            if ((e = fmtgp_solve(M, y.data(), c.data()))) throw Fail{e, fmtgp_last_error()};
+        });
+        if (rc) return rc;
+    }
     double s = 0.0;
     for (double v : c) s += v * v;
     *loss = s / (trace * trace);

@@ -17,6 +17,7 @@ void apply_inverse(Plan* P, fmtgp_model* M, const void* in_slots, void* out_slot
 void apply_gram(Plan* P, fmtgp_model* M, const void* in_slots, void* out_slots);
 void extract_pi(Plan* P, fmtgp_model* M, double* Pi);
 void extract_h(Plan* P, fmtgp_model* M, double* Hre, double* Him);
+double trace_inverse(Plan* P, fmtgp_model* M);
 void coefficients(Plan* P, fmtgp_model* M, double* d_out);
 void posterior_var(Plan* P, fmtgp_model* M, int task, const double* X, int64_t count, double* out);
 void posterior_cov(Plan* P, fmtgp_model* M, int task, const double* X, int task2, const double* Xp, int64_t count,

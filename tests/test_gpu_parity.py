@@ -275,15 +275,6 @@ def test_gcv_matches_reference(ref, Model, kind, m):
     assert abs(g["gcv"] - g["num"] / g["trace"] ** 2) <= 1e-14 * abs(g["gcv"])
 
 
-def test_gcv_unequal_unsupported(Model):
-    from paper_2603_16014_b200.fast_gram import Unsupported
-    dz, hp, y = instance(LATTICE, [3, 2])
-    M = Model(dz)
-    M.set_y(y)
-    with pytest.raises(Unsupported):
-        M.gcv(hp)
-
-
 @pytest.mark.parametrize("kind,m", [(LATTICE, [8, 8]), (DIGITAL, [7, 7, 7]), (LATTICE, [9, 7, 5]), (DIGITAL, [6, 4, 4, 2])])
 def test_posterior_cov_cross_terms(ref, Model, kind, m):
     """posterior_cov(task, x, task2, x') (gp_core.cpp:423-445) with x != x' and task != task2: the
@@ -302,3 +293,21 @@ def test_posterior_cov_cross_terms(ref, Model, kind, m):
     assert np.abs(got - want).max() <= 1e-8 * max(1.0, np.abs(want).max())
     same = M.posterior_cov(t2, X, t2, X)  # x = x': the variance path
     assert np.abs(same - M.posterior_var(t2, X)).max() <= 1e-10 * max(1.0, np.abs(same).max())
+
+
+@pytest.mark.parametrize("kind,m", [(LATTICE, [9, 7, 5]), (DIGITAL, [6, 4, 4, 2]), (LATTICE, [3, 2, 1]),
+                                    (DIGITAL, [12, 10]), (LATTICE, [14, 12, 10, 8])])
+def test_unequal_trace_and_gcv(ref, Model, kind, m):
+    """trace_inverse for unequal n by selected inversion of the fold (the reference sums the
+    diagonal blocks of Algorithm 1's grid, fast_gram.cpp:301-309) and the GCV loss with tau_GCV
+    from H (gp_core.cpp:84-87, 213-226)."""
+    dz, hp, y = instance(kind, m)
+    _, _, _, tr_ref, _ = ref.invert_solve(dz, hp, y)
+    M = Model(dz)
+    M.set_y(y)
+    M.build_spectrum(hp)
+    M.invert_and_logdet()
+    assert abs(M.trace_inverse() - tr_ref) <= 1e-10 * abs(tr_ref)
+    g = M.gcv(hp)
+    want = ref.Model(dz, hp, y).loss(1)
+    assert abs(g["gcv"] - want) <= 1e-9 * abs(want), (g, want)
