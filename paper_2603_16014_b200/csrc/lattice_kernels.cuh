@@ -337,23 +337,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
     //   kept when k2a <= N2/2
     const bool row0 = selfrow && rank == 0;
     const int pbeg = (selfrow ? 0 : rank * (N2 / 2)), pend = row0 ? N2 : pbeg + N2 / 2;
+    const double2 wrow = twiddle(a.tw, uint64_t(rowA), a.m);  // w_n^rowA (real-FFT post-processing)
     const double2* yp = a.yperm;
-    // L2-prefetch this CTA's yhat rows (independent of L1)
-    if (threadIdx.x < 2 * T) {
-        const int t = threadIdx.x >> 1, side = threadIdx.x & 1;
-        const long long r0 = side ? rowB : rowA;
-        const long long lo = side ? (row0 ? 0 : N2 - pend) : pbeg, hi = side ? (row0 ? N2 : N2 - pbeg) : pend;
-        const double2* base = yp + size_t(t) * half + (r0 << l2) + lo;
-        const unsigned bytes = unsigned((hi - lo) * sizeof(double2));
+    // L2 prefetches (cp.async.bulk.prefetch.L2): this CTA's yhat rows (independent of L1), and —
+    // after L1 — the exchange-block rows and yhat rows of the CTA one wave later on this SM
+    // (local row li + 148: clusters launch in blockIdx order), so its load phase hits L2
+    auto bulk_prefetch = [](const void* base, unsigned bytes) {
         for (unsigned off = 0; off < bytes; off += 32768u) {
             const unsigned n = bytes - off < 32768u ? bytes - off : 32768u;
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(reinterpret_cast<const char*>(base) + off),
                          "r"(n)
                          : "memory");
         }
-    }
+    };
+    auto prefetch_yhat = [&](int lrow, int t, int side) {
+        const int q2 = a.rank * a.QP + (lrow >> 1), rk = lrow & 1;
+        const bool self2 = q2 == 0, row02 = self2 && rk == 0;
+        const int r2 = lat_row_of(q2, rk, N1);
+        const long long ra = self2 ? r2 : q2, rb = self2 ? r2 : N1 - q2;
+        const int pb = self2 ? 0 : rk * (N2 / 2), pe = row02 ? N2 : pb + N2 / 2;
+        const long long r0 = side ? rb : ra;
+        const long long lo = side ? (row02 ? 0 : N2 - pe) : pb, hi = side ? (row02 ? N2 : N2 - pb) : pe;
+        bulk_prefetch(yp + size_t(t) * half + (r0 << l2) + lo, unsigned((hi - lo) * sizeof(double2)));
+    };
+    constexpr int WAVE = 148;
+    if (threadIdx.x < 2 * T) prefetch_yhat(li, threadIdx.x >> 1, threadIdx.x & 1);
+    else if (threadIdx.x >= 64 && threadIdx.x < 64 + 2 * T && li + WAVE < a.R)
+        prefetch_yhat(li + WAVE, (threadIdx.x - 64) >> 1, (threadIdx.x - 64) & 1);
     pdl_wait();
     pdl_trigger();
+    if (threadIdx.x >= 32 && threadIdx.x < 32 + a.nrank * V && li + WAVE < a.R) {
+        const int sr = (threadIdx.x - 32) / V, oo = (threadIdx.x - 32) - sr * V;
+        bulk_prefetch(a.Y + size_t(c) * a.V * a.half + xoff(a, sr, oo, li + WAVE, 0),
+                      unsigned(a.WC * sizeof(double2)));
+    }
     double2* const Yc = a.Y + size_t(c) * a.V * a.half;
     for (int e = threadIdx.x; e < (V << l2); e += NT) {
         const int oo = e >> l2, k2 = e & (N2 - 1);
@@ -455,7 +472,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
             continue;
         }
         const bool self = slA == slB;  // k = N'/2 (row 0, k2 = N2/2)
-        const double2 wA = twiddle(a.tw, uint64_t(kA), a.m);  // exp(-2 pi i k / n)
+        // exp(-2 pi i k / n) = w_n^rowA w_{2 N2}^k2a (k = rowA + N1 k2a): a per-CTA factor and one read
+        // of a small (hot) table instead of two reads of the 2^m-level table
+        const double2 wA = cmul(wrow, twiddle(a.tw, uint64_t(k2a), l2 + 1));
         const double2 wB = make_double2(-wA.x, wA.y);          // exp(-2 pi i (N' - k)/n) = -conj(wA)
         double2 HA[P], HB[P];
 #pragma unroll
