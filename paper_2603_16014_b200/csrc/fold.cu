@@ -370,6 +370,37 @@ void fold_selinv_trace(const FoldDims& D, const void* lam, void* z, double* part
     }
 }
 
+// Gradient adjoint on the pattern: M_ab[i] = Z_ab[i] - chat_a[i] conj(chat_b[i mod n_b]), in place
+// over z (M = Lam^-1 - chat chat^H, the same M the equal-n solves form per frequency)
+template <bool CX>
+__global__ void __launch_bounds__(256) k_adjoint(FoldDims D, void* z_v, const void* chat_v) {
+    using S = Sc<CX>;
+    using V = typename S::T;
+    int a = 0, b = 0;
+    for (int q = blockIdx.y;; ++a) {  // pair blockIdx.y -> (a <= b), row by row
+        if (q < D.T - a) {
+            b = a + q;
+            break;
+        }
+        q -= D.T - a;
+    }
+    V* z = static_cast<V*>(z_v) + D.poff[D.pid[a][b]];
+    const V* ca = static_cast<const V*>(chat_v) + D.toff[a];
+    const V* cb = static_cast<const V*>(chat_v) + D.toff[b];
+    const long long H = D.H[a], nb = D.n[b];
+    for (long long i = blockIdx.x * 256ll + threadIdx.x; i < H; i += (long long)gridDim.x * 256)
+        z[i] = S::sub(z[i], S::mulc(ca[i], getv<CX>(cb, nb, i % nb)));
+}
+
+void fold_adjoint(const FoldDims& D, void* z, const void* chat, cudaStream_t s) {
+    ProfScope ps("fold_adjoint", s);
+    long long work = 0;
+    for (int t = 0; t < D.T; ++t) work = work > D.H[t] ? work : D.H[t];
+    dim3 g(blocks_for(work), D.T * (D.T + 1) / 2);
+    if (D.lattice) k_adjoint<true><<<g, 256, 0, s>>>(D, z, chat);
+    else k_adjoint<false><<<g, 256, 0, s>>>(D, z, chat);
+}
+
 // ------------------------------------------------------------------ Gram apply (gram_matvec)
 template <bool CX>
 __global__ void __launch_bounds__(256) k_gram_nat(FoldDims D, const void* lam_v, const void* v_v, void* out_v) {

@@ -55,6 +55,8 @@ void fold_cross_quad(const FoldDims& D, const void* lam, const void* rhs, int nq
 // trace(Lam^-1) by selected inversion on the factor's own pattern: z (tot_pair entries) receives
 // Z = Lam^-1 on that pattern, part[s][blk] the per-stage partial traces
 void fold_selinv_trace(const FoldDims& D, const void* lam, void* z, double* part, int nblk, cudaStream_t s);
+// z <- z - chat chat^H on the pattern (z from fold_selinv_trace, chat natural [tot_task])
+void fold_adjoint(const FoldDims& D, void* z, const void* chat, cudaStream_t s);
 // out = Lam v (unfolded spectrum, natural layout), one right-hand side
 void fold_gram_apply(const FoldDims& D, const void* lam, const void* v, void* out, cudaStream_t s);
 

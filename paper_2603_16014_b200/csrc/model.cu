@@ -1530,23 +1530,6 @@ struct PackedHyper {
 // sits at log 0 = -inf where the reference's difference quotient is not finite (gradient 0); with
 // several non-zero orders the log b_k components use the reference's own central difference.
 double fit_loss(fmtgp_model* M, PackedHyper& P, const std::vector<double>& th, std::vector<double>* grad) {
-    if (grad && !M->equal) {
-        // unequal n: no analytic gradient yet -> the reference's own central
-        // difference on theta (gp_core.cpp:341-351), every evaluation on the device
-        const double f0 = fit_loss(M, P, th, nullptr);
-        grad->assign(th.size(), 0.0);
-        for (size_t i = 0; i < th.size(); ++i) {
-            const double hstep = 1e-4 * std::max(1.0, std::abs(th[i]));
-            std::vector<double> tp = th;
-            tp[i] = th[i] + hstep;
-            const double fp = fit_loss(M, P, tp, nullptr);
-            tp[i] = th[i] - hstep;
-            const double fm = fit_loss(M, P, tp, nullptr);
-            (*grad)[i] = (std::isfinite(fp) && std::isfinite(fm)) ? (fp - fm) / (2.0 * hstep) : 0.0;
-        }
-        P.unpack(th);
-        return f0;
-    }
     P.unpack(th);
     fmtgp_result r{};
     try {

@@ -20,8 +20,8 @@ them onto the C ABI's internal order.  Deliberate differences, all raised loudly
   round-trip exactly; a reference-written document (no generator) raises ``Unsupported``.
 * ``"se-dense"`` (the reference's dense squared-exponential path) is not on the B200 fast path
   (out of scope): ``Unsupported``.
-* ``fit`` with ``loss="gcv"`` and GCV for unequal task sizes: ``Unsupported`` (the library's GCV is
-  equal-n, ``fmtgp_gcv``).
+* ``fit`` with ``loss="gcv"``: ``Unsupported`` (the GPU fit loop optimises the NMLL; the GCV loss
+  itself, equal or unequal n, is ``loss()``).
 """
 from __future__ import annotations
 

@@ -104,8 +104,12 @@ def test_nll_tau_coefficients(ref, Model, kind, m):
 
 
 @pytest.mark.parametrize("kind", [LATTICE, DIGITAL], ids=["lattice", "digital"])
-@pytest.mark.parametrize("m", [[0], [1], [2, 2], [3, 3, 3], [5, 5], [6, 6, 6, 6]], ids=lambda m: "m" + "-".join(map(str, m)))
+@pytest.mark.parametrize("m", [[0], [1], [2, 2], [3, 3, 3], [5, 5], [6, 6, 6, 6],
+                               [5, 3], [3, 2, 1], [6, 4, 4, 2], [9, 7, 5]],
+                         ids=lambda m: "m" + "-".join(map(str, m)))
 def test_gradient_vs_reference_fd(ref, Model, kind, m):
+    """Analytic gradient (equal n: per-frequency M; unequal n: selected inversion of the fold)
+    vs Richardson central differences of the reference NLL."""
     dz, hp, y = instance(kind, m)
     M = Model(dz)
     M.set_y(y)
@@ -120,12 +124,13 @@ def test_gradient_vs_reference_fd(ref, Model, kind, m):
 
 
 @pytest.mark.parametrize("case", [(LATTICE, [6, 6], None), (DIGITAL, [6, 6, 6], (0.0, 0.0, 0.0, 1.0)),
-                                  (DIGITAL, [5, 5], (0.5, 0.2, 0.1, 1.0)), (LATTICE, [6, 4], None)],
-                         ids=["lattice", "digital-order4", "digital-mixed-b", "lattice-unequal"])
+                                  (DIGITAL, [5, 5], (0.5, 0.2, 0.1, 1.0)), (LATTICE, [6, 4], None),
+                                  (DIGITAL, [6, 4, 4], (0.0, 0.0, 0.0, 1.0))],
+                         ids=["lattice", "digital-order4", "digital-mixed-b", "lattice-unequal", "digital-unequal"])
 def test_fit_matches_reference(ref, Model, case):
     """iRprop- fit (gp_core.cpp:317-382): the analytic-gradient loop follows the reference's
     FD-gradient trajectory (the update uses gradient signs only); best-so-far loss trace within
-    the NLL tolerance at every step.  Unequal n uses the reference's own difference quotient."""
+    the NLL tolerance at every step (unequal n: the selected-inversion gradient)."""
     kind, m, b = case
     dz, hp, y = instance(kind, m)
     if b is not None:
