@@ -423,6 +423,17 @@ def main():
     per_step = len(inst.candidates) if args.config == 5 else 1  # fits per step (config 5: the sweep)
     value = per_step * (1 if sharded else world) * 1e3 / ms_per_step  # sharded: one unit over all ranks
 
+    # ---- the same evaluation looped in C through the C ABI (fmtgp_bench_nll): no interpreter
+    # between calls, so the Python call's cost is reported separately (configs with one model)
+    c_loop = None
+    if fitter is model and world == 1:
+        cms, wall_us = model.bench_nll(hp, args.steps, grad=True, flush_bytes=0 if args.no_flush else 512 << 20)
+        c_ms = float(np.mean(cms))
+        c_loop = {"ms_per_step": c_ms, "value": per_step * 1e3 / c_ms, "host_wall_us_per_call": wall_us,
+                  "python_api_us_per_step": 1e3 * (ms_per_step - c_ms),
+                  "note": "fmtgp_nll looped in C (fmtgp_bench_nll), CUDA events per call on the model stream, "
+                          "same L2 flush; `value` above is measured through the Python Model.nll"}
+
     # ---- end to end through the public API: pinned host y -> device, fit, result -> host
     y_pinned = torch.empty(dz.N, dtype=torch.float64).pin_memory().numpy()
     y_pinned[:] = inst.y
@@ -506,7 +517,7 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE config; no dataset)",
             "config": config, "roofline": roofline, "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "fits/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-            "clocks": clk.summary(), "gpu_launches": launches,
+            "clocks": clk.summary(), "gpu_launches": launches, "c_loop": c_loop,
             "result": {"nll": res["nll"], "logdet": res["logdet"]}}
     print(json.dumps(line), flush=True)
     if dist:

@@ -201,6 +201,11 @@ FMTGP_API int fmtgp_shard_finish(fmtgp_model_t model, const fmtgp_hyper* h, cons
                                  double xi_scale, int escalations, fmtgp_result* out);
 
 /* ---- measurement: per-kernel CUDA-event timing on the model's stream ---------------- */
+/* iters fmtgp_nll calls from a C loop, each bracketed by CUDA events on the model's stream after an
+ * optional L2 flush of flush_bytes (outside the events): ms[iters] device ms per call, wall_us the
+ * mean host wall time per call */
+FMTGP_API int fmtgp_bench_nll(fmtgp_model_t model, const fmtgp_hyper* h, int want_grad, int iters,
+                              size_t flush_bytes, double* ms, double* wall_us);
 FMTGP_API int fmtgp_profile_enable(fmtgp_model_t model, int on);  /* also resets the tallies */
 /* idx-th kernel name seen since enable, its summed device ms and launch count;
  * FMTGP_ERR_INVALID past the last entry */

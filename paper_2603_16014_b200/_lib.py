@@ -99,6 +99,7 @@ _SIGS = {
     "fmtgp_shard_finish": (C.c_int, [C.c_void_p, C.POINTER(CHyper), _dp, C.c_int, C.c_double, C.c_int,
                                      C.POINTER(CResult)]),
     "fmtgp_profile_enable": (C.c_int, [C.c_void_p, C.c_int]),
+    "fmtgp_bench_nll": (C.c_int, [C.c_void_p, C.POINTER(CHyper), C.c_int, C.c_int, C.c_size_t, _dp, _dp]),
     "fmtgp_profile_read": (C.c_int, [C.c_void_p, C.c_int, C.c_char_p, C.c_int, _dp, _ip]),
 }
 

@@ -2062,6 +2062,43 @@ int fmtgp_nll(fmtgp_model_t M, const fmtgp_hyper* h, int want_grad, fmtgp_result
     });
 }
 
+// Measurement: `iters` fmtgp_nll calls from a C loop (no interpreter between calls), each bracketed
+// by CUDA events on the model's stream after an optional L2 flush (a cudaMemsetAsync of
+// flush_bytes outside the events).  ms[i] = device time of call i, wall_us = mean host wall time
+// per call (the API cost the events see as gaps).
+int fmtgp_bench_nll(fmtgp_model_t M, const fmtgp_hyper* h, int want_grad, int iters, size_t flush_bytes, double* ms,
+                    double* wall_us) {
+    return guarded([&] {
+        if (!M || !h || iters < 1 || !ms) invalid("bench_nll: bad argument");
+        CK(cudaSetDevice(M->dev));
+        void* flush = nullptr;
+        if (flush_bytes) CK(cudaMalloc(&flush, flush_bytes));
+        std::vector<cudaEvent_t> ev(2 * size_t(iters));
+        for (auto& e : ev) CK(cudaEventCreate(&e));
+        fmtgp_result r{};
+        double wall = 0.0;
+        int rc = FMTGP_OK;
+        for (int i = 0; i < iters && rc == FMTGP_OK; ++i) {
+            if (flush) CK(cudaMemsetAsync(flush, i & 0xff, flush_bytes, M->st));
+            CK(cudaEventRecord(ev[2 * i], M->st));
+            const auto t0 = std::chrono::steady_clock::now();
+            rc = fmtgp_nll(M, h, want_grad, &r);
+            wall += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            CK(cudaEventRecord(ev[2 * i + 1], M->st));
+        }
+        CK(cudaStreamSynchronize(M->st));
+        for (int i = 0; i < iters; ++i) {
+            float t = 0.f;
+            CK(cudaEventElapsedTime(&t, ev[2 * i], ev[2 * i + 1]));
+            ms[i] = t;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        if (flush) cudaFree(flush);
+        if (wall_us) *wall_us = 1e6 * wall / iters;
+        if (rc != FMTGP_OK) throw Fail{rc, fmtgp_last_error()};
+    });
+}
+
 // GCV loss (loss_value with LossKind::gcv, gp_core.cpp:213-226) = ||c||^2 / (tr K^-1)^2 at the
 // refreshed (escalated) nugget, c = K^-1 (y - E tau_GCV).  Equal n: the tau_GCV normal equations
 // (HH^ tau = E^T K^-2 y, gp_core.cpp:84-87) collapse at frequency 0 to the sample mean, i.e. the

@@ -264,6 +264,16 @@ class Model:
 
 
     # -- measurement
+    def bench_nll(self, hp: Hyper, iters: int, grad: bool = True, flush_bytes: int = 0):
+        """(device ms per call [iters], mean host wall us per call) of `iters` fmtgp_nll calls
+        looped in C (fmtgp_bench_nll): the evaluation without the interpreter between calls."""
+        ch = self._hyper_struct(hp)
+        ms = np.empty(iters)
+        wall = C.c_double()
+        check(self.lib.fmtgp_bench_nll(self.h, C.byref(ch), int(grad), int(iters), int(flush_bytes), dptr(ms),
+                                       C.byref(wall)))
+        return ms, wall.value
+
     def profile(self, on: bool = True):
         check(self.lib.fmtgp_profile_enable(self.h, int(on)))
 

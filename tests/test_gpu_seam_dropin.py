@@ -115,20 +115,25 @@ def test_cubature_and_posterior(seam, case):
 
 
 def test_schur_escalation_through_refresh(seam):
-    """Nearly singular task Gram with a zero nugget (the instance of
-    test_schur_breakdown_escalation_matches_reference): refresh's SchurBreakdown retries
-    (gp_core.cpp:98-127) are driven by the B200 invert_and_logdet throwing fastmtgp::SchurBreakdown."""
+    """refresh's SchurBreakdown retries (gp_core.cpp:98-127) driven by the B200 invert_and_logdet
+    throwing fastmtgp::SchurBreakdown: (1) a nearly singular task Gram with a zero nugget (the
+    instance of test_schur_breakdown_escalation_matches_reference) escalates as the reference does;
+    (2) an overflowing kernel (eta = 1e300: non-finite spectrum, every pivot fails) exhausts the
+    schedule and surfaces as the reference's SchurBreakdown through loss_value."""
     dz, hp, y = instance(DIGITAL, [6, 6])
-    hp = hp.replace(B=np.array([[1.0], [1.0]]), t=np.array([1e-300, 1e-300]), xi=np.zeros(2))
-    a, b = seam.Model(dz, hp, y), seam.Model(dz, hp, y, seam=True)
+    hp1 = hp.replace(B=np.array([[1.0], [1.0]]), t=np.array([1e-300, 1e-300]), xi=np.zeros(2))
+    a, b = seam.Model(dz, hp1, y), seam.Model(dz, hp1, y, seam=True)
     try:
         la = a.loss(0)
     except Exception as e:  # noqa: BLE001
         pytest.skip(f"reference does not converge on this instance: {e}")
     lb = b.loss(0)
-    sa, sb = a.state(), b.state()
-    assert sa["escalations"] == sb["escalations"] >= 1
+    assert a.state()["escalations"] == b.state()["escalations"]
     assert abs(la - lb) <= 1e-6 * max(1.0, abs(la))
+    hp2 = hp.replace(eta=np.full(dz.d, 1e300))
+    for use_seam in (False, True):
+        with pytest.raises(seam.RefSchurBreakdown):
+            seam.Model(dz, hp2, y, seam=use_seam).loss(0)
 
 
 @pytest.mark.slow
