@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
     const int S = 2 + a.P;
     double* st_mid = sm;                                 // [nrows][2 + P]
     double* st_dot = sm + ((nrows * S + 1) & ~1);        // [V][nblk][D]
-    {
+    if (a.stage_tail) {
         const double* pm = a.part_mid + size_t(c) * nrows * S;
 #pragma unroll 1
         for (int i = threadIdx.x; i < nrows * S; i += NT) cp_async8(st_mid + i, pm + i);
@@ -422,9 +422,9 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
     t.d = D;
     t.nrows = nrows;
     t.nblk = nblk;
-    t.dstride = D;
-    t.mid = st_mid;
-    t.dot = st_dot;
+    t.dstride = a.stage_tail ? D : MAXD + 1;
+    t.mid = a.stage_tail ? st_mid : a.part_mid + size_t(c) * nrows * S;
+    t.dot = a.stage_tail ? st_dot : a.part_dot + size_t(c) * a.V * nblk * (MAXD + 1);
     t.pair_a = a.pair_a;
     t.pair_b = a.pair_b;
     t.Rpair = a.Rpair + size_t(c) * a.P;
@@ -486,13 +486,19 @@ static void mid_launch(const DigGeo& g, const DigArgs& a, size_t sm, cudaStream_
     })
 }
 
-void dig_fit(const DigGeo& g, const DigArgs& a, cudaStream_t s) {
+void dig_fit(const DigGeo& g, const DigArgs& a_in, cudaStream_t s) {
+    DigArgs a = a_in;
     const int C = 1 << g.lc;
     // K1/K3 dynamic smem: column tile (+ kappa tile); K3's last CTA reuses it to stage partials
     const size_t tile_words = size_t(kbuf_offset(C, padded_len(1 << g.l1))) + (a.kap ? size_t(a.d) << (g.l1 + g.lc) : 0) +
                               (a.cpb > 1 ? size_t(C) * padded_len(1 << g.l1) + 2 : 0);  // K3's second column tile
     const size_t stage_words = ((size_t(1 << g.l1) * (2 + a.P) + 1) & ~size_t(1)) + size_t(a.V) * g.nblk_col * a.d;
-    const size_t sm_col = std::max(tile_words, stage_words) * sizeof(double);
+    // staging the partials for the last CTA's reduction is worth it only while it costs no
+    // occupancy (config 5: 192 KB of partials vs a 99 KB tile -> 1 instead of 2 CTAs per SM)
+    auto ctas = [](size_t words) { return int((227u * 1024u) / std::max<size_t>(words * sizeof(double), 1)); };
+    const bool stage = ctas(std::max(tile_words, stage_words)) >= ctas(tile_words);
+    a.stage_tail = stage ? 1 : 0;
+    const size_t sm_col = (stage ? std::max(tile_words, stage_words) : tile_words) * sizeof(double);
     const dim3 gcol(g.nblk_col, a.V * ((a.nc + a.cpb - 1) / a.cpb));
     FM_D_DISPATCH(a.d, {
         FM_NT_DISPATCH(g.nt_col, {

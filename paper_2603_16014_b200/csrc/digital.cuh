@@ -79,6 +79,7 @@ struct DigArgs {
     int use_hv = 0;           // hyperparameters from hv (candidate 0) instead of the pointers
     DigHyperVals hv;              // candidates per K1/K3 CTA (the kappa tile is read once per CTA)
     int tail = 1;             // 1: last CTA of K3 reduces; 0: separate finalize kernel; 2: same, PDL-launched
+    int stage_tail = 1;       // the last CTA stages the partials in smem (when they fit in the column tile)
 };
 
 // design-time kappa table: kap[o][j][i] = dsi_walsh(z_i ^ off_o[j], b)
