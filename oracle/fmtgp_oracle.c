@@ -464,7 +464,10 @@ static int solve(const Ctx* c, const Inv* iv, const double* y, double* out) {
             lre = fmax(lre, fabs(creal(w[c->off[l] + k])));
             out[c->off[l] + k] = creal(w[c->off[l] + k]);
         }
-        if (lim > 1e-8 * fmax(1.0, lre)) st = fail(1, "solve: abnormal imaginary residue");
+        /* ORC_RESIDUE_GUARD=0 (tests only): keep the real projection where the reference's guard
+         * would throw — BASELINE config 3 at full size, SURVEY.md §8c caveat 1 */
+        const char* g = getenv("ORC_RESIDUE_GUARD");
+        if (lim > 1e-8 * fmax(1.0, lre) && !(g && g[0] == '0')) st = fail(1, "solve: abnormal imaginary residue");
     }
     free(z);
     free(w);

@@ -59,6 +59,8 @@ struct LatArgs {
     const double2* tw;
     int want_grad;
     int distinct;             // pair_ofs is the all-shifts-distinct map (cls_distinct in lattice.cu)
+    int next_pf = 0;          // L2 prefetch of the next wave's rows (bit 0 yhat, bit 1 exchange rows): measured
+                              // slower, and the early lines are evicted before use (+1.2 GB DRAM): off
     // ---- frequency sharding over G ranks (G = 1: one GPU).  Rank g owns the
     // column blocks [g ncb, (g+1) ncb) of L1 / L3 (WC = N2 / G columns) and the row clusters
     // [g QP, (g+1) QP) of L2 (R = 2 QP rows: cluster q = rows {q, N1 - q}, or {0, N1/2} for q = 0).

@@ -362,11 +362,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
     };
     constexpr int WAVE = 148;
     if (threadIdx.x < 2 * T) prefetch_yhat(li, threadIdx.x >> 1, threadIdx.x & 1);
-    else if (threadIdx.x >= 64 && threadIdx.x < 64 + 2 * T && li + WAVE < a.R)
+    else if ((a.next_pf & 1) && threadIdx.x >= 64 && threadIdx.x < 64 + 2 * T && li + WAVE < a.R)
         prefetch_yhat(li + WAVE, (threadIdx.x - 64) >> 1, (threadIdx.x - 64) & 1);
     pdl_wait();
     pdl_trigger();
-    if (threadIdx.x >= 32 && threadIdx.x < 32 + a.nrank * V && li + WAVE < a.R) {
+    if ((a.next_pf & 2) && threadIdx.x >= 32 && threadIdx.x < 32 + a.nrank * V && li + WAVE < a.R) {
         const int sr = (threadIdx.x - 32) / V, oo = (threadIdx.x - 32) - sr * V;
         bulk_prefetch(a.Y + size_t(c) * a.V * a.half + xoff(a, sr, oo, li + WAVE, 0),
                       unsigned(a.WC * sizeof(double2)));

@@ -753,6 +753,7 @@ LatArgs lat_args(fmtgp_model* M, int nc, int si_alpha, bool grad) {
     while ((1 << a.lqp) < a.QP) ++a.lqp;
     a.ncb = lg.nblk_col / a.nrank;
     a.Cbuf = a.Y;
+    if (const char* e = std::getenv("FMTGP_LAT_PF")) a.next_pf = std::atoi(e) & 3;
     return a;
 }
 

@@ -316,3 +316,22 @@ def test_unequal_trace_and_gcv(ref, Model, kind, m):
     g = M.gcv(hp)
     want = ref.Model(dz, hp, y).loss(1)
     assert abs(g["gcv"] - want) <= 1e-9 * abs(want), (g, want)
+
+
+@pytest.mark.slow
+def test_config3_full_size_vs_restated_oracle(port, Model, monkeypatch):
+    """BASELINE config 3 at full size (N = 1 392 640, B4, unequal n) against the plain-C restatement
+    of the reference (Algorithm 1's dense grid, oracle/fmtgp_oracle.c) with its copy of solve's
+    residue guard switched off — the reference itself throws there (SURVEY.md §8c caveat 1).
+    Tolerances: logdet / NLL 1e-8 N; coefficients 10x the measured fp64 floor of two correct
+    implementations at this shape (2.4e-7 norm-wise, SURVEY.md §8c caveat 2)."""
+    monkeypatch.setenv("ORC_RESIDUE_GUARD", "0")
+    inst = configs.make(3)
+    dz, hp, y = inst.design, inst.hyper, inst.y
+    want = port.fit(dz, hp, y)
+    M = Model(dz)
+    M.set_y(y)
+    r = M.nll(hp, grad=False)
+    assert abs(r["logdet"] - want["logdet"]) <= 1e-8 * dz.N
+    assert abs(r["nll"] - want["nll"]) <= 1e-8 * dz.N
+    assert rel(M.coefficients(), want["c"]) <= 2.4e-6
