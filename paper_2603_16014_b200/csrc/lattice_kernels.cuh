@@ -300,7 +300,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
     constexpr auto S = sidx<true>;
     __shared__ double s_coef[P], s_xi[P], s_wR[P];
     __shared__ int s_cls[P];
-    __shared__ double2 s_ostep[16];
+    __shared__ double2 s_ostep[16], s_rstep[16];
     cg::cluster_group cl = cg::this_cluster();
     const int rank = int(cl.block_rank());
     const int q = a.rank * a.QP + (blockIdx.x >> 1), c = blockIdx.y, V = DIST ? P - T + 1 : a.V;
@@ -323,6 +323,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
     } else if (threadIdx.x >= 32 && threadIdx.x < 48) {
         const int u = threadIdx.x - 32;  // four-step step table: w^(row M u), M = N2 / 16
         s_ostep[u] = twiddle(a.tw, (uint64_t(u) << M_log) * uint64_t(row), lt);
+    } else if (threadIdx.x >= 64 && threadIdx.x < 80) {
+        // real-FFT step table: the solve's position pA advances by NT per iteration, i.e. the top
+        // DIF digit by NT / 2^(l2-4), so k2a advances by that much: w_{2 N2}^(u (NT >> (l2-4)))
+        const int u = threadIdx.x - 64;
+        s_rstep[u] = twiddle(a.tw, uint64_t(u) * uint64_t(L2 >= 4 ? (NT >> (L2 - 4)) : 0), l2 + 1);
     }
     // this thread's radix-16 group of stage 0 / the last DIT stage: class gvec, offset gj1
     const bool has_g = int(threadIdx.x) < (V << M_log);
@@ -337,7 +342,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
     //   kept when k2a <= N2/2
     const bool row0 = selfrow && rank == 0;
     const int pbeg = (selfrow ? 0 : rank * (N2 / 2)), pend = row0 ? N2 : pbeg + N2 / 2;
-    const double2 wrow = twiddle(a.tw, uint64_t(rowA), a.m);  // w_n^rowA (real-FFT post-processing)
+    // real-FFT post-processing twiddle exp(-2 pi i k / n), k = rowA + N1 k2a: w_n^rowA w_{2N2}^k2a =
+    // (per-thread base at the first position) x (per-CTA step table, s_rstep): no table walk per slot
+    const double2 wrow = cmul(twiddle(a.tw, uint64_t(rowA), a.m),
+                              twiddle(a.tw, uint64_t(IP::freq(pbeg + int(threadIdx.x)) & (N2 - 1)), l2 + 1));
     const double2* yp = a.yperm;
     // L2 prefetches (cp.async.bulk.prefetch.L2): this CTA's yhat rows (independent of L1), and —
     // after L1 — the exchange-block rows and yhat rows of the CTA one wave later on this SM
@@ -415,7 +423,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
         return N2 - 1 - pA;
     };
 #pragma unroll 1
-    for (int pA = pbeg + int(threadIdx.x); pA < pend; pA += NT) {
+    for (int pA = pbeg + int(threadIdx.x), it = 0; pA < pend; pA += NT, ++it) {
         const int k2a = IP::freq(pA);
         if (row0 && k2a > N2 / 2) continue;  // its partner's thread owns the pair
         int k2b;
@@ -472,9 +480,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
             continue;
         }
         const bool self = slA == slB;  // k = N'/2 (row 0, k2 = N2/2)
-        // exp(-2 pi i k / n) = w_n^rowA w_{2 N2}^k2a (k = rowA + N1 k2a): a per-CTA factor and one read
-        // of a small (hot) table instead of two reads of the 2^m-level table
-        const double2 wA = cmul(wrow, twiddle(a.tw, uint64_t(k2a), l2 + 1));
+        const double2 wA = cmul(wrow, s_rstep[it]);  // exp(-2 pi i k / n), k = rowA + N1 k2a
         const double2 wB = make_double2(-wA.x, wA.y);          // exp(-2 pi i (N' - k)/n) = -conj(wA)
         double2 HA[P], HB[P];
 #pragma unroll
