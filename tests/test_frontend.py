@@ -88,3 +88,31 @@ def test_fit_and_json_round_trip():
     m2 = fastmtgp.Model.from_json(doc)
     assert m2.loss() == pytest.approx(m.loss(), rel=1e-13)
     assert json.loads(m2.to_json()) == json.loads(doc)
+
+
+def test_cli_points(tmp_path):
+    from paper_2603_16014_b200 import cli
+    out = tmp_path / "pts.csv"
+    assert cli.main(["points", "--kernel", "si-lattice", "--n", "16,4", "--d", "3", "--seed", "5", "--out", str(out)]) == 0
+    rows = out.read_text().strip().splitlines()
+    assert rows[0] == "task,index,x1,x2,x3" and len(rows) == 1 + 16 + 4
+    pts = fastmtgp.design_points("lattice", 3, [16, 4], 5)
+    first = [float(v) for v in rows[1].split(",")[2:]]
+    assert first == list(pts[0][0])
+
+
+@pytest.mark.gpu
+def test_cli_fit_and_cubature(tmp_path):
+    from paper_2603_16014_b200 import cli
+    rng = np.random.default_rng(4)
+    n = [64, 32]
+    m = fastmtgp.Model("dsi-digital", 2, n, seed=9, y=[rng.standard_normal(v) for v in n])
+    doc = tmp_path / "m.json"
+    doc.write_text(m.to_json())
+    rep, cub, fitted = tmp_path / "rep.json", tmp_path / "cub.json", tmp_path / "fitted.json"
+    assert cli.main(["fit", "--model", str(doc), "--steps", "3", "--model-out", str(fitted), "--out", str(rep)]) == 0
+    r = json.loads(rep.read_text())
+    assert len(r["loss_trace"]) == 3 and r["loss"] <= r["loss_trace"][0] + 1e-9 * abs(r["loss_trace"][0])
+    assert cli.main(["cubature", "--model", str(fitted), "--out", str(cub)]) == 0
+    c = json.loads(cub.read_text())
+    assert len(c["mu"]) == 2 and len(c["Sigma"]) == 2
