@@ -253,6 +253,8 @@ struct fmtgp_model {
     double* h_tau_raw = nullptr;
     bool tau_pending = false;
     cudaEvent_t ev_h2d = nullptr;
+    cudaStream_t st_copy = nullptr;     // set_y: per-task H2D copies overlapped with the transforms
+    cudaEvent_t ev_set = nullptr, ev_task[MAXT] = {};
 
     // state of the last spectrum / fit (candidate 0)
     bool have_spec = false, have_inv = false, have_fit = false;
@@ -506,9 +508,43 @@ void inverse_vector(fmtgp_model* M, const void* dslots, double* dvec) {
     CK(cudaGetLastError());
 }
 
+void compute_tau(fmtgp_model* M);
+
 void compute_yhat_tau(fmtgp_model* M) {
     forward_vector(M, M->d_y, M->d_yhat);
     if (M->lat) lat_perm_yhat(M->lgeo, M->T, M->pslots[0], M->d_yhat, M->d_yperm, M->st);
+    compute_tau(M);
+}
+
+// set_y from host memory with the upload pipelined against the transform: task t's copy runs on
+// the copy stream, its transform (and the fused path's yhat permutation) on the model stream as
+// soon as that copy has landed, so the next task's H2D overlaps the previous task's transform
+void upload_yhat_tau(fmtgp_model* M, const double* y) {
+    CK(cudaEventRecord(M->ev_set, M->st));
+    CK(cudaStreamWaitEvent(M->st_copy, M->ev_set, 0));
+    for (int t = 0; t < M->T; ++t) {
+        CK(cudaMemcpyAsync(M->d_y + M->off[t], y + M->off[t], sizeof(double) * M->n[t], cudaMemcpyHostToDevice,
+                           M->st_copy));
+        CK(cudaEventRecord(M->ev_task[t], M->st_copy));
+    }
+    CK(cudaEventRecord(M->ev_h2d, M->st_copy));
+    const size_t es = elem_size(M);
+    for (auto& tg : M->tgroups)
+        for (size_t i = 0; i < tg.tasks.size(); ++i) {
+            const int t = tg.tasks[i];
+            CK(cudaStreamWaitEvent(M->st, M->ev_task[t], 0));
+            ArraySrc src{M->d_y, tg.d_yoff + i, tg.m, M->lattice};
+            ScaleSink snk{M->d_yhat, tg.d_soff + i, 1.0 / std::sqrt(double(1ll << tg.m))};
+            fwd_array(M->lattice, tg.geo, 1, src, snk, M->d_work, M->tw, M->st);
+            if (M->lat)
+                lat_perm_yhat(M->lgeo, 1, M->pslots[0], static_cast<char*>(M->d_yhat) + M->toff_slots[t] * es,
+                              static_cast<char*>(M->d_yperm) + M->toff_slots[t] * es, M->st);
+        }
+    CK(cudaGetLastError());
+    compute_tau(M);
+}
+
+void compute_tau(fmtgp_model* M) {
     // tau: equal n -> tau_l = yhat_l(0) / sqrt(n) (the sample mean, gp_core.cpp:67-88 with
     // V̄ 1 = sqrt(n) e_0); unequal n -> class-0 normal equations at fit time.
     if (M->equal) {
@@ -1409,6 +1445,9 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
         M->d_tau_raw = M->d_res + size_t(max_cand) * (NOUT + 1 + 2 * MAXT);
         M->h_tau_raw = M->h_res + size_t(max_cand) * (NOUT + 1 + 2 * MAXT);
         CK(cudaEventCreateWithFlags(&M->ev_h2d, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&M->ev_set, cudaEventDisableTiming));
+        for (int t = 0; t < M->T; ++t) CK(cudaEventCreateWithFlags(&M->ev_task[t], cudaEventDisableTiming));
+        CK(cudaStreamCreateWithFlags(&M->st_copy, cudaStreamNonBlocking));
         M->d_out = M->d_res;
         M->d_bad = reinterpret_cast<int*>(M->d_res + size_t(max_cand) * NOUT);
         M->d_imre = reinterpret_cast<unsigned long long*>(M->d_res + size_t(max_cand) * (NOUT + 1));
@@ -1710,6 +1749,10 @@ int fmtgp_model_destroy(fmtgp_model_t M) {
     F(M->d_res);
     if (M->h_res) cudaFreeHost(M->h_res);
     if (M->ev_h2d) cudaEventDestroy(M->ev_h2d);
+    if (M->ev_set) cudaEventDestroy(M->ev_set);
+    for (int t = 0; t < MAXT; ++t)
+        if (M->ev_task[t]) cudaEventDestroy(M->ev_task[t]);
+    if (M->st_copy) cudaStreamDestroy(M->st_copy);
     F(M->d_vecA);
     F(M->d_vecB);
     F(M->d_sA);
@@ -1728,10 +1771,15 @@ int fmtgp_model_set_y(fmtgp_model_t M, const double* y) {
         ProfGuard pg_(M);
         if (!M || !y) invalid("set_y: null argument");
         CK(cudaSetDevice(M->dev));
-        // (splitting this copy over several copy engines measured slower at these sizes)
-        CK(cudaMemcpyAsync(M->d_y, y, sizeof(double) * M->N, cudaMemcpyHostToDevice, M->st));
-        CK(cudaEventRecord(M->ev_h2d, M->st));
-        compute_yhat_tau(M);
+        // (splitting one copy over several copy engines measured slower at these sizes; the per-task
+        // pipeline overlaps the transforms instead)
+        if (M->T > 1 && M->N >= (1ll << 20)) {
+            upload_yhat_tau(M, y);
+        } else {
+            CK(cudaMemcpyAsync(M->d_y, y, sizeof(double) * M->N, cudaMemcpyHostToDevice, M->st));
+            CK(cudaEventRecord(M->ev_h2d, M->st));
+            compute_yhat_tau(M);
+        }
         // the caller may reuse y on return: wait for the copy only (the transform runs on)
         CK(cudaEventSynchronize(M->ev_h2d));
         M->have_fit = false;
