@@ -106,6 +106,12 @@ FMTGP_API int fmtgp_model_destroy(fmtgp_model_t model);
 FMTGP_API int fmtgp_model_set_y(fmtgp_model_t model, const double* y);
 /* same from a device pointer (no host round trip) */
 FMTGP_API int fmtgp_model_set_y_device(fmtgp_model_t model, const double* y_dev);
+/* benchmark observations on the device (bench.cpp:84-101, problems.cpp): y = problem(level
+ * user_of_internal[l] + 1, x_{l,i}) + noise * N(0,1) (rng::normal(seed, 0x401 + user, i)) at the
+ * model's own design points, then the same yhat / tau as set_y.  problem: "rosenbrock" (d 2, 3
+ * fidelities), "ackley" (4, 2), "borehole" (8, 2), "elliptic" (16, 3).  y_host [N] optional. */
+FMTGP_API int fmtgp_model_problem_y(fmtgp_model_t model, const char* problem, const int* user_of_internal,
+                                    double noise, uint64_t seed, double* y_host);
 /* stream the model's work is ordered on (cudaStream_t as void*) */
 FMTGP_API void* fmtgp_model_stream(fmtgp_model_t model);
 

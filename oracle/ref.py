@@ -82,6 +82,7 @@ def _load(path):
         L.ref_build_spectrum.argtypes = [P, D, dp, dp]
         L.ref_invert_solve.argtypes = [P, D, dp, dp, dp, dp, dp, dp]
         L.ref_pi_h.argtypes = [P, D, dp, dp, dp]
+        L.ref_problem_y.argtypes = [P, C.c_char_p, C.POINTER(C.c_int), C.c_double, C.c_uint64, dp]
         L.ref_model_create.restype = C.c_void_p
         L.ref_model_create.argtypes = [P, D, dp]
         L.ref_model_free.argtypes = [C.c_void_p]
@@ -149,6 +150,15 @@ def build_spectrum(dz: Design, hp: Hyper, seam: bool = False):
         out.append(re[o:o + n] + 1j * im[o:o + n])
         o += n
     return out
+
+
+def problem_y(dz: Design, name: str, users, noise: float, seed: int) -> np.ndarray:
+    """Benchmark observations as the reference's bench makes them (bench.cpp:84-101)."""
+    cd, k1 = make_cdesign(dz)
+    u = (C.c_int * dz.L)(*[int(v) for v in users])
+    y = np.empty(dz.N)
+    _check(lib().ref_problem_y(C.byref(cd), name.encode(), u, float(noise), int(seed), dptr(y)))
+    return y
 
 
 def pi_h(dz: Design, hp: Hyper, seam: bool = False):

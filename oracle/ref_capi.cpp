@@ -24,6 +24,7 @@
 #include "fastmtgp/gp_core.hpp"
 #include "fastmtgp/kernels.hpp"
 #include "fastmtgp/ld_sequences.hpp"
+#include "fastmtgp/problems.hpp"
 #include "fastmtgp/rng.hpp"
 #include "fastmtgp/transforms.hpp"
 
@@ -32,6 +33,7 @@
 namespace fastmtgp::embedded {
 extern const char* const lattice_table = "";
 extern const char* const sobol_table = "";
+extern const char* const reference_json = "{}";  // problems.cpp's integral table (not used here)
 }  // namespace fastmtgp::embedded
 
 using namespace fastmtgp;
@@ -255,6 +257,28 @@ int ref_pi_h(const RefDesign* rd, const RefHyper* rh, double* Pi, double* H_re, 
                 H_im[l * inv.r + k] = ph.H(l, static_cast<Eigen::Index>(k)).imag();
             }
         }
+    });
+}
+
+// Benchmark observations as bench.cpp:84-101 makes them: problem(level user + 1, x) + noise *
+// rng::normal(seed, 0x401 + user, i) at the design points (internal order, users[l] = user task of l).
+int ref_problem_y(const RefDesign* rd, const char* name, const int* users, double noise, std::uint64_t seed,
+                  double* y) {
+    return guarded([&] {
+        LdDesign dz = make_ld(*rd);
+        const std::string nm(name);
+        double (*f)(int, const double*) = nm == "rosenbrock" ? &rosenbrock
+                                          : nm == "ackley"   ? &ackley
+                                          : nm == "borehole" ? &borehole
+                                          : nm == "elliptic" ? &elliptic_pde
+                                                             : nullptr;
+        if (!f) throw FastMtgpError("unknown problem " + nm);
+        for (int l = 0; l < dz.L; ++l)
+            for (std::size_t i = 0; i < dz.n[l]; ++i) {
+                double v = f(users[l] + 1, dz.point(l, i));
+                if (noise > 0.0) v += noise * rng::normal(seed, 0x401 + static_cast<std::uint64_t>(users[l]), i);
+                y[dz.offset[l] + i] = v;
+            }
     });
 }
 

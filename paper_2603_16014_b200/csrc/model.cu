@@ -24,6 +24,7 @@
 #include "digital.cuh"
 #include "lattice.cuh"
 #include "fold.cuh"
+#include "problems.cuh"
 #include "posterior.cuh"
 #include "unequal.cuh"
 
@@ -1782,6 +1783,44 @@ int fmtgp_model_set_y(fmtgp_model_t M, const double* y) {
         }
         // the caller may reuse y on return: wait for the copy only (the transform runs on)
         CK(cudaEventSynchronize(M->ev_h2d));
+        M->have_fit = false;
+        M->fit_lazy = false;
+    });
+}
+
+// Benchmark observations on the device (bench.cpp:84-101 with problems.cpp): y = problem at the
+// design points (level user + 1) + noise; then the same yhat / tau as set_y.  y_host optional.
+int fmtgp_model_problem_y(fmtgp_model_t M, const char* problem, const int* user_of_internal, double noise,
+                          uint64_t seed, double* y_host) {
+    return guarded([&] {
+        ProfGuard pg_(M);
+        if (!M || !problem || !user_of_internal) invalid("problem_y: null argument");
+        int pd_d = 0, levels = 0;
+        const int k = problem_index(problem, &pd_d, &levels);
+        if (k < 0) invalid(std::string("problem_y: unknown problem ") + problem);
+        if (pd_d != M->d) invalid("problem_y: the problem's dimension differs from the design's");
+        for (int l = 0; l < M->T; ++l)
+            if (user_of_internal[l] < 0 || user_of_internal[l] >= levels)
+                invalid("problem_y: more tasks than the problem has fidelities");
+        CK(cudaSetDevice(M->dev));
+        ProblemDesign pd{};
+        pd.d = M->d;
+        pd.T = M->T;
+        pd.lattice = M->lattice ? 1 : 0;
+        pd.mgen = M->mgen;
+        pd.m_cols = M->m_cols;
+        pd.n_max = M->n_max;
+        pd.g = M->d_g;
+        pd.cols = M->d_cols;
+        pd.shifts = M->d_shifts;
+        for (int l = 0; l <= M->T; ++l) pd.off[l] = M->off[l];
+        problem_y(k, pd, user_of_internal, noise, seed, M->d_y, M->st);
+        CK(cudaGetLastError());
+        compute_yhat_tau(M);
+        if (y_host) {
+            CK(cudaMemcpyAsync(y_host, M->d_y, sizeof(double) * M->N, cudaMemcpyDeviceToHost, M->st));
+            CK(cudaStreamSynchronize(M->st));
+        }
         M->have_fit = false;
         M->fit_lazy = false;
     });

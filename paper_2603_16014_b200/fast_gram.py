@@ -154,6 +154,15 @@ class Model:
         check(self.lib.fmtgp_extract_pi(self.h, dptr(Pi)))
         return Pi
 
+    def problem_y(self, name: str, user_of_internal, noise: float = 0.0, seed: int = 0) -> np.ndarray:
+        """Benchmark observations computed on the device at this design's points (bench.cpp:84-101:
+        level user + 1, noise * rng::normal(seed, 0x401 + user, i)); sets them as y and returns them."""
+        u = np.ascontiguousarray(user_of_internal, dtype=np.int32)
+        y = np.empty(self.design.N)
+        check(self.lib.fmtgp_model_problem_y(self.h, name.encode(), u.ctypes.data_as(C.POINTER(C.c_int)),
+                                             float(noise), int(seed), dptr(y)))
+        return y
+
     def extract_pi_h(self):
         """(Pi [L, L], H [L, r] complex) of extract_pi_h (fast_gram.cpp:311-335), r = N / n_{L-1}."""
         L = self.design.L

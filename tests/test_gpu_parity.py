@@ -335,3 +335,22 @@ def test_config3_full_size_vs_restated_oracle(port, Model, monkeypatch):
     assert abs(r["logdet"] - want["logdet"]) <= 1e-8 * dz.N
     assert abs(r["nll"] - want["nll"]) <= 1e-8 * dz.N
     assert rel(M.coefficients(), want["c"]) <= 2.4e-6
+
+
+@pytest.mark.parametrize("name,d,L", [("rosenbrock", 2, 3), ("ackley", 4, 2), ("borehole", 8, 2), ("elliptic", 16, 3)])
+@pytest.mark.parametrize("kind", [LATTICE, DIGITAL], ids=["lattice", "digital"])
+def test_problem_observations_on_device(ref, Model, name, d, L, kind):
+    """Benchmark observations (bench.cpp:84-101 with problems.cpp) computed on the device at the
+    design points vs the reference's own functions at its materialised points; the model then fits
+    them (NLL vs the reference on the same y)."""
+    m = [7, 6, 5][:L]
+    dz = (lattice_design if kind == LATTICE else digital_design)(d, m, seed=21)
+    users = list(range(L))[::-1]  # internal l <- user task L-1-l
+    M = Model(dz)
+    y = M.problem_y(name, users, noise=1e-3, seed=5)
+    want = ref.problem_y(dz, name, users, 1e-3, 5)
+    assert np.abs(y - want).max() <= 1e-12 * max(1.0, np.abs(want).max())
+    hp = Hyper(gamma=1.0, eta=np.full(d, 0.5), B=np.full((L, 1), 0.3), t=np.full(L, 0.2), xi=np.full(L, 1e-6),
+               b=(0.0, 0.0, 0.0, 1.0))
+    r = M.nll(hp, grad=False)
+    assert abs(r["nll"] - ref.Model(dz, hp, want).loss(0)) <= max(1e-8 * dz.N, 1e-9 * abs(r["nll"]))
