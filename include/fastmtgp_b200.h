@@ -112,6 +112,11 @@ FMTGP_API int fmtgp_model_set_y_device(fmtgp_model_t model, const double* y_dev)
  * fidelities), "ackley" (4, 2), "borehole" (8, 2), "elliptic" (16, 3).  y_host [N] optional. */
 FMTGP_API int fmtgp_model_problem_y(fmtgp_model_t model, const char* problem, const int* user_of_internal,
                                     double noise, uint64_t seed, double* y_host);
+/* the same problems at arbitrary points, on the device (eval_batch, problems.cpp:145-154): out[i] =
+ * problem(level, X[i*d .. i*d+d-1]); X host [count][d] with the problem's d, out host [count].
+ * The held-out truth of the benchmark's l2 error (bench.cpp:159-170). */
+FMTGP_API int fmtgp_problem_eval(const char* problem, int level, const double* X, uint64_t count, double* out,
+                                 int device);
 /* stream the model's work is ordered on (cudaStream_t as void*) */
 FMTGP_API void* fmtgp_model_stream(fmtgp_model_t model);
 

@@ -83,6 +83,7 @@ def _load(path):
         L.ref_invert_solve.argtypes = [P, D, dp, dp, dp, dp, dp, dp]
         L.ref_pi_h.argtypes = [P, D, dp, dp, dp]
         L.ref_problem_y.argtypes = [P, C.c_char_p, C.POINTER(C.c_int), C.c_double, C.c_uint64, dp]
+        L.ref_problem_eval.argtypes = [C.c_char_p, C.c_int, C.c_int, dp, C.c_size_t, dp]
         L.ref_model_create.restype = C.c_void_p
         L.ref_model_create.argtypes = [P, D, dp]
         L.ref_model_free.argtypes = [C.c_void_p]
@@ -159,6 +160,14 @@ def problem_y(dz: Design, name: str, users, noise: float, seed: int) -> np.ndarr
     y = np.empty(dz.N)
     _check(lib().ref_problem_y(C.byref(cd), name.encode(), u, float(noise), int(seed), dptr(y)))
     return y
+
+
+def problem_eval(name: str, level: int, X: np.ndarray) -> np.ndarray:
+    """The reference's problem functions at the rows of X (problems.cpp)."""
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    out = np.empty(X.shape[0])
+    _check(lib().ref_problem_eval(name.encode(), int(level), X.shape[1], dptr(X), X.shape[0], dptr(out)))
+    return out
 
 
 def pi_h(dz: Design, hp: Hyper, seam: bool = False):

@@ -260,6 +260,24 @@ int ref_pi_h(const RefDesign* rd, const RefHyper* rh, double* Pi, double* H_re, 
     });
 }
 
+static double (*problem_fn(const std::string& nm))(int, const double*) {
+    double (*f)(int, const double*) = nm == "rosenbrock" ? &rosenbrock
+                                      : nm == "ackley"   ? &ackley
+                                      : nm == "borehole" ? &borehole
+                                      : nm == "elliptic" ? &elliptic_pde
+                                                         : nullptr;
+    if (!f) throw FastMtgpError("unknown problem " + nm);
+    return f;
+}
+
+// problem(level, X[i]) at arbitrary points (eval_batch's loop, problems.cpp), X [count][d]
+int ref_problem_eval(const char* name, int level, int d, const double* X, std::size_t count, double* out) {
+    return guarded([&] {
+        double (*f)(int, const double*) = problem_fn(name);
+        for (std::size_t i = 0; i < count; ++i) out[i] = f(level, X + i * static_cast<std::size_t>(d));
+    });
+}
+
 // Benchmark observations as bench.cpp:84-101 makes them: problem(level user + 1, x) + noise *
 // rng::normal(seed, 0x401 + user, i) at the design points (internal order, users[l] = user task of l).
 int ref_problem_y(const RefDesign* rd, const char* name, const int* users, double noise, std::uint64_t seed,
@@ -267,12 +285,7 @@ int ref_problem_y(const RefDesign* rd, const char* name, const int* users, doubl
     return guarded([&] {
         LdDesign dz = make_ld(*rd);
         const std::string nm(name);
-        double (*f)(int, const double*) = nm == "rosenbrock" ? &rosenbrock
-                                          : nm == "ackley"   ? &ackley
-                                          : nm == "borehole" ? &borehole
-                                          : nm == "elliptic" ? &elliptic_pde
-                                                             : nullptr;
-        if (!f) throw FastMtgpError("unknown problem " + nm);
+        double (*f)(int, const double*) = problem_fn(nm);
         for (int l = 0; l < dz.L; ++l)
             for (std::size_t i = 0; i < dz.n[l]; ++i) {
                 double v = f(users[l] + 1, dz.point(l, i));

@@ -73,6 +73,7 @@ _SIGS = {
     "fmtgp_model_set_y": (C.c_int, [C.c_void_p, _dp]),
     "fmtgp_model_set_y_device": (C.c_int, [C.c_void_p, C.c_void_p]),
     "fmtgp_model_problem_y": (C.c_int, [C.c_void_p, C.c_char_p, _ip, C.c_double, C.c_uint64, _dp]),
+    "fmtgp_problem_eval": (C.c_int, [C.c_char_p, C.c_int, _dp, C.c_uint64, _dp, C.c_int]),
     "fmtgp_model_stream": (C.c_void_p, [C.c_void_p]),
     "fmtgp_build_spectrum": (C.c_int, [C.c_void_p, C.POINTER(CHyper)]),
     "fmtgp_spectrum_read": (C.c_int, [C.c_void_p, C.c_int, C.c_int, _dp, _dp]),

@@ -1826,6 +1826,34 @@ int fmtgp_model_problem_y(fmtgp_model_t M, const char* problem, const int* user_
     });
 }
 
+int fmtgp_problem_eval(const char* problem, int level, const double* X, uint64_t count, double* out, int device) {
+    return guarded([&] {
+        if (!problem || (count && (!X || !out))) invalid("problem_eval: null argument");
+        int pd_d = 0, levels = 0;
+        const int k = problem_index(problem, &pd_d, &levels);
+        if (k < 0) invalid(std::string("problem_eval: unknown problem ") + problem);
+        if (level < 1 || level > levels) invalid("problem_eval: level out of range");
+        if (count == 0) return;
+        CK(cudaSetDevice(device));
+        cudaStream_t s;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        double* d_buf = nullptr;
+        const size_t nx = size_t(count) * pd_d;
+        cudaError_t e = cudaMallocAsync(&d_buf, sizeof(double) * (nx + count), s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d_buf, X, sizeof(double) * nx, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) {
+            problem_eval(k, level, pd_d, d_buf, count, d_buf + nx, s);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaMemcpyAsync(out, d_buf + nx, sizeof(double) * count, cudaMemcpyDeviceToHost, s);
+        if (d_buf) cudaFreeAsync(d_buf, s);
+        const cudaError_t e2 = cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+        CK(e);
+        CK(e2);
+    });
+}
+
 int fmtgp_model_set_y_device(fmtgp_model_t M, const double* y) {
     return guarded([&] {
         ProfGuard pg_(M);

@@ -21,5 +21,7 @@ int problem_index(const char* name, int* d, int* levels);
 // rng::normal(seed, 0x401 + user[l], i)
 void problem_y(int problem, const ProblemDesign& pd, const int* user, double noise, uint64_t seed, double* y,
                cudaStream_t s);
+// out[i] (device) = problem(level, X[i*d ..]) for X device [count][d] (eval_batch, problems.cpp:145-154)
+void problem_eval(int problem, int level, int d, const double* X, uint64_t count, double* out, cudaStream_t s);
 
 }  // namespace fmtgp

@@ -326,3 +326,18 @@ def trace_inverse(model: Model) -> float:
 
 def gram_matvec(model: Model, y: np.ndarray) -> np.ndarray:
     return model.gram_matvec(y)
+
+
+# ---- benchmark problems (problems.cpp) on the device ---------------------------------------
+
+PROBLEMS = {"rosenbrock": (2, 3), "ackley": (4, 2), "borehole": (8, 2), "elliptic": (16, 3)}  # name: (d, levels)
+
+
+def problem_eval(name: str, level: int, X, device: int = 0) -> np.ndarray:
+    """problem(level, x) at each row of X (eval_batch, problems.cpp:145-154), evaluated on the device."""
+    if name not in PROBLEMS:
+        raise FastMtgpError(f"unknown problem {name}")
+    X = np.ascontiguousarray(X, dtype=np.float64).reshape(-1, PROBLEMS[name][0])
+    out = np.empty(X.shape[0])
+    check(_lib.load().fmtgp_problem_eval(name.encode(), int(level), dptr(X), X.shape[0], dptr(out), int(device)))
+    return out

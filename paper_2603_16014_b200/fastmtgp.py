@@ -3,10 +3,12 @@
 I/O of gp_core.cpp:447-508 (``to_json`` / ``from_json``).
 
     m = Model("si-lattice", d=4, n=[2**18, 2**16], seed=7, y=[y0, y1], loss="nmll", task_rank=1)
+    m = Model.from_problem("ackley", "si-lattice", n=[2**18, 2**16], seed=7, noise=0.01)  # bench.cpp fit_trial
     rep = m.fit(10)              # iRprop- (gp_core.cpp:317-382) with the analytic gradient
     m.loss(); m.tau()            # loss_value / optimal_tau
     m.posterior_mean(0, x); m.posterior_mean_batch(1, X); m.posterior_cov(0, x, 1, xp)
     mu, Sigma = m.cubature()     # multitask_cubature (single-task formula when L = 1)
+    m.l2_relative_error(u, X)    # held-out error against the problem (bench.cpp:159-170)
     doc = m.to_json(); m2 = Model.from_json(doc)
 
 Task indices are USER indices (the reference's make_design sorts tasks by descending size and
@@ -33,10 +35,12 @@ import numpy as np
 from . import designs as dz_mod
 from ._lib import Unsupported
 from .designs import DIGITAL, LATTICE, Design, Hyper
+from .fast_gram import PROBLEMS, problem_eval
 from .fast_gram import Model as _GpuModel
 
 KERNELS = {"si-lattice": LATTICE, "dsi-digital": DIGITAL}
 _INIT_STREAM = 0xB011  # init_hyperparams' B stream (gp_core.cpp:169-185)
+_TEST_STREAM = 0x7E57  # the benchmark's held-out set (bench.cpp:22, 155-157)
 
 
 def _log2_exact(n: int) -> int:
@@ -78,6 +82,21 @@ def design_points(kind: str, d: int, n: Sequence[int], seed: int = 0) -> List[np
     return out  # type: ignore[return-value]
 
 
+def test_points(kernel: str, d: int, count: int, seed: int) -> np.ndarray:
+    """The benchmark's held-out set (bench.cpp:155-157: shifted_points(kind, d, 0, count, seed,
+    0x7E57)): the first `count` points of this module's generator for `seed` (count a power of two,
+    at most the lattice's n_max) under the test-stream shift; count x d."""
+    kind = KERNELS[kernel]
+    m = _log2_exact(count)
+    design, _ = make_design(kind, d, [m], seed)
+    shifts = dz_mod.bits53(seed, _TEST_STREAM, np.arange(d)).reshape(1, d)
+    if kind == LATTICE:
+        t = Design(LATTICE, d, [m], shifts, g=design.g, n_max=design.n_max)
+    else:
+        t = Design(DIGITAL, d, [m], shifts, columns=design.columns)
+    return t.points(0)
+
+
 def optimal_weights(mu, Sigma, chi):
     """Task combination weights minimising the posterior MSE and that MSE (cubature.cpp:76-85)."""
     mu, Sigma, chi = (np.asarray(a, dtype=np.float64) for a in (mu, Sigma, chi))
@@ -111,7 +130,7 @@ class Model:
         for u in range(L):
             if self.y_user[u].size != (1 << m_user[u]):
                 raise ValueError("make_model: observation size mismatch")
-        if _state is not None:
+        if _state is not None and "hyper" in _state:
             self.hyper = _state["hyper"]
         else:  # init_hyperparams (gp_core.cpp:169-185), user order
             y_all = np.concatenate(self.y_user)
@@ -120,9 +139,48 @@ class Model:
                            for k in range(s)] for u in range(L)]).reshape(L, s)
             self.hyper = Hyper(gamma=max(float(np.var(y_all)), 1e-12), eta=np.ones(d), B=B, t=np.full(L, 0.1),
                                xi=np.full(L, float(jitter)), si_alpha=1, b=(1.0, 1.0, 1.0, 1.0))
-        self.gpu = _GpuModel(self.design, device=device)
-        self.gpu.set_y(np.concatenate([self.y_user[u] for u in self.i2u]))
+        if _state is not None and "gpu" in _state:
+            self.gpu = _state["gpu"]  # observations already on the device (from_problem)
+        else:
+            self.gpu = _GpuModel(self.design, device=device)
+            self.gpu.set_y(np.concatenate([self.y_user[u] for u in self.i2u]))
         self._fresh = None
+
+    @staticmethod
+    def from_problem(problem: str, kernel: str, n: Sequence[int], seed: int = 0, noise: float = 0.0,
+                     loss: str = "nmll", task_rank: int = 1, jitter: float = 1e-8, device: int = 0) -> "Model":
+        """fit_trial's model (bench.cpp:84-107): the design for `seed`, observations of the problem's
+        fidelity u + 1 for user task u plus noise * N(0, 1) (stream 0x401 + u) computed ON THE
+        DEVICE at the design points (fmtgp_model_problem_y), init_hyperparams from them."""
+        if problem not in PROBLEMS:
+            raise ValueError(f"unknown problem {problem}")
+        if kernel not in KERNELS:
+            raise Unsupported(f"{kernel}: not on the B200 fast path") if kernel == "se-dense" else ValueError(kernel)
+        d, levels = PROBLEMS[problem]
+        m_user = [_log2_exact(v) for v in n]
+        if len(m_user) > levels:
+            raise ValueError("more tasks requested than the problem has fidelities")
+        design, i2u = make_design(KERNELS[kernel], d, m_user, seed)
+        gpu = _GpuModel(design, device=device)
+        y_int = gpu.problem_y(problem, i2u, noise, seed)
+        y_user: List[Optional[np.ndarray]] = [None] * design.L
+        for l, u in enumerate(i2u):
+            y_user[u] = y_int[design.offset[l]:design.offset[l + 1]]
+        m = Model(kernel, d, n, seed, y_user, loss=loss, task_rank=task_rank, jitter=jitter, device=device,
+                  _state={"design": design, "i2u": i2u, "gpu": gpu})
+        m.problem = problem
+        return m
+
+    def l2_relative_error(self, task: int, X) -> float:
+        """||mean - truth|| / ||truth|| over the rows of X, truth = the problem's fidelity task + 1
+        on the device (l2_relative_error, bench.cpp:159-170)."""
+        name = getattr(self, "problem", None)
+        if name is None:
+            raise ValueError("l2_relative_error: the model was not made from a problem")
+        X = np.asarray(X, dtype=np.float64).reshape(-1, self.d)
+        truth = problem_eval(name, task + 1, X)
+        pred = np.asarray(self.posterior_mean_batch(task, X))
+        return float(np.sqrt(np.sum((pred - truth) ** 2) / np.sum(truth * truth)))
 
     # -- user <-> internal
     def _internal(self, h: Hyper) -> Hyper:
@@ -240,4 +298,5 @@ class Model:
                      loss=doc["loss"], device=device, _state={"design": design, "i2u": i2u, "hyper": hyper})
 
 
-__all__ = ["Model", "design_points", "optimal_weights", "make_design", "KERNELS"]
+__all__ = ["Model", "design_points", "optimal_weights", "make_design", "test_points", "problem_eval", "KERNELS",
+           "PROBLEMS"]

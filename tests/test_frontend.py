@@ -116,3 +116,57 @@ def test_cli_fit_and_cubature(tmp_path):
     assert cli.main(["cubature", "--model", str(fitted), "--out", str(cub)]) == 0
     c = json.loads(cub.read_text())
     assert len(c["mu"]) == 2 and len(c["Sigma"]) == 2
+
+
+def test_test_points_and_problem_errors():
+    """The held-out set (bench.cpp:155-157): generator points under the test-stream shift — in the
+    unit cube, distinct from the design's own points; problem arguments checked before the device."""
+    X = fastmtgp.test_points("si-lattice", 4, 256, seed=3)
+    assert X.shape == (256, 4) and np.all((X >= 0) & (X < 1))
+    D = fastmtgp.design_points("lattice", 4, [256], 3)[0]
+    assert not np.allclose(X, D)
+    Xd = fastmtgp.test_points("dsi-digital", 2, 64, seed=3)
+    assert Xd.shape == (64, 2) and len(np.unique(Xd[:, 0])) == 64
+    with pytest.raises(ValueError):
+        fastmtgp.Model.from_problem("nosuch", "si-lattice", [64])
+    with pytest.raises(ValueError):
+        fastmtgp.Model.from_problem("ackley", "si-lattice", [64, 32, 16])  # ackley has 2 fidelities
+    with pytest.raises(Unsupported):
+        fastmtgp.Model.from_problem("ackley", "se-dense", [64])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kernel", ["si-lattice", "dsi-digital"])
+def test_model_from_problem(ref, kernel):
+    """fit_trial on a benchmark problem (bench.cpp:84-107): device observations equal the
+    reference's functions at the design points plus the noise stream; fitting lowers the loss and
+    the held-out l2 error of the top fidelity is small on a smooth problem."""
+    n = [1024, 256]
+    m = fastmtgp.Model.from_problem("ackley", kernel, n, seed=2, noise=1e-4)
+    for u in range(2):
+        want = ref.problem_eval("ackley", u + 1, fastmtgp.design_points(
+            "lattice" if kernel == "si-lattice" else "digital", 4, n, 2)[u])
+        assert np.abs(m.y_user[u] - want).max() <= 1e-3  # noise 1e-4 * N(0,1)
+    l0 = m.loss()
+    rep = m.fit(8)
+    assert m.loss() <= l0 and len(rep["loss_trace"]) == 8
+    X = fastmtgp.test_points(kernel, 4, 512, seed=2)
+    errs = [m.l2_relative_error(u, X) for u in range(2)]
+    assert all(np.isfinite(errs)) and errs[0] < 0.5, errs
+
+
+@pytest.mark.gpu
+def test_cli_problem_fit_cubature_bench(tmp_path):
+    from paper_2603_16014_b200 import cli
+    rep, cub, bench = tmp_path / "r.json", tmp_path / "c.json", tmp_path / "b.csv"
+    assert cli.main(["fit", "--problem", "rosenbrock", "--kernel", "si-lattice", "--n", "256,64,16", "--steps", "4",
+                     "--noise", "1e-3", "--test-points", "128", "--out", str(rep)]) == 0
+    r = json.loads(rep.read_text())
+    assert r["n"] == "256x64x16" and len(r["l2_rel_error"]) == 3 and len(r["report"]["loss_trace"]) == 4
+    assert cli.main(["cubature", "--problem", "borehole", "--n", "128,32", "--steps", "3", "--out", str(cub)]) == 0
+    c = json.loads(cub.read_text())
+    assert len(c["mu"]) == 2 and len(c["weights"]) == 2 and c["problem"] == "borehole"
+    assert cli.main(["bench", "--problem", "ackley", "--n", "128,64", "--steps", "3", "--trials", "2",
+                     "--test-points", "64", "--out", str(bench)]) == 0
+    rows = bench.read_text().strip().splitlines()
+    assert rows[0].startswith("problem,method,n,trial") and len(rows) == 4 and rows[-1].split(",")[3] == "median"

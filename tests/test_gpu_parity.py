@@ -354,3 +354,18 @@ def test_problem_observations_on_device(ref, Model, name, d, L, kind):
                b=(0.0, 0.0, 0.0, 1.0))
     r = M.nll(hp, grad=False)
     assert abs(r["nll"] - ref.Model(dz, hp, want).loss(0)) <= max(1e-8 * dz.N, 1e-9 * abs(r["nll"]))
+
+
+@pytest.mark.parametrize("name,d,L", [("rosenbrock", 2, 3), ("ackley", 4, 2), ("borehole", 8, 2), ("elliptic", 16, 3)])
+def test_problem_eval_at_points(ref, name, d, L):
+    """fmtgp_problem_eval (the held-out truth of bench.cpp:159-170) at arbitrary points, edges
+    included (0 and 1 - 2^-53 exercise the clamp of the inverse-normal problems), every fidelity."""
+    from paper_2603_16014_b200.fast_gram import problem_eval
+    X = np.random.default_rng(d).random((1000, d))
+    X[0], X[1] = 0.0, 1.0 - 2.0 ** -53
+    for level in range(1, L + 1):
+        got, want = problem_eval(name, level, X), ref.problem_eval(name, level, X)
+        nan = np.isnan(want)  # borehole at the clamped edge: rw < 0, log of a negative ratio, in both
+        assert np.array_equal(np.isnan(got), nan), level
+        assert np.abs(got[~nan] - want[~nan]).max() <= 1e-12 * max(1.0, np.abs(want[~nan]).max()), level
+    assert problem_eval(name, 1, np.empty((0, d))).shape == (0,)
