@@ -261,6 +261,8 @@ def main():
                     help="BASELINE config; default 4 = the largest single-GPU config (headline)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="diagnostics only: skip the L2 flush")
+    ap.add_argument("--chunks", type=int, default=2,
+                    help="config 4 at N > 1: all-to-all pipeline depth (fmtgp_shard_chunks; 1 = unpipelined)")
     args = ap.parse_args()
     warmup = max(args.warmup, 3)
 
@@ -279,7 +281,8 @@ def main():
     P, T = dz.L * (dz.L + 1) // 2, dz.L
     parallelism = "single"
     if args.gpus > 1:
-        parallelism = {4: f"frequency-sharded over {world} GPUs (2 NCCL all-to-alls per fit)",
+        parallelism = {4: f"frequency-sharded over {world} GPUs (2 NCCL all-to-alls per fit, each in "
+                          f"{args.chunks} chunk(s) under the L1 / L2 kernels)",
                        5: f"candidate-sharded over {world} GPUs (gather of the records)"}.get(args.config,
                                                                                       f"{world} replicas")
     config = {"workload": WORKLOADS[args.config], "N": dz.N, "T": T, "d": dz.d, "n": dz.n[0],
@@ -322,8 +325,19 @@ def main():
         # ranks (strong scaling): column pass -> NCCL all-to-all -> row pass + solve -> all-to-all ->
         # inverse column pass + gradient dot -> gather of the 101-double records
         from paper_2603_16014_b200 import sharding
-        shard = sharding.ShardedLatticeFit(dz, rank, world, device=local_rank, model=model)
+        shard = sharding.ShardedLatticeFit(dz, rank, world, device=local_rank, model=model, chunks=args.chunks)
         ex, ga = sharding.dist_exchange(shard), sharding.dist_gather(shard)
+        # guard (untimed): the pipelined exchange must reproduce the unpipelined one bit for bit
+        if args.chunks > 1:
+            ref_shard = sharding.ShardedLatticeFit(dz, rank, world, device=local_rank, model=model)
+            a = sharding.sharded_nll([ref_shard], hp, grad=True, exchange=sharding.dist_exchange(ref_shard),
+                                     gather=sharding.dist_gather(ref_shard))
+            from paper_2603_16014_b200._lib import check
+            check(model.lib.fmtgp_shard_chunks(model.h, args.chunks))  # ref_shard's setup reset it
+            b = sharding.sharded_nll([shard], hp, grad=True, exchange=ex, gather=ga)
+            if not (a["nll"] == b["nll"] and np.array_equal(a["deta"], b["deta"])):
+                raise RuntimeError(f"pipelined exchange differs: {a['nll']} vs {b['nll']}")
+            del ref_shard
 
         class _Sharded:
             def nll(self, h, grad=True):

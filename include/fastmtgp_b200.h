@@ -210,6 +210,18 @@ FMTGP_API int fmtgp_shard_mid(fmtgp_model_t model, void* Y2);
 FMTGP_API int fmtgp_shard_end(fmtgp_model_t model, const void* Y3, double* rec);
 FMTGP_API int fmtgp_shard_finish(fmtgp_model_t model, const fmtgp_hyper* h, const double* rec, int want_grad,
                                  double xi_scale, int escalations, fmtgp_result* out);
+/* Pipelined exchange: split each all-to-all into `chunks` (a power of two dividing the rank's
+ * column blocks and row pairs; 1 = the unchunked phases above).  Chunk k is the contiguous range
+ * [k, k+1) * exchange_elems / chunks of every buffer (itself `world` equal blocks), so
+ *   for k: begin_chunk(k) -> Y;   all-to-all of chunk k, Y -> Y2   (overlaps begin_chunk(k+1))
+ *   for k: mid_chunk(Y2, Y, k);   all-to-all of chunk k, Y -> Y3   (overlaps mid_chunk(k+1))
+ *   end(Y3)
+ * begin_chunk(0) stages the hyperparameters; every mid_chunk needs all forward chunks received,
+ * and writes Y (free once the forward exchange is done) — never Y2 in place. */
+FMTGP_API int fmtgp_shard_chunks(fmtgp_model_t model, int chunks);
+FMTGP_API int fmtgp_shard_begin_chunk(fmtgp_model_t model, const fmtgp_hyper* h, int want_grad, double xi_scale,
+                                      void* Y, int chunk);
+FMTGP_API int fmtgp_shard_mid_chunk(fmtgp_model_t model, void* Y2, void* Yout, int chunk);
 
 /* ---- measurement: per-kernel CUDA-event timing on the model's stream ---------------- */
 /* iters fmtgp_nll calls from a C loop, each bracketed by CUDA events on the model's stream after an

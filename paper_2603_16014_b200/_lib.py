@@ -97,6 +97,9 @@ _SIGS = {
     "fmtgp_shard_setup": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int64)]),
     "fmtgp_shard_begin": (C.c_int, [C.c_void_p, C.POINTER(CHyper), C.c_int, C.c_double, C.c_void_p]),
     "fmtgp_shard_mid": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "fmtgp_shard_chunks": (C.c_int, [C.c_void_p, C.c_int]),
+    "fmtgp_shard_begin_chunk": (C.c_int, [C.c_void_p, C.POINTER(CHyper), C.c_int, C.c_double, C.c_void_p, C.c_int]),
+    "fmtgp_shard_mid_chunk": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
     "fmtgp_shard_end": (C.c_int, [C.c_void_p, C.c_void_p, _dp]),
     "fmtgp_shard_finish": (C.c_int, [C.c_void_p, C.POINTER(CHyper), _dp, C.c_int, C.c_double, C.c_int,
                                      C.POINTER(CResult)]),

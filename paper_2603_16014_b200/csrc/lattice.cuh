@@ -73,6 +73,15 @@ struct LatArgs {
     int QP = 0, R = 0, WC = 0, ncb = 0;
     int lwc = 0, lqp = 0;     // log2 WC, log2 QP (world sizes are powers of two): no integer division
     const double2* Cbuf = nullptr;
+    // ---- pipelined exchange (K = 2^lkc chunks; K = 1: the layout above).  The forward blocks are
+    // stored column-chunked, Y[kc][h][o][i][jl - kc WC/K] (chunk kc = local columns [kc WC/K,
+    // (kc+1) WC/K)), the return blocks row-chunked, [kr][h][o][i - kr R/K][jl] (rows [kr R/K,
+    // (kr+1) R/K)): chunk k of every rank's buffer is one contiguous all-to-all of G equal blocks.
+    // L1 launches per column chunk and L2 per row chunk (`chunk`; -1 = all), so chunk k's exchange
+    // runs under chunk k+1's kernel.  L2 writes Yout (the return send buffer; nullptr = in place).
+    int lkc = 0, lg = 0;      // log2 K, log2 nrank
+    int chunk = -1;
+    double2* Yout = nullptr;
 };
 
 void lat_fit(const LatGeo& g, const LatArgs& a, cudaStream_t s);

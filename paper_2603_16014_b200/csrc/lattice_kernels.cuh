@@ -122,6 +122,17 @@ __device__ __forceinline__ unsigned xoff(const LatArgs& a, int h, int o, int i, 
 __device__ __forceinline__ size_t xaddr(const LatArgs& a, int c, int h, int o, int i, int jl) {
     return size_t(c) * a.V * a.half + (((size_t(h) * a.V + o) * a.R + i) << a.lwc) + jl;
 }
+// forward blocks (L1 -> L2), column-chunked: [kc][h][o][i][jl mod WC/K] (== xoff when K = 1)
+__device__ __forceinline__ unsigned xoff_f(const LatArgs& a, int h, int o, int i, int jl) {
+    const int lw = a.lwc - a.lkc, kc = jl >> lw;
+    return ((unsigned(((kc << a.lg) + h) * a.V + o) * unsigned(a.R) + unsigned(i)) << lw) +
+           unsigned(jl & ((1 << lw) - 1));
+}
+// return blocks (L2 -> L3), row-chunked: [kr][h][o][i mod R/K][jl] (== xoff when K = 1)
+__device__ __forceinline__ unsigned xoff_r(const LatArgs& a, int h, int o, int i, int jl) {
+    const int lr = a.lqp + 1 - a.lkc, kr = i >> lr;
+    return ((unsigned((((kr << a.lg) + h) * a.V + o) << lr) + unsigned(i & ((1 << lr) - 1))) << a.lwc) + unsigned(jl);
+}
 
 // ------------------------------------------------------------------ L1: generator x column FFT
 // In-place DIF column FFT (ipfft.cuh) of C = 2^lc columns of N1 = 2^l1 rows (C N1 = 16 NT):
@@ -168,19 +179,21 @@ __global__ void __launch_bounds__(NT) k_lat_col_fwd(LatArgs a, int l2, int lc) {
     Tw16 t0;
     t0.load(a.tw, j1, L1);  // the same for every tile
     // zero the per-fit flags once per fit (L2 / L3 run after this kernel)
-    if (blockIdx.x == 0) {
+    if (blockIdx.x == 0 && a.chunk <= 0) {
         for (int t = threadIdx.x; t < a.nc; t += NT) a.bad[t] = 0x7f7f7f7f;
         for (int t = threadIdx.x; t < a.nc * MAXT * 2; t += NT) a.imre[t] = 0ull;
     }
     pdl_trigger();
     // persistent over cluster tiles (K column blocks x class x candidate): a tile's exchange-block
     // stores drain while the next tile's generator (registers only) runs
-    const int ncbk = a.ncb >> lk;
+    // a chunked launch (a.chunk >= 0) covers the cluster blocks of column chunk a.chunk only
+    const int ncbk = a.ncb >> (lk + (a.chunk >= 0 ? a.lkc : 0));
+    const int bk0 = a.chunk >= 0 ? a.chunk * ncbk : 0;
     const int ntiles = ncbk * a.V * a.nc, nclus = int(gridDim.x) >> lk, cid = int(blockIdx.x) >> lk;
     cluster_arrive_relaxed();
 #pragma unroll 1
     for (int tile = cid; tile < ntiles; tile += nclus) {
-        const int bk = tile % ncbk, v = tile / ncbk, c = v / a.V, o = v - c * a.V;
+        const int bk = bk0 + tile % ncbk, v = tile / ncbk, c = v / a.V, o = v - c * a.V;
         const int bx = (bk << lk) + crank;
         const uint32_t c0 = uint32_t(a.rank * a.ncb + bx) << lc;  // global first column of this CTA
         double2 x[16];
@@ -223,7 +236,7 @@ __global__ void __launch_bounds__(NT) k_lat_col_fwd(LatArgs a, int l2, int lc) {
             const int k1 = IP::freq(p);
             int i;
             const int h = row_owner(k1, N1, a.lqp, i);
-            Yc[xoff(a, h, o, i, jlb + cc)] = src[cc >> lc][(cc & (C - 1)) * ld + S(p)];
+            Yc[xoff_f(a, h, o, i, jlb + cc)] = src[cc >> lc][(cc & (C - 1)) * ld + S(p)];
         }
         // relaxed: the remote reads above have completed (their values were stored), and a
         // release here would wait for every outstanding exchange-block store to drain
@@ -303,8 +316,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
     __shared__ double2 s_ostep[16], s_rstep[16];
     cg::cluster_group cl = cg::this_cluster();
     const int rank = int(cl.block_rank());
-    const int q = a.rank * a.QP + (blockIdx.x >> 1), c = blockIdx.y, V = DIST ? P - T + 1 : a.V;
-    const int li = blockIdx.x;  // local row index of this CTA's row in the exchange blocks
+    // local row index of this CTA's row in the exchange blocks (a chunked launch: row chunk a.chunk)
+    const int li = (a.chunk >= 0 ? a.chunk << (a.lqp + 1 - a.lkc) : 0) + int(blockIdx.x);
+    const int q = a.rank * a.QP + (li >> 1), c = blockIdx.y, V = DIST ? P - T + 1 : a.V;
     auto cls = [&](int y) { return DIST ? cls_distinct<T>(y) : s_cls[y]; };
     constexpr int N2 = 1 << L2, lds = padded_len(N2);
     const int N1 = 1 << l1, lt = l1 + l2;
@@ -374,7 +388,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
         prefetch_yhat(li + WAVE, (threadIdx.x - 64) >> 1, (threadIdx.x - 64) & 1);
     pdl_wait();
     pdl_trigger();
-    if ((a.next_pf & 2) && threadIdx.x >= 32 && threadIdx.x < 32 + a.nrank * V && li + WAVE < a.R) {
+    if ((a.next_pf & 2) && a.lkc == 0 && threadIdx.x >= 32 && threadIdx.x < 32 + a.nrank * V && li + WAVE < a.R) {
         const int sr = (threadIdx.x - 32) / V, oo = (threadIdx.x - 32) - sr * V;
         bulk_prefetch(a.Y + size_t(c) * a.V * a.half + xoff(a, sr, oo, li + WAVE, 0),
                       unsigned(a.WC * sizeof(double2)));
@@ -383,7 +397,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
     for (int e = threadIdx.x; e < (V << l2); e += NT) {
         const int oo = e >> l2, k2 = e & (N2 - 1);
         const int sr = k2 >> a.lwc;  // column owner
-        cp_async16(&sm[oo * lds + S(k2)], &Yc[xoff(a, sr, oo, li, k2 & (a.WC - 1))]);
+        cp_async16(&sm[oo * lds + S(k2)], &Yc[xoff_f(a, sr, oo, li, k2 & (a.WC - 1))]);
     }
     cp_async_wait_all();
     __syncthreads();
@@ -547,7 +561,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
     __shared__ double redv[(NT / 32) * (2 + P)];
     block_sum_vec<NT, 2 + P>(acc, redv);
     if (threadIdx.x == 0) {
-        double* pm = a.part_mid + (size_t(c) * gridDim.x + blockIdx.x) * (2 + P);
+        double* pm = a.part_mid + (size_t(c) * a.R + li) * (2 + P);
 #pragma unroll
         for (int x = 0; x < 2 + P; ++x) pm[x] = acc[x];
     }
@@ -578,10 +592,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
 #pragma unroll
         for (int r = 0; r < 16; ++r) x[r] = xs[ip_off<M_log>(r)];
         dit16_regs(x, t0);
+        double2* const Yo = (a.Yout ? a.Yout : a.Y) + size_t(c) * a.V * a.half;
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
             const int j2 = gj1 + (brev_c<16>(r) << M_log);
-            Yc[xoff(a, j2 >> a.lwc, gvec, li, j2 & (a.WC - 1))] =
+            Yo[xoff_r(a, j2 >> a.lwc, gvec, li, j2 & (a.WC - 1))] =
                 cmulc(x[r], cmul(obase, s_ostep[brev_c<16>(r)]));
         }
     }
@@ -617,7 +632,7 @@ __global__ void __launch_bounds__(NT) k_lat_col_inv(LatArgs a, int l2, int lc) {
         for (int r = 0; r < 16; ++r) {
             int i;
             const int h = row_owner(kb | IP::freq_lo(r), N1, a.lqp, i);
-            cp_async16(xs + r, &Cc[xoff(a, h, o, i, jl)]);
+            cp_async16(xs + r, &Cc[xoff_r(a, h, o, i, jl)]);
         }
     };
     pdl_wait();
@@ -767,8 +782,9 @@ static int lat_cluster_grid(Kern kern, int K, size_t smem, int tiles) {
 
 template <int DC, int ALPHA, int L1>
 static void lat_cols(const LatGeo& g, const LatArgs& a, size_t sm_col, bool inverse, cudaStream_t s) {
-    const int K = lat_cluster_k(a.ncb);
-    const int tiles = (a.ncb / K) * a.V * a.nc;
+    const int nb = a.chunk >= 0 ? a.ncb >> a.lkc : a.ncb;  // column blocks of this launch
+    const int K = lat_cluster_k(nb);
+    const int tiles = (nb / K) * a.V * a.nc;
     if (!inverse) {
         auto k = k_lat_col_fwd<LAT_NT, DC, ALPHA, L1>;
         set_smem_lat(k, sm_col);
@@ -807,7 +823,8 @@ static void lat_mid_t(const LatGeo& g, const LatArgs& a, cudaStream_t s) {
     auto k = a.distinct ? k_lat_mid<LAT_NT, T, true, L2> : k_lat_mid<LAT_NT, T, false, L2>;
     set_smem_lat(k, sm);
     ProfScope ps("lat_mid", s);
-    CK_LAUNCH(launch_pdl(k, dim3(unsigned(a.R), a.nc), dim3(LAT_NT), sm, s, true, a, g.l1));
+    const int rows = a.chunk >= 0 ? a.R >> a.lkc : a.R;
+    CK_LAUNCH(launch_pdl(k, dim3(unsigned(rows), a.nc), dim3(LAT_NT), sm, s, true, a, g.l1));
 }
 
 template <int L2>

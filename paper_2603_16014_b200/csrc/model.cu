@@ -337,6 +337,7 @@ struct fmtgp_model {
     unsigned long long done_seq = 0;
     // frequency sharding of the fused lattice fit (fmtgp_shard_*): world size / rank
     int sh_G = 1, sh_g = 0;
+    int sh_lkc = 0;  // log2 exchange chunks (fmtgp_shard_chunks)
     LatArgs sh_args{};
     fmtgp_hyper sh_h{};
     bool sh_grad = false;
@@ -789,6 +790,8 @@ LatArgs lat_args(fmtgp_model* M, int nc, int si_alpha, bool grad) {
     while ((1 << a.lwc) < a.WC) ++a.lwc;
     while ((1 << a.lqp) < a.QP) ++a.lqp;
     a.ncb = lg.nblk_col / a.nrank;
+    while ((1 << a.lg) < a.nrank) ++a.lg;
+    a.lkc = M->sh_lkc;
     a.Cbuf = a.Y;
     if (const char* e = std::getenv("FMTGP_LAT_PF")) a.next_pf = std::atoi(e) & 3;
     return a;
@@ -2305,7 +2308,61 @@ int fmtgp_shard_setup(fmtgp_model_t M, int rank, int world, int64_t* exchange_el
             invalid("shard_setup: the world size must be a power of two dividing the row clusters and column blocks");
         M->sh_G = world;
         M->sh_g = rank;
+        M->sh_lkc = 0;
         *exchange_elems = (int64_t)M->nofs * M->pslots[0] / world;
+    });
+}
+
+int fmtgp_shard_chunks(fmtgp_model_t M, int chunks) {
+    return guarded([&] {
+        if (!M) invalid("shard_chunks: null argument");
+        if (!M->lat) invalid("shard_chunks: model is not sharded (fmtgp_shard_setup)");
+        const LatGeo& g = M->lgeo;
+        const int rows = (1 << g.l1) / M->sh_G, ncb = g.nblk_col / M->sh_G;  // rows R, column blocks per rank
+        if (chunks < 1 || (chunks & (chunks - 1)) || ncb % chunks || rows % (2 * chunks))
+            invalid("shard_chunks: chunks must be a power of two dividing the rank's column blocks and row pairs");
+        int l = 0;
+        while ((1 << l) < chunks) ++l;
+        M->sh_lkc = l;
+    });
+}
+
+// one column chunk of L1 (chunk 0 also stages the hyperparameters); Y: the forward send buffer
+int fmtgp_shard_begin_chunk(fmtgp_model_t M, const fmtgp_hyper* h, int want_grad, double xi_scale, void* Y,
+                            int chunk) {
+    return guarded([&] {
+        if (!M || !h || !Y) invalid("shard_begin_chunk: null argument");
+        if (!M->lat) invalid("shard_begin_chunk: model is not sharded (fmtgp_shard_setup)");
+        if (chunk < 0 || chunk >= (1 << M->sh_lkc)) invalid("shard_begin_chunk: chunk out of range");
+        CK(cudaSetDevice(M->dev));
+        if (chunk == 0) {
+            if (!M->have_y) invalid("nll: observations not set (fmtgp_model_set_y)");
+            validate_hyper(M, h);
+            const fmtgp_hyper* hs[1] = {h};
+            fill_hyper(M, 1, hs, &xi_scale);
+            copy_hyper(M);
+            M->sh_args = lat_args(M, 1, h->si_alpha, want_grad != 0);
+            M->sh_grad = want_grad != 0;
+        }
+        M->sh_args.Y = static_cast<double2*>(Y);
+        M->sh_args.chunk = chunk;
+        lat_phase(M->lgeo, M->sh_args, 1, M->st);
+        CK(cudaGetLastError());
+    });
+}
+
+// one row chunk of L2: reads the forward receive buffer Y, writes the return send buffer Yout
+int fmtgp_shard_mid_chunk(fmtgp_model_t M, void* Y, void* Yout, int chunk) {
+    return guarded([&] {
+        if (!M || !Y || !Yout) invalid("shard_mid_chunk: null argument");
+        if (chunk < 0 || chunk >= (1 << M->sh_lkc)) invalid("shard_mid_chunk: chunk out of range");
+        if (Y == Yout && M->sh_lkc > 0) invalid("shard_mid_chunk: chunked L2 cannot work in place");
+        CK(cudaSetDevice(M->dev));
+        M->sh_args.Y = static_cast<double2*>(Y);
+        M->sh_args.Yout = static_cast<double2*>(Yout);
+        M->sh_args.chunk = chunk;
+        lat_phase(M->lgeo, M->sh_args, 2, M->st);
+        CK(cudaGetLastError());
     });
 }
 
@@ -2319,6 +2376,7 @@ int fmtgp_shard_begin(fmtgp_model_t M, const fmtgp_hyper* h, int want_grad, doub
         const fmtgp_hyper* hs[1] = {h};
         fill_hyper(M, 1, hs, &xi_scale);
         copy_hyper(M);
+        if (M->sh_lkc) invalid("shard_begin: the exchange is chunked (fmtgp_shard_begin_chunk)");
         M->sh_args = lat_args(M, 1, h->si_alpha, want_grad != 0);
         M->sh_args.Y = static_cast<double2*>(Y);
         M->sh_grad = want_grad != 0;
@@ -2331,7 +2389,10 @@ int fmtgp_shard_mid(fmtgp_model_t M, void* Y) {
     return guarded([&] {
         if (!M || !Y) invalid("shard_mid: null argument");
         CK(cudaSetDevice(M->dev));
+        if (M->sh_lkc) invalid("shard_mid: the exchange is chunked (fmtgp_shard_mid_chunk)");
         M->sh_args.Y = static_cast<double2*>(Y);
+        M->sh_args.Yout = nullptr;
+        M->sh_args.chunk = -1;
         lat_phase(M->lgeo, M->sh_args, 2, M->st);
         CK(cudaGetLastError());
     });

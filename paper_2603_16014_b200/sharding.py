@@ -96,9 +96,13 @@ class ShardedLatticeFit:
     `exchange(send, recv)` is an all-to-all of `world` equal chunks (default: torch.distributed
     all_to_all_single on the model's stream) and `gather(rec)` returns every rank's record in
     rank order (default: torch.distributed.all_gather).  Both are injectable so the same
-    orchestration runs with virtual ranks on one device (tests)."""
+    orchestration runs with virtual ranks on one device (tests).
 
-    def __init__(self, design, rank: int, world: int, device: int = 0, model=None):
+    `chunks` > 1 pipelines each all-to-all (fmtgp_shard_chunks): L1 runs per column chunk and L2
+    per row chunk, and chunk k's all-to-all runs on a separate communication stream under chunk
+    k+1's kernel (buffers: 0 = L1 out / L2 out, 1 = forward receive, 2 = return receive)."""
+
+    def __init__(self, design, rank: int, world: int, device: int = 0, model=None, chunks: int = 1):
         import torch
 
         from .fast_gram import Model
@@ -108,9 +112,18 @@ class ShardedLatticeFit:
         n = C.c_int64()
         check(self.model.lib.fmtgp_shard_setup(self.model.h, rank, world, C.byref(n)))
         self.elems = int(n.value)  # complex values per exchange buffer
+        self.chunks = int(chunks)
+        if self.chunks > 1:
+            check(self.model.lib.fmtgp_shard_chunks(self.model.h, self.chunks))
         dev = torch.device("cuda", device)
-        self.bufs = [torch.empty(2 * self.elems, dtype=torch.float64, device=dev) for _ in range(2)]
+        self.bufs = [torch.empty(2 * self.elems, dtype=torch.float64, device=dev)
+                     for _ in range(2 if self.chunks == 1 else 3)]
         self.stream = torch.cuda.ExternalStream(self.model.stream, device=dev)
+        self.comm = torch.cuda.Stream(device=dev) if self.chunks > 1 else self.stream
+
+    def region(self, b: int, k: int):
+        """Chunk k of buffer b (a contiguous view: `world` equal blocks of exchange_elems / chunks)."""
+        return self.bufs[b].view(self.chunks, -1)[k]
 
     def set_y(self, y):
         self.model.set_y(y)
@@ -126,9 +139,21 @@ class ShardedLatticeFit:
         check(self.model.lib.fmtgp_shard_mid(self.model.h, C.c_void_p(self.bufs[1].data_ptr())))
         return self.bufs[1]
 
+    def begin_chunk(self, hp, grad: bool, xi_scale: float, k: int):
+        ch = self.model._hyper_struct(hp)
+        check(self.model.lib.fmtgp_shard_begin_chunk(self.model.h, C.byref(ch), int(grad), float(xi_scale),
+                                                     C.c_void_p(self.bufs[0].data_ptr()), int(k)))
+        return self.region(0, k)
+
+    def mid_chunk(self, k: int):
+        check(self.model.lib.fmtgp_shard_mid_chunk(self.model.h, C.c_void_p(self.bufs[1].data_ptr()),
+                                                   C.c_void_p(self.bufs[0].data_ptr()), int(k)))
+        return self.region(0, k)
+
     def end(self):
         rec = np.zeros(SHARD_REC_LEN)
-        check(self.model.lib.fmtgp_shard_end(self.model.h, C.c_void_p(self.bufs[0].data_ptr()),
+        back = self.bufs[0 if self.chunks == 1 else 2]
+        check(self.model.lib.fmtgp_shard_end(self.model.h, C.c_void_p(back.data_ptr()),
                                              rec.ctypes.data_as(C.POINTER(C.c_double))))
         return rec
 
@@ -141,10 +166,24 @@ class ShardedLatticeFit:
         return _result(r, self.model.design, hp)
 
     def default_exchange(self, send, recv, group=None):
+        """NCCL all-to-all ordered after the work queued so far on the model's stream; with chunks
+        it runs on the communication stream (so the next chunk's kernel overlaps it) until join()."""
         import torch
         import torch.distributed as dist
-        with torch.cuda.stream(self.stream):
+        if self.comm is not self.stream:
+            ev = torch.cuda.Event()
+            ev.record(self.stream)
+            self.comm.wait_event(ev)
+        with torch.cuda.stream(self.comm):
             dist.all_to_all_single(recv, send, group=group)
+
+    def join(self):
+        """The model's stream waits for every exchange issued so far."""
+        if self.comm is not self.stream:
+            import torch
+            ev = torch.cuda.Event()
+            ev.record(self.comm)
+            self.stream.wait_event(ev)
 
     def default_gather(self, rec, group=None):
         import torch
@@ -162,14 +201,24 @@ def sharded_nll(ranks, hp, grad: bool = True, exchange=None, gather=None, max_re
     `ranks` is this process's ShardedLatticeFit (one element, multi-process) or all of them
     (virtual ranks on one device, in which case `exchange` / `gather` act on the list)."""
     local = list(ranks)
+    K = getattr(local[0], "chunks", 1)
+    join = getattr(exchange, "join", None) or (lambda: None)
     scale, attempt = 1.0, 0
     while True:
-        sends = [r.begin(hp, grad, scale) for r in local]
-        recvs = [r.bufs[1] for r in local]
-        exchange(sends, recvs)  # column blocks -> row owners
-        mids = [r.mid() for r in local]
-        backs = [r.bufs[0] for r in local]
-        exchange(mids, backs)  # row blocks -> column owners
+        if K == 1:
+            sends = [r.begin(hp, grad, scale) for r in local]
+            exchange(sends, [r.bufs[1] for r in local])  # column blocks -> row owners
+            mids = [r.mid() for r in local]
+            exchange(mids, [r.bufs[0] for r in local])  # row blocks -> column owners
+        else:  # pipelined: chunk k's all-to-all under chunk k+1's kernel
+            for k in range(K):
+                sends = [r.begin_chunk(hp, grad, scale, k) for r in local]
+                exchange(sends, [r.region(1, k) for r in local])
+            join()  # L2 needs every forward chunk
+            for k in range(K):
+                outs = [r.mid_chunk(k) for r in local]
+                exchange(outs, [r.region(2, k) for r in local])
+        join()
         recs = [r.end() for r in local]
         allrec = gather(recs)
         rec = combine_records(allrec)
@@ -201,9 +250,11 @@ def local_exchange(world: int):
 
 
 def dist_exchange(rank_obj, group=None):
-    """Multi-process all-to-all (torch.distributed; NCCL on GPUs), ordered on the model's stream."""
+    """Multi-process all-to-all (torch.distributed; NCCL on GPUs), ordered after the model's
+    stream; `ex.join()` orders the model's stream after it (chunked exchanges)."""
     def ex(sends, recvs):
         rank_obj.default_exchange(sends[0], recvs[0], group)
+    ex.join = rank_obj.join
     return ex
 
 

@@ -151,6 +151,9 @@ class _FakeRank:
 
     def end(self):
         self._check(self.bufs[0], 2)
+        return self._rec()
+
+    def _rec(self):
         rec = np.zeros(sharding.NOUT + 1 + 16)
         rec[: sharding.NOUT] = np.arange(sharding.NOUT) * (self.rank + 1)
         rec[sharding.NOUT] = 0x7f7f7f7f if self.scale >= 100.0 else 5 + self.rank  # Schur until xi x 100
@@ -164,12 +167,71 @@ class _FakeRank:
                 "xi_scale": xi_scale, "escalations": escalations}
 
 
-def _shard_worker(rank, world, port, q):
+class _FakeChunkedRank(_FakeRank):
+    """The pipelined exchange (chunks = 2): forward blocks column-chunked [kc][h][o][i][jl'],
+    return blocks row-chunked [kr][h][o][i'][jl], three buffers (fmtgp_shard_chunks layouts)."""
+    V, R, WC = 2, 4, 4
+    chunks = 2
+
+    def __init__(self, rank, world):
+        import torch
+        super().__init__(rank, world)
+        self.bufs.append(torch.zeros(2 * self.elems, dtype=torch.float64))
+        self.log = []
+
+    def region(self, b, k):
+        return self.bufs[b].view(self.chunks, -1)[k]
+
+    def begin_chunk(self, hp, grad, xi_scale, k):
+        self.scale = xi_scale
+        self.log.append(("begin", k))
+        wk = self.WC // self.chunks
+        v = self.region(0, k).view(self.world, self.V, self.R, wk, 2)
+        for h in range(self.world):
+            for o in range(self.V):
+                for i in range(self.R):
+                    for j in range(wk):
+                        v[h, o, i, j, 0] = self._stamp(self.rank, h, o, i, k * wk + j, 1)
+        return self.region(0, k)
+
+    def mid_chunk(self, k):
+        self.log.append(("mid", k))
+        wk, rk = self.WC // self.chunks, self.R // self.chunks
+        if k == 0:  # every forward chunk has arrived before the first row chunk
+            for kc in range(self.chunks):
+                v = self.region(1, kc).view(self.world, self.V, self.R, wk, 2)
+                for s in range(self.world):
+                    for o in range(self.V):
+                        for i in range(self.R):
+                            for j in range(wk):
+                                assert v[s, o, i, j, 0].item() == self._stamp(s, self.rank, o, i, kc * wk + j, 1)
+        v = self.region(0, k).view(self.world, self.V, rk, self.WC, 2)
+        for h in range(self.world):
+            for o in range(self.V):
+                for i in range(rk):
+                    for jl in range(self.WC):
+                        v[h, o, i, jl, 0] = self._stamp(self.rank, h, o, k * rk + i, jl, 2)
+        return self.region(0, k)
+
+    def end(self):
+        rk = self.R // self.chunks
+        for kr in range(self.chunks):
+            v = self.region(2, kr).view(self.world, self.V, rk, self.WC, 2)
+            for s in range(self.world):
+                for o in range(self.V):
+                    for i in range(rk):
+                        for jl in range(self.WC):
+                            assert v[s, o, i, jl, 0].item() == self._stamp(s, self.rank, o, kr * rk + i, jl, 2)
+        assert self.log[-2 * self.chunks:] == [("begin", 0), ("begin", 1), ("mid", 0), ("mid", 1)]
+        return self._rec()
+
+
+def _shard_worker(rank, world, port, q, chunked=False):
     import torch
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        fr = _FakeRank(rank, world)
+        fr = (_FakeChunkedRank if chunked else _FakeRank)(rank, world)
 
         def ex(sends, recvs):
             dist.all_to_all_single(recvs[0], sends[0])
@@ -188,11 +250,12 @@ def _shard_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_sharded_nll_orchestration_gloo_world2():
+@pytest.mark.parametrize("chunked", [False, True], ids=["whole", "chunked"])
+def test_sharded_nll_orchestration_gloo_world2(chunked):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     p = _free_port()
-    procs = [ctx.Process(target=_shard_worker, args=(r, 2, p, q)) for r in range(2)]
+    procs = [ctx.Process(target=_shard_worker, args=(r, 2, p, q, chunked)) for r in range(2)]
     for pr in procs:
         pr.start()
     out = [q.get(timeout=120) for _ in procs]

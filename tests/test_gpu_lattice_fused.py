@@ -198,6 +198,31 @@ def test_frequency_sharded_virtual_ranks(case):
     assert abs(nog["nll"] - want["nll"]) <= 1e-11 * abs(want["nll"])
 
 
+@pytest.mark.parametrize("case", [(18, 2, 4, 1, 1, 2), (18, 2, 4, 1, 2, 4), (17, 3, 5, 2, 2, 2), (19, 4, 3, 1, 4, 8),
+                                  (18, 1, 2, 1, 2, 2)], ids=lambda c: "m%d-T%d-d%d-a%d-G%d-K%d" % c)
+def test_frequency_sharded_chunked_exchange(case):
+    """The pipelined exchange (fmtgp_shard_chunks: L1 per column chunk, L2 per row chunk, chunk k's
+    all-to-all under chunk k+1's kernel; column-chunked forward and row-chunked return layouts):
+    the same arithmetic in the same order as the unchunked exchange, so the results are identical
+    to the last bit, with and without the gradient."""
+    from paper_2603_16014_b200 import sharding
+    from paper_2603_16014_b200._lib import FastMtgpError
+    m, T, d, alpha, G, K = case
+    dz, hp, y = make(m, T, d, alpha)
+    ex, ga = sharding.local_exchange(G), (lambda r: r)
+    plain = [sharding.ShardedLatticeFit(dz, g, G, model=model(dz, y, True)) for g in range(G)]
+    chunked = [sharding.ShardedLatticeFit(dz, g, G, model=model(dz, y, True), chunks=K) for g in range(G)]
+    for grad in (True, False):
+        a = sharding.sharded_nll(plain, hp, grad=grad, exchange=ex, gather=ga)
+        b = sharding.sharded_nll(chunked, hp, grad=grad, exchange=ex, gather=ga)
+        for k in ("nll", "logdet", "quad") + (("deta", "dB", "dt", "dgamma") if grad else ()):
+            assert np.array_equal(np.asarray(a[k]), np.asarray(b[k])), (k, a[k], b[k])
+    with pytest.raises(FastMtgpError):
+        sharding.ShardedLatticeFit(dz, 0, G, model=model(dz, y, True), chunks=3)
+    with pytest.raises(FastMtgpError):  # more chunks than the rank has column blocks
+        sharding.ShardedLatticeFit(dz, 0, G, model=model(dz, y, True), chunks=1 << 12)
+
+
 def test_frequency_sharded_escalation_matches_single():
     """A rank-deficient task Gram with zero nugget escalates the same number of times sharded."""
     from paper_2603_16014_b200 import sharding

@@ -28,7 +28,7 @@ def _case():
     return inst.design, inst.hyper, inst.y
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, chunks, port, q):
     import torch.distributed as dist
 
     from paper_2603_16014_b200 import sharding
@@ -36,7 +36,7 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         dz, hp, y = _case()
-        shard = sharding.ShardedLatticeFit(dz, rank, world, device=0)
+        shard = sharding.ShardedLatticeFit(dz, rank, world, device=0, chunks=chunks)
         shard.set_y(y)
         res = sharding.sharded_nll([shard], hp, grad=True, exchange=sharding.host_exchange(shard),
                                    gather=sharding.host_gather(shard))
@@ -45,8 +45,8 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_sharded_fit_real_ranks(world):
+@pytest.mark.parametrize("world,chunks", [(2, 1), (4, 1), (2, 4)])
+def test_sharded_fit_real_ranks(world, chunks):
     from paper_2603_16014_b200.fast_gram import Model
     dz, hp, y = _case()
     M = Model(dz)
@@ -55,7 +55,7 @@ def test_sharded_fit_real_ranks(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, chunks, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     got = dict(q.get(timeout=300) for _ in range(world))
