@@ -99,8 +99,20 @@ __device__ __forceinline__ void dit16_regs(double2 (&v)[16], const Tw16& t) {
     reg_dft<16>(v, +1);
 }
 
-// One middle radix-16 stage s over nvec vectors (stride ld), then a barrier.
-template <int NT, int LOG, int S_, bool DIT>
+// Every stage after DIF stage 0 (and every DIT stage before the last) works inside blocks of
+// N/16 positions, and group gi of a stage lies in block gi >> (LOG - 8) — the block of chunk gi
+// of the tail stage too.  Thread tid handles the groups gi = tid + j NT, so the 2^(LOG-8) <= 32
+// threads that touch a block are lanes of ONE warp (LOG <= 13): those stages need __syncwarp,
+// not a CTA barrier (WL = warp-local), and the warps of a CTA drift apart instead of running
+// every stage in lock step.
+template <bool WL>
+__device__ __forceinline__ void ip_sync() {
+    if constexpr (WL) __syncwarp();
+    else __syncthreads();
+}
+
+// One middle radix-16 stage s over nvec vectors (stride ld), then a barrier (WL: warp barrier).
+template <int NT, int LOG, int S_, bool DIT, bool WL = false>
 __device__ __forceinline__ void ip_stage(double2* sm, int nvec, int ld, const double2* __restrict__ tw) {
     constexpr int ML = LOG - 4 * (S_ + 1);
     constexpr int GPV = LOG - 4;  // log2 groups per vector
@@ -121,19 +133,22 @@ __device__ __forceinline__ void ip_stage(double2* sm, int nvec, int ld, const do
 #pragma unroll
         for (int r = 0; r < 16; ++r) x[ip_off<ML>(brev_c<16>(r))] = v[r];
     }
-    __syncthreads();
+    ip_sync<WL>();
 }
 
 // Middle radix-16 stages 1 .. A16-1 (stage 0 is fused by the kernels): DIF ascending, DIT descending.
-template <int NT, int LOG, bool DIT>
+// WL: warp barriers between them; the DIT form ends with a CTA barrier anyway (stage 0 reads
+// across blocks), unless LAST_WL (the caller synchronises the CTA itself).
+template <int NT, int LOG, bool DIT, bool WL = false>
 __device__ __forceinline__ void ip_mid_stages(double2* sm, int nvec, int ld, const double2* __restrict__ tw) {
+    static_assert(!WL || LOG <= 13, "warp-local stages need blocks of <= 32 groups");
     constexpr int A = Ip<LOG>::A16;
     if constexpr (!DIT) {
-        if constexpr (A > 1) ip_stage<NT, LOG, 1, false>(sm, nvec, ld, tw);
-        if constexpr (A > 2) ip_stage<NT, LOG, 2, false>(sm, nvec, ld, tw);
+        if constexpr (A > 1) ip_stage<NT, LOG, 1, false, WL>(sm, nvec, ld, tw);
+        if constexpr (A > 2) ip_stage<NT, LOG, 2, false, WL>(sm, nvec, ld, tw);
     } else {
-        if constexpr (A > 2) ip_stage<NT, LOG, 2, true>(sm, nvec, ld, tw);
-        if constexpr (A > 1) ip_stage<NT, LOG, 1, true>(sm, nvec, ld, tw);
+        if constexpr (A > 2) ip_stage<NT, LOG, 2, true, WL>(sm, nvec, ld, tw);
+        if constexpr (A > 1) ip_stage<NT, LOG, 1, true, false>(sm, nvec, ld, tw);
     }
 }
 
@@ -156,7 +171,7 @@ __host__ __device__ constexpr int tail_out_pos(int i) {
 }
 
 // Tail stage over whole smem vectors: thread owns 16 contiguous positions (conflict-free).
-template <int NT, int LOG>
+template <int NT, int LOG, bool WL = false>
 __device__ __forceinline__ void ip_tail_stage(double2* sm, int nvec, int ld, int dir) {
     constexpr int CPV = LOG - 4;
     const int total = nvec << CPV;
@@ -171,7 +186,7 @@ __device__ __forceinline__ void ip_tail_stage(double2* sm, int nvec, int ld, int
 #pragma unroll
         for (int r = 0; r < 16; ++r) x[tail_out_pos<LOG>(r)] = v[r];
     }
-    __syncthreads();
+    ip_sync<WL>();
 }
 
 }  // namespace fmtgp

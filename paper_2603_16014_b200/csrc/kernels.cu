@@ -667,7 +667,7 @@ void fwd_array(int lattice, const Geo& g, int nvec, const ArraySrc& src, const S
 // coordinate (x_p = t 2^-m + sh_lo 2^-53, the same value as QuerySrc's 64-bit chain) and the
 // floating difference to the query coordinate (kernel_against_data, gp_core.cpp:386-397).
 // Bound per vector (query, task): every per-dimension constant lives in registers, the element
-// costs per dimension one 32-bit IMAD + LOP, one conversion, diff = (x_q - sh_lo 2^-53) - t 2^-m
+// costs per dimension one 32-bit IMAD + LOP, one DADD (u32_to_f64), diff = (x_q - sh_lo 2^-53) - t 2^-m
 // (one DFMA), u = frac(diff) and the Bernoulli polynomial in w = u^2 - u (symmetric under
 // u -> 1 - u, so the reference's min(frac(d), frac(-d)) of kernels.cpp:28-32 is implied), then
 // f = A + B v as in lattice.cu's LatGen (B2: v = w; B4: v = w^2).
@@ -709,9 +709,10 @@ struct QuerySrcLat {
 #pragma unroll
             for (int j = 0; j < DC; ++j) {
                 const uint32_t t = (uint32_t(idx) * gm[j] + oh[j]) & mask;
-                const double diff = fma(-double(t), inv_n, c[j]);
-                const double u = diff - floor(diff);
-                const double w = fma(u, u, -u);
+                // |diff| < 1, and w = u^2 - u of u = frac(diff) equals a^2 - a for a = |diff| on
+                // both sides of 0 ((1 - a)(-a) for diff < 0): no floor, no I2F (both quarter rate)
+                const double a = fabs(fma(-u32_to_f64(t), inv_n, c[j]));
+                const double w = fma(a, a, -a);
                 prod *= fma(B[j], ALPHA == 1 ? w : w * w, A[j]);
             }
             return prod;

@@ -20,25 +20,27 @@ constexpr int LAT_NT = 512;  // one radix-16 group per thread per FFT stage, 2^1
 // Lattice coordinate of real DFT-order index i against the class offset (lattice_word in
 // generator.cuh, ld_sequences.cpp:31-53): with off = oh 2^(53-m) + olo (olo < 2^(53-m)),
 //   D = ((i g + oh) mod 2^m) 2^(53-m) + olo,   x = D 2^-53 = t 2^-m + olo 2^-53  (exact in fp64),
-// so the 64-bit multiply / shift / mask chain becomes one 32-bit IMAD + LOP and one DFMA.
-// The Bernoulli kernels are polynomials in w = x^2 - x = -u (1 - u), symmetric under
+// so the 64-bit multiply / shift / mask chain becomes one 32-bit IMAD + LOP, the conversion of t
+// one exact DADD (u32_to_f64: no quarter-rate I2F.F64) and one DFMA.  The generator works with
+// y = x - 1/2 = t 2^-m + (olo 2^-53 - 1/2), exact (a multiple of 2^-53 below 1/2 in magnitude).
+// The Bernoulli kernels are polynomials in w = x^2 - x = y^2 - 1/4 = -u (1 - u), symmetric under
 // u -> 1 - u, so the reference's symmetrisation u = min(x, 1 - x) (kernels.cpp:28-32) is implied:
-//   B2: kappa = 2 pi^2 (u^2 - u + 1/6)            = ka w + kb,       ka = 2 pi^2,      kb = pi^2 / 3
+//   B2: kappa = 2 pi^2 (u^2 - u + 1/6)            = ka y^2 + kb,     ka = 2 pi^2,      kb = -pi^2 / 6
 //   B4: kappa = -(2/3) pi^4 (u^2 (u - 1)^2 - 1/30) = ka w^2 + kb,     ka = -(2/3) pi^4, kb = pi^4 / 45
-// and f = 1 + eta kappa = A + B v with v = w (B2) or w^2 (B4), A = 1 + eta kb, B = eta ka:
-// two DFMAs per dimension after x.  Dimensions are padded to the register cap DC with A = 1,
-// B = 0 (f = 1 exactly), so the unrolled loops carry no per-dimension predicates.
+// and f = 1 + eta kappa = A + B v with v = y^2 (B2) or w^2 (B4), A = 1 + eta kb, B = eta ka:
+// two fp64 operations per dimension after y (three for B4).  Dimensions are padded to the register
+// cap DC with A = 1, B = 0 (f = 1 exactly), so the unrolled loops carry no per-dimension predicates.
 template <int ALPHA>
 struct LatPoly {
     static constexpr double pi2 = 9.869604401089358618834491;
     static constexpr double ka = ALPHA == 1 ? 2.0 * pi2 : -(2.0 / 3.0) * pi2 * pi2;
-    static constexpr double kb = ALPHA == 1 ? pi2 / 3.0 : pi2 * pi2 / 45.0;
+    static constexpr double kb = ALPHA == 1 ? -pi2 / 6.0 : pi2 * pi2 / 45.0;  // B2: pi^2/3 - ka/4 (y form)
 };
 
 template <int DC, int ALPHA>
 struct LatGen {
     uint32_t gm[DC], oh[DC];
-    double ol[DC], A[DC], B[DC];
+    double ol[DC], A[DC], B[DC];  // ol: olo 2^-53 - 1/2
     double gam, inv_n;
     uint32_t mask;
     __device__ __forceinline__ void init(const LatArgs& a, int c, int o) {
@@ -53,22 +55,24 @@ struct LatGen {
                 const double eta = __ldg(a.eta + size_t(c) * a.d + j);
                 gm[j] = uint32_t(__ldg(a.g + j)) & mask;
                 oh[j] = uint32_t(off >> sh) & mask;
-                ol[j] = double(off & ((uint64_t(1) << sh) - 1)) * 0x1p-53;
+                ol[j] = fma(double(off & ((uint64_t(1) << sh) - 1)), 0x1p-53, -0.5);  // exact
                 A[j] = fma(eta, LatPoly<ALPHA>::kb, 1.0);
                 B[j] = eta * LatPoly<ALPHA>::ka;
             } else {
                 gm[j] = oh[j] = 0u;
-                ol[j] = B[j] = 0.0;
+                ol[j] = -0.5;
+                B[j] = 0.0;
                 A[j] = 1.0;
             }
         }
     }
-    // v_j = w (B2) or w^2 (B4) of dimension j at real DFT-order index i
+    // v_j = y^2 (B2) or w^2 (B4) of dimension j at real DFT-order index i
     __device__ __forceinline__ double v(int j, uint32_t i) const {
         const uint32_t t = (i * gm[j] + oh[j]) & mask;
-        const double x = fma(double(t), inv_n, ol[j]);
-        const double w = fma(x, x, -x);
-        return ALPHA == 1 ? w : w * w;
+        const double y = fma(u32_to_f64(t), inv_n, ol[j]);  // x - 1/2, exact
+        if (ALPHA == 1) return y * y;
+        const double w = fma(y, y, -0.25);
+        return w * w;
     }
     // q(i) = gamma prod_j (1 + eta_j kappa_j)  (SpatialKernel, kernels.cpp:91-103)
     __device__ __forceinline__ double q(uint32_t i) const {
@@ -214,7 +218,7 @@ __global__ void __launch_bounds__(NT) k_lat_col_fwd(LatArgs a, int l2, int lc) {
             for (int r = 0; r < 16; ++r) xs[ip_off<M_log>(brev_c<16>(r))] = x[r];
         }
         __syncthreads();
-        ip_mid_stages<NT, L1, false>(sm, C, ld, a.tw);
+        ip_mid_stages<NT, L1, false, true>(sm, C, ld, a.tw);  // warp-local after stage 0 (ipfft.cuh)
         // tail stage, results back in place
         {
             double2* xs = sm + vec * ld + S(p0);
@@ -411,8 +415,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
         for (int r = 0; r < 16; ++r) xs[ip_off<M_log>(brev_c<16>(r))] = x[r];
     }
     __syncthreads();
-    ip_mid_stages<NT, L2, false>(sm, V, lds, a.tw);
-    ip_tail_stage<NT, L2>(sm, V, lds, -1);
+    ip_mid_stages<NT, L2, false, true>(sm, V, lds, a.tw);  // warp-local after stage 0 (ipfft.cuh)
+    ip_tail_stage<NT, L2, true>(sm, V, lds, -1);
     cl.sync();  // both rows transformed: partner rows readable over DSMEM
 
     double2* rem = cl.map_shared_rank(sm, rank ^ 1);
@@ -582,8 +586,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
     if (!grad) return;
     // inverse row FFT (block_sum_vec's barriers ordered the solve's writes): DIT tail, middle
     // stages, then stage 0 fused with the conjugate four-step twiddle and the store
-    ip_tail_stage<NT, L2>(sm, V, lds, +1);
-    ip_mid_stages<NT, L2, true>(sm, V, lds, a.tw);
+    ip_tail_stage<NT, L2, (IP::A16 > 1)>(sm, V, lds, +1);  // warp-local unless stage 0 follows
+    ip_mid_stages<NT, L2, true, true>(sm, V, lds, a.tw);
     if (has_g) {
         t0.load(a.tw, gj1, l2);
         obase = twiddle(a.tw, uint64_t(gj1) * uint64_t(row), lt);
@@ -652,7 +656,7 @@ __global__ void __launch_bounds__(NT) k_lat_col_inv(LatArgs a, int l2, int lc) {
 #pragma unroll
             for (int r = 0; r < 16; ++r) xs[tail_out_pos<L1>(r)] = x[r];
         }
-        __syncthreads();
+        __syncthreads();  // (warp-local barriers here measured slower: the kernel spills)
         ip_mid_stages<NT, L1, true>(sm, 1 << lc, ld, a.tw);
         {
             const double2* xs = sm + vec * ld + S(j1);
