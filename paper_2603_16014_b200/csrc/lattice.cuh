@@ -33,6 +33,9 @@ struct LatGeo {
     Geo slot_geo() const;
 };
 
+// L3 grid cap (one gradient-dot slot per candidate x class and CTA; model.cu sizes part_dot for it)
+constexpr int LAT_MAX_INV_GRID = 256;
+
 struct LatArgs {
     int T, P, V, d, nc, m;
     long long half;           // n' slots per vector
@@ -51,10 +54,10 @@ struct LatArgs {
     const double2* yperm;     // [T][n'] yhat with each row in DIF position order (lat_perm_yhat)
     double2* Y;               // [nc][V][n'] intermediate
     double* part_mid;         // [nc][N1][2 + P]
-    double* part_dot;         // [nc][V][nblk_col][MAXD + 1]
+    double* part_dot;         // [nc][V][max(nblk_col, L3 grid)][MAXD + 1]
     int* bad;                 // [nc]
     unsigned long long* imre; // [nc][MAXT][2]
-    unsigned int* counter;    // [nc] last-CTA tickets (self-resetting)
+    unsigned int* counter;    // [0]: L3 last-CTA ticket (self-resetting)
     double* out;              // [nc][NOUT]
     const double2* tw;
     int want_grad;

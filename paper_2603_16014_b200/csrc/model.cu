@@ -1422,7 +1422,8 @@ void model_create_impl(const fmtgp_design* dz, int device, int max_cand, fmtgp_m
         if (M->lat) {
             const LatGeo& g = M->lgeo;
             M->d_part_mid = dalloc<double>(size_t(max_cand) * (size_t(1) << g.l1) * (2 + M->P));
-            M->d_part_dot = dalloc<double>(size_t(max_cand) * M->nofs * g.nblk_col * (MAXD + 1));
+            // L3 writes one gradient-dot slot per (candidate x class, CTA): grid <= LAT_MAX_INV_GRID
+            M->d_part_dot = dalloc<double>(size_t(max_cand) * M->nofs * std::max(g.nblk_col, LAT_MAX_INV_GRID) * (MAXD + 1));
             M->d_counter = dalloc<unsigned int>(size_t(max_cand) * (1 + M->nofs));
             CK(cudaMemset(M->d_counter, 0, sizeof(unsigned int) * max_cand * (1 + M->nofs)));
         }
