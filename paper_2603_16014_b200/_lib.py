@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfmtgp_b200.so")
+# FMTGP_LIB: a developer override for A/B runs of two builds of the same library (tools/r03_ab.sh)
+LIB_PATH = os.environ.get("FMTGP_LIB") or os.path.join(HERE, "libfmtgp_b200.so")
 SHARD_REC_LEN = 4 + 16 + 8 * 8 + 1 + 2 * 8  # FMTGP_SHARD_REC_LEN
 MAX_D = 16
 MAX_T = 8

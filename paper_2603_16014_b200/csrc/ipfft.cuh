@@ -88,13 +88,55 @@ struct Tw16 {
     }
 };
 
+// Stage-0 twiddles of a row transform merged with a common factor b (the per-thread base of the
+// four-step twiddle): f(k2, b w^(j1 k2)) for k2 = 0..15, from b, b w^4, b w^8, b w^12 and w:
+// 12 products per use, and the base never has to be multiplied into the 16 inputs.
+struct Tw16B {
+    double2 b0, b4, b8, b12, w1;
+    __device__ __forceinline__ void load(const double2* __restrict__ tw, int j1, int L, double2 base) {
+        w1 = tw_small(tw, uint32_t(j1), L);
+        b0 = base;
+        b4 = cmul(base, tw_small(tw, uint32_t(4 * j1), L));
+        b8 = cmul(base, tw_small(tw, uint32_t(8 * j1), L));
+        b12 = cmul(base, tw_small(tw, uint32_t(12 * j1), L));
+    }
+    template <class F>
+    __device__ __forceinline__ void each0(F&& f) const {
+        double2 cur = b0;
+#pragma unroll
+        for (int k2 = 0; k2 < 16; ++k2) {
+            if (k2 == 0) cur = b0;
+            else if (k2 == 4) cur = b4;
+            else if (k2 == 8) cur = b8;
+            else if (k2 == 12) cur = b12;
+            else cur = cmul(cur, w1);
+            f(k2, cur);
+        }
+    }
+};
+
+// The same 15 twiddles read from a shared-memory table [k2 - 1][j1] (lanes of a warp read
+// consecutive j1: conflict-free, immediate offsets): no products, no global loads.  Used by the
+// middle stages whose stride is small (few distinct j1), see IpTw below.
+template <int ML>
+struct Tw16S {
+    const double2* p;  // table + j1
+    template <class F>
+    __device__ __forceinline__ void each(F&& f) const {
+#pragma unroll
+        for (int k2 = 1; k2 < 16; ++k2) f(k2, p[(k2 - 1) << ML]);
+    }
+};
+
 // DIF radix-16 group in registers: v[j2] natural in; out v[r] = Y[brev4(r)] * w^(j1 brev4(r)).
-__device__ __forceinline__ void dif16_regs(double2 (&v)[16], const Tw16& t) {
+template <class TW>
+__device__ __forceinline__ void dif16_regs(double2 (&v)[16], const TW& t) {
     reg_dft<16>(v, -1);
     t.each([&](int k2, double2 w) { v[brev_c<16>(k2)] = cmul(v[brev_c<16>(k2)], w); });
 }
 // DIT radix-16 group: v[k2] natural in; untwiddle, conjugate DFT; out v[r] = y[brev4(r)].
-__device__ __forceinline__ void dit16_regs(double2 (&v)[16], const Tw16& t) {
+template <class TW>
+__device__ __forceinline__ void dit16_regs(double2 (&v)[16], const TW& t) {
     t.each([&](int k2, double2 w) { v[k2] = cmulc(v[k2], w); });
     reg_dft<16>(v, +1);
 }
@@ -111,9 +153,40 @@ __device__ __forceinline__ void ip_sync() {
     else __syncthreads();
 }
 
+// Shared-memory twiddle tables of the middle stages (stage s >= 1, stride 2^ML, ML = LOG - 4(s+1)):
+// 15 2^ML entries per stage, kept for the stages with ML <= LAT_STW_MAXML.  A kernel declares
+// `__shared__ double2 stw[IpTw<LOG>::N]`, fills it once (ip_tw_fill, then a CTA barrier) and
+// passes it to ip_mid_stages<..., STW = true>.  Measured on config 4: the row kernel (L2) gains
+// 1.5 %; the column kernels (L1, L3) spill with it and lose 3 - 20 %, so they keep Tw16.
+#ifndef LAT_STW_MAXML
+#define LAT_STW_MAXML 5
+#endif
+template <int LOG>
+struct IpTw {
+    static constexpr int A = Ip<LOG>::A16;
+    static constexpr int ml(int s) { return LOG - 4 * (s + 1); }
+    static constexpr bool on(int s) { return s >= 1 && s < A && ml(s) <= LAT_STW_MAXML; }
+    static constexpr int n(int s) { return on(s) ? (15 << ml(s)) : 0; }
+    static constexpr int off(int s) { return s <= 1 ? 0 : n(1); }  // stages 1, 2 only (LOG <= 13)
+    static constexpr int N = n(1) + n(2) > 0 ? n(1) + n(2) : 1;
+};
+template <int NT, int LOG>
+__device__ __forceinline__ void ip_tw_fill(double2* stw, const double2* __restrict__ tw) {
+#pragma unroll
+    for (int s = 1; s <= 2; ++s) {
+        if (!IpTw<LOG>::on(s)) continue;
+        const int ML = IpTw<LOG>::ml(s);
+        for (int e = threadIdx.x; e < (15 << ML); e += NT) {
+            const int k2 = (e >> ML) + 1, j1 = e & ((1 << ML) - 1);
+            stw[IpTw<LOG>::off(s) + e] = tw_small(tw, uint32_t(j1 * k2), ML + 4);
+        }
+    }
+}
+
 // One middle radix-16 stage s over nvec vectors (stride ld), then a barrier (WL: warp barrier).
-template <int NT, int LOG, int S_, bool DIT, bool WL = false>
-__device__ __forceinline__ void ip_stage(double2* sm, int nvec, int ld, const double2* __restrict__ tw) {
+template <int NT, int LOG, int S_, bool DIT, bool WL = false, bool STW = false>
+__device__ __forceinline__ void ip_stage(double2* sm, int nvec, int ld, const double2* __restrict__ tw,
+                                         const double2* stw) {
     constexpr int ML = LOG - 4 * (S_ + 1);
     constexpr int GPV = LOG - 4;  // log2 groups per vector
     const int total = nvec << GPV;
@@ -122,16 +195,23 @@ __device__ __forceinline__ void ip_stage(double2* sm, int nvec, int ld, const do
         const int vec = gi >> GPV, q = gi & ((1 << GPV) - 1);
         const int j1 = q & ((1 << ML) - 1);
         const int base = ((q >> ML) << (ML + 4)) + j1;
-        Tw16 t;
-        t.load(tw, j1, ML + 4);
         double2* x = sm + vec * ld + sidx<true>(base);
         double2 v[16];
+        auto body = [&](const auto& t) {
 #pragma unroll
-        for (int r = 0; r < 16; ++r) v[r] = x[ip_off<ML>(r)];
-        if (DIT) dit16_regs(v, t);
-        else dif16_regs(v, t);
+            for (int r = 0; r < 16; ++r) v[r] = x[ip_off<ML>(r)];
+            if (DIT) dit16_regs(v, t);
+            else dif16_regs(v, t);
 #pragma unroll
-        for (int r = 0; r < 16; ++r) x[ip_off<ML>(brev_c<16>(r))] = v[r];
+            for (int r = 0; r < 16; ++r) x[ip_off<ML>(brev_c<16>(r))] = v[r];
+        };
+        if constexpr (STW && IpTw<LOG>::on(S_)) {  // the kernel passes its filled table
+            body(Tw16S<ML>{stw + IpTw<LOG>::off(S_) + j1});
+        } else {
+            Tw16 t;
+            t.load(tw, j1, ML + 4);
+            body(t);
+        }
     }
     ip_sync<WL>();
 }
@@ -139,16 +219,17 @@ __device__ __forceinline__ void ip_stage(double2* sm, int nvec, int ld, const do
 // Middle radix-16 stages 1 .. A16-1 (stage 0 is fused by the kernels): DIF ascending, DIT descending.
 // WL: warp barriers between them; the DIT form ends with a CTA barrier anyway (stage 0 reads
 // across blocks), unless LAST_WL (the caller synchronises the CTA itself).
-template <int NT, int LOG, bool DIT, bool WL = false>
-__device__ __forceinline__ void ip_mid_stages(double2* sm, int nvec, int ld, const double2* __restrict__ tw) {
+template <int NT, int LOG, bool DIT, bool WL = false, bool STW = false>
+__device__ __forceinline__ void ip_mid_stages(double2* sm, int nvec, int ld, const double2* __restrict__ tw,
+                                              const double2* stw = nullptr) {
     static_assert(!WL || LOG <= 13, "warp-local stages need blocks of <= 32 groups");
     constexpr int A = Ip<LOG>::A16;
     if constexpr (!DIT) {
-        if constexpr (A > 1) ip_stage<NT, LOG, 1, false, WL>(sm, nvec, ld, tw);
-        if constexpr (A > 2) ip_stage<NT, LOG, 2, false, WL>(sm, nvec, ld, tw);
+        if constexpr (A > 1) ip_stage<NT, LOG, 1, false, WL, STW>(sm, nvec, ld, tw, stw);
+        if constexpr (A > 2) ip_stage<NT, LOG, 2, false, WL, STW>(sm, nvec, ld, tw, stw);
     } else {
-        if constexpr (A > 2) ip_stage<NT, LOG, 2, true, WL>(sm, nvec, ld, tw);
-        if constexpr (A > 1) ip_stage<NT, LOG, 1, true, false>(sm, nvec, ld, tw);
+        if constexpr (A > 2) ip_stage<NT, LOG, 2, true, WL, STW>(sm, nvec, ld, tw, stw);
+        if constexpr (A > 1) ip_stage<NT, LOG, 1, true, false, STW>(sm, nvec, ld, tw, stw);
     }
 }
 

@@ -16,6 +16,15 @@ namespace cg = cooperative_groups;
 
 constexpr int LAT_NT = 512;  // one radix-16 group per thread per FFT stage, 2^13-element tiles
 
+// compile-time switches of measured variants (tools/r03_variants.sh builds A/B libraries)
+#ifndef LAT_L2_PAIRFORM
+#define LAT_L2_PAIRFORM 1  // L2 solve: pair form of the real-FFT post/pre-processing, branch-free main loop
+#endif
+#ifndef LAT_L2_UNROLL
+#define LAT_L2_UNROLL 1    // unroll factor of that loop
+#endif
+constexpr int LAT_UNROLL_V = LAT_L2_UNROLL;
+
 // ------------------------------------------------------------------ generator on the fly
 // Lattice coordinate of real DFT-order index i against the class offset (lattice_word in
 // generator.cuh, ld_sequences.cpp:31-53): with off = oh 2^(53-m) + olo (olo < 2^(53-m)),
@@ -254,14 +263,17 @@ __global__ void __launch_bounds__(NT) k_lat_col_fwd(LatArgs a, int l2, int lc) {
 // product det into pm 2^pe, quad = r^H A^-1 r, chat = A^-1 r, A^-1, the non-real / pivot maxima
 // of Algorithm 1's two stages, fast_gram.cpp:167-178) with one reciprocal instead of two and no
 // triangular solves.  A = [A00, A01, A11] (pair order), status 1 on a non-positive pivot.
+template <bool TRACK_IM = true>
 __device__ __forceinline__ int herm2_solve(const double2* A, const double2* r, double& pm, int& pe, double& quad,
                                            double2* chat, double2* Ainv, double* imx, double* rex) {
     int status = 0;
     double a = A[0].x;
     const double d = A[2].x;
     const double2 b = A[1];
-    imx[0] = fmax(imx[0], fabs(A[0].y));
-    imx[1] = fmax(imx[1], fabs(A[2].y));
+    if constexpr (TRACK_IM) {  // (the pair-form loop tracks max |Im H| of the diagonal class instead)
+        imx[0] = fmax(imx[0], fabs(A[0].y));
+        imx[1] = fmax(imx[1], fabs(A[2].y));
+    }
     if (!(a > 0.0)) status = 1, a = 1.0;
     double det = fma(a, d, -(b.x * b.x + b.y * b.y));  // a * (second pivot)
     if (!(det > 0.0)) status = 1, det = a;              // second pivot -> 1, as ldl_core
@@ -278,8 +290,16 @@ __device__ __forceinline__ int herm2_solve(const double2* A, const double2* r, d
     Ainv[1] = make_double2(-b.x * idet, -b.y * idet);
     Ainv[2] = make_double2(a * idet, 0.0);
     // chat = A^-1 r: A^-1 = [[d, -b], [-conj b, a]] / det
-    chat[0] = cscale(csub(cscale(r[0], d), cmul(b, r[1])), idet);
-    chat[1] = cscale(csub(cscale(r[1], a), cmulc(r[0], b)), idet);
+    if constexpr (TRACK_IM) {
+        chat[0] = cscale(csub(cscale(r[0], d), cmul(b, r[1])), idet);
+        chat[1] = cscale(csub(cscale(r[1], a), cmulc(r[0], b)), idet);
+    } else {  // from the entries of A^-1 just formed: 6 operations per component instead of 10
+        const double2 o = Ainv[1];
+        chat[0] = make_double2(fma(o.x, r[1].x, fma(-o.y, r[1].y, Ainv[0].x * r[0].x)),
+                               fma(o.x, r[1].y, fma(o.y, r[1].x, Ainv[0].x * r[0].y)));
+        chat[1] = make_double2(fma(o.x, r[0].x, fma(o.y, r[0].y, Ainv[2].x * r[1].x)),
+                               fma(o.x, r[0].y, fma(-o.y, r[0].x, Ainv[2].x * r[1].y)));
+    }
     quad = r[0].x * chat[0].x + r[0].y * chat[0].y + r[1].x * chat[1].x + r[1].y * chat[1].y;
     return status;
 }
@@ -301,12 +321,24 @@ __host__ __device__ constexpr int cls_distinct(int y) {
     return 0;
 }
 
+template <int T>
+__host__ __device__ constexpr bool pair_is_diag(int y) {
+    int q = 0;
+    for (int a = 0; a < T; ++a)
+        for (int b = a; b < T; ++b, ++q)
+            if (q == y) return a == b;
+    return false;
+}
+
 // DIST: the class map is cls_distinct<T> (compile time: no per-pair class selects); otherwise
 // it comes from LatArgs::pair_ofs.
 // Row transforms are in place (ipfft.cuh): DIF stage 0 applies the four-step twiddle
-// w_{n'}^(row j2) to its inputs, the solve walks the DIF output in POSITION order (bank-conflict
-// free; yhat comes in the matching permuted layout, LatArgs::yperm), and the last DIT stage
-// applies the conjugate twiddle on its way to HBM.
+// w_{n'}^(row j2), j2 = gj1 + r N2/16, split as a per-CTA step table on its inputs (s_ostep[r])
+// and a per-thread base merged into the stage's output twiddles (Tw16B: the base is never
+// multiplied into the inputs); the middle stage reads its twiddles from a shared-memory table
+// (IpTw); the solve walks the DIF output in POSITION order (bank-conflict free; yhat comes in the
+// matching permuted layout, LatArgs::yperm), and the last DIT stage applies the conjugates on
+// its way to HBM.
 template <int NT, int T, bool DIST, int L2>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArgs a, int l1) {
     constexpr int l2 = L2;
@@ -316,8 +348,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
     double2* sm = reinterpret_cast<double2*>(smraw);  // [V][padded N2]
     constexpr auto S = sidx<true>;
     __shared__ double s_coef[P], s_xi[P], s_wR[P];
+    __shared__ double s_coefh[P], s_wRh[P];  // halves: the pair-form loop works with 2 H and Z / 2
     __shared__ int s_cls[P];
     __shared__ double2 s_ostep[16], s_rstep[16];
+    __shared__ double2 s_tw[IpTw<L2>::N];  // middle-stage twiddles, filled in the prologue
     cg::cluster_group cl = cg::this_cluster();
     const int rank = int(cl.block_rank());
     // local row index of this CTA's row in the exchange blocks (a chunked launch: row chunk a.chunk)
@@ -337,6 +371,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
         s_coef[p] = __ldg(a.coef + size_t(c) * P + p);
         s_xi[p] = __ldg(a.xi + size_t(c) * P + p);
         s_wR[p] = (a.pair_a[p] == a.pair_b[p] ? 1.0 : 2.0) * __ldg(a.Rpair + size_t(c) * P + p);
+        s_coefh[p] = 0.5 * s_coef[p];
+        s_wRh[p] = 0.5 * s_wR[p];
         s_cls[p] = a.pair_ofs[p];
     } else if (threadIdx.x >= 32 && threadIdx.x < 48) {
         const int u = threadIdx.x - 32;  // four-step step table: w^(row M u), M = N2 / 16
@@ -347,12 +383,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
         const int u = threadIdx.x - 64;
         s_rstep[u] = twiddle(a.tw, uint64_t(u) * uint64_t(L2 >= 4 ? (NT >> (L2 - 4)) : 0), l2 + 1);
     }
+    ip_tw_fill<NT, L2>(s_tw, a.tw);
     // this thread's radix-16 group of stage 0 / the last DIT stage: class gvec, offset gj1
     const bool has_g = int(threadIdx.x) < (V << M_log);
     const int gvec = threadIdx.x >> M_log, gj1 = threadIdx.x & ((1 << M_log) - 1);
-    double2 obase = twiddle(a.tw, uint64_t(gj1) * uint64_t(row), lt);
-    Tw16 t0;
-    t0.load(a.tw, gj1, l2);
+    // stage-0 twiddles w_{N2}^(gj1 k2) merged with this thread's four-step base w_{n'}^(row gj1)
+    Tw16B t0;
+    t0.load(a.tw, gj1, l2, twiddle(a.tw, uint64_t(gj1) * uint64_t(row), lt));
     // solve iteration space (positions pA of row A; Hermitian partner position pB of row B):
     //   non-self clusters: rank r takes pA in [r N2/2, (r+1) N2/2), partner N2-1-k2a -> pB = N2-1-pA
     //   row N1/2 (rank 1 of cluster 0): pA in [0, N2/2), same partner map
@@ -409,13 +446,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
         double2* xs = sm + gvec * lds + S(gj1);
         double2 x[16];
 #pragma unroll
-        for (int r = 0; r < 16; ++r) x[r] = cmul(xs[ip_off<M_log>(r)], cmul(obase, s_ostep[r]));
-        dif16_regs(x, t0);
+        for (int r = 0; r < 16; ++r) x[r] = cmul(xs[ip_off<M_log>(r)], s_ostep[r]);
+        reg_dft<16>(x, -1);
+        t0.each0([&](int k2, double2 w) { x[brev_c<16>(k2)] = cmul(x[brev_c<16>(k2)], w); });
 #pragma unroll
         for (int r = 0; r < 16; ++r) xs[ip_off<M_log>(brev_c<16>(r))] = x[r];
     }
     __syncthreads();
-    ip_mid_stages<NT, L2, false, true>(sm, V, lds, a.tw);  // warp-local after stage 0 (ipfft.cuh)
+    ip_mid_stages<NT, L2, false, true, true>(sm, V, lds, a.tw, s_tw);  // warp-local after stage 0 (ipfft.cuh)
     ip_tail_stage<NT, L2, true>(sm, V, lds, -1);
     cl.sync();  // both rows transformed: partner rows readable over DSMEM
 
@@ -440,8 +478,118 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
         k2b = N2 - 1 - k2a;
         return N2 - 1 - pA;
     };
+#if LAT_L2_PAIRFORM
+    // Main loop of every cluster but q = 0 (no packed slot 0, no self-paired slot): both sides of a
+    // Hermitian pair in one pass.  With S = za + conj(zb), D = za - conj(zb), w = exp(-2 pi i k / n):
+    //   2 H(k) = S - i w D,   2 H(N' - k) = conj(S) - i conj(w) conj(D)   (r2c_post of both sides),
+    // and for the class adjoints ZA, ZB (computed with half weights): E = ZA + conj(ZB),
+    // D' = ZA - conj(ZB), O = D' conj(w): z(k) = E + i O, z(N' - k) = conj(E) + i conj(O) (c2r_pre
+    // of both sides) — 12 fp64 operations per class each instead of 2 x 14.  The factors 1/2 move
+    // into the per-pair tables (s_coefh, s_wRh) and the Parseval weight 2.
+    if (!selfrow) {
+        double hmax = 0.0;  // T = 2: max |Im 2H| of the diagonal class (both diagonal entries scale it)
+#pragma unroll(LAT_UNROLL_V)
+        for (int pA = pbeg + int(threadIdx.x), it = 0; pA < pend; pA += NT, ++it) {
+            const int k2a = IP::freq(pA), pB = N2 - 1 - pA, k2b = N2 - 1 - k2a;
+            double2 rA[T], rB[T];
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+                rA[t] = yp[size_t(t) * half + ((long long)rowA << l2) + pA];
+                rB[t] = yp[size_t(t) * half + ((long long)rowB << l2) + pB];
+            }
+            const double2 w = cmul(wrow, s_rstep[it]);
+            double2 HA[P], HB[P];
+            auto post2 = [&](int o, double2& ha, double2& hb) {
+                const double2 za = bufA[o * lds + S(pA)], zb = bufB[o * lds + S(pB)];
+                const double Sx = za.x + zb.x, Sy = za.y - zb.y, Dx = za.x - zb.x, Dy = za.y + zb.y;
+                const double P1 = fma(w.x, Dy, w.y * Dx), P2 = fma(w.y, Dy, -(w.x * Dx));
+                ha = make_double2(Sx + P1, Sy + P2);
+                hb = make_double2(Sx - P1, P2 - Sy);
+            };
+            if constexpr (DIST) {
+                double2 ca[P - T + 1], cb[P - T + 1];
+#pragma unroll
+                for (int o = 0; o < P - T + 1; ++o) post2(o, ca[o], cb[o]);
+#pragma unroll
+                for (int x = 0; x < P; ++x) HA[x] = ca[cls_distinct<T>(x)], HB[x] = cb[cls_distinct<T>(x)];
+            } else {
+#pragma unroll
+                for (int x = 0; x < P; ++x) post2(s_cls[x], HA[x], HB[x]);
+            }
+            if constexpr (T == 2) hmax = fmax(hmax, fmax(fabs(HA[0].y), fabs(HB[0].y)));
+            double2 ZA[P], ZB[P];
+#pragma unroll
+            for (int side = 0; side < 2; ++side) {
+                const double2* H = side == 0 ? HA : HB;
+                double2 A[P], r[T], ch[T], Ai[P];
+#pragma unroll
+                for (int x = 0; x < P; ++x)
+                    A[x] = make_double2(fma(s_coefh[x], H[x].x, s_xi[x]), s_coefh[x] * H[x].y);
+#pragma unroll
+                for (int t = 0; t < T; ++t) r[t] = side == 0 ? rA[t] : rB[t];
+                double qd;
+                int st;
+                if constexpr (T == 2) st = herm2_solve<false>(A, r, lpm, lpe, qd, ch, Ai, imx, rex);
+                else st = ldl_core<T, true>(A, r, grad, lpm, lpe, qd, ch, Ai, imx, rex);
+                if (st == 1) {
+                    const long long sl = side == 0 ? ((long long)rowA << l2) + k2a : ((long long)rowB << l2) + k2b;
+                    if (sl < first_bad) first_bad = sl;
+                }
+                acc[1] += 2.0 * qd;  // slot k >= 1 stands for frequencies k and n - k
+                if (grad) {
+                    // M = A^-1 - chat chat^H; its diagonal is real (Im = 0 exactly, not a rounding residue)
+                    double2 Mq[P];
+                    int x = 0;
+#pragma unroll
+                    for (int i = 0; i < T; ++i)
+#pragma unroll
+                        for (int j = i; j < T; ++j, ++x) {
+                            if (i == j) Mq[x] = make_double2(Ai[x].x - fma(ch[i].x, ch[i].x, ch[i].y * ch[i].y), 0.0);
+                            else Mq[x] = csub(Ai[x], cmulc(ch[i], ch[j]));
+                        }
+                    x = 0;
+#pragma unroll
+                    for (int i = 0; i < T; ++i)
+#pragma unroll
+                        for (int j = i; j < T; ++j, ++x) {  // H holds 2 H: the Parseval weight 2
+                            if (i == j) acc[2 + x] = fma(Mq[x].x, H[x].x, acc[2 + x]);
+                            else acc[2 + x] += Mq[x].x * H[x].x + Mq[x].y * H[x].y;
+                        }
+#pragma unroll
+                    for (int o = 0; o < P; ++o) {
+                        double2 z = make_double2(0.0, 0.0);
+#pragma unroll
+                        for (int y = 0; y < P; ++y)
+                            if (cls(y) == o) {
+                                z.x = fma(s_wRh[y], Mq[y].x, z.x);
+                                if (!pair_is_diag<T>(y)) z.y = fma(s_wRh[y], Mq[y].y, z.y);
+                            }
+                        if (side == 0) ZA[o] = z;
+                        else ZB[o] = z;
+                    }
+                }
+            }
+            if (grad) {
+#pragma unroll
+                for (int o = 0; o < P; ++o) {
+                    if (o >= V) break;
+                    const double Ex = ZA[o].x + ZB[o].x, Ey = ZA[o].y - ZB[o].y;
+                    const double Dx = ZA[o].x - ZB[o].x, Dy = ZA[o].y + ZB[o].y;
+                    const double Ox = fma(Dx, w.x, Dy * w.y), Oy = fma(Dy, w.x, -(Dx * w.y));
+                    bufA[o * lds + S(pA)] = make_double2(Ex - Oy, Ey + Ox);
+                    bufB[o * lds + S(pB)] = make_double2(Ex + Oy, Ox - Ey);
+                }
+            }
+        }
+        if constexpr (T == 2) {
+            imx[0] = fmax(imx[0], fabs(s_coefh[0]) * hmax);
+            imx[1] = fmax(imx[1], fabs(s_coefh[2]) * hmax);
+        }
+    }
+#endif
 #pragma unroll 1
     for (int pA = pbeg + int(threadIdx.x), it = 0; pA < pend; pA += NT, ++it) {
+        if (LAT_L2_PAIRFORM && !selfrow) break;  // done above
         const int k2a = IP::freq(pA);
         if (row0 && k2a > N2 / 2) continue;  // its partner's thread owns the pair
         int k2b;
@@ -587,21 +735,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
     // inverse row FFT (block_sum_vec's barriers ordered the solve's writes): DIT tail, middle
     // stages, then stage 0 fused with the conjugate four-step twiddle and the store
     ip_tail_stage<NT, L2, (IP::A16 > 1)>(sm, V, lds, +1);  // warp-local unless stage 0 follows
-    ip_mid_stages<NT, L2, true, true>(sm, V, lds, a.tw);
+    ip_mid_stages<NT, L2, true, true, true>(sm, V, lds, a.tw, s_tw);
     if (has_g) {
-        t0.load(a.tw, gj1, l2);
-        obase = twiddle(a.tw, uint64_t(gj1) * uint64_t(row), lt);
+        t0.load(a.tw, gj1, l2, twiddle(a.tw, uint64_t(gj1) * uint64_t(row), lt));
         const double2* xs = sm + gvec * lds + S(gj1);
         double2 x[16];
 #pragma unroll
         for (int r = 0; r < 16; ++r) x[r] = xs[ip_off<M_log>(r)];
-        dit16_regs(x, t0);
+        t0.each0([&](int k2, double2 w) { x[k2] = cmulc(x[k2], w); });  // conj of the merged twiddles
+        reg_dft<16>(x, +1);
         double2* const Yo = (a.Yout ? a.Yout : a.Y) + size_t(c) * a.V * a.half;
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
             const int j2 = gj1 + (brev_c<16>(r) << M_log);
             Yo[xoff_r(a, j2 >> a.lwc, gvec, li, j2 & (a.WC - 1))] =
-                cmulc(x[r], cmul(obase, s_ostep[brev_c<16>(r)]));
+                cmulc(x[r], s_ostep[brev_c<16>(r)]);
         }
     }
 }
