@@ -115,6 +115,50 @@ struct Tw16B {
     }
 };
 
+// Stride-2 stage (ML = 1): j1 is 0 or 1, so the twiddles are 1 or the constants w_32^k2 — selected
+// per lane (FSEL, off the fp64 pipe) instead of 4 table reads and 11 products (ip_stage<..., C1>).
+// Measured on config 4: L1 -1 %, L3 +2 % (it spills more), so only the forward column kernel uses it.
+struct Tw16C1 {
+    int j1;
+    template <class F>
+    __device__ __forceinline__ void each(F&& f) const {
+        constexpr double C32[16] = {1.0,
+                                    0.9807852804032304491261822,
+                                    0.9238795325112867561281832,
+                                    0.8314696123025452370787884,
+                                    0.7071067811865475244008444,
+                                    0.5555702330196022247428308,
+                                    0.38268343236508977172846,
+                                    0.1950903220161282678482849,
+                                    0.0,
+                                    -0.1950903220161282678482849,
+                                    -0.38268343236508977172846,
+                                    -0.5555702330196022247428308,
+                                    -0.7071067811865475244008444,
+                                    -0.8314696123025452370787884,
+                                    -0.9238795325112867561281832,
+                                    -0.9807852804032304491261822};
+        constexpr double S32[16] = {0.0,
+                                    0.1950903220161282678482849,
+                                    0.38268343236508977172846,
+                                    0.5555702330196022247428308,
+                                    0.7071067811865475244008444,
+                                    0.8314696123025452370787884,
+                                    0.9238795325112867561281832,
+                                    0.9807852804032304491261822,
+                                    1.0,
+                                    0.9807852804032304491261822,
+                                    0.9238795325112867561281832,
+                                    0.8314696123025452370787884,
+                                    0.7071067811865475244008444,
+                                    0.5555702330196022247428308,
+                                    0.38268343236508977172846,
+                                    0.1950903220161282678482849};
+#pragma unroll
+        for (int k2 = 1; k2 < 16; ++k2) f(k2, make_double2(j1 ? C32[k2] : 1.0, j1 ? -S32[k2] : 0.0));
+    }
+};
+
 // The same 15 twiddles read from a shared-memory table [k2 - 1][j1] (lanes of a warp read
 // consecutive j1: conflict-free, immediate offsets): no products, no global loads.  Used by the
 // middle stages whose stride is small (few distinct j1), see IpTw below.
@@ -184,7 +228,7 @@ __device__ __forceinline__ void ip_tw_fill(double2* stw, const double2* __restri
 }
 
 // One middle radix-16 stage s over nvec vectors (stride ld), then a barrier (WL: warp barrier).
-template <int NT, int LOG, int S_, bool DIT, bool WL = false, bool STW = false>
+template <int NT, int LOG, int S_, bool DIT, bool WL = false, bool STW = false, bool C1 = false>
 __device__ __forceinline__ void ip_stage(double2* sm, int nvec, int ld, const double2* __restrict__ tw,
                                          const double2* stw) {
     constexpr int ML = LOG - 4 * (S_ + 1);
@@ -207,6 +251,8 @@ __device__ __forceinline__ void ip_stage(double2* sm, int nvec, int ld, const do
         };
         if constexpr (STW && IpTw<LOG>::on(S_)) {  // the kernel passes its filled table
             body(Tw16S<ML>{stw + IpTw<LOG>::off(S_) + j1});
+        } else if constexpr (ML == 1 && C1) {
+            body(Tw16C1{j1});
         } else {
             Tw16 t;
             t.load(tw, j1, ML + 4);
@@ -219,17 +265,17 @@ __device__ __forceinline__ void ip_stage(double2* sm, int nvec, int ld, const do
 // Middle radix-16 stages 1 .. A16-1 (stage 0 is fused by the kernels): DIF ascending, DIT descending.
 // WL: warp barriers between them; the DIT form ends with a CTA barrier anyway (stage 0 reads
 // across blocks), unless LAST_WL (the caller synchronises the CTA itself).
-template <int NT, int LOG, bool DIT, bool WL = false, bool STW = false>
+template <int NT, int LOG, bool DIT, bool WL = false, bool STW = false, bool C1 = false>
 __device__ __forceinline__ void ip_mid_stages(double2* sm, int nvec, int ld, const double2* __restrict__ tw,
                                               const double2* stw = nullptr) {
     static_assert(!WL || LOG <= 13, "warp-local stages need blocks of <= 32 groups");
     constexpr int A = Ip<LOG>::A16;
     if constexpr (!DIT) {
-        if constexpr (A > 1) ip_stage<NT, LOG, 1, false, WL, STW>(sm, nvec, ld, tw, stw);
-        if constexpr (A > 2) ip_stage<NT, LOG, 2, false, WL, STW>(sm, nvec, ld, tw, stw);
+        if constexpr (A > 1) ip_stage<NT, LOG, 1, false, WL, STW, C1>(sm, nvec, ld, tw, stw);
+        if constexpr (A > 2) ip_stage<NT, LOG, 2, false, WL, STW, C1>(sm, nvec, ld, tw, stw);
     } else {
-        if constexpr (A > 2) ip_stage<NT, LOG, 2, true, WL, STW>(sm, nvec, ld, tw, stw);
-        if constexpr (A > 1) ip_stage<NT, LOG, 1, true, false, STW>(sm, nvec, ld, tw, stw);
+        if constexpr (A > 2) ip_stage<NT, LOG, 2, true, WL, STW, C1>(sm, nvec, ld, tw, stw);
+        if constexpr (A > 1) ip_stage<NT, LOG, 1, true, false, STW, C1>(sm, nvec, ld, tw, stw);
     }
 }
 

@@ -17,6 +17,9 @@ namespace cg = cooperative_groups;
 constexpr int LAT_NT = 512;  // one radix-16 group per thread per FFT stage, 2^13-element tiles
 
 // compile-time switches of measured variants (tools/r03_variants.sh builds A/B libraries)
+#ifndef LAT_GEN_PROD
+#define LAT_GEN_PROD 1     // L1 / L3 lattice generator in product form (LatGen::init_prod)
+#endif
 #ifndef LAT_L2_PAIRFORM
 #define LAT_L2_PAIRFORM 1  // L2 solve: pair form of the real-FFT post/pre-processing, branch-free main loop
 #endif
@@ -89,6 +92,85 @@ struct LatGen {
 #pragma unroll
         for (int j = 0; j < DC; ++j) prod *= fma(B[j], v(j, i), A[j]);
         return prod;
+    }
+    // ---- product form (every eta_j kappa-slope B_j != 0): f_j = B_j g_j with g_j = v_j + A_j / B_j, so
+    //   q = Gam prod_j g_j,  Gam = gamma prod_j B_j,   g_j = fma(y, y, c_j)  (B2; B4: fma(w, w, c_j))
+    // — one fp64 operation per dimension less than A + B v — and kappa_j = ka h_j, h_j = v_j + kb / ka:
+    //   dq/deta_j = [gamma ka prod_{k != j} B_k] h_j prod_{k != j} g_k,
+    // the bracket applied once per reduced sum (dscale).  Padded dimensions generate y = 0 and g = 1.
+    // init_prod() returns false when some B_j is too small to divide by (callers then use q / dq_acc).
+    static constexpr double ke = LatPoly<ALPHA>::kb / LatPoly<ALPHA>::ka;  // -1/12 (B2), -1/30 (B4)
+    __device__ __forceinline__ bool init_prod(const LatArgs& a, int c, int o) {
+        init(a, c, o);
+        bool ok = true;
+        double G = gam;
+#pragma unroll
+        for (int j = 0; j < DC; ++j) {
+            if (j < a.d) {
+                ok = ok && fabs(B[j]) > 1e-100;
+                G *= B[j];
+                A[j] = A[j] / B[j];  // c_j
+            } else {
+                ol[j] = 0.0;                              // y = 0
+                A[j] = ALPHA == 1 ? 1.0 : 15.0 / 16.0;    // g = 1 exactly
+            }
+        }
+        if (ok) gam = G;
+        return ok;
+    }
+    __device__ __forceinline__ double yv(int j, uint32_t i) const {
+        const uint32_t t = (i * gm[j] + oh[j]) & mask;
+        const double y = fma(u32_to_f64(t), inv_n, ol[j]);
+        return ALPHA == 1 ? y : fma(y, y, -0.25);
+    }
+    __device__ __forceinline__ double q_prod(uint32_t i) const {
+        double prod = gam;
+#pragma unroll
+        for (int j = 0; j < DC; ++j) {
+            const double u = yv(j, i);
+            prod *= fma(u, u, A[j]);
+        }
+        return prod;
+    }
+    // acc_j += W h_j prod_{k != j} g_k (unscaled; see dscale)
+    __device__ __forceinline__ void dq_acc_prod(uint32_t i, double W, double* acc) const {
+        double g[DC], h[DC];
+#pragma unroll
+        for (int j = 0; j < DC; ++j) {
+            const double u = yv(j, i);
+            g[j] = fma(u, u, A[j]);
+            h[j] = fma(u, u, ke);
+        }
+        if constexpr (DC == 4) {  // pair tree: 12 operations instead of 14
+            const double Wa = W * (g[0] * g[1]), Wb = W * (g[2] * g[3]);
+            acc[0] = fma(h[0], g[1] * Wb, acc[0]);
+            acc[1] = fma(h[1], g[0] * Wb, acc[1]);
+            acc[2] = fma(h[2], g[3] * Wa, acc[2]);
+            acc[3] = fma(h[3], g[2] * Wa, acc[3]);
+        } else if constexpr (DC == 2) {
+            acc[0] = fma(h[0], g[1] * W, acc[0]);
+            acc[1] = fma(h[1], g[0] * W, acc[1]);
+        } else {
+            double pre = W, t[DC];
+#pragma unroll
+            for (int j = 0; j < DC; ++j) {
+                t[j] = pre * h[j];
+                pre *= g[j];
+            }
+            double suf = 1.0;
+#pragma unroll
+            for (int j = DC - 1; j >= 0; --j) {
+                acc[j] = fma(t[j], suf, acc[j]);
+                suf *= g[j];
+            }
+        }
+    }
+    // factor of acc_j after the reduction: gamma ka prod_{k != j, k < d} B_k (from the hyperparameters)
+    static __device__ double dscale(const LatArgs& a, int c, int j) {
+        double s = __ldg(a.gamma + c) * LatPoly<ALPHA>::ka;
+        for (int k = 0; k < a.d; ++k)
+            if (k != j) s *= __ldg(a.eta + size_t(c) * a.d + k) * LatPoly<ALPHA>::ka;
+        return s;
     }
     // acc_j += W dq/deta_j = W gamma kappa_j prod_{k != j} f_k  (prefix / suffix products: f may vanish)
     __device__ __forceinline__ void dq_acc(uint32_t i, double W, double* acc) const {
@@ -212,11 +294,22 @@ __global__ void __launch_bounds__(NT) k_lat_col_fwd(LatArgs a, int l2, int lc) {
         double2 x[16];
         {
             LatGen<DC, ALPHA> G;
-            G.init(a, c, o);
+#if LAT_GEN_PROD
+            if (G.init_prod(a, c, o)) {
 #pragma unroll
-            for (int r = 0; r < 16; ++r) {
-                const uint32_t J = (uint32_t(j1 + (r << M_log)) << l2) + c0 + uint32_t(vec);
-                x[r] = make_double2(G.q(2u * J), G.q(2u * J + 1u));
+                for (int r = 0; r < 16; ++r) {
+                    const uint32_t J = (uint32_t(j1 + (r << M_log)) << l2) + c0 + uint32_t(vec);
+                    x[r] = make_double2(G.q_prod(2u * J), G.q_prod(2u * J + 1u));
+                }
+            } else
+#endif
+            {
+                G.init(a, c, o);
+#pragma unroll
+                for (int r = 0; r < 16; ++r) {
+                    const uint32_t J = (uint32_t(j1 + (r << M_log)) << l2) + c0 + uint32_t(vec);
+                    x[r] = make_double2(G.q(2u * J), G.q(2u * J + 1u));
+                }
             }
         }
         dif16_regs(x, t0);
@@ -227,7 +320,7 @@ __global__ void __launch_bounds__(NT) k_lat_col_fwd(LatArgs a, int l2, int lc) {
             for (int r = 0; r < 16; ++r) xs[ip_off<M_log>(brev_c<16>(r))] = x[r];
         }
         __syncthreads();
-        ip_mid_stages<NT, L1, false, true>(sm, C, ld, a.tw);  // warp-local after stage 0 (ipfft.cuh)
+        ip_mid_stages<NT, L1, false, true, false, true>(sm, C, ld, a.tw);  // warp-local after stage 0 (ipfft.cuh)
         // tail stage, results back in place
         {
             double2* xs = sm + vec * ld + S(p0);
@@ -446,7 +539,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
         double2* xs = sm + gvec * lds + S(gj1);
         double2 x[16];
 #pragma unroll
-        for (int r = 0; r < 16; ++r) x[r] = cmul(xs[ip_off<M_log>(r)], s_ostep[r]);
+        for (int r = 0; r < 16; ++r) x[r] = r ? cmul(xs[ip_off<M_log>(r)], s_ostep[r]) : xs[0];  // s_ostep[0] = 1
         reg_dft<16>(x, -1);
         t0.each0([&](int k2, double2 w) { x[brev_c<16>(k2)] = cmul(x[brev_c<16>(k2)], w); });
 #pragma unroll
@@ -748,8 +841,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
             const int j2 = gj1 + (brev_c<16>(r) << M_log);
-            Yo[xoff_r(a, j2 >> a.lwc, gvec, li, j2 & (a.WC - 1))] =
-                cmulc(x[r], s_ostep[brev_c<16>(r)]);
+            Yo[xoff_r(a, j2 >> a.lwc, gvec, li, j2 & (a.WC - 1))] = r ? cmulc(x[r], s_ostep[brev_c<16>(r)]) : x[0];
         }
     }
 }
@@ -796,14 +888,16 @@ __global__ void __launch_bounds__(NT) k_lat_col_inv(LatArgs a, int l2, int lc) {
     for (int j = 0; j < DC; ++j) acc[j] = 0.0;
     int vcur = -1;
     auto slot = [&](int vv) { return a.part_dot + (size_t(vv) * nslot + blockIdx.x) * (MAXD + 1); };
+    bool prodrun = false;  // the current run accumulates in product form (same candidate: CTA-uniform)
     auto flush = [&](int vv) {
         block_sum_vec<NT, DC>(acc, redv);
         if (threadIdx.x == 0) {
             double* out = slot(vv);
 #pragma unroll
             for (int j = 0; j < DC; ++j)
-                if (j < a.d) out[j] = acc[j];
+                if (j < a.d) out[j] = prodrun ? 2.0 * acc[j] * LatGen<DC, ALPHA>::dscale(a, vv / a.V, j) : acc[j];
         }
+        prodrun = false;
 #pragma unroll
         for (int j = 0; j < DC; ++j) acc[j] = 0.0;
     };
@@ -846,12 +940,26 @@ __global__ void __launch_bounds__(NT) k_lat_col_inv(LatArgs a, int l2, int lc) {
         }
         {
             LatGen<DC, ALPHA> G;
-            G.init(a, c, o);
+#if LAT_GEN_PROD
+            // product form (LatGen::init_prod): the run's sums are unscaled, flush applies dscale
+            if (G.init_prod(a, c, o)) {
+                prodrun = true;
 #pragma unroll
-            for (int r = 0; r < 16; ++r) {
-                const uint32_t J = (uint32_t(j1 + (brev_c<16>(r) << M_log)) << l2) + c0 + uint32_t(vec);
-                G.dq_acc(2u * J, 2.0 * x[r].x, acc);  // W(2j) = 2 Re z, W(2j+1) = 2 Im z
-                G.dq_acc(2u * J + 1u, 2.0 * x[r].y, acc);
+                for (int r = 0; r < 16; ++r) {
+                    const uint32_t J = (uint32_t(j1 + (brev_c<16>(r) << M_log)) << l2) + c0 + uint32_t(vec);
+                    G.dq_acc_prod(2u * J, x[r].x, acc);  // W(2j) = 2 Re z, W(2j+1) = 2 Im z: the 2 is in flush
+                    G.dq_acc_prod(2u * J + 1u, x[r].y, acc);
+                }
+            } else
+#endif
+            {
+                G.init(a, c, o);
+#pragma unroll
+                for (int r = 0; r < 16; ++r) {
+                    const uint32_t J = (uint32_t(j1 + (brev_c<16>(r) << M_log)) << l2) + c0 + uint32_t(vec);
+                    G.dq_acc(2u * J, 2.0 * x[r].x, acc);  // W(2j) = 2 Re z, W(2j+1) = 2 Im z
+                    G.dq_acc(2u * J + 1u, 2.0 * x[r].y, acc);
+                }
             }
         }
     }
