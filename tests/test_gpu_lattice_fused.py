@@ -193,7 +193,9 @@ def test_frequency_sharded_virtual_ranks(case):
         r = sharding.ShardedLatticeFit(dz, g, G, model=model(dz, y, True))
         ranks.append(r)
     got = sharding.sharded_nll(ranks, hp, grad=True, exchange=sharding.local_exchange(G), gather=lambda recs: recs)
-    close_results(got, want, dz.N, 1e-11)
+    # 3e-11: the gradient dot is a cancelling sum (terms of both signs ~1e3 x the result at B4, d = 5);
+    # the ranks group its partials differently from the one-GPU grid (measured 1.2e-11 at m17-T3-d5-a2)
+    close_results(got, want, dz.N, 3e-11)
     nog = sharding.sharded_nll(ranks, hp, grad=False, exchange=sharding.local_exchange(G), gather=lambda recs: recs)
     assert abs(nog["nll"] - want["nll"]) <= 1e-11 * abs(want["nll"])
 
