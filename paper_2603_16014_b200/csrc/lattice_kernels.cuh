@@ -666,6 +666,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_lat_mid(LatArg
 #pragma unroll
                 for (int o = 0; o < P; ++o) {
                     if (o >= V) break;
+                    if (DIST && o == 0) {  // class 0 = the diagonal pairs: a real adjoint (5 operations)
+                        const double Ex = ZA[0].x + ZB[0].x, Dx = ZA[0].x - ZB[0].x, Ox = Dx * w.x;
+                        bufA[S(pA)] = make_double2(fma(Dx, w.y, Ex), Ox);
+                        bufB[S(pB)] = make_double2(fma(-Dx, w.y, Ex), Ox);
+                        continue;
+                    }
                     const double Ex = ZA[o].x + ZB[o].x, Ey = ZA[o].y - ZB[o].y;
                     const double Dx = ZA[o].x - ZB[o].x, Dy = ZA[o].y + ZB[o].y;
                     const double Ox = fma(Dx, w.x, Dy * w.y), Oy = fma(Dy, w.x, -(Dx * w.y));

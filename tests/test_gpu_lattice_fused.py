@@ -123,6 +123,25 @@ def test_fused_batch_equals_single():
         assert np.array_equal(rs["deta"], rb["deta"]) and np.array_equal(rs["dB"], rb["dB"])
 
 
+@pytest.mark.parametrize("alpha", [1, 2])
+def test_fused_product_form_fallback(alpha):
+    """The column kernels' lattice generator runs in product form f_j = B_j (v + A_j / B_j) unless some
+    B_j = eta_j k_a is too small to divide by (LatGen::init_prod); eta_j = 0 and a tiny eta_j must take
+    the A + B v form and agree with the generic path, also next to product-form candidates in one batch."""
+    dz, hp, y = make(17, 2, 4, alpha)
+    zero = hp.replace(eta=hp.eta * np.array([1.0, 0.0, 1.0, 1.0]))
+    tiny = hp.replace(eta=hp.eta * np.array([1.0, 1.0, 1e-130, 1.0]))
+    Mf = model(dz, y, True, max_candidates=3)
+    Mg = model(dz, y, False)
+    for h in (zero, tiny):
+        rf, rg = Mf.nll(h, grad=True), Mg.nll(h, grad=True)
+        close_results(rf, rg, dz.N, floor_of(Mg, dz, h))
+    batch = Mf.nll_batch([hp, zero, tiny], grad=True)
+    for h, rb in zip([hp, zero, tiny], batch):
+        rg = Mg.nll(h, grad=True)
+        close_results(rb, rg, dz.N, floor_of(Mg, dz, h))
+
+
 def test_fused_gradient_vs_reference_fd(ref):
     dz, hp, y = make(17, 2, 2, 1)
     M = model(dz, y, True)
