@@ -7,6 +7,11 @@ namespace fmtgp {
 
 thread_local std::vector<DigLaunchRec>* dig_rec = nullptr;
 
+// Column FWHT radix of K1 / K3 (wht_radix_cap): a radix-16 stage of a 2^10-element tile has 64 groups
+// for 256 threads.  Measured on config 5 (256-candidate sweep, K1 / K3 totals): radix 16 5.76 / 9.14 ms,
+// radix 8 (half the CTA busy) 5.42 / 12.0 ms, radix 4 (all of it) 6.96 / 13.9 ms — the idle threads'
+// issue slots go to the SM's other CTAs, so K1 takes radix 8 and K3 stays at radix 16.
+
 // hyperparameters of candidate c (kernel parameters when use_hv, else the device block)
 template <int D>
 __device__ __forceinline__ double hv_eta(const DigArgs& a, int c, int j) {
@@ -125,6 +130,11 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_fwd(DigArgs a, int l1, int l2
 #pragma unroll
         for (int j = 0; j < D; ++j) off[j] = __ldg(a.cofs + size_t(o) * MAXD + j);
     }
+    const int rstep = NT >> lc;
+    const bool lin = (NT & (C - 1)) == 0 && (rstep & 15) == 0;
+    const int so0 = (int(threadIdx.x) & (C - 1)) * ld + sidx<true>(int(threadIdx.x) >> lc), sstep = rstep + (rstep >> 4);
+    const long long go0 = ((long long)(int(threadIdx.x) >> lc) << l2) + c0 + (int(threadIdx.x) & (C - 1));
+    const long long gstep = (long long)rstep << l2;
 #pragma unroll 1
     for (int c = cb; c < ce; ++c) {
         double eta[D];
@@ -163,11 +173,17 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_fwd(DigArgs a, int l1, int l2
             }
         }
         __syncthreads();
-        smem_wht<NT, true>(sm, l1, C, ld);
+        smem_wht<NT, true>(sm, l1, C, ld, wht_radix_cap<NT>(l1, C, 1));  // >= half of the CTA busy per stage
         double* out = a.Y + (size_t(c) * a.V + o) * n;
-        for (int e = threadIdx.x; e < (C << l1); e += NT) {
-            const int k1 = e >> lc, cc = e & (C - 1);
-            out[((long long)k1 << l2) + c0 + cc] = sm[cc * ld + sidx<true>(k1)];
+        if (lin) {  // affine offsets (see k_dig_col_inv's load_tile)
+            const double* s0 = sm + so0;
+            double* o0 = out + go0;
+            for (int i = 0, e = threadIdx.x; e < tile; ++i, e += NT) o0[i * gstep] = s0[i * sstep];
+        } else {
+            for (int e = threadIdx.x; e < (C << l1); e += NT) {
+                const int k1 = e >> lc, cc = e & (C - 1);
+                out[((long long)k1 << l2) + c0 + cc] = sm[cc * ld + sidx<true>(k1)];
+            }
         }
     }
     dig_trace(a.trace, 1, false);
@@ -317,15 +333,30 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
     __shared__ double redv[(NT / 32) * D];
     // candidate groups double-buffer the column tile: candidate c + 1's tile streams in while c is
     // transformed and reduced (second buffer after the kappa tile)
-    double* tiles[2] = {sm, kbuf + (a.kap ? D * tile : 0) + 2};
+    double* const tile1 = kbuf + (a.kap ? D * tile : 0) + 2;
+    auto tile_of = [&](int k) { return (k & 1) ? tile1 : sm; };  // (no local pointer array: it would live in local memory)
+    // element e_i = tid + i NT of a tile sits at row k1 = (tid >> lc) + i (NT >> lc), column tid & (C - 1):
+    // when NT / C is a multiple of 16 both its padded smem offset and its global offset are affine in
+    // i, and a candidate's tile load is one multiply-add pair per copy instead of the index math
+    const int rstep = NT >> lc;
+    const bool lin = (NT & (C - 1)) == 0 && (rstep & 15) == 0;
+    const int so0 = (int(threadIdx.x) & (C - 1)) * ld + sidx<true>(int(threadIdx.x) >> lc), sstep = rstep + (rstep >> 4);
+    const long long go0 = ((long long)(int(threadIdx.x) >> lc) << l2) + c0 + (int(threadIdx.x) & (C - 1));
+    const long long gstep = (long long)rstep << l2;
     auto load_tile = [&](double* dst, int cand) {
         const double* x = a.Y + (size_t(cand) * a.V + o) * n;
-        for (int e = threadIdx.x; e < tile; e += NT) {
-            const int k1 = e >> lc, cc = e & (C - 1);
-            cp_async8(&dst[cc * ld + sidx<true>(k1)], &x[((long long)k1 << l2) + c0 + cc]);
+        if (lin) {
+            double* d0 = dst + so0;
+            const double* x0 = x + go0;
+            for (int i = 0, e = threadIdx.x; e < tile; ++i, e += NT) cp_async8(d0 + i * sstep, x0 + i * gstep);
+        } else {
+            for (int e = threadIdx.x; e < tile; e += NT) {
+                const int k1 = e >> lc, cc = e & (C - 1);
+                cp_async8(&dst[cc * ld + sidx<true>(k1)], &x[((long long)k1 << l2) + c0 + cc]);
+            }
         }
     };
-    load_tile(tiles[0], cb);
+    load_tile(tile_of(0), cb);
     GenSrc g{};
     if (!kp) {  // XOR tables of the digital net (candidate-independent)
         g.sp = a.sp;
@@ -335,7 +366,7 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
     }
 #pragma unroll 1
     for (int cc2 = cb; cc2 < ce; ++cc2) {
-        double* tb = tiles[(cc2 - cb) & 1];
+        double* tb = tile_of(cc2 - cb);
         double eta[D];
 #pragma unroll
         for (int j = 0; j < D; ++j) eta[j] = eta_nx[j];
@@ -350,8 +381,8 @@ __global__ void __launch_bounds__(NT, 3) k_dig_col_inv(DigArgs a, int l1, int l2
         for (int j = 0; j < D; ++j) acc[j] = 0.0;
         cp_async_wait_all();  // this candidate's tile (and, first time, the kappa tile)
         __syncthreads();      // ... visible to all; the previous candidate is done with the other buffer
-        if (cc2 + 1 < ce) load_tile(tiles[(cc2 + 1 - cb) & 1], cc2 + 1);
-        smem_wht<NT, true>(tb, l1, C, ld);
+        if (cc2 + 1 < ce) load_tile(tile_of(cc2 + 1 - cb), cc2 + 1);
+        smem_wht<NT, true>(tb, l1, C, ld);  // radix 16 (smaller radices measured slower here: 9.1 -> 12.0 / 13.9 ms)
         if (kp) {
             for (int e = threadIdx.x; e < tile; e += NT) {
                 const double W = tb[(e & (C - 1)) * ld + sidx<true>(e >> lc)];  // W = H M, natural index

@@ -234,12 +234,23 @@ __device__ __forceinline__ void wht_stage(double* buf, int logN, int s, int nvec
     __syncthreads();
 }
 
+// Largest radix (log2, 1..4) whose stages still give at least `share` of the NT threads a group.
+template <int NT>
+__device__ __forceinline__ int wht_radix_cap(int logN, int nvec, int share_log) {
+    const int elems = nvec << logN;
+    int cap = 4;
+    while (cap > 1 && (elems >> cap) < (NT >> share_log)) --cap;
+    return cap;
+}
+
 // Unnormalised Walsh-Hadamard transform of nvec vectors of length 2^logN in smem.
+// `cap` bounds the radix of a stage (log2): a radix-16 stage has 2^logN nvec / 16 groups, one per
+// thread, so small tiles leave most of the CTA waiting at the stage's barrier (wht_radix_cap).
 template <int NT, bool PADDED = false>
-__device__ void smem_wht(double* buf, int logN, int nvec, int vstride) {
+__device__ void smem_wht(double* buf, int logN, int nvec, int vstride, int cap = 4) {
     int done = 0;
     while (done < logN) {
-        const int left = logN - done;
+        const int left = min(logN - done, cap);
         if (left >= 4) {
             wht_stage<NT, 16, 4, PADDED>(buf, logN, done, nvec, vstride);
             done += 4;
